@@ -1,0 +1,455 @@
+"""bench.py -- decode tokens/s of the LeoAM selection + sparse-decode hot path on B200.
+
+Workload (BASELINE.json metric "decode tokens/s @ LLaMA-7B shape, 64K ctx"): one decode
+step = for every one of the 32 layers, for every (batch row, head) lane: chunk bounds (K3),
+lower-bound pruning (plan), canonical f64 scoring of candidate keys (K4), exact top-k
+(K5, rate 0.5 in layers 0-1 and 0.1 after, engine.py:83-86), runs (K6) and sparse
+attention over the selected set (K7).  LLaMA-7B attention shape: 32 layers x 32 heads x
+d=128, 64K tokens of resident bf16 KV per lane, synthetic planted-desert KV
+(trace.py:270-315 model, generated on device) or N(0,1) KV.  The dense model body (QKV/O/MLP
+GEMMs) is not part of the hot path and is not run.
+
+Timing: W warm-up steps, then K steps replayed from one CUDA graph, bracketed by
+barrier + synchronize, CUDA events on the launching stream, max over ranks.  KV is
+>= 32 GiB per GPU, far beyond the 126 MB L2, so no flush is needed.  `e2e` repeats the
+measurement through the same public API with the step's queries copied from pinned host
+memory and the attention outputs copied back every step.
+
+Multi-GPU (torchrun): every rank owns a disjoint batch of lanes (batch x head sharding,
+no collective on the data path); value = all ranks' tokens / max-over-ranks time.
+
+--impl reference: the reference algorithm (kvtier's branch-and-bound select_top_k +
+attention_output, restated in C in oracle/, the reference itself is pure Python and
+cannot travel to the GPU box) on a bounded sample of the same workload's lanes, all host
+threads, extrapolated to the whole step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+N_LAYERS, N_HEADS, HEAD_DIM = 32, 32, 128  # LLaMA-7B attention shape
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--batch", type=int, default=1, help="batch rows per GPU")
+    p.add_argument("--ctx", type=int, default=65536)
+    p.add_argument("--data", choices=["planted", "random"], default="planted")
+    p.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
+    p.add_argument("--layers", type=int, default=N_LAYERS)
+    p.add_argument("--cpu-lanes", type=int, default=16, help="lanes in the CPU baseline sample")
+    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--json-out", type=str, default="")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+# synthetic workload
+# ------------------------------------------------------------------------------------------------
+
+
+def planted_regions(rng, n, desert_rate=0.7, n_regions=3):
+    """Hot-region placement of trace.py:220-267 (multinomial gaps between 3 runs)."""
+    n_hot = math.ceil((1.0 - desert_rate) * n)
+    r = min(n_regions, n_hot, n - n_hot + 1)
+    base, extra = divmod(n_hot, r)
+    sizes = [base + (1 if i < extra else 0) for i in range(r)]
+    slack = n - n_hot - (r - 1)
+    gaps = rng.multinomial(slack, [1.0 / (r + 1)] * (r + 1)) if slack > 0 else [0] * (r + 1)
+    out, pos = [], int(gaps[0])
+    for i, s in enumerate(sizes):
+        out.append((pos, pos + s))
+        pos += s + (1 + int(gaps[i + 1]) if i < r - 1 else 0)
+    return out
+
+
+def fill_layer(torch, K, V, n, d, data, rng, gen, u_out):
+    """Fill one layer's K/V [lanes, n_cap, d] on device; returns per-lane unit directions."""
+    lanes = K.shape[0]
+    dev = K.device
+    if data == "random":
+        for i in range(lanes):
+            K[i, :n].normal_(generator=gen)
+            V[i, :n].normal_(generator=gen)
+        u = torch.randn((lanes, d), device=dev, generator=gen)
+        u_out.copy_(u)
+        return
+    u = torch.randn((lanes, d), device=dev, generator=gen, dtype=torch.float64)
+    u /= u.norm(dim=1, keepdim=True)
+    u_out.copy_(u)
+    scale = 0.05 / math.sqrt(d)
+    for i in range(lanes):
+        amps = rng.uniform(-0.25, 0.25, size=n)
+        hot_base = 0.25 + 1.0 + 0.02
+        for s, e in planted_regions(rng, n):
+            amps[s:e] = hot_base + rng.uniform(0.0, 0.5, size=e - s)
+        a = torch.from_numpy(amps).to(dev)
+        noise = torch.randn((n, d), device=dev, generator=gen, dtype=torch.float32) * scale
+        ui = u[i].float()
+        noise -= (noise @ ui)[:, None] * ui[None, :]
+        K[i, :n] = (a.float()[:, None] * ui[None, :] + noise).to(K.dtype)
+        V[i, :n].normal_(generator=gen)
+
+
+def make_queries(torch, u, steps, data, gen):
+    """[steps, L, lanes, d] f32: gain*u for planted lanes (trace.py:309-310), N(0,1) otherwise."""
+    L, lanes, d = u.shape
+    if data == "random":
+        return torch.randn((steps, L, lanes, d), device=u.device, generator=gen)
+    gains = torch.rand((steps, L, lanes, 1), device=u.device, generator=gen, dtype=torch.float64) + 1.0
+    return (gains * u[None].double()).float()
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks
+# ------------------------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [x for x in out.splitlines() if x.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# reference arm / cpu baseline
+# ------------------------------------------------------------------------------------------------
+
+
+def cpu_sample_lanes(args):
+    """Bounded sample of the workload's lanes: heads 0..h-1 of layer 0 (rate 0.5, C=8) and
+    layer 16 (rate 0.1, C=64) -- BASELINE.md sec. 3 -- generated on the host."""
+    from oracle import synth
+    h = max(1, args.cpu_lanes // 2)
+    n, d = args.ctx, HEAD_DIM
+    groups = []
+    for layer, rate, C in ((0, 0.5, 8), (16, 0.1, 64)):
+        K = np.empty((h, n, d), np.float32)
+        V = np.empty((h, n, d), np.float32)
+        Q = np.empty((args.cpu_steps, h, d), np.float32)
+        for i in range(h):
+            if args.data == "planted":
+                k, q, v, _ = synth.lane(synth.Profile(0.7, 3, 1.0, args.seed), layer, i, n, d, args.cpu_steps)
+            else:
+                rng = np.random.default_rng([args.seed, layer, i])
+                k = rng.normal(size=(n, d)).astype(np.float32)
+                v = rng.normal(size=(n, d)).astype(np.float32)
+                q = rng.normal(size=(args.cpu_steps, d)).astype(np.float32)
+            K[i], V[i], Q[:, i] = k, v, q
+        groups.append((layer, rate, C, K, V, Q))
+    return groups
+
+
+def cpu_baseline(args, lanes_per_layer):
+    """Time the reference algorithm on the sample with all host threads; extrapolate."""
+    from oracle import oracle as O
+    threads = O.host_threads()
+    groups = cpu_sample_lanes(args)
+    per_lane = {}
+    total_lane_steps = 0
+    wall = 0.0
+    for layer, rate, C, K, V, Q in groups:
+        n = K.shape[1]
+        r = O.bench_lanes(K, V, Q, math.ceil(rate * n), O.next_pow2(n) // C, threads)
+        lane_steps = K.shape[0] * Q.shape[0]
+        per_lane[layer] = r["lane_step_s"]  # thread-seconds per lane-step (select + attention)
+        total_lane_steps += lane_steps
+        wall += r["wall_s"]
+    early = 2
+    cpu_s = (early * lanes_per_layer * per_lane[0] + (args.layers - early) * lanes_per_layer * per_lane[16])
+    step_s = cpu_s / threads
+    return {"step_s": step_s, "threads": threads, "per_lane_s": per_lane, "sample_wall_s": wall,
+            "sample": (f"{total_lane_steps} lane-steps: heads 0-{K.shape[0]-1} of layers 0 (rate 0.5, C=8) and 16 "
+                       f"(rate 0.1, C=64), {args.ctx} tokens, {args.data} KV; extrapolated linearly to "
+                       f"{args.layers}x{lanes_per_layer} lanes per step, ideal scaling over {threads} threads")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    lanes = args.batch * N_HEADS * max(1, world)
+    samples = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline(args, lanes)
+        if s >= args.warmup:
+            samples.append(r)
+    step_s = float(np.mean([r["step_s"] for r in samples]))
+    value = args.batch * max(1, world) / step_s
+    line = {
+        "metric": "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline",
+        "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic {args.data} KV (host, oracle.synth)",
+        "config": workload_config(args, max(1, world)),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": samples[0]["threads"], "kind": "port",
+                         "sample": samples[0]["sample"]},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world):
+    return {"workload": f"llama7b-attn-{args.ctx // 1024}k-b{args.batch * world}-{args.dtype}-{args.data}",
+            "layers": args.layers, "heads": N_HEADS, "head_dim": HEAD_DIM, "context": args.ctx,
+            "global_batch": args.batch * world, "batch_per_gpu": args.batch, "importance_rate": 0.10,
+            "early_layer_rate": 0.50, "chunk": {"early_layers": 8, "other": 64},
+            "parallelism": f"batch x head sharding over {world} GPU(s), no collective",
+            "l2": "inputs (KV >= 32 GiB/GPU) >> 126 MB L2; no flush"}
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20187_b200 import ops
+    from paper_2506_20187_b200.decode import SparseDecoder
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    L = args.layers
+    dec = SparseDecoder(L, args.batch, N_HEADS, HEAD_DIM, args.ctx, dtype=dt, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 * args.seed + rank)
+    rng = np.random.default_rng([args.seed, rank])
+    u = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
+    for l in range(L):
+        fill_layer(torch, dec.K[l], dec.V[l], args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
+    dec.set_length(args.ctx)
+    steps_total = args.warmup + args.steps
+    Q = make_queries(torch, u, steps_total, args.data, gen)
+    q_static = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
+    out_static = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.Stream(device=dev)
+    graph = None
+    with torch.cuda.stream(stream):
+        for s in range(args.warmup):
+            q_static.copy_(Q[s])
+            dec.step(q_static, out_static)
+        stream.synchronize()
+        if not args.no_graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                dec.step(q_static, out_static)
+            graph.replay()
+            stream.synchronize()
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            dec.step(q_static, out_static)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- timed region (device-resident inputs) ----
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for s in range(args.steps):
+                q_static.copy_(Q[args.warmup + s])
+                one_step()
+            ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clocks = clk.summary()
+    ms_all = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_all, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_all.item())
+    value = args.batch * world / (ms_max / 1e3)
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hq = torch.empty((args.steps, L, dec.lanes, HEAD_DIM), dtype=torch.float32, pin_memory=True)
+        hq.copy_(Q[args.warmup:].cpu())
+        ho = torch.empty((args.steps, L, dec.lanes, HEAD_DIM), dtype=torch.float32, pin_memory=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for s in range(args.steps):
+                q_static.copy_(hq[s], non_blocking=True)
+                one_step()
+                ho[s].copy_(out_static, non_blocking=True)
+            e1.record(stream)
+        e1.synchronize()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        nb = L * dec.lanes * HEAD_DIM * 4
+        e2e = {"value": args.batch * world / (float(ems.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": float(ems.item())}
+
+    # ---- per-kernel attribution: staged pipeline with events on the launching stream ----
+    stages = ["bounds", "plan", "score", "select", "runs", "attn"]
+    st_ms = {s: 0.0 for s in stages}
+    n_cand = [[0] * dec.lanes for _ in range(L)]
+    reps = 2
+    with torch.cuda.stream(stream):
+        for rep in range(reps):
+            q_static.copy_(Q[args.warmup + rep % args.steps])
+            for l in range(L):
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
+                C, n, k = dec.C[l], dec.n, dec.k_for(l)
+                evs[0].record(stream)
+                U, Lo = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C)
+                evs[1].record(stream)
+                plan = ops.select_plan(U, Lo, n, k, C)
+                evs[2].record(stream)
+                cs, ct = ops.cand_score(q_static[l], dec.K[l], plan, n)
+                evs[3].record(stream)
+                st, ss, ns = ops.topk_select(cs, ct, plan["n_cand"], k)
+                evs[4].record(stream)
+                ops.runs_scan(st, ns, n, want_partition=False)
+                evs[5].record(stream)
+                ops.sparse_decode_attn(dec.V[l], st, ss, ns)
+                evs[6].record(stream)
+                evs[6].synchronize()
+                for i, sname in enumerate(stages):
+                    st_ms[sname] += evs[i].elapsed_time(evs[i + 1]) / reps
+                if rep == 0:
+                    n_cand[l] = plan["n_cand"].cpu().tolist()
+    algo = dec.algorithmic_bytes(n_cand)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    dom = max(stages, key=lambda s: st_ms[s])
+    per_kernel = {s: {"ms_per_step": st_ms[s], "algo_bytes": algo[s],
+                      "gbs": algo[s] / (st_ms[s] / 1e3) / 1e9 if st_ms[s] > 0 else None} for s in stages}
+    staged_total = sum(st_ms.values())
+    launches_per_layer = 7  # bounds, plan, score, select (cluster), runs, attn split, attn merge
+    sel_gather_bytes = algo["bounds"] + algo["score"] + algo["select"] + algo["attn"]
+    frac_of = "measured" if "hbm_gbs" in peaks else "fallback"
+    line = {
+        "metric": "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if True else args.dtype,
+        "kv_dtype": args.dtype,
+        "data": f"synthetic {args.data} KV generated on device (trace.py:270-315 model); no model weights",
+        "config": workload_config(args, world),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": per_kernel[dom]["gbs"], "peak": hbm_peak,
+                     "unit": "GB/s", "frac": (per_kernel[dom]["gbs"] or 0) / hbm_peak,
+                     "traffic": None, "peak_source": frac_of,
+                     "algo_bytes_per_step": algo[dom], "kernel_ms_per_step": st_ms[dom],
+                     "kernel_share_of_staged_step": st_ms[dom] / staged_total if staged_total else None},
+        "selection_gather_gbs": sel_gather_bytes / (ms_max / 1e3) / 1e9,
+        "selection_gather_frac": sel_gather_bytes / (ms_max / 1e3) / 1e9 / hbm_peak,
+        "per_kernel": per_kernel,
+        "candidate_fraction": float(np.sum(n_cand) / (L * dec.lanes * dec.n)),
+        "gpu_launches": launches_per_layer * L * args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args, dec.lanes)
+        line["cpu_baseline"] = {"value": args.batch / cb["step_s"], "unit": "tokens/s", "cores": cb["threads"],
+                                "kind": "port", "sample": cb["sample"], "ms_per_step": cb["step_s"] * 1e3}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.json_out:
+            Path(args.json_out).write_text(s + "\n")
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

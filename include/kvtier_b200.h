@@ -1,0 +1,181 @@
+/*
+ * kvtier_b200.h -- C ABI of the B200 (sm_100a) KV-selection + sparse-decode library.
+ *
+ * Drop-in boundary for the reference's hot path (kvtier 0.1.0, pure Python/numpy):
+ * every entry point below replaces one reference function, cited as file:line under
+ * /root/reference/pkg/src/kvtier/.  The Python host package paper_2506_20187_b200 keeps
+ * the reference's module/function names on top of these calls.
+ *
+ * Conventions
+ *   - Pointers are DEVICE pointers unless stated; the caller owns all memory.
+ *   - A "lane" is one (batch row, head) KV sequence (reference: one (layer, head),
+ *     engine.py:316).  Lane i's rows start at base + i * lane_stride (elements); rows are
+ *     contiguous with stride d.
+ *   - Token positions are int32 (context < 2^31).
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy default)
+ *     and returns a kvt_status; nothing throws across the ABI; no global mutable state.
+ *   - Scores are the canonical float64 logits fl(q.k)/fl(sqrt d);
+ *     bounds are widened to be sound for them.  Order for top-k: score desc, index asc.
+ */
+#ifndef KVTIER_B200_H
+#define KVTIER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KVT_API __attribute__((visibility("default")))
+#else
+#define KVT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KVT_OK = 0,
+    KVT_ERR_SHAPE = -1,      /* ValueError: shape mismatch (importance.py:31-32) */
+    KVT_ERR_K = -2,          /* ValueError: k out of [0, n] (chunk_tree.py:251-252) */
+    KVT_ERR_COLD = -3,       /* RuntimeError: cold leaf without a store (chunk_tree.py:275-277) */
+    KVT_ERR_OOM = -4,        /* workspace too small */
+    KVT_ERR_CUDA = -5,       /* CUDA launch/runtime error */
+    KVT_ERR_DTYPE = -6,      /* unsupported dtype combination */
+    KVT_ERR_ARG = -7         /* other invalid argument (ValueError) */
+} kvt_status;
+
+typedef enum { KVT_F32 = 0, KVT_F64 = 1, KVT_BF16 = 2, KVT_F16 = 3 } kvt_dtype;
+
+/* Library version (major*10000 + minor*100 + patch) and status text. */
+KVT_API int kvt_version(void);
+KVT_API const char* kvt_status_string(int status);
+/* Last CUDA error text recorded by this thread (for KVT_ERR_CUDA). */
+KVT_API const char* kvt_last_error(void);
+
+/* ---- K1: chunk abstracts -------------------------------------------------------------
+ * Replaces importance.py:80-87 make_abstract (and the per-leaf loop of chunk_tree.py:
+ * 199-208 build_partition).  Uniform grid: chunk c of lane i covers tokens
+ * [c*C, min((c+1)*C, n)); chunks [c_begin, c_end) are (re)built.  Outputs are the
+ * element-wise max / min key rows, dtype F32 for F32/BF16/F16 keys and F64 for F64 keys,
+ * at amax + i*abs_lane_stride + c*d. */
+KVT_API int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lanes, int64_t lane_stride,
+                       int64_t n, int d, int C, int64_t c_begin, int64_t c_end,
+                       void* amax, void* amin, int64_t abs_lane_stride, void* stream);
+
+/* Arbitrary spans (exact abstracts of keys[start:end) of lane lane_of[j]); used for
+ * partition leaves and merged desert runs (importance.py:90-100 merge_abstracts,
+ * chunk_tree.py:344-379 merge_desert).  Output row j at amax + j*d. */
+KVT_API int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_stride, int d,
+                       int64_t n_spans, const int32_t* lane_of, const int32_t* starts,
+                       const int32_t* ends, void* amax, void* amin, void* stream);
+
+/* ---- K3: query-vs-abstract bounds ----------------------------------------------------
+ * Replaces importance.py:108-137 bound_chunk / bound_chunks_batch (logit mode).
+ * Leaves of lane i: if leaf_start == NULL the uniform grid of size C over [0, n)
+ * (n_leaves = ceil(n/C)); otherwise leaf j = [leaf_start[i*leaf_stride + j],
+ * leaf_start[i*leaf_stride + j + 1]) for j < n_leaves[i] (the last end is n).
+ * q: [n_lanes][d] of q_dtype (F32 or F64).  U/L: float64 at U + i*bnd_stride + j. */
+KVT_API int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int d, int64_t n, int C,
+                     const int32_t* leaf_start, const int32_t* n_leaves, int64_t leaf_stride,
+                     const void* amax, const void* amin, int abs_dtype, int64_t abs_lane_stride,
+                     double* U, double* L, int64_t bnd_stride, void* stream);
+
+/* ---- K4 (brute force): canonical token logits -----------------------------------------
+ * Replaces importance.py:27-33 attention_logits / :46-53 score_tokens (logit mode) for
+ * all n tokens of every lane.  out: float64 [n_lanes][n] (row stride out_stride). */
+KVT_API int kvt_token_scores(const void* q, int q_dtype, const void* keys, int key_dtype,
+                     int64_t n_lanes, int64_t lane_stride, int64_t n, int d,
+                     double* out, int64_t out_stride, void* stream);
+
+/* ---- plan: lower-bound threshold tau and candidate work items -------------------------
+ * The pruning half of chunk_tree.py:233-338 select_top_k: tau = the k-th largest lower
+ * bound counting each leaf's rows; every leaf with U >= tau is a candidate (no top-k
+ * token can lie elsewhere).  Candidate leaves are cut into items of <= 64 tokens.
+ * Outputs per lane: items (tok_start, count, out_pos) int32 x3 at items + i*item_stride*3,
+ * n_items[i], n_cand[i] (candidate tokens), cand_leaf flags (int8, may be NULL) and
+ * evals[i] = n_leaves + n_cand (eval_count, chunk_tree.py:256-268,322). */
+KVT_API int kvt_select_plan(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start,
+                    const int32_t* n_leaves, int64_t leaf_stride, const double* U, const double* L,
+                    int64_t bnd_stride, int64_t k, int32_t* items, int64_t item_stride,
+                    int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf, int64_t* evals,
+                    void* stream);
+
+/* ---- K4: candidate scoring -------------------------------------------------------------
+ * Canonical float64 logits of every candidate token (the exact-score half of
+ * select_top_k: singleton bounds, chunk_tree.py:291-296,321).  Writes cand_score
+ * [i*cand_stride + pos] and cand_tok (token index) for pos < n_cand[i]. */
+KVT_API int kvt_cand_score(const void* q, int q_dtype, const void* keys, int key_dtype,
+                   int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,
+                   int64_t item_stride, const int32_t* n_items, double* cand_score,
+                   int32_t* cand_tok, int64_t cand_stride, int blocks_per_lane, void* stream);
+
+/* ---- K5: exact top-k ---------------------------------------------------------------------
+ * Result contract of select_top_k (chunk_tree.py:233-338) / brute force
+ * (engine.py:337-339): the k best candidates by (score desc, token asc).  One thread-
+ * block cluster per lane runs a 64-bit radix select over the candidates with the
+ * histograms reduced through distributed shared memory.  Output ascending token order:
+ * sel_tok[i*sel_stride + r], sel_score (float64), n_sel[i] = k. */
+KVT_API int kvt_topk_select(const double* cand_score, const int32_t* cand_tok, const int32_t* n_cand,
+                    int64_t cand_stride, int64_t n_lanes, int64_t k, int32_t* sel_tok,
+                    double* sel_score, int64_t sel_stride, int32_t* n_sel, void* stream);
+
+/* ---- K6: runs / canonical partition --------------------------------------------------------
+ * engine.py:176-183 _token_runs and the leaf shape of select_top_k + merge_desert
+ * (chunk_tree.py:331-379): the selected runs and their complement (desert runs) tile [0,n).
+ * run_start/run_len: [i*run_stride + r], n_runs[i].  If part_start != NULL also writes
+ * the canonical partition (leaf starts; state 1 = important, 2 = desert) with n_part[i]. */
+KVT_API int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t sel_stride,
+                  int64_t n_lanes, int64_t n, int32_t* run_start, int32_t* run_len,
+                  int64_t run_stride, int32_t* n_runs, int32_t* part_start, int8_t* part_state,
+                  int64_t part_stride, int32_t* n_part, void* stream);
+
+/* ---- K7: sparse decode attention -----------------------------------------------------------
+ * engine.py:145-154 attention_output over the selected set: softmax(sel_score) @ V[sel].
+ * sel_score are the canonical logits from K5 (keys are not re-read).  Split over
+ * `splits` blocks per lane with an online-softmax (m, l, o) merge.  out: float32
+ * [n_lanes][d] (out64: optional float64 copy).  ws: workspace of
+ * kvt_attn_workspace_bytes(n_lanes, d, splits) bytes. */
+KVT_API size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits);
+KVT_API int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride,
+                           int d, const int32_t* sel_tok, const double* sel_score,
+                           const int32_t* n_sel, int64_t sel_stride, int splits, void* ws,
+                           float* out, double* out64, void* stream);
+
+/* ---- fused per-layer pipeline -----------------------------------------------------------------
+ * K3 -> plan -> K4 -> K5 -> K6 -> K7 for n_lanes lanes on the uniform grid C (or the
+ * leaf table), i.e. the body of the engine's per-lane loop (engine.py:316-357) for a whole
+ * layer at once.  Workspace size from kvt_layer_workspace_bytes.  Outputs: sel_tok /
+ * sel_score / n_sel (K5), runs (K6), out (K7), evals. */
+typedef struct {
+    int64_t n_lanes, n, k;
+    int d, C;
+    int key_dtype, v_dtype, q_dtype, abs_dtype;
+    const void* q;              /* [n_lanes][d] */
+    const void* keys;           /* lane i at keys + i*lane_stride */
+    const void* values;
+    int64_t lane_stride;
+    const void* amax;           /* abstracts [n_lanes][abs_lane_stride] */
+    const void* amin;
+    int64_t abs_lane_stride;
+    const int32_t* leaf_start;  /* NULL = uniform grid C */
+    const int32_t* n_leaves;
+    int64_t leaf_stride;
+    int32_t* sel_tok;           /* [n_lanes][k] */
+    double* sel_score;
+    int32_t* n_sel;
+    int32_t* run_start;         /* [n_lanes][k] (may be NULL: skip K6) */
+    int32_t* run_len;
+    int32_t* n_runs;
+    float* out;                 /* [n_lanes][d] */
+    int64_t* evals;             /* [n_lanes] (may be NULL) */
+    int attn_splits;            /* 0 = auto */
+    int score_blocks;           /* 0 = auto */
+} kvt_layer_args;
+
+KVT_API size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d);
+KVT_API int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVTIER_B200_H */

@@ -534,7 +534,8 @@ static void* bench_worker(void* p) {
  * *max_thread_s).  Setup (widening, build_partition) is excluded, as in BASELINE.md sec. 3. */
 ORA_API double ora_bench_lanes(int64_t lanes, int64_t n, int d, int64_t m, int64_t k, int steps,
                                int merge, const float* keys, const float* vals, const float* q,
-                               int nthreads, double* out, int64_t* evals, double* max_thread_s) {
+                               int nthreads, double* out, int64_t* evals, double* max_thread_s,
+                               double* sum_thread_s) {
     if (nthreads < 1) nthreads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
     bench_arg_t* args = (bench_arg_t*)calloc((size_t)nthreads, sizeof(bench_arg_t));
@@ -546,13 +547,15 @@ ORA_API double ora_bench_lanes(int64_t lanes, int64_t n, int d, int64_t m, int64
         a->tid = t; a->nthreads = nthreads; a->out = out; a->evals = evals;
         pthread_create(&th[t], NULL, bench_worker, a);
     }
-    double mx = 0.0;
+    double mx = 0.0, sum = 0.0;
     for (int t = 0; t < nthreads; ++t) {
         pthread_join(th[t], NULL);
         if (args[t].timed_s > mx) mx = args[t].timed_s;
+        sum += args[t].timed_s;
     }
     double wall = now_s() - t0;
     if (max_thread_s) *max_thread_s = mx;
+    if (sum_thread_s) *sum_thread_s = sum;
     free(th); free(args);
     return wall;
 }

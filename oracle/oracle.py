@@ -76,7 +76,7 @@ def lib():
         L.ora_bench_lanes.restype = ctypes.c_double
         L.ora_bench_lanes.argtypes = [_i64, _i64, ctypes.c_int, _i64, _i64, ctypes.c_int,
                                       ctypes.c_int, _fp, _fp, _fp, ctypes.c_int, _dp, _ip,
-                                      ctypes.POINTER(ctypes.c_double)]
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         _lib = L
     return _lib
 
@@ -252,10 +252,12 @@ def bench_lanes(keys: np.ndarray, values: np.ndarray, queries: np.ndarray, k: in
     evals = np.zeros((steps, lanes), dtype=np.int64)
     out = np.zeros((steps, lanes, d)) if want_out else None
     mx = ctypes.c_double(0.0)
+    sm = ctypes.c_double(0.0)
     wall = lib().ora_bench_lanes(lanes, n, d, m, k, steps, int(merge), _p(K, _fp), _p(V, _fp),
                                  _p(Q, _fp), nthreads, None if out is None else _p(out),
-                                 _p(evals, _ip), ctypes.byref(mx))
-    return {"wall_s": wall, "max_thread_s": mx.value, "evals": evals, "out": out,
+                                 _p(evals, _ip), ctypes.byref(mx), ctypes.byref(sm))
+    return {"wall_s": wall, "max_thread_s": mx.value, "sum_thread_s": sm.value,
+            "lane_step_s": sm.value / max(1, lanes * steps), "evals": evals, "out": out,
             "lanes": lanes, "steps": steps, "threads": nthreads}
 
 

@@ -1,0 +1,111 @@
+"""ctypes binding of lib/libkvtier_b200.so (the C ABI declared in include/kvtier_b200.h).
+
+There is no fallback: if the library is missing this module raises ImportError, and
+every compute entry point requires a CUDA device.  Status codes from the ABI map onto the
+reference's exception types (ValueError / RuntimeError, chunk_tree.py:251-252,275-279,
+importance.py:31-32).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libkvtier_b200.so"
+HEADER = _PKG.parent / "include" / "kvtier_b200.h"
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the sm_100a extension first "
+        "(python -c 'import __graft_entry__ as g; g.build()' or make -C paper_2506_20187_b200/csrc). "
+        "This package has no CPU fallback."
+    )
+
+_L = ctypes.CDLL(str(LIB_PATH))
+
+# status codes (kvt_status)
+OK, ERR_SHAPE, ERR_K, ERR_COLD, ERR_OOM, ERR_CUDA, ERR_DTYPE, ERR_ARG = 0, -1, -2, -3, -4, -5, -6, -7
+# dtype codes (kvt_dtype)
+F32, F64, BF16, F16 = 0, 1, 2, 3
+
+_i64, _i32, _vp, _dp, _fp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p
+_sz = ctypes.c_size_t
+
+
+class KvtLayerArgs(ctypes.Structure):
+    """Mirror of kvt_layer_args (include/kvtier_b200.h)."""
+
+    _fields_ = [
+        ("n_lanes", _i64), ("n", _i64), ("k", _i64),
+        ("d", _i32), ("C", _i32),
+        ("key_dtype", _i32), ("v_dtype", _i32), ("q_dtype", _i32), ("abs_dtype", _i32),
+        ("q", _vp), ("keys", _vp), ("values", _vp), ("lane_stride", _i64),
+        ("amax", _vp), ("amin", _vp), ("abs_lane_stride", _i64),
+        ("leaf_start", _vp), ("n_leaves", _vp), ("leaf_stride", _i64),
+        ("sel_tok", _vp), ("sel_score", _vp), ("n_sel", _vp),
+        ("run_start", _vp), ("run_len", _vp), ("n_runs", _vp),
+        ("out", _vp), ("evals", _vp),
+        ("attn_splits", _i32), ("score_blocks", _i32),
+    ]
+
+
+def _sig(name, restype, *argtypes):
+    f = getattr(_L, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+    return f
+
+
+kvt_version = _sig("kvt_version", ctypes.c_int)
+kvt_status_string = _sig("kvt_status_string", ctypes.c_char_p, ctypes.c_int)
+kvt_last_error = _sig("kvt_last_error", ctypes.c_char_p)
+kvt_abstract_build = _sig("kvt_abstract_build", ctypes.c_int, _vp, _i32, _i64, _i64, _i64, _i32, _i32, _i64, _i64,
+                          _vp, _vp, _i64, _vp)
+kvt_abstract_spans = _sig("kvt_abstract_spans", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _vp,
+                          _vp)
+kvt_chunk_bounds = _sig("kvt_chunk_bounds", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _i32, _vp, _vp, _i64, _vp,
+                        _vp, _i32, _i64, _vp, _vp, _i64, _vp)
+kvt_token_scores = _sig("kvt_token_scores", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i64,
+                        _vp)
+kvt_select_plan = _sig("kvt_select_plan", ctypes.c_int, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
+                       _i64, _vp, _vp, _vp, _vp, _vp)
+kvt_cand_score = _sig("kvt_cand_score", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _vp, _vp,
+                      _vp, _i64, _i32, _vp)
+kvt_topk_select = _sig("kvt_topk_select", ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp)
+kvt_runs_scan = _sig("kvt_runs_scan", ctypes.c_int, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
+                     _vp, _vp)
+kvt_attn_workspace_bytes = _sig("kvt_attn_workspace_bytes", _sz, _i64, _i32, _i32)
+kvt_sparse_decode_attn = _sig("kvt_sparse_decode_attn", ctypes.c_int, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp,
+                              _i64, _i32, _vp, _vp, _vp, _vp)
+kvt_layer_workspace_bytes = _sig("kvt_layer_workspace_bytes", _sz, _i64, _i64, _i64, _i32)
+kvt_select_attend = _sig("kvt_select_attend", ctypes.c_int, ctypes.POINTER(KvtLayerArgs), _vp, _sz, _vp)
+
+EXPORTED = [
+    "kvt_version", "kvt_status_string", "kvt_last_error", "kvt_abstract_build", "kvt_abstract_spans",
+    "kvt_chunk_bounds", "kvt_token_scores", "kvt_select_plan", "kvt_cand_score", "kvt_topk_select",
+    "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
+    "kvt_select_attend",
+]
+
+
+class KvtCudaError(RuntimeError):
+    pass
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a kvt_status onto the reference's exception types."""
+    if status == OK:
+        return
+    msg = f"{what}: {kvt_status_string(status).decode()}"
+    if status == ERR_CUDA:
+        raise KvtCudaError(f"{msg} ({kvt_last_error().decode()})")
+    if status == ERR_COLD:
+        raise RuntimeError(msg)
+    if status in (ERR_SHAPE, ERR_K, ERR_ARG, ERR_DTYPE):
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def handle() -> ctypes.CDLL:
+    return _L

@@ -1,0 +1,338 @@
+// abstract_bounds.cu -- K1 chunk abstracts and K3 query-vs-abstract bounds.
+//
+// K1 replaces importance.py:80-87 make_abstract (+ the per-leaf loop of build_partition,
+// chunk_tree.py:199-208): element-wise max / min of a chunk's key rows.  One warp per
+// chunk; lane l owns dims 4l..4l+3 (+128r), so a 128-dim bf16 row is one coalesced 256 B
+// warp load; 8 rows are kept in flight per lane.  HBM-bound: reads C*d*s_K, writes 2*d*4.
+//
+// K3 replaces importance.py:108-137 bound_chunk / bound_chunks_batch: per dimension the
+// query sign picks the max or min key, U = sum q*hi, L = sum q*lo, in the canonical f64
+// order, widened by 2*gamma*A (A = sum |q| max(|hi|,|lo|)) so U >= every canonical token
+// score in the chunk >= L.  Exact for single-row chunks.  One warp per chunk, reads the
+// 2*d abstract floats once.  HBM-bound on abstract bytes (m*2*d*4 per lane).
+#include "common.cuh"
+
+namespace kvt {
+
+template <typename T> struct AbsOf { using type = float; };
+template <> struct AbsOf<double> { using type = double; };
+
+template <typename T, int G, bool VEC>
+__global__ void __launch_bounds__(256) abstract_grid_kernel(
+    const T* __restrict__ keys, int64_t lane_stride, int64_t n, int d, int C, int64_t c_begin,
+    int64_t c_end, typename AbsOf<T>::type* __restrict__ amax,
+    typename AbsOf<T>::type* __restrict__ amin, int64_t abs_lane_stride) {
+    using A = typename AbsOf<T>::type;
+    const int lane = threadIdx.x & 31;
+    const int64_t lane_i = blockIdx.y;
+    const int64_t nchunks = c_end - c_begin;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const T* base = keys + lane_i * lane_stride;
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks; w += warps) {
+        const int64_t c = c_begin + w;
+        const int64_t s = c * C, e = min(n, s + C);
+        double mx[G][4], mn[G][4];
+#pragma unroll
+        for (int r = 0; r < G; ++r)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { mx[r][i] = -INFINITY; mn[r][i] = INFINITY; }
+        int64_t t = s;
+        for (; t + 8 <= e; t += 8) {
+            double v[8][G][4];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int r = 0; r < G; ++r) {
+                    const int g = lane + 32 * r;
+                    if (4 * g < d) load_group<T, VEC>(base + (t + u) * d, g, d, v[u][r]);
+                }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int r = 0; r < G; ++r)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        mx[r][i] = fmax(mx[r][i], v[u][r][i]);
+                        mn[r][i] = fmin(mn[r][i], v[u][r][i]);
+                    }
+        }
+        for (; t < e; ++t) {
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                const int g = lane + 32 * r;
+                if (4 * g < d) {
+                    double v[4];
+                    load_group<T, VEC>(base + t * d, g, d, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) { mx[r][i] = fmax(mx[r][i], v[i]); mn[r][i] = fmin(mn[r][i], v[i]); }
+                }
+            }
+        }
+        A* omx = amax + lane_i * abs_lane_stride + c * d;
+        A* omn = amin + lane_i * abs_lane_stride + c * d;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const int g = lane + 32 * r;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = 4 * g + i;
+                if (j < d) { omx[j] = (A)mx[r][i]; omn[j] = (A)mn[r][i]; }
+            }
+        }
+    }
+}
+
+template <typename T, int G, bool VEC>
+__global__ void __launch_bounds__(256) abstract_spans_kernel(
+    const T* __restrict__ keys, int64_t lane_stride, int d, int64_t n_spans,
+    const int32_t* __restrict__ lane_of, const int32_t* __restrict__ starts,
+    const int32_t* __restrict__ ends, typename AbsOf<T>::type* __restrict__ amax,
+    typename AbsOf<T>::type* __restrict__ amin) {
+    using A = typename AbsOf<T>::type;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n_spans; w += warps) {
+        const T* base = keys + (int64_t)lane_of[w] * lane_stride;
+        const int64_t s = starts[w], e = ends[w];
+        double mx[G][4], mn[G][4];
+#pragma unroll
+        for (int r = 0; r < G; ++r)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { mx[r][i] = -INFINITY; mn[r][i] = INFINITY; }
+        for (int64_t t = s; t < e; ++t) {
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                const int g = lane + 32 * r;
+                if (4 * g < d) {
+                    double v[4];
+                    load_group<T, VEC>(base + t * d, g, d, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) { mx[r][i] = fmax(mx[r][i], v[i]); mn[r][i] = fmin(mn[r][i], v[i]); }
+                }
+            }
+        }
+        A* omx = amax + w * d;
+        A* omn = amin + w * d;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const int g = lane + 32 * r;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = 4 * g + i;
+                if (j < d) { omx[j] = (A)mx[r][i]; omn[j] = (A)mn[r][i]; }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 bounds
+// ------------------------------------------------------------------------------------------
+
+template <typename QT, typename AT, int G>
+__global__ void __launch_bounds__(256) bounds_kernel(
+    const QT* __restrict__ q, int d, int64_t n, int C, const int32_t* __restrict__ leaf_start,
+    const int32_t* __restrict__ n_leaves, int64_t leaf_stride, const AT* __restrict__ amax,
+    const AT* __restrict__ amin, int64_t abs_lane_stride, double* __restrict__ U,
+    double* __restrict__ L, int64_t bnd_stride) {
+    const int lane = threadIdx.x & 31;
+    const int64_t lane_i = blockIdx.y;
+    const int64_t nl = leaf_start ? (int64_t)n_leaves[lane_i] : (n + C - 1) / C;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    double qr[G][4];
+#pragma unroll
+    for (int r = 0; r < G; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = 4 * (lane + 32 * r) + i;
+            qr[r][i] = j < d ? (double)q[lane_i * d + j] : 0.0;
+        }
+    const double sd = sqrt((double)d);
+    const double fac = slack_factor(d);
+    const AT* mxb = amax + lane_i * abs_lane_stride;
+    const AT* mnb = amin + lane_i * abs_lane_stride;
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nl; c += warps) {
+        int64_t rows;
+        if (leaf_start) {
+            const int32_t* ls = leaf_start + lane_i * leaf_stride;
+            const int64_t e = (c + 1 < nl) ? (int64_t)ls[c + 1] : n;
+            rows = e - ls[c];
+        } else {
+            rows = min((int64_t)C, n - c * C);
+        }
+        const AT* M = mxb + c * d;
+        const AT* N = mnb + c * d;
+        double pu = 0.0, pl = 0.0, pa = 0.0;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const int g = lane + 32 * r;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = 4 * g + i;
+                if (j < d) {
+                    const double hi_ = (double)M[j], lo_ = (double)N[j];
+                    const double qj = qr[r][i];
+                    const double hi = qj >= 0.0 ? hi_ : lo_;
+                    const double lo = qj >= 0.0 ? lo_ : hi_;
+                    pu = fma(qj, hi, pu);
+                    pl = fma(qj, lo, pl);
+                    pa = fma(fabs(qj), fmax(fabs(hi_), fabs(lo_)), pa);
+                }
+            }
+        }
+        double u = tree_allreduce(pu), l = tree_allreduce(pl), a = tree_allreduce(pa);
+        if (rows > 1) {
+            const double slack = a * fac;
+            u = u + slack;
+            l = l - slack;
+        }
+        if (lane == 0) {
+            U[lane_i * bnd_stride + c] = u / sd;
+            L[lane_i * bnd_stride + c] = l / sd;
+        }
+    }
+}
+
+}  // namespace kvt
+
+using namespace kvt;
+
+static inline int groups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <= 512 ? 4 : d <= 1024 ? 8 : 0; }
+
+static inline bool aligned16(const void* p, int64_t elem_bytes, int64_t lane_stride, int d) {
+    return ((uintptr_t)p % (4 * elem_bytes) == 0) && (d % 4 == 0) && (lane_stride % 4 == 0);
+}
+
+template <typename T, int G, bool VEC>
+static void launch_abs_grid(const void* keys, int64_t n_lanes, int64_t lane_stride, int64_t n, int d, int C,
+                            int64_t cb, int64_t ce, void* amax, void* amin, int64_t als, cudaStream_t st) {
+    using A = typename AbsOf<T>::type;
+    const int64_t nch = ce - cb;
+    int gx = (int)kvt::imin((nch + 7) / 8, 4096);
+    if (gx < 1) gx = 1;
+    dim3 grid(gx, (unsigned)n_lanes);
+    abstract_grid_kernel<T, G, VEC><<<grid, 256, 0, st>>>((const T*)keys, lane_stride, n, d, C, cb, ce, (A*)amax,
+                                                          (A*)amin, als);
+}
+
+template <typename T>
+static int dispatch_abs_grid(const void* keys, int64_t n_lanes, int64_t lane_stride, int64_t n, int d, int C,
+                             int64_t cb, int64_t ce, void* amax, void* amin, int64_t als, cudaStream_t st) {
+    const bool vec = aligned16(keys, sizeof(T), lane_stride, d);
+    switch (groups_for(d)) {
+#define KVT_CASE(GG)                                                                                        \
+    case GG:                                                                                                \
+        if (vec) launch_abs_grid<T, GG, true>(keys, n_lanes, lane_stride, n, d, C, cb, ce, amax, amin, als, st); \
+        else launch_abs_grid<T, GG, false>(keys, n_lanes, lane_stride, n, d, C, cb, ce, amax, amin, als, st);   \
+        break;
+        KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
+#undef KVT_CASE
+        default: return KVT_ERR_SHAPE;
+    }
+    return kvt_check_launch();
+}
+
+extern "C" int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lanes, int64_t lane_stride, int64_t n,
+                                  int d, int C, int64_t c_begin, int64_t c_end, void* amax, void* amin,
+                                  int64_t abs_lane_stride, void* stream) {
+    if (!keys || !amax || !amin || n_lanes < 0 || n < 0 || d < 1 || C < 1) return KVT_ERR_ARG;
+    if (c_begin < 0 || c_end < c_begin || c_end > (n + C - 1) / C) return KVT_ERR_SHAPE;
+    if (n_lanes == 0 || c_end == c_begin) return KVT_OK;
+    if (n_lanes > 65535) return KVT_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (key_dtype) {
+        case KVT_F32: return dispatch_abs_grid<float>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
+        case KVT_F64: return dispatch_abs_grid<double>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
+        case KVT_BF16: return dispatch_abs_grid<__nv_bfloat16>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
+        case KVT_F16: return dispatch_abs_grid<__half>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
+        default: return KVT_ERR_DTYPE;
+    }
+}
+
+template <typename T, int G, bool VEC>
+static void launch_abs_spans(const void* keys, int64_t lane_stride, int d, int64_t ns, const int32_t* lane_of,
+                             const int32_t* s, const int32_t* e, void* amax, void* amin, cudaStream_t st) {
+    using A = typename AbsOf<T>::type;
+    int gx = (int)kvt::imin((ns + 7) / 8, 8192);
+    abstract_spans_kernel<T, G, VEC><<<gx, 256, 0, st>>>((const T*)keys, lane_stride, d, ns, lane_of, s, e,
+                                                         (A*)amax, (A*)amin);
+}
+
+template <typename T>
+static int dispatch_abs_spans(const void* keys, int64_t lane_stride, int d, int64_t ns, const int32_t* lane_of,
+                              const int32_t* s, const int32_t* e, void* amax, void* amin, cudaStream_t st) {
+    const bool vec = aligned16(keys, sizeof(T), lane_stride, d);
+    switch (groups_for(d)) {
+#define KVT_CASE(GG)                                                                                  \
+    case GG:                                                                                          \
+        if (vec) launch_abs_spans<T, GG, true>(keys, lane_stride, d, ns, lane_of, s, e, amax, amin, st); \
+        else launch_abs_spans<T, GG, false>(keys, lane_stride, d, ns, lane_of, s, e, amax, amin, st);    \
+        break;
+        KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
+#undef KVT_CASE
+        default: return KVT_ERR_SHAPE;
+    }
+    return kvt_check_launch();
+}
+
+extern "C" int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_stride, int d, int64_t n_spans,
+                                  const int32_t* lane_of, const int32_t* starts, const int32_t* ends, void* amax,
+                                  void* amin, void* stream) {
+    if (!keys || !lane_of || !starts || !ends || !amax || !amin || d < 1 || n_spans < 0) return KVT_ERR_ARG;
+    if (n_spans == 0) return KVT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (key_dtype) {
+        case KVT_F32: return dispatch_abs_spans<float>(keys, lane_stride, d, n_spans, lane_of, starts, ends, amax, amin, st);
+        case KVT_F64: return dispatch_abs_spans<double>(keys, lane_stride, d, n_spans, lane_of, starts, ends, amax, amin, st);
+        case KVT_BF16: return dispatch_abs_spans<__nv_bfloat16>(keys, lane_stride, d, n_spans, lane_of, starts, ends, amax, amin, st);
+        case KVT_F16: return dispatch_abs_spans<__half>(keys, lane_stride, d, n_spans, lane_of, starts, ends, amax, amin, st);
+        default: return KVT_ERR_DTYPE;
+    }
+}
+
+template <typename QT, typename AT, int G>
+static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
+                          const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
+                          double* U, double* L, int64_t bs, int64_t max_leaves, cudaStream_t st) {
+    int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 7) / 8, 1024));
+    // keep ~8 CTAs per SM in total when lanes are few
+    dim3 grid(gx, (unsigned)n_lanes);
+    bounds_kernel<QT, AT, G><<<grid, 256, 0, st>>>((const QT*)q, d, n, C, ls, nl, lstr, (const AT*)amax,
+                                                   (const AT*)amin, als, U, L, bs);
+}
+
+template <typename QT, typename AT>
+static int dispatch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
+                           const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
+                           double* U, double* L, int64_t bs, int64_t max_leaves, cudaStream_t st) {
+    switch (groups_for(d)) {
+#define KVT_CASE(GG) \
+    case GG: launch_bounds<QT, AT, GG>(q, n_lanes, d, n, C, ls, nl, lstr, amax, amin, als, U, L, bs, max_leaves, st); break;
+        KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
+#undef KVT_CASE
+        default: return KVT_ERR_SHAPE;
+    }
+    return kvt_check_launch();
+}
+
+extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int d, int64_t n, int C,
+                                const int32_t* leaf_start, const int32_t* n_leaves, int64_t leaf_stride,
+                                const void* amax, const void* amin, int abs_dtype, int64_t abs_lane_stride, double* U,
+                                double* L, int64_t bnd_stride, void* stream) {
+    if (!q || !amax || !amin || !U || !L || d < 1 || n < 0 || n_lanes < 0) return KVT_ERR_ARG;
+    if (!leaf_start && C < 1) return KVT_ERR_ARG;
+    if (leaf_start && !n_leaves) return KVT_ERR_ARG;
+    if (n_lanes == 0 || n == 0) return KVT_OK;
+    if (n_lanes > 65535) return KVT_ERR_ARG;
+    const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (q_dtype == KVT_F32 && abs_dtype == KVT_F32)
+        return dispatch_bounds<float, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+    if (q_dtype == KVT_F64 && abs_dtype == KVT_F32)
+        return dispatch_bounds<double, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+    if (q_dtype == KVT_F32 && abs_dtype == KVT_F64)
+        return dispatch_bounds<float, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+    if (q_dtype == KVT_F64 && abs_dtype == KVT_F64)
+        return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+    return KVT_ERR_DTYPE;
+}

@@ -1,0 +1,148 @@
+// api.cu -- C ABI plumbing: status codes, error text, workspace sizing and the fused
+// per-layer pipeline kvt_select_attend (K3 -> plan -> K4 -> K5 -> K6 -> K7), i.e. the body
+// of the reference's per-lane loop (engine.py:316-357) for every lane of a layer at once.
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+
+#include "common.cuh"
+
+static thread_local char g_err[256] = "";
+
+int kvt_set_cuda_error(cudaError_t e) {
+    snprintf(g_err, sizeof g_err, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return KVT_ERR_CUDA;
+}
+
+int kvt_check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return kvt_set_cuda_error(e);
+    return KVT_OK;
+}
+
+extern "C" int kvt_version(void) { return 100; }  // 0.1.0
+
+extern "C" const char* kvt_status_string(int s) {
+    switch (s) {
+        case KVT_OK: return "ok";
+        case KVT_ERR_SHAPE: return "shape mismatch";
+        case KVT_ERR_K: return "k out of range";
+        case KVT_ERR_COLD: return "cold chunk but no store was given";
+        case KVT_ERR_OOM: return "workspace too small";
+        case KVT_ERR_CUDA: return "CUDA error";
+        case KVT_ERR_DTYPE: return "unsupported dtype";
+        case KVT_ERR_ARG: return "invalid argument";
+        default: return "unknown status";
+    }
+}
+
+extern "C" const char* kvt_last_error(void) { return g_err; }
+
+namespace {
+
+constexpr int ITEM_TOKENS = 64;
+constexpr int MAX_SPLITS = 64;
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carve {
+    char* p;
+    size_t used = 0;
+    explicit Carve(void* base) : p((char*)base) {}
+    template <typename T> T* take(size_t count) {
+        T* r = p ? (T*)(p + used) : nullptr;
+        used += align_up(count * sizeof(T));
+        return r;
+    }
+};
+
+struct LayerWs {
+    double *U, *L;
+    int32_t *items, *n_items, *n_cand;
+    double* cand_score;
+    int32_t* cand_tok;
+    double* attn_part;
+    size_t bytes;
+};
+
+LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d) {
+    Carve c(base);
+    LayerWs w;
+    const int64_t item_cap = (n + ITEM_TOKENS - 1) / ITEM_TOKENS + max_leaves;
+    w.U = c.take<double>((size_t)(n_lanes * max_leaves));
+    w.L = c.take<double>((size_t)(n_lanes * max_leaves));
+    w.items = c.take<int32_t>((size_t)(n_lanes * item_cap * 3));
+    w.n_items = c.take<int32_t>((size_t)n_lanes);
+    w.n_cand = c.take<int32_t>((size_t)n_lanes);
+    w.cand_score = c.take<double>((size_t)(n_lanes * n));
+    w.cand_tok = c.take<int32_t>((size_t)(n_lanes * n));
+    w.attn_part = c.take<double>((size_t)(n_lanes * MAX_SPLITS * (d + 2)));
+    w.bytes = c.used;
+    return w;
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+}  // namespace
+
+extern "C" size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d) {
+    return carve(nullptr, n_lanes, n, max_leaves, d).bytes;
+}
+
+extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream) {
+    if (!a || !ws) return KVT_ERR_ARG;
+    if (a->k < 0 || a->k > a->n) return KVT_ERR_K;
+    if (a->n_lanes <= 0 || a->n <= 0) return a->n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
+    if (!a->leaf_start && a->C < 1) return KVT_ERR_ARG;
+    const int64_t max_leaves = a->leaf_start ? a->leaf_stride : (a->n + a->C - 1) / a->C;
+    LayerWs w = carve(ws, a->n_lanes, a->n, max_leaves, a->d);
+    if (w.bytes > ws_bytes) return KVT_ERR_OOM;
+    const int64_t item_cap = (a->n + ITEM_TOKENS - 1) / ITEM_TOKENS + max_leaves;
+    int rc;
+    rc = kvt_chunk_bounds(a->q, a->q_dtype, a->n_lanes, a->d, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride,
+                          a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L, max_leaves, stream);
+    if (rc) return rc;
+    rc = kvt_select_plan(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L, max_leaves,
+                         a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals, stream);
+    if (rc) return rc;
+    int blocks = a->score_blocks;
+    if (blocks <= 0) {
+        const int64_t target = (int64_t)num_sms() * 8;  // 8 CTAs of 256 threads per SM
+        const int64_t per_lane = (target + a->n_lanes - 1) / a->n_lanes;
+        const int64_t need = (item_cap + 7) / 8;
+        blocks = (int)kvt::imax(1, kvt::imin(per_lane, need));
+    }
+    rc = kvt_cand_score(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items, item_cap,
+                        w.n_items, w.cand_score, w.cand_tok, a->n, blocks, stream);
+    if (rc) return rc;
+    rc = kvt_topk_select(w.cand_score, w.cand_tok, w.n_cand, a->n, a->n_lanes, a->k, a->sel_tok, a->sel_score, a->k,
+                         a->n_sel, stream);
+    if (rc) return rc;
+    if (a->run_start) {
+        rc = kvt_runs_scan(a->sel_tok, a->n_sel, a->k, a->n_lanes, a->n, a->run_start, a->run_len, a->k, a->n_runs,
+                           nullptr, nullptr, 0, nullptr, stream);
+        if (rc) return rc;
+    }
+    if (a->out && a->values) {
+        int splits = a->attn_splits;
+        if (splits <= 0) {
+            const int64_t target = (int64_t)num_sms() * 6;
+            const int64_t per_lane = (target + a->n_lanes - 1) / a->n_lanes;
+            const int64_t need = (a->k + 255) / 256;
+            splits = (int)kvt::imax(1, kvt::imin(kvt::imin(per_lane, need), MAX_SPLITS));
+        }
+        if (splits > MAX_SPLITS) splits = MAX_SPLITS;
+        rc = kvt_sparse_decode_attn(a->values, a->v_dtype, a->n_lanes, a->lane_stride, a->d, a->sel_tok, a->sel_score,
+                                    a->n_sel, a->k, splits, w.attn_part, a->out, nullptr, stream);
+        if (rc) return rc;
+    }
+    return KVT_OK;
+}

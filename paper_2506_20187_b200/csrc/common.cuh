@@ -1,0 +1,206 @@
+// common.cuh -- shared device helpers for the kvtier B200 kernels (sm_100a).
+//
+// Canonical float64 dot product (the score definition shared with oracle/kvt_oracle.c,
+// implemented independently there):
+//   dim j is accumulated by warp lane (j >> 2) & 31 with an IEEE fma chain in increasing j,
+//   then the 32 lane partials are combined by the fixed tree over lane bits 4,3,2,1,0
+//   (xor-butterfly: pairs (l, l^16), then (l, l^8), ...).  fp32/bf16/fp16 inputs are exact
+//   in f64, so products are exact and the result is bit-reproducible on the host.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kvtier_b200.h"
+
+#define KVT_FULL 0xffffffffu
+
+namespace kvt {
+
+template <typename A, typename B>
+__host__ __device__ __forceinline__ int64_t imin(A a, B b) { return (int64_t)a < (int64_t)b ? (int64_t)a : (int64_t)b; }
+template <typename A, typename B>
+__host__ __device__ __forceinline__ int64_t imax(A a, B b) { return (int64_t)a > (int64_t)b ? (int64_t)a : (int64_t)b; }
+
+// ------------------------------------------------------------------------------------------
+// element loads (4 consecutive elements, widened)
+// ------------------------------------------------------------------------------------------
+
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+    static constexpr int code = KVT_F32;
+    __device__ __forceinline__ static void load4(const float* p, double v[4]) {
+        float4 x = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    __device__ __forceinline__ static void load4f(const float* p, float v[4]) {
+        float4 x = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    __device__ __forceinline__ static double ld1(const float* p) { return (double)__ldg(p); }
+    __device__ __forceinline__ static float ld1f(const float* p) { return __ldg(p); }
+};
+template <> struct Elem<double> {
+    static constexpr int code = KVT_F64;
+    __device__ __forceinline__ static void load4(const double* p, double v[4]) {
+        double2 a = __ldg(reinterpret_cast<const double2*>(p));
+        double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+    __device__ __forceinline__ static void load4f(const double* p, double v[4]) { load4(p, v); }
+    __device__ __forceinline__ static double ld1(const double* p) { return __ldg(p); }
+    __device__ __forceinline__ static double ld1f(const double* p) { return __ldg(p); }
+};
+template <> struct Elem<__nv_bfloat16> {
+    static constexpr int code = KVT_BF16;
+    __device__ __forceinline__ static void unpack(uint2 u, float f[4]) {
+        f[0] = __uint_as_float(u.x << 16);
+        f[1] = __uint_as_float(u.x & 0xffff0000u);
+        f[2] = __uint_as_float(u.y << 16);
+        f[3] = __uint_as_float(u.y & 0xffff0000u);
+    }
+    __device__ __forceinline__ static void load4(const __nv_bfloat16* p, double v[4]) {
+        uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+        float f[4];
+        unpack(u, f);
+        v[0] = f[0]; v[1] = f[1]; v[2] = f[2]; v[3] = f[3];
+    }
+    __device__ __forceinline__ static void load4f(const __nv_bfloat16* p, float v[4]) {
+        uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+        unpack(u, v);
+    }
+    __device__ __forceinline__ static double ld1(const __nv_bfloat16* p) { return (double)__bfloat162float(p[0]); }
+    __device__ __forceinline__ static float ld1f(const __nv_bfloat16* p) { return __bfloat162float(p[0]); }
+};
+template <> struct Elem<__half> {
+    static constexpr int code = KVT_F16;
+    __device__ __forceinline__ static void load4(const __half* p, double v[4]) {
+        uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+        __half2 a = *reinterpret_cast<__half2*>(&u.x), b = *reinterpret_cast<__half2*>(&u.y);
+        float2 fa = __half22float2(a), fb = __half22float2(b);
+        v[0] = fa.x; v[1] = fa.y; v[2] = fb.x; v[3] = fb.y;
+    }
+    __device__ __forceinline__ static void load4f(const __half* p, float v[4]) {
+        uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+        __half2 a = *reinterpret_cast<__half2*>(&u.x), b = *reinterpret_cast<__half2*>(&u.y);
+        float2 fa = __half22float2(a), fb = __half22float2(b);
+        v[0] = fa.x; v[1] = fa.y; v[2] = fb.x; v[3] = fb.y;
+    }
+    __device__ __forceinline__ static double ld1(const __half* p) { return (double)__half2float(p[0]); }
+    __device__ __forceinline__ static float ld1f(const __half* p) { return __half2float(p[0]); }
+};
+
+// Load the (up to) 4 dims of group g of row `row` (d dims).  VEC: d % 4 == 0 and aligned.
+template <typename T, bool VEC>
+__device__ __forceinline__ void load_group(const T* row, int g, int d, double v[4]) {
+    int j0 = 4 * g;
+    if (VEC) {
+        Elem<T>::load4(row + j0, v);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = (j0 + i < d) ? Elem<T>::ld1(row + j0 + i) : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// canonical reductions
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ double tree_allreduce(double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(KVT_FULL, v, off);
+    return v;
+}
+
+// Reduce-scatter of 8 per-lane partials (tokens 0..7) with the canonical tree; on return
+// lane L holds the full dot of token (L >> 2) & 7 (same value on the 4 lanes of a quad).
+__device__ __forceinline__ double tree_8tok(double p[8], int lane) {
+    {
+        const bool b = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double send = b ? p[i] : p[4 + i];
+            double keep = b ? p[4 + i] : p[i];
+            p[i] = keep + __shfl_xor_sync(KVT_FULL, send, 16);
+        }
+    }
+    {
+        const bool b = lane & 8;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            double send = b ? p[i] : p[2 + i];
+            double keep = b ? p[2 + i] : p[i];
+            p[i] = keep + __shfl_xor_sync(KVT_FULL, send, 8);
+        }
+    }
+    {
+        const bool b = lane & 4;
+        double send = b ? p[0] : p[1];
+        double keep = b ? p[1] : p[0];
+        p[0] = keep + __shfl_xor_sync(KVT_FULL, send, 4);
+    }
+    double v = p[0];
+    v = v + __shfl_xor_sync(KVT_FULL, v, 2);
+    v = v + __shfl_xor_sync(KVT_FULL, v, 1);
+    return v;
+}
+
+// Chain length (<= 4*ceil(d/128)) + tree depth; the soundness widening factor.
+__host__ __device__ __forceinline__ int chain_len(int d) { return 4 * ((d + 127) / 128) + 5; }
+__host__ __device__ __forceinline__ double slack_factor(int d) {
+    return (double)(2 * chain_len(d) + 4) * 0x1p-53;
+}
+
+// Orderable 64-bit key of a finite double (larger score -> larger key); -0 == +0.
+__device__ __forceinline__ uint64_t ord_key(double s) {
+    if (s == 0.0) s = 0.0;
+    uint64_t b = (uint64_t)__double_as_longlong(s);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_to_double(uint64_t k) {
+    uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+// ------------------------------------------------------------------------------------------
+// block-level scans (blockDim.x multiple of 32, <= 1024)
+// ------------------------------------------------------------------------------------------
+
+template <typename V>
+__device__ __forceinline__ V warp_incl_scan(V v, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        V t = __shfl_up_sync(KVT_FULL, v, off);
+        if (lane >= off) v += t;
+    }
+    return v;
+}
+
+// Exclusive scan across the block; returns this thread's exclusive prefix and the total.
+// `sh` must hold >= 33 V.  Contains __syncthreads().
+template <typename V>
+__device__ __forceinline__ V block_excl_scan(V v, V* sh, V& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    V inc = warp_incl_scan(v, lane);
+    if (lane == 31) sh[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        V w = lane < nw ? sh[lane] : V(0);
+        V wi = warp_incl_scan(w, lane);
+        if (lane < nw) sh[lane] = wi - w;
+        if (lane == 31) sh[32] = wi;
+    }
+    __syncthreads();
+    V res = sh[warp] + inc - v;
+    total = sh[32];
+    __syncthreads();
+    return res;
+}
+
+}  // namespace kvt
+
+// status plumbing (api.cu)
+int kvt_set_cuda_error(cudaError_t e);
+int kvt_check_launch();

@@ -1,0 +1,154 @@
+// plan.cu -- lower-bound threshold tau and candidate work items (pruning half of
+// chunk_tree.py:233-338 select_top_k).
+//
+// tau = max{x : sum of rows over leaves with L >= x is >= k}: at least k tokens score
+// >= tau, so the k-th best score is >= tau and any leaf with U < tau holds no top-k token
+// (strictly below, ties included).  Found with an 8-pass weighted radix select over the
+// orderable 64-bit keys of L (one CTA per lane; histogram weights are row counts).
+// Candidate leaves (U >= tau) are emitted in ascending token order as work items of
+// <= 64 tokens: (tok_start, count, out_pos), out_pos = exclusive prefix of candidate rows.
+#include "common.cuh"
+
+namespace kvt {
+
+constexpr int PLAN_THREADS = 512;
+constexpr int ITEM_TOKENS = 64;
+
+__device__ __forceinline__ int64_t leaf_rows(const int32_t* ls, int64_t nl, int64_t c, int64_t n, int C) {
+    if (ls) {
+        const int64_t e = (c + 1 < nl) ? (int64_t)ls[c + 1] : n;
+        return e - ls[c];
+    }
+    return min((int64_t)C, n - c * C);
+}
+__device__ __forceinline__ int64_t leaf_begin(const int32_t* ls, int64_t c, int C) {
+    return ls ? (int64_t)ls[c] : c * C;
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
+    int64_t n, int C, const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ n_leaves,
+    int64_t leaf_stride, const double* __restrict__ U, const double* __restrict__ L, int64_t bnd_stride,
+    int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
+    int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals) {
+    __shared__ unsigned long long hist[256];
+    __shared__ long long scan_sh[33];
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ long long s_remaining;
+    __shared__ int s_done;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t li = blockIdx.x;
+    const int32_t* ls = leaf_start ? leaf_start + li * leaf_stride : nullptr;
+    const int64_t nl = leaf_start ? (int64_t)n_leaves[li] : (n + C - 1) / C;
+    const double* Ul = U + li * bnd_stride;
+    const double* Ll = L + li * bnd_stride;
+
+    if (tid == 0) { s_prefix = 0; s_mask = 0; s_remaining = k; s_done = (k <= 0); }
+    __syncthreads();
+
+    // ---- weighted radix select: largest key T with W(key >= T) >= k ----
+    for (int shift = 56; shift >= 0 && !s_done; shift -= 8) {
+        for (int i = tid; i < 256; i += PLAN_THREADS) hist[i] = 0;
+        __syncthreads();
+        const unsigned long long prefix = s_prefix, mask = s_mask;
+        for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
+            const int64_t c = base + tid;
+            int digit = 256;
+            unsigned long long w = 0;
+            if (c < nl) {
+                const uint64_t key = ord_key(Ll[c]);
+                if ((key & mask) == prefix) {
+                    digit = (int)((key >> shift) & 0xff);
+                    w = (unsigned long long)leaf_rows(ls, nl, c, n, C);
+                }
+            }
+            const unsigned peers = __match_any_sync(KVT_FULL, digit);
+            unsigned long long sum = 0;
+#pragma unroll 4
+            for (int src = 0; src < 32; ++src) {
+                const unsigned long long ws = __shfl_sync(KVT_FULL, w, src);
+                if (peers & (1u << src)) sum += ws;
+            }
+            if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], sum);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // lane covers bins 255-8*lane .. 248-8*lane (descending)
+            unsigned long long loc = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) loc += hist[255 - 8 * lane - i];
+            unsigned long long inc = warp_incl_scan(loc, lane);
+            const unsigned long long exc = inc - loc;
+            const unsigned long long rem = (unsigned long long)s_remaining;
+            const bool mine = exc < rem && rem <= inc;
+            if (mine) {
+                unsigned long long run = exc;
+                for (int i = 0; i < 8; ++i) {
+                    const int b = 255 - 8 * lane - i;
+                    if (run + hist[b] >= rem) {
+                        s_prefix = prefix | ((unsigned long long)b << shift);
+                        s_mask = mask | (0xffull << shift);
+                        s_remaining = (long long)(rem - run);
+                        break;
+                    }
+                    run += hist[b];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const double tau = (k <= 0) ? INFINITY : key_to_double(s_prefix);
+
+    // ---- candidate compaction -> items ----
+    long long carry_items = 0, carry_tok = 0;
+    for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
+        const int64_t c = base + tid;
+        long long it = 0, tk = 0;
+        int64_t rows = 0;
+        bool cand = false;
+        if (c < nl) {
+            rows = leaf_rows(ls, nl, c, n, C);
+            cand = Ul[c] >= tau;
+            if (cand) { tk = rows; it = (rows + ITEM_TOKENS - 1) / ITEM_TOKENS; }
+            if (cand_leaf) cand_leaf[li * leaf_stride + c] = cand ? 1 : 0;
+        }
+        long long tot_it, tot_tk;
+        const long long ex_it = block_excl_scan<long long>(it, scan_sh, tot_it);
+        const long long ex_tk = block_excl_scan<long long>(tk, scan_sh, tot_tk);
+        if (cand) {
+            const int64_t s = leaf_begin(ls, c, C);
+            int32_t* out = items + li * item_stride * 3;
+            for (long long j = 0; j < it; ++j) {
+                const int64_t pos = carry_items + ex_it + j;
+                out[pos * 3 + 0] = (int32_t)(s + j * ITEM_TOKENS);
+                out[pos * 3 + 1] = (int32_t)kvt::imin(ITEM_TOKENS, rows - j * ITEM_TOKENS);
+                out[pos * 3 + 2] = (int32_t)(carry_tok + ex_tk + j * ITEM_TOKENS);
+            }
+        }
+        carry_items += tot_it;
+        carry_tok += tot_tk;
+    }
+    if (tid == 0) {
+        n_items[li] = (int32_t)carry_items;
+        n_cand[li] = (int32_t)carry_tok;
+        if (evals) evals[li] = (int64_t)nl + carry_tok;
+    }
+}
+
+}  // namespace kvt
+
+using namespace kvt;
+
+extern "C" int kvt_select_plan(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start, const int32_t* n_leaves,
+                               int64_t leaf_stride, const double* U, const double* L, int64_t bnd_stride, int64_t k,
+                               int32_t* items, int64_t item_stride, int32_t* n_items, int32_t* n_cand,
+                               int8_t* cand_leaf, int64_t* evals, void* stream) {
+    if (!U || !L || !items || !n_items || !n_cand || n_lanes < 0 || n < 0) return KVT_ERR_ARG;
+    if (!leaf_start && C < 1) return KVT_ERR_ARG;
+    if (k < 0 || k > n) return KVT_ERR_K;
+    if (n_lanes == 0) return KVT_OK;
+    if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
+    plan_kernel<<<(unsigned)n_lanes, PLAN_THREADS, 0, (cudaStream_t)stream>>>(
+        n, C, leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand,
+        cand_leaf, evals);
+    return kvt_check_launch();
+}

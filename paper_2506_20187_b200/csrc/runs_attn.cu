@@ -1,0 +1,304 @@
+// runs_attn.cu -- K6 runs scan / canonical partition and K7 sparse decode attention.
+//
+// K6: engine.py:176-183 _token_runs turns the (sorted) selected tokens into contiguous
+// runs; the leaf shape that select_top_k + merge_desert leave behind (chunk_tree.py:
+// 331-379) is those runs plus their complement (maximal desert runs).  One CTA per lane:
+// flag run heads, block-scan run ids, emit (start, len) and the interleaved partition.
+//
+// K7: engine.py:145-154 attention_output = softmax(q.K_sel^T/sqrt d) @ V_sel.  The logits
+// are the canonical f64 scores K5 already produced, so K is not re-read; only V rows of
+// the selected tokens are gathered (ascending token order => runs are contiguous rows and
+// each 128-dim bf16 row is one coalesced 256 B warp load).  Flash-decoding split: each CTA
+// reduces a slice of the selected set to (m, l, o[d]) with f32 accumulation (f64 for f64
+// values), a merge kernel rescales and combines the slices.  HBM-bound on k*d*s_V.
+#include "common.cuh"
+
+namespace kvt {
+
+constexpr int RUNS_THREADS = 512;
+
+__global__ void __launch_bounds__(RUNS_THREADS) runs_kernel(
+    const int32_t* __restrict__ sel_tok, const int32_t* __restrict__ n_sel, int64_t sel_stride, int64_t n,
+    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs,
+    int32_t* __restrict__ part_start, int8_t* __restrict__ part_state, int64_t part_stride,
+    int32_t* __restrict__ n_part) {
+    __shared__ long long scan_sh[33];
+    const int tid = threadIdx.x;
+    const int64_t li = blockIdx.x;
+    const int64_t k = n_sel[li];
+    const int32_t* tok = sel_tok + li * sel_stride;
+    int32_t* rs = run_start + li * run_stride;
+    int32_t* rl = run_len + li * run_stride;
+    // pass 1: run heads -> run ids; store first position of each run in rl
+    long long carry = 0;
+    for (int64_t base = 0; base < k; base += RUNS_THREADS) {
+        const int64_t i = base + tid;
+        long long head = 0;
+        if (i < k) head = (i == 0 || tok[i] != tok[i - 1] + 1) ? 1 : 0;
+        long long tot;
+        const long long ex = block_excl_scan<long long>(head, scan_sh, tot);
+        if (head) {
+            rs[carry + ex] = tok[i];
+            rl[carry + ex] = (int32_t)i;
+        }
+        carry += tot;
+    }
+    const int64_t R = carry;
+    __syncthreads();
+    // pass 2: lengths from consecutive first positions (read r and r+1 before writing)
+    for (int64_t base = 0; base < R; base += RUNS_THREADS) {
+        const int64_t r = base + tid;
+        int32_t f0 = 0, f1 = 0;
+        if (r < R) { f0 = rl[r]; f1 = (r + 1 < R) ? rl[r + 1] : (int32_t)k; }
+        __syncthreads();
+        if (r < R) rl[r] = f1 - f0;
+        __syncthreads();
+    }
+    if (tid == 0) n_runs[li] = (int32_t)R;
+    if (!part_start) return;
+    // pass 3: canonical partition = [gap0] run0 [gap1] run1 ... [gap_last]
+    int32_t* ps = part_start + li * part_stride;
+    int8_t* pst = part_state + li * part_stride;
+    const long long pre = (R == 0) ? (n > 0 ? 1 : 0) : (rs[0] > 0 ? 1 : 0);
+    if (tid == 0 && pre) { ps[0] = 0; pst[0] = 2; }
+    long long carry2 = pre;
+    for (int64_t base = 0; base < R; base += RUNS_THREADS) {
+        const int64_t r = base + tid;
+        long long cntl = 0;
+        int32_t s = 0, e = 0, nxt = 0;
+        if (r < R) {
+            s = rs[r]; e = s + rl[r];
+            nxt = (r + 1 < R) ? rs[r + 1] : (int32_t)n;
+            cntl = 1 + (e < nxt ? 1 : 0);
+        }
+        long long tot;
+        const long long ex = block_excl_scan<long long>(cntl, scan_sh, tot);
+        if (r < R) {
+            const int64_t p = carry2 + ex;
+            ps[p] = s; pst[p] = 1;
+            if (e < nxt) { ps[p + 1] = e; pst[p + 1] = 2; }
+        }
+        carry2 += tot;
+    }
+    if (tid == 0) n_part[li] = (int32_t)carry2;
+}
+
+// ------------------------------------------------------------------------------------------
+// K7
+// ------------------------------------------------------------------------------------------
+
+constexpr int ATTN_THREADS = 256;
+constexpr int ATTN_WARPS = ATTN_THREADS / 32;
+
+template <typename T> struct AccOf { using type = float; };
+template <> struct AccOf<double> { using type = double; };
+
+template <typename T, bool VEC>
+__device__ __forceinline__ void load_group_acc(const T* row, int g, int d, typename AccOf<T>::type v[4]) {
+    const int j0 = 4 * g;
+    if (VEC) {
+        Elem<T>::load4f(row + j0, v);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = (j0 + i < d) ? Elem<T>::ld1f(row + j0 + i) : 0;
+    }
+}
+
+// partial record per (lane, split): m (f64), l, o[d] (Acc); stored as doubles for simplicity
+template <typename T, int G, bool VEC>
+__global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
+    const T* __restrict__ values, int64_t lane_stride, int d, const int32_t* __restrict__ sel_tok,
+    const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits,
+    double* __restrict__ part) {
+    using Acc = typename AccOf<T>::type;
+    __shared__ double red_m[ATTN_WARPS];
+    __shared__ Acc red_o[ATTN_WARPS][4 * 32 * G];
+    __shared__ Acc red_l[ATTN_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t li = blockIdx.y;
+    const int s = blockIdx.x;
+    const int64_t k = n_sel[li];
+    const int64_t per = (k + splits - 1) / splits;
+    const int64_t a = kvt::imin(k, s * per), b = kvt::imin(k, a + per);
+    const int32_t* tok = sel_tok + li * sel_stride;
+    const double* sc = sel_score + li * sel_stride;
+    const T* base = values + li * lane_stride;
+    // slice max
+    double m = -INFINITY;
+    for (int64_t i = a + threadIdx.x; i < b; i += ATTN_THREADS) m = fmax(m, sc[i]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(KVT_FULL, m, off));
+    if (lane == 0) red_m[warp] = m;
+    __syncthreads();
+    m = red_m[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_WARPS; ++w) m = fmax(m, red_m[w]);
+
+    Acc o[G][4];
+#pragma unroll
+    for (int r = 0; r < G; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[r][i] = 0;
+    Acc l = 0;
+    constexpr int U = 4;
+    int64_t i = a + warp;
+    for (; i + (U - 1) * ATTN_WARPS < b; i += U * ATTN_WARPS) {
+        Acc v[U][G][4];
+        Acc w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ii = i + u * ATTN_WARPS;
+            const T* row = base + (int64_t)tok[ii] * d;
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                const int g = lane + 32 * r;
+                if (4 * g < d) load_group_acc<T, VEC>(row, g, d, v[u][r]);
+                else { v[u][r][0] = v[u][r][1] = v[u][r][2] = v[u][r][3] = 0; }
+            }
+            w[u] = (Acc)exp(sc[ii] - m);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            l += w[u];
+#pragma unroll
+            for (int r = 0; r < G; ++r)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[r][q] = fma(w[u], v[u][r][q], o[r][q]);
+        }
+    }
+    for (; i < b; i += ATTN_WARPS) {
+        const T* row = base + (int64_t)tok[i] * d;
+        const Acc w = (Acc)exp(sc[i] - m);
+        l += w;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const int g = lane + 32 * r;
+            if (4 * g < d) {
+                Acc v[4];
+                load_group_acc<T, VEC>(row, g, d, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[r][q] = fma(w, v[q], o[r][q]);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < G; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red_o[warp][4 * (lane + 32 * r) + q] = o[r][q];
+    if (lane == 0) red_l[warp] = l;
+    __syncthreads();
+    double* P = part + ((int64_t)li * splits + s) * (d + 2);
+    for (int j = threadIdx.x; j < d; j += ATTN_THREADS) {
+        Acc acc = 0;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) acc += red_o[w][j];
+        P[2 + j] = (double)acc;
+    }
+    if (threadIdx.x == 0) {
+        Acc ls = 0;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) ls += red_l[w];
+        P[0] = m;
+        P[1] = (double)ls;
+    }
+}
+
+__global__ void attn_merge_kernel(const double* __restrict__ part, int splits, int d, float* __restrict__ out,
+                                  double* __restrict__ out64) {
+    const int64_t li = blockIdx.x;
+    const double* P = part + (int64_t)li * splits * (d + 2);
+    double M = -INFINITY;
+    for (int s = 0; s < splits; ++s)
+        if (P[s * (d + 2) + 1] > 0) M = fmax(M, P[s * (d + 2)]);
+    double denom = 0.0;
+    for (int s = 0; s < splits; ++s) {
+        const double ls = P[s * (d + 2) + 1];
+        if (ls > 0) denom += exp(P[s * (d + 2)] - M) * ls;
+    }
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < splits; ++s) {
+            const double ls = P[s * (d + 2) + 1];
+            if (ls > 0) acc += exp(P[s * (d + 2)] - M) * P[s * (d + 2) + 2 + j];
+        }
+        const double r = denom > 0 ? acc / denom : 0.0;
+        if (out) out[li * d + j] = (float)r;
+        if (out64) out64[li * d + j] = r;
+    }
+}
+
+}  // namespace kvt
+
+using namespace kvt;
+
+extern "C" int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t sel_stride, int64_t n_lanes,
+                             int64_t n, int32_t* run_start, int32_t* run_len, int64_t run_stride, int32_t* n_runs,
+                             int32_t* part_start, int8_t* part_state, int64_t part_stride, int32_t* n_part,
+                             void* stream) {
+    if (!sel_tok || !n_sel || !run_start || !run_len || !n_runs || n_lanes < 0) return KVT_ERR_ARG;
+    if (part_start && (!part_state || !n_part)) return KVT_ERR_ARG;
+    if (n_lanes == 0) return KVT_OK;
+    runs_kernel<<<(unsigned)n_lanes, RUNS_THREADS, 0, (cudaStream_t)stream>>>(
+        sel_tok, n_sel, sel_stride, n, run_start, run_len, run_stride, n_runs, part_start, part_state, part_stride,
+        n_part);
+    return kvt_check_launch();
+}
+
+extern "C" size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits) {
+    return (size_t)n_lanes * (size_t)(splits < 1 ? 1 : splits) * (size_t)(d + 2) * sizeof(double);
+}
+
+static inline int agroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <= 512 ? 4 : 0; }
+
+template <typename T, int G, bool VEC>
+static void launch_attn(const void* values, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* sel_tok,
+                        const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, double* part,
+                        cudaStream_t st) {
+    dim3 grid(splits, (unsigned)n_lanes);
+    attn_split_kernel<T, G, VEC><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score,
+                                                                n_sel, sel_stride, splits, part);
+}
+
+template <typename T>
+static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* sel_tok,
+                         const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, double* part,
+                         cudaStream_t st) {
+    const bool vec = ((uintptr_t)values % (4 * sizeof(T)) == 0) && d % 4 == 0 && lane_stride % 4 == 0;
+    switch (agroups_for(d)) {
+#define KVT_CASE(GG)                                                                                                   \
+    case GG:                                                                                                           \
+        if (vec) launch_attn<T, GG, true>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride,     \
+                                          splits, part, st);                                                           \
+        else launch_attn<T, GG, false>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, \
+                                       part, st);                                                                      \
+        break;
+        KVT_CASE(1) KVT_CASE(2) KVT_CASE(4)
+#undef KVT_CASE
+        default: return KVT_ERR_SHAPE;
+    }
+    return kvt_check_launch();
+}
+
+extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride, int d,
+                                      const int32_t* sel_tok, const double* sel_score, const int32_t* n_sel,
+                                      int64_t sel_stride, int splits, void* ws, float* out, double* out64,
+                                      void* stream) {
+    if (!values || !sel_tok || !sel_score || !n_sel || !ws || (!out && !out64) || d < 1 || n_lanes < 0)
+        return KVT_ERR_ARG;
+    if (n_lanes == 0) return KVT_OK;
+    if (n_lanes > 65535) return KVT_ERR_ARG;
+    if (splits < 1) splits = 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    double* part = (double*)ws;
+    int rc;
+    switch (v_dtype) {
+        case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
+        case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
+        case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
+        case KVT_F16: rc = dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
+        default: return KVT_ERR_DTYPE;
+    }
+    if (rc != KVT_OK) return rc;
+    attn_merge_kernel<<<(unsigned)n_lanes, 128, 0, st>>>(part, splits, d, out, out64);
+    return kvt_check_launch();
+}

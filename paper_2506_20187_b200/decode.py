@@ -1,0 +1,134 @@
+"""Batched decode-step API: a resident KV cache with per-layer chunk abstracts and the
+fused per-layer select + sparse-attend pipeline (the body of engine.run's lane loop,
+engine.py:307-357, for every (batch row, head) lane of a layer at once).
+
+Layout in HBM:
+  K, V       [L][B*H][N_cap][d]   key/value rows, lanes contiguous (bf16 by default)
+  amax/amin  per layer [B*H][ceil(N_cap/C_l)][d] f32 chunk abstracts (importance.py:56-87)
+  C_l        ChunkPlanConfig: early layers use early_chunk_size, the rest default_chunk_size
+             (chunk_tree.py:111-123, steady state after the early steps)
+  k_l        ceil(rate_l * n), rate 0.5 for layers < early_layers else 0.1 (engine.py:83-86,312)
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import ops
+from .chunk_tree import ChunkPlanConfig
+
+
+class SparseDecoder:
+    def __init__(self, n_layers: int, batch: int, n_heads: int, head_dim: int, n_cap: int,
+                 dtype: torch.dtype = torch.bfloat16, plan: ChunkPlanConfig | None = None,
+                 importance_rate: float = 0.10, early_layer_rate: float = 0.50, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("SparseDecoder needs a CUDA device (B200, sm_100a)")
+        self.L, self.B, self.H, self.d = n_layers, batch, n_heads, head_dim
+        self.lanes = batch * n_heads
+        self.n_cap = n_cap
+        self.dtype = dtype
+        self.plan = plan or ChunkPlanConfig()
+        self.rates = [early_layer_rate if l < self.plan.early_layers else importance_rate for l in range(n_layers)]
+        self.C = [self.plan.early_chunk_size if l < self.plan.early_layers else self.plan.default_chunk_size
+                  for l in range(n_layers)]
+        self.device = torch.device(device or "cuda")
+        self.K = torch.empty((n_layers, self.lanes, n_cap, head_dim), dtype=dtype, device=self.device)
+        self.V = torch.empty_like(self.K)
+        adt = ops.abs_dtype_for(dtype)
+        self.amax = [torch.empty((self.lanes, ops.n_grid_leaves(n_cap, C), head_dim), dtype=adt, device=self.device)
+                     for C in self.C]
+        self.amin = [torch.empty_like(a) for a in self.amax]
+        self.n = 0
+        self._ws = None
+        self._bufs = None
+
+    # -- cache maintenance ------------------------------------------------------------------------
+
+    def set_length(self, n: int) -> None:
+        """Declare K/V[:, :, :n] filled (prefill) and (re)build every chunk abstract (K1)."""
+        if n > self.n_cap:
+            raise ValueError("n exceeds cache capacity")
+        self.n = n
+        for l in range(self.L):
+            ops.abstract_build(self.K[l], n, self.C[l], self.amax[l], self.amin[l])
+        self._bufs = None
+
+    def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
+        """Append one token per lane ([L, lanes, d]) and refresh the tail chunk abstracts."""
+        if self.n >= self.n_cap:
+            raise ValueError("cache full")
+        self.K[:, :, self.n] = k_new.to(self.dtype)
+        self.V[:, :, self.n] = v_new.to(self.dtype)
+        self.n += 1
+        for l in range(self.L):
+            c = (self.n - 1) // self.C[l]
+            ops.abstract_build(self.K[l], self.n, self.C[l], self.amax[l], self.amin[l], c, c + 1)
+        self._bufs = None
+
+    def k_for(self, layer: int) -> int:
+        return math.ceil(self.rates[layer] * self.n)
+
+    # -- the hot path -------------------------------------------------------------------------------
+
+    def _buffers(self):
+        if self._bufs is not None:
+            return self._bufs
+        dev, lanes, d = self.device, self.lanes, self.d
+        bufs = []
+        for l in range(self.L):
+            k = self.k_for(l)
+            bufs.append({
+                "sel_tok": torch.empty((lanes, max(k, 1)), dtype=torch.int32, device=dev),
+                "sel_score": torch.empty((lanes, max(k, 1)), dtype=torch.float64, device=dev),
+                "n_sel": torch.empty(lanes, dtype=torch.int32, device=dev),
+                "run_start": torch.empty((lanes, max(k, 1)), dtype=torch.int32, device=dev),
+                "run_len": torch.empty((lanes, max(k, 1)), dtype=torch.int32, device=dev),
+                "n_runs": torch.empty(lanes, dtype=torch.int32, device=dev),
+                "out": torch.empty((lanes, d), dtype=torch.float32, device=dev),
+                "evals": torch.empty(lanes, dtype=torch.int64, device=dev),
+            })
+        maxl = max(ops.n_grid_leaves(self.n_cap, C) for C in self.C)
+        if self._ws is None or self._ws.key != (lanes, self.n_cap, maxl, d):
+            self._ws = ops.LayerWorkspace(lanes, self.n_cap, maxl, d, dev)
+        self._bufs = bufs
+        return bufs
+
+    def layer(self, l: int, q: torch.Tensor) -> dict:
+        """Select + attend for layer l; q: [lanes, d] (f32 or f64).  Returns the layer buffers."""
+        bufs = self._buffers()
+        ops.select_attend(q, self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l), self.C[l],
+                          self._ws, bufs[l])
+        return bufs[l]
+
+    def step(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """All layers for one decode step; q: [L, lanes, d] -> attention outputs [L, lanes, d] f32."""
+        if out is None:
+            out = torch.empty((self.L, self.lanes, self.d), dtype=torch.float32, device=self.device)
+        for l in range(self.L):
+            b = self.layer(l, q[l])
+            out[l].copy_(b["out"])
+        return out
+
+    # -- accounting ---------------------------------------------------------------------------------
+
+    def algorithmic_bytes(self, n_cand: list[list[int]]) -> dict:
+        """Per-kernel algorithmic HBM bytes for one step (SURVEY.md sec. 8(d) formulas).
+        n_cand[l][lane] = candidate tokens of that lane at layer l."""
+        sK = self.K.element_size()
+        sA = self.amax[0].element_size()
+        d = self.d
+        out = {"bounds": 0, "score": 0, "select": 0, "attn": 0, "plan": 0, "runs": 0}
+        for l in range(self.L):
+            m = ops.n_grid_leaves(self.n, self.C[l])
+            k = self.k_for(l)
+            nc = sum(n_cand[l])
+            out["bounds"] += self.lanes * (m * 2 * d * sA + d * 8 + m * 16)
+            out["plan"] += self.lanes * m * 16 + nc // 64 * 12
+            out["score"] += nc * (d * sK + 12)
+            out["select"] += nc * 8 + self.lanes * k * 12
+            out["runs"] += self.lanes * k * 4 * 3
+            out["attn"] += self.lanes * k * (d * sK + 4 + 8) + self.lanes * d * 4
+        return out

@@ -1,0 +1,275 @@
+"""Torch-level wrappers of the C ABI (device tensors in, device tensors out).
+
+Every function launches on torch's current CUDA stream and checks the returned
+kvt_status.  Lanes are the leading dimension: keys/values are [n_lanes, N_cap, d] with
+contiguous rows (lane stride = tensor.stride(0)), queries are [n_lanes, d].
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib as L
+
+ITEM_TOKENS = 64
+_DT = {torch.float32: L.F32, torch.float64: L.F64, torch.bfloat16: L.BF16, torch.float16: L.F16}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}") from None
+
+
+def abs_dtype_for(key_dtype: torch.dtype) -> torch.dtype:
+    """Abstract storage dtype: f64 for f64 keys, f32 otherwise (importance.py:75-77 wire f32)."""
+    return torch.float64 if key_dtype == torch.float64 else torch.float32
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else t.data_ptr()
+
+
+def _nz(t: torch.Tensor) -> torch.Tensor:
+    """Never hand a NULL pointer to the ABI for an empty (k = 0) operand."""
+    if t.numel() == 0:
+        return torch.zeros(1, dtype=t.dtype, device=t.device)
+    return t.contiguous()
+
+
+def require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise RuntimeError("paper_2506_20187_b200 runs on CUDA (sm_100a) only; got a CPU tensor")
+
+
+def _lanes(t: torch.Tensor) -> tuple[int, int]:
+    """(lane_stride, d) of a [n_lanes, N, d] tensor with contiguous rows."""
+    if t.dim() != 3 or t.stride(2) != 1 or t.stride(1) != t.shape[2]:
+        raise ValueError(f"expected [n_lanes, N, d] with contiguous rows, got shape {tuple(t.shape)} strides {t.stride()}")
+    return t.stride(0), t.shape[2]
+
+
+def n_grid_leaves(n: int, C: int) -> int:
+    return (n + C - 1) // C
+
+
+# -- K1 ----------------------------------------------------------------------------------------
+
+
+def abstract_build(keys: torch.Tensor, n: int, C: int, amax: torch.Tensor | None = None,
+                   amin: torch.Tensor | None = None, c_begin: int = 0, c_end: int | None = None):
+    """Uniform-grid chunk abstracts (importance.py:80-87) -> (amax, amin) [n_lanes, m_cap, d]."""
+    require_cuda(keys)
+    ls, d = _lanes(keys)
+    nl = keys.shape[0]
+    m = n_grid_leaves(n, C)
+    c_end = m if c_end is None else c_end
+    adt = abs_dtype_for(keys.dtype)
+    if amax is None:
+        amax = torch.empty((nl, m, d), dtype=adt, device=keys.device)
+        amin = torch.empty_like(amax)
+    if amax.dtype != adt or amin.dtype != adt or amax.stride(2) != 1:
+        raise ValueError("abstract buffers must be contiguous rows of the abstract dtype")
+    L.check(L.kvt_abstract_build(keys.data_ptr(), dtype_code(keys), nl, ls, n, d, C, c_begin, c_end,
+                                 amax.data_ptr(), amin.data_ptr(), amax.stride(0), _stream()), "abstract_build")
+    return amax, amin
+
+
+def abstract_spans(keys: torch.Tensor, lane_of: torch.Tensor, starts: torch.Tensor, ends: torch.Tensor):
+    """Exact abstracts of arbitrary spans -> (amax, amin) [S, d]."""
+    require_cuda(keys)
+    ls, d = _lanes(keys)
+    S = starts.numel()
+    adt = abs_dtype_for(keys.dtype)
+    amax = torch.empty((S, d), dtype=adt, device=keys.device)
+    amin = torch.empty_like(amax)
+    if S:
+        lane_of = lane_of.to(device=keys.device, dtype=torch.int32).contiguous()
+        starts = starts.to(device=keys.device, dtype=torch.int32).contiguous()
+        ends = ends.to(device=keys.device, dtype=torch.int32).contiguous()
+        L.check(L.kvt_abstract_spans(keys.data_ptr(), dtype_code(keys), ls, d, S, lane_of.data_ptr(),
+                                     starts.data_ptr(), ends.data_ptr(), amax.data_ptr(), amin.data_ptr(),
+                                     _stream()), "abstract_spans")
+    return amax, amin
+
+
+# -- K3 ----------------------------------------------------------------------------------------
+
+
+def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int, C: int = 0,
+                 leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None):
+    """Sound canonical (U, L) per leaf (importance.py:108-137) -> float64 [n_lanes, max_leaves]."""
+    require_cuda(q, amax, amin)
+    nl, d = q.shape
+    if leaf_start is not None:
+        lstride = leaf_start.shape[1]
+        maxl = lstride
+    else:
+        lstride = 0
+        maxl = n_grid_leaves(n, C)
+    U = torch.empty((nl, max(maxl, 1)), dtype=torch.float64, device=q.device)
+    Lo = torch.empty_like(U)
+    L.check(L.kvt_chunk_bounds(q.data_ptr(), dtype_code(q), nl, d, n, C, _p(leaf_start), _p(n_leaves), lstride,
+                               amax.data_ptr(), amin.data_ptr(), dtype_code(amax), amax.stride(0), U.data_ptr(),
+                               Lo.data_ptr(), U.stride(0), _stream()), "chunk_bounds")
+    return U, Lo
+
+
+# -- K4 ----------------------------------------------------------------------------------------
+
+
+def token_scores(q: torch.Tensor, keys: torch.Tensor, n: int | None = None) -> torch.Tensor:
+    """Canonical f64 logits of all tokens (importance.py:27-33) -> [n_lanes, n]."""
+    require_cuda(q, keys)
+    ls, d = _lanes(keys)
+    nl = keys.shape[0]
+    n = keys.shape[1] if n is None else n
+    if q.shape != (nl, d):
+        raise ValueError(f"shape mismatch: keys {tuple(keys.shape)} vs query {tuple(q.shape)}")
+    out = torch.empty((nl, max(n, 1)), dtype=torch.float64, device=q.device)
+    L.check(L.kvt_token_scores(q.data_ptr(), dtype_code(q), keys.data_ptr(), dtype_code(keys), nl, ls, n, d,
+                               out.data_ptr(), out.stride(0), _stream()), "token_scores")
+    return out[:, :n]
+
+
+def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
+                leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
+                want_cand_leaf: bool = False):
+    """tau + candidate items -> dict(items, n_items, n_cand, cand_leaf, evals)."""
+    nl = U.shape[0]
+    maxl = leaf_start.shape[1] if leaf_start is not None else n_grid_leaves(n, C)
+    item_cap = (n + ITEM_TOKENS - 1) // ITEM_TOKENS + maxl
+    dev = U.device
+    items = torch.empty((nl, item_cap, 3), dtype=torch.int32, device=dev)
+    n_items = torch.empty(nl, dtype=torch.int32, device=dev)
+    n_cand = torch.empty(nl, dtype=torch.int32, device=dev)
+    evals = torch.empty(nl, dtype=torch.int64, device=dev)
+    cand_leaf = torch.zeros((nl, max(maxl, 1)), dtype=torch.int8, device=dev) if want_cand_leaf else None
+    lstride = leaf_start.shape[1] if leaf_start is not None else maxl
+    L.check(L.kvt_select_plan(nl, n, C, _p(leaf_start), _p(n_leaves), lstride, U.data_ptr(), Lo.data_ptr(),
+                              U.stride(0), k, items.data_ptr(), item_cap, n_items.data_ptr(), n_cand.data_ptr(),
+                              _p(cand_leaf), evals.data_ptr(), _stream()), "select_plan")
+    return {"items": items, "n_items": n_items, "n_cand": n_cand, "cand_leaf": cand_leaf, "evals": evals,
+            "item_cap": item_cap}
+
+
+def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_per_lane: int = 0):
+    """Canonical logits of candidate tokens -> (cand_score f64 [n_lanes, n], cand_tok i32)."""
+    require_cuda(q, keys)
+    ls, d = _lanes(keys)
+    nl = keys.shape[0]
+    cs = torch.empty((nl, max(n, 1)), dtype=torch.float64, device=q.device)
+    ct = torch.empty((nl, max(n, 1)), dtype=torch.int32, device=q.device)
+    if blocks_per_lane <= 0:
+        blocks_per_lane = max(1, min((plan["item_cap"] + 7) // 8, (148 * 8 + nl - 1) // nl))
+    L.check(L.kvt_cand_score(q.data_ptr(), dtype_code(q), keys.data_ptr(), dtype_code(keys), nl, ls, d,
+                             plan["items"].data_ptr(), plan["item_cap"], plan["n_items"].data_ptr(), cs.data_ptr(),
+                             ct.data_ptr(), cs.stride(0), blocks_per_lane, _stream()), "cand_score")
+    return cs, ct
+
+
+def topk_select(cs: torch.Tensor, ct: torch.Tensor, n_cand: torch.Tensor, k: int):
+    """Exact top-k (score desc, token asc) -> (sel_tok i32 [n_lanes,k] ascending, sel_score f64, n_sel)."""
+    nl = cs.shape[0]
+    dev = cs.device
+    st = torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev)
+    ss = torch.empty((nl, max(k, 1)), dtype=torch.float64, device=dev)
+    ns = torch.empty(nl, dtype=torch.int32, device=dev)
+    L.check(L.kvt_topk_select(cs.data_ptr(), ct.data_ptr(), n_cand.data_ptr(), cs.stride(0), nl, k, st.data_ptr(),
+                              ss.data_ptr(), st.stride(0), ns.data_ptr(), _stream()), "topk_select")
+    return st[:, :k], ss[:, :k], ns
+
+
+def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition: bool = True):
+    """Selected runs (+ canonical partition) -> dict."""
+    nl = sel_tok.shape[0]
+    k = sel_tok.shape[1]
+    dev = sel_tok.device
+    st = _nz(sel_tok)
+    sstride = sel_tok.shape[1] if k > 0 else 1
+    rs = torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev)
+    rl = torch.empty_like(rs)
+    nr = torch.empty(nl, dtype=torch.int32, device=dev)
+    ps = pst = npart = None
+    pcap = 2 * k + 2
+    if want_partition:
+        ps = torch.empty((nl, pcap), dtype=torch.int32, device=dev)
+        pst = torch.empty((nl, pcap), dtype=torch.int8, device=dev)
+        npart = torch.empty(nl, dtype=torch.int32, device=dev)
+    L.check(L.kvt_runs_scan(st.data_ptr(), n_sel.data_ptr(), sstride, nl, n, rs.data_ptr(), rl.data_ptr(),
+                            rs.stride(0), nr.data_ptr(), _p(ps), _p(pst), pcap, _p(npart), _stream()), "runs_scan")
+    return {"run_start": rs, "run_len": rl, "n_runs": nr, "part_start": ps, "part_state": pst, "n_part": npart}
+
+
+def auto_splits(n_lanes: int, k: int) -> int:
+    target = 148 * 6
+    return max(1, min((target + n_lanes - 1) // n_lanes, (k + 255) // 256, 64))
+
+
+def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor,
+                       splits: int = 0, want_f64: bool = False):
+    """softmax(sel_score) @ V[sel] (engine.py:145-154) -> out f32 [n_lanes, d] (and f64)."""
+    require_cuda(values)
+    ls, d = _lanes(values)
+    nl = values.shape[0]
+    k = sel_tok.shape[1]
+    if splits <= 0:
+        splits = auto_splits(nl, k)
+    ws = torch.empty(max(1, L.kvt_attn_workspace_bytes(nl, d, splits)), dtype=torch.uint8, device=values.device)
+    out = torch.empty((nl, d), dtype=torch.float32, device=values.device)
+    out64 = torch.empty((nl, d), dtype=torch.float64, device=values.device) if want_f64 else None
+    st = _nz(sel_tok)
+    ss = _nz(sel_score)
+    sstride = sel_tok.shape[1] if k > 0 else 1
+    L.check(L.kvt_sparse_decode_attn(values.data_ptr(), dtype_code(values), nl, ls, d, st.data_ptr(), ss.data_ptr(),
+                                     n_sel.data_ptr(), sstride, splits, ws.data_ptr(), out.data_ptr(), _p(out64),
+                                     _stream()), "sparse_decode_attn")
+    return (out, out64) if want_f64 else out
+
+
+# -- fused per-layer pipeline ---------------------------------------------------------------------
+
+
+class LayerWorkspace:
+    """Caller-owned scratch for kvt_select_attend, sized once for (n_lanes, n_cap, leaves, d)."""
+
+    def __init__(self, n_lanes: int, n_cap: int, max_leaves: int, d: int, device):
+        self.bytes = int(L.kvt_layer_workspace_bytes(n_lanes, n_cap, max_leaves, d))
+        self.buf = torch.empty(self.bytes, dtype=torch.uint8, device=device)
+        self.key = (n_lanes, n_cap, max_leaves, d)
+
+
+def select_attend(q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor,
+                  n: int, k: int, C: int, ws: LayerWorkspace, out: dict, attn_splits: int = 0,
+                  score_blocks: int = 0) -> None:
+    """One layer, all lanes: K3 -> plan -> K4 -> K5 -> K6 -> K7 into the caller's `out` buffers
+    (sel_tok, sel_score, n_sel, run_start, run_len, n_runs, out, evals)."""
+    ls, d = _lanes(keys)
+    a = L.KvtLayerArgs()
+    a.n_lanes, a.n, a.k, a.d, a.C = keys.shape[0], n, k, d, C
+    a.key_dtype, a.v_dtype, a.q_dtype, a.abs_dtype = dtype_code(keys), dtype_code(values), dtype_code(q), dtype_code(amax)
+    a.q, a.keys, a.values, a.lane_stride = q.data_ptr(), keys.data_ptr(), values.data_ptr(), ls
+    if values.stride(0) != ls:
+        raise ValueError("keys and values must share the lane stride")
+    a.amax, a.amin, a.abs_lane_stride = amax.data_ptr(), amin.data_ptr(), amax.stride(0)
+    a.leaf_start, a.n_leaves, a.leaf_stride = None, None, 0
+    a.sel_tok, a.sel_score, a.n_sel = out["sel_tok"].data_ptr(), out["sel_score"].data_ptr(), out["n_sel"].data_ptr()
+    a.run_start = _p(out.get("run_start"))
+    a.run_len = _p(out.get("run_len"))
+    a.n_runs = _p(out.get("n_runs"))
+    a.out = _p(out.get("out"))
+    a.evals = _p(out.get("evals"))
+    a.attn_splits, a.score_blocks = attn_splits, score_blocks
+    L.check(L.kvt_select_attend(a, ws.buf.data_ptr(), ws.bytes, _stream()), "select_attend")
+
+
+def sqrt_d(d: int) -> float:
+    return math.sqrt(d)

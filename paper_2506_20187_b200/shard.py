@@ -1,0 +1,70 @@
+"""Multi-GPU partitioning of the hot path.
+
+* batch x head sharding: lanes (b, h) are independent trees, so each
+  rank owns a disjoint, contiguous block of lanes and needs NO collective on the data path.
+* sequence sharding (config 5): each rank owns a contiguous token range of every lane and
+  produces a partial softmax state (m, l, o[d]) over its slice of the selected set; the
+  states are merged exactly with a log-sum-exp combine after an all-gather.  This is the
+  only collective in the design, and it moves (d + 2) floats per lane per rank.
+
+Everything here is device-agnostic torch so the same code runs under NCCL on the GPUs and
+under gloo in the CPU tests (tests/test_dist_gloo.py).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def lane_block(n_lanes: int, world: int, rank: int) -> tuple[int, int]:
+    """[start, end) of the lanes owned by `rank` (balanced contiguous blocks)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(n_lanes, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def batch_block(batch: int, world: int, rank: int) -> tuple[int, int]:
+    """Batch rows owned by `rank`; a row keeps all its heads together (no TP)."""
+    return lane_block(batch, world, rank)
+
+
+def token_block(n: int, world: int, rank: int, align: int = 64) -> tuple[int, int]:
+    """Contiguous token range of `rank` for sequence sharding, aligned to chunk boundaries."""
+    chunks = (n + align - 1) // align
+    a, b = lane_block(chunks, world, rank)
+    return min(n, a * align), min(n, b * align)
+
+
+def lse_merge(m: torch.Tensor, l: torch.Tensor, o: torch.Tensor) -> torch.Tensor:
+    """Combine partial softmax states.  m, l: [P, lanes]; o: [P, lanes, d] holding
+    sum_i exp(s_i - m_p) v_i.  Returns softmax-weighted outputs [lanes, d]; parts with
+    l == 0 (no selected token) are ignored."""
+    valid = l > 0
+    mm = torch.where(valid, m, torch.full_like(m, -torch.inf))
+    M = mm.max(dim=0).values
+    w = torch.where(valid, torch.exp(mm - M[None]), torch.zeros_like(m))
+    den = (w * l).sum(dim=0)
+    num = (w[..., None] * o).sum(dim=0)
+    return num / den.clamp_min(torch.finfo(num.dtype).tiny)[..., None]
+
+
+def allgather_lse_merge(m: torch.Tensor, l: torch.Tensor, o: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather every rank's (m, l, o) for its token shard and merge (NCCL on GPUs)."""
+    world = dist.get_world_size(group)
+    packed = torch.cat([m[..., None], l[..., None], o], dim=-1).contiguous()  # [lanes, d+2]
+    parts = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(parts, packed, group=group)
+    out = torch.stack(parts)
+    return lse_merge(out[..., 0], out[..., 1], out[..., 2:])
+
+
+def max_over_ranks(x: float, device=None, group=None) -> float:
+    """Max of a per-rank scalar (multi-GPU timing is the slowest rank)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

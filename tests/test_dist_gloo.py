@@ -1,0 +1,81 @@
+"""World-size-2 gloo runs of the multi-GPU host logic (CPU): batch x head sharding needs no
+collective and reproduces the single-process result; the sequence-sharded LSE merge
+(all-gather + log-sum-exp combine) equals softmax attention over the union."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _partial_state(q, K, V, idx):
+    """(m, l, o) of softmax attention over rows idx -- what K7 emits per split."""
+    if len(idx) == 0:
+        return -np.inf, 0.0, np.zeros(K.shape[1])
+    s = O.scores(q, K[idx])
+    m = s.max()
+    w = np.exp(s - m)
+    return m, w.sum(), w @ V[idx]
+
+
+def _worker(rank, world, port, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_20187_b200.shard import allgather_lse_merge, lane_block, max_over_ranks, token_block
+    rng = np.random.default_rng(0)
+    lanes, n, d, k = 6, 512, 16, 51
+    K = rng.normal(size=(lanes, n, d))
+    V = rng.normal(size=(lanes, n, d))
+    Q = rng.normal(size=(lanes, d))
+    # --- sequence sharding: global exact top-k, per-rank partial softmax, LSE merge ---
+    t0, t1 = token_block(n, world, rank)
+    ms, ls, os_ = [], [], []
+    for i in range(lanes):
+        sel = O.select(Q[i], K[i], k)             # global threshold (exact set)
+        mine = sel[(sel >= t0) & (sel < t1)]      # this rank's slice of the selected set
+        m, l, o = _partial_state(Q[i], K[i], V[i], mine)
+        ms.append(m); ls.append(l); os_.append(o)
+    out = allgather_lse_merge(torch.tensor(ms), torch.tensor(ls), torch.tensor(np.stack(os_)))
+    ref = np.stack([O.attention(Q[i], K[i], V[i], O.select(Q[i], K[i], k)) for i in range(lanes)])
+    err_seq = float(np.abs(out.numpy() - ref).max())
+    # --- batch x head sharding: disjoint lanes, results gathered only for checking ---
+    a, b = lane_block(lanes, world, rank)
+    local = torch.tensor(np.stack([O.attention(Q[i], K[i], V[i], O.select(Q[i], K[i], k)) for i in range(a, b)]
+                                  or [np.zeros(d)])[: b - a])
+    sizes = [None] * world
+    dist.all_gather_object(sizes, (a, b, local.numpy()))
+    full = np.concatenate([x[2] for x in sorted(sizes, key=lambda x: x[0])])
+    err_lane = float(np.abs(full - ref).max())
+    t = max_over_ranks(float(rank + 1))
+    if rank == 0:
+        ret.put((err_seq, err_lane, t))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_sharding(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err_seq, err_lane, t = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err_seq < 1e-12 and err_lane == 0.0 and t == float(world)

@@ -1,0 +1,183 @@
+"""Kernel-level parity on the B200: every C-ABI stage against the C oracle.
+
+Bar (BASELINE.json north_star): logits, bounds, abstracts, selected sets, runs and
+partitions bit-exact; attention within 2e-3 relative (f32 values) / 1e-2 (bf16)."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from oracle import synth  # noqa: E402
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16, "f64": torch.float64}
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_20187_b200 import ops as _ops
+    return _ops
+
+
+def _keys(rng, lanes, n, d, dt):
+    k = rng.normal(size=(lanes, n, d)).astype(np.float32)
+    t = torch.from_numpy(k).to(DT[dt]).cuda()
+    return t, t.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16", "f16", "f64"])
+@pytest.mark.parametrize("d", [1, 4, 16, 64, 100, 128, 256])
+def test_token_scores_bitexact(ops, dt, d):
+    rng = np.random.default_rng(d)
+    lanes, n = 3, 301
+    kt, kh = _keys(rng, lanes, n, d, dt)
+    q = rng.normal(size=(lanes, d))
+    qt = torch.from_numpy(q).cuda()
+    got = ops.token_scores(qt, kt, n).cpu().numpy()
+    for i in range(lanes):
+        ref = O.scores(q[i], kh[i])
+        assert np.array_equal(got[i], ref), (dt, d, i)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16", "f64"])
+@pytest.mark.parametrize("d,C", [(4, 1), (16, 8), (64, 64), (128, 64), (128, 8), (100, 7)])
+def test_abstracts_and_bounds_bitexact(ops, dt, d, C):
+    rng = np.random.default_rng(7 * d + C)
+    lanes, n = 2, 517
+    kt, kh = _keys(rng, lanes, n, d, dt)
+    q = rng.normal(size=(lanes, d)) * rng.choice([0.1, 1.0, 10.0])
+    q[:, 0] = 0.0
+    amax, amin = ops.abstract_build(kt, n, C)
+    U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, n, C)
+    m = ops.n_grid_leaves(n, C)
+    for i in range(lanes):
+        mx = np.stack([kh[i, c * C:(c + 1) * C].max(0) for c in range(m)])
+        mn = np.stack([kh[i, c * C:(c + 1) * C].min(0) for c in range(m)])
+        assert np.array_equal(amax[i, :m].double().cpu().numpy(), mx)
+        assert np.array_equal(amin[i, :m].double().cpu().numpy(), mn)
+        rows = [min(C, n - c * C) for c in range(m)]
+        Ur, Lr = O.bounds(q[i], mx, mn, rows)
+        assert np.array_equal(U[i, :m].cpu().numpy(), Ur)
+        assert np.array_equal(L[i, :m].cpu().numpy(), Lr)
+        s = O.scores(q[i], kh[i])
+        for c in range(m):
+            seg = s[c * C:(c + 1) * C]
+            assert Lr[c] <= seg.min() and seg.max() <= Ur[c]  # sound for canonical logits
+
+
+def test_bound_soundness_c02(ops):
+    """test_acceptance.py:101-123 criterion 2, on canonical logits (no tolerance)."""
+    rng = np.random.default_rng(2024)
+    d, lanes, C = 64, 64, 64
+    for rep in range(25):
+        scale = float(rng.lognormal(0.0, 1.0))
+        k = rng.normal(scale=scale, size=(lanes, C, d))
+        k[rng.random(lanes) < 0.1] = k[:1, :1]
+        q = rng.normal(scale=scale, size=(lanes, d))
+        q[rng.random(lanes) < 0.05] = 0.0
+        kt = torch.from_numpy(k).cuda()
+        amax, amin = ops.abstract_build(kt, C, C)
+        U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, C, C)
+        s = ops.token_scores(torch.from_numpy(q).cuda(), kt, C).cpu().numpy()
+        assert np.all(L[:, 0].cpu().numpy() <= s.min(1))
+        assert np.all(s.max(1) <= U[:, 0].cpu().numpy())
+
+
+def _lane_data(kind, lanes, n, d, seed):
+    if kind == "random":
+        rng = np.random.default_rng(seed)
+        return (rng.normal(size=(lanes, n, d)).astype(np.float32), rng.normal(size=(lanes, n, d)).astype(np.float32),
+                rng.normal(size=(lanes, d)).astype(np.float32))
+    if kind == "ties":
+        rng = np.random.default_rng(seed)
+        K = np.ones((lanes, n, d), np.float32)
+        K[:, ::7] = 2.0
+        return K, rng.normal(size=(lanes, n, d)).astype(np.float32), np.ones((lanes, d), np.float32)
+    K = np.empty((lanes, n, d), np.float32)
+    V = np.empty_like(K)
+    Q = np.empty((lanes, d), np.float32)
+    for i in range(lanes):
+        k, q, v, _ = synth.lane(synth.Profile(desert_rate=0.7, seed=seed), 0, i, n, d, 1)
+        K[i], V[i], Q[i] = k, v, q[0]
+    return K, V, Q
+
+
+@pytest.mark.parametrize("kind", ["random", "planted", "ties"])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("n,C,rate", [(4096, 64, 0.10), (1000, 8, 0.5), (65536, 64, 0.10), (33, 4, 0.1)])
+def test_fused_select_attend_matches_oracle(ops, kind, dt, n, C, rate):
+    lanes, d = (4 if n <= 4096 else 2), 128
+    K, V, Q = _lane_data(kind, lanes, n, d, seed=n + C)
+    k = math.ceil(rate * n)
+    kt = torch.from_numpy(K).to(DT[dt]).cuda()
+    vt = torch.from_numpy(V).to(DT[dt]).cuda()
+    qt = torch.from_numpy(Q).cuda()
+    amax, amin = ops.abstract_build(kt, n, C)
+    ws = ops.LayerWorkspace(lanes, n, ops.n_grid_leaves(n, C), d, kt.device)
+    out = {"sel_tok": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "sel_score": torch.empty((lanes, k), dtype=torch.float64, device="cuda"),
+           "n_sel": torch.empty(lanes, dtype=torch.int32, device="cuda"),
+           "run_start": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "run_len": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "n_runs": torch.empty(lanes, dtype=torch.int32, device="cuda"),
+           "out": torch.empty((lanes, d), dtype=torch.float32, device="cuda"),
+           "evals": torch.empty(lanes, dtype=torch.int64, device="cuda")}
+    ops.select_attend(qt, kt, vt, amax, amin, n, k, C, ws, out)
+    torch.cuda.synchronize()
+    Kh = kt.double().cpu().numpy()
+    Vh = vt.double().cpu().numpy()
+    tol = 2e-3 if dt == "f32" else 1e-2
+    for i in range(lanes):
+        s = O.scores(Q[i], Kh[i])
+        ref = O.topk(s, k)
+        got = out["sel_tok"][i].cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, ref), (kind, dt, n, i)
+        assert np.array_equal(out["sel_score"][i].cpu().numpy(), s[ref])
+        runs = O.runs(ref)
+        nr = int(out["n_runs"][i])
+        assert nr == len(runs)
+        rs = out["run_start"][i, :nr].cpu().numpy()
+        rl = out["run_len"][i, :nr].cpu().numpy()
+        assert [(int(a), int(a + b)) for a, b in zip(rs, rl)] == runs
+        att = O.attention(Q[i], Kh[i], Vh[i], ref)
+        err = np.linalg.norm(out["out"][i].cpu().numpy() - att) / np.linalg.norm(att)
+        assert err <= tol, err
+        assert int(out["evals"][i]) >= ops.n_grid_leaves(n, C) + k
+
+
+def test_select_plan_prunes_planted(ops):
+    n, d, C = 65536, 128, 64
+    K, V, Q = _lane_data("planted", 2, n, d, seed=3)
+    kt = torch.from_numpy(K).cuda()
+    amax, amin = ops.abstract_build(kt, n, C)
+    U, L = ops.chunk_bounds(torch.from_numpy(Q).cuda(), amax, amin, n, C)
+    plan = ops.select_plan(U, L, n, math.ceil(0.1 * n), C)
+    frac = plan["n_cand"].cpu().numpy() / n
+    assert np.all(frac < 0.45), frac  # ~30% hot + boundary chunks
+
+
+def test_runs_partition(ops):
+    rng = np.random.default_rng(0)
+    n = 5000
+    for trial in range(20):
+        k = int(rng.integers(0, 300))
+        sel = np.sort(rng.choice(n, size=k, replace=False)) if k else np.zeros(0, np.int64)
+        st = torch.from_numpy(sel.astype(np.int32))[None].cuda()
+        ns = torch.tensor([k], dtype=torch.int32).cuda()
+        r = ops.runs_scan(st if k else torch.zeros((1, 0), dtype=torch.int32, device="cuda"), ns, n)
+        npart = int(r["n_part"][0])
+        ps = r["part_start"][0, :npart].cpu().numpy()
+        pst = r["part_state"][0, :npart].cpu().numpy()
+        pe = np.append(ps[1:], n)
+        got = [(int(a), int(b), "important" if c == 1 else "desert") for a, b, c in zip(ps, pe, pst)]
+        ref = [x for x in O.canonical_partition(sel, n) if x[2] != "pad"]
+        assert got == ref

@@ -1,0 +1,82 @@
+"""CPU-only checks: the C ABI library loads and exports every declared symbol; host-side
+logic (chunk plan, cost model, grid metrics) equals the reference's frozen values."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from tests import golden_io as G
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "kvtier_b200.h").read_text()
+    return re.findall(r"KVT_API\s+[\w\s\*]+?\b(kvt_\w+)\s*\(", text)
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2506_20187_b200 import _lib
+    names = declared_symbols()
+    assert len(names) >= 15
+    for nm in names:
+        assert hasattr(_lib.handle(), nm), nm
+    assert set(names) == set(_lib.EXPORTED)
+    assert _lib.kvt_version() == 100
+    assert _lib.kvt_status_string(-2).decode() == "k out of range"
+
+
+def test_abi_rejects_bad_arguments_without_gpu():
+    """Argument validation happens before any CUDA call, so it is testable on CPU."""
+    from paper_2506_20187_b200 import _lib as L
+    assert L.kvt_select_plan(1, 10, 4, None, None, 0, 1, 1, 3, 11, 1, 1, 1, 1, None, None, None) == L.ERR_K
+    assert L.kvt_chunk_bounds(None, 0, 1, 4, 10, 4, None, None, 0, None, None, 0, 0, None, None, 0, None) == L.ERR_ARG
+    assert L.kvt_topk_select(1, 1, 1, 1, 1, -1, 1, 1, 1, 1, None) == L.ERR_K
+    with pytest.raises(ValueError):
+        L.check(L.ERR_K, "x")
+    with pytest.raises(RuntimeError):
+        L.check(L.ERR_COLD, "x")
+
+
+def test_chunk_plan_matches_reference_values():
+    from paper_2506_20187_b200 import chunk_tree as ct
+    s = G.load_json("scalars.json")
+    for m, n, rho, v in s["chunk_cost"]:
+        assert ct.chunk_cost(m, n, rho) == pytest.approx(v, abs=1e-12)
+    for n, rho, lo, hi, v in s["plan_chunk_count"]:
+        assert ct.plan_chunk_count(n, rho, min_chunk_size=lo, max_chunk_size=hi) == v
+    for rho, layer, step, nst, nctx, v in s["chunk_size_for"]:
+        cfg = ct.ChunkPlanConfig(rho=None if rho is None else tuple(rho))
+        assert cfg.chunk_size_for(layer, step, nst, nctx) == v
+    for n, v in s["next_pow2"]:
+        assert ct.next_pow2(n) == v
+    with pytest.raises(ValueError):
+        ct.chunk_cost(16, 1024, 1.0)
+    with pytest.raises(ValueError):
+        ct.plan_chunk_count(1024, 1.5)
+    with pytest.raises(ValueError):
+        ct.ChunkPlanConfig(default_chunk_size=48)
+    with pytest.raises(ValueError):
+        ct.ChunkPlanConfig(early_chunk_size=128, default_chunk_size=64)
+
+
+def test_grid_metrics_match_reference_values():
+    from paper_2506_20187_b200.engine import desert_rate_on_grid
+    for sel, n, g, v in G.load_json("scalars.json")["desert_rate_on_grid"]:
+        assert desert_rate_on_grid(set(sel), n, g) == v
+
+
+def test_shard_blocks_cover_disjointly():
+    from paper_2506_20187_b200.shard import lane_block, token_block
+    for n in (1, 7, 32, 256, 1000):
+        for w in (1, 2, 4, 8):
+            blocks = [lane_block(n, w, r) for r in range(w)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+            toks = [token_block(n * 64 + 3, w, r) for r in range(w)]
+            assert toks[0][0] == 0 and toks[-1][1] == n * 64 + 3
+            assert all(a[1] == b[0] and (a[1] % 64 == 0 or a[1] == n * 64 + 3) for a, b in zip(toks, toks[1:]))
