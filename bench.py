@@ -370,35 +370,63 @@ def run_ours(args):
         e2e = {"value": args.batch * world / (float(ems.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": float(ems.item())}
 
-    # ---- per-kernel attribution: staged pipeline with events on the launching stream ----
-    stages = ["bounds", "plan", "score", "select", "runs", "attn"]
-    st_ms = {s: 0.0 for s in stages}
-    n_cand = [[0] * dec.lanes for _ in range(L)]
-    reps = 2
+    # ---- per-kernel attribution ----
+    # The staged pipeline (same kernels as the fused call) is run once to materialise every
+    # layer's intermediates; then each stage's 32 per-layer launches are captured in their
+    # own CUDA graph and replayed between CUDA events on the launching stream, so each
+    # number is the device time of that kernel alone (no host gaps), averaged over reps.
+    stages = ["bounds", "plan", "score", "select", "attn"]
+    inter = []
+    n_cand = []
     with torch.cuda.stream(stream):
-        for rep in range(reps):
-            q_static.copy_(Q[args.warmup + rep % args.steps])
+        q_static.copy_(Q[args.warmup])
+        for l in range(L):
+            C, n, k = dec.C[l], dec.n, dec.k_for(l)
+            U, Lo = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C)
+            plan = ops.select_plan(U, Lo, n, k, C)
+            cs, ct = ops.cand_score(q_static[l], dec.K[l], plan, n)
+            st_, ss_, ns_, _ = ops.topk_select(cs, ct, plan["n_cand"], k, want_runs=True)
+            inter.append((U, Lo, plan, cs, ct, st_, ss_, ns_))
+        stream.synchronize()
+    n_cand = [x[2]["n_cand"].cpu().tolist() for x in inter]
+
+    def stage_fn(name):
+        def run():
             for l in range(L):
-                evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
                 C, n, k = dec.C[l], dec.n, dec.k_for(l)
-                evs[0].record(stream)
-                U, Lo = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C)
-                evs[1].record(stream)
-                plan = ops.select_plan(U, Lo, n, k, C)
-                evs[2].record(stream)
-                cs, ct = ops.cand_score(q_static[l], dec.K[l], plan, n)
-                evs[3].record(stream)
-                st, ss, ns = ops.topk_select(cs, ct, plan["n_cand"], k)
-                evs[4].record(stream)
-                ops.runs_scan(st, ns, n, want_partition=False)
-                evs[5].record(stream)
-                ops.sparse_decode_attn(dec.V[l], st, ss, ns)
-                evs[6].record(stream)
-                evs[6].synchronize()
-                for i, sname in enumerate(stages):
-                    st_ms[sname] += evs[i].elapsed_time(evs[i + 1]) / reps
-                if rep == 0:
-                    n_cand[l] = plan["n_cand"].cpu().tolist()
+                U, Lo, plan, cs, ct, st_, ss_, ns_ = inter[l]
+                if name == "bounds":
+                    ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C)
+                elif name == "plan":
+                    ops.select_plan(U, Lo, n, k, C)
+                elif name == "score":
+                    ops.cand_score(q_static[l], dec.K[l], plan, n)
+                elif name == "select":
+                    ops.topk_select(cs, ct, plan["n_cand"], k, want_runs=True)
+                elif name == "attn":
+                    ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)
+        return run
+
+    st_ms = {}
+    reps = 3
+    for name in stages:
+        fn = stage_fn(name)
+        with torch.cuda.stream(stream):
+            fn()  # warm (allocator, attributes)
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+            g.replay()
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            e1.record(stream)
+            e1.synchronize()
+        st_ms[name] = e0.elapsed_time(e1) / reps
+        del g
     algo = dec.algorithmic_bytes(n_cand)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -406,7 +434,7 @@ def run_ours(args):
     per_kernel = {s: {"ms_per_step": st_ms[s], "algo_bytes": algo[s],
                       "gbs": algo[s] / (st_ms[s] / 1e3) / 1e9 if st_ms[s] > 0 else None} for s in stages}
     staged_total = sum(st_ms.values())
-    launches_per_layer = 7  # bounds, plan, score, select (cluster), runs, attn split, attn merge
+    launches_per_layer = 5  # bounds, plan, score (TMA), select+runs (cluster), attn (split + ticket merge)
     sel_gather_bytes = algo["bounds"] + algo["score"] + algo["select"] + algo["attn"]
     frac_of = "measured" if "hbm_gbs" in peaks else "fallback"
     line = {

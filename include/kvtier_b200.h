@@ -119,6 +119,14 @@ KVT_API int kvt_topk_select(const double* cand_score, const int32_t* cand_tok, c
                     int64_t cand_stride, int64_t n_lanes, int64_t k, int32_t* sel_tok,
                     double* sel_score, int64_t sel_stride, int32_t* n_sel, void* stream);
 
+/* K5 with the K6 run scan fused into the same cluster kernel (what kvt_select_attend uses):
+ * additionally writes run_start/run_len [i*run_stride + r] and n_runs[i] for the selected
+ * tokens (engine.py:176-183).  run_start == NULL behaves as kvt_topk_select. */
+KVT_API int kvt_topk_select_runs(const double* cand_score, const int32_t* cand_tok, const int32_t* n_cand,
+                    int64_t cand_stride, int64_t n_lanes, int64_t k, int32_t* sel_tok,
+                    double* sel_score, int64_t sel_stride, int32_t* n_sel, int32_t* run_start,
+                    int32_t* run_len, int64_t run_stride, int32_t* n_runs, void* stream);
+
 /* ---- K6: runs / canonical partition --------------------------------------------------------
  * engine.py:176-183 _token_runs and the leaf shape of select_top_k + merge_desert
  * (chunk_tree.py:331-379): the selected runs and their complement (desert runs) tile [0,n).
@@ -134,7 +142,9 @@ KVT_API int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t 
  * sel_score are the canonical logits from K5 (keys are not re-read).  Split over
  * `splits` blocks per lane with an online-softmax (m, l, o) merge.  out: float32
  * [n_lanes][d] (out64: optional float64 copy).  ws: workspace of
- * kvt_attn_workspace_bytes(n_lanes, d, splits) bytes. */
+ * kvt_attn_workspace_bytes(n_lanes, d, splits) bytes, zero-filled once by the caller (the
+ * per-lane merge tickets are left at zero by every call).  The last split CTA of each lane
+ * performs the log-sum-exp merge, so this is a single kernel launch. */
 KVT_API size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits);
 KVT_API int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride,
                            int d, const int32_t* sel_tok, const double* sel_score,

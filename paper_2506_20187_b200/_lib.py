@@ -73,6 +73,8 @@ kvt_select_plan = _sig("kvt_select_plan", ctypes.c_int, _i64, _i64, _i32, _vp, _
 kvt_cand_score = _sig("kvt_cand_score", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _vp, _vp,
                       _vp, _i64, _i32, _vp)
 kvt_topk_select = _sig("kvt_topk_select", ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp)
+kvt_topk_select_runs = _sig("kvt_topk_select_runs", ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64,
+                            _vp, _vp, _vp, _i64, _vp, _vp)
 kvt_runs_scan = _sig("kvt_runs_scan", ctypes.c_int, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
                      _vp, _vp)
 kvt_attn_workspace_bytes = _sig("kvt_attn_workspace_bytes", _sz, _i64, _i32, _i32)
@@ -84,6 +86,7 @@ kvt_select_attend = _sig("kvt_select_attend", ctypes.c_int, ctypes.POINTER(KvtLa
 EXPORTED = [
     "kvt_version", "kvt_status_string", "kvt_last_error", "kvt_abstract_build", "kvt_abstract_spans",
     "kvt_chunk_bounds", "kvt_token_scores", "kvt_select_plan", "kvt_cand_score", "kvt_topk_select",
+    "kvt_topk_select_runs",
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
     "kvt_select_attend",
 ]

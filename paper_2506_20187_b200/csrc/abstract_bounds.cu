@@ -135,10 +135,12 @@ __global__ void __launch_bounds__(256) bounds_kernel(
     const int32_t* __restrict__ n_leaves, int64_t leaf_stride, const AT* __restrict__ amax,
     const AT* __restrict__ amin, int64_t abs_lane_stride, double* __restrict__ U,
     double* __restrict__ L, int64_t bnd_stride) {
+    // 8 chunks per warp step: 16 independent 16 B abstract loads in flight per lane, then
+    // three reduce-scatter trees (U, L, A) leave chunk (lane >> 2) & 7 on each lane quad.
     const int lane = threadIdx.x & 31;
     const int64_t lane_i = blockIdx.y;
     const int64_t nl = leaf_start ? (int64_t)n_leaves[lane_i] : (n + C - 1) / C;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5) * 8;
     double qr[G][4];
 #pragma unroll
     for (int r = 0; r < G; ++r)
@@ -151,44 +153,60 @@ __global__ void __launch_bounds__(256) bounds_kernel(
     const double fac = slack_factor(d);
     const AT* mxb = amax + lane_i * abs_lane_stride;
     const AT* mnb = amin + lane_i * abs_lane_stride;
-    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nl; c += warps) {
-        int64_t rows;
-        if (leaf_start) {
-            const int32_t* ls = leaf_start + lane_i * leaf_stride;
-            const int64_t e = (c + 1 < nl) ? (int64_t)ls[c + 1] : n;
-            rows = e - ls[c];
-        } else {
-            rows = min((int64_t)C, n - c * C);
-        }
-        const AT* M = mxb + c * d;
-        const AT* N = mnb + c * d;
-        double pu = 0.0, pl = 0.0, pa = 0.0;
+    const int32_t* ls = leaf_start ? leaf_start + lane_i * leaf_stride : nullptr;
+    for (int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; c0 < nl; c0 += wstride) {
+        double pu[8], pl[8], pa[8];
 #pragma unroll
-        for (int r = 0; r < G; ++r) {
-            const int g = lane + 32 * r;
+        for (int u = 0; u < 8; ++u) {
+            pu[u] = 0.0; pl[u] = 0.0; pa[u] = 0.0;
+            const int64_t c = c0 + u;
+            if (c < nl) {
+                const AT* M = mxb + c * d;
+                const AT* N = mnb + c * d;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int j = 4 * g + i;
-                if (j < d) {
-                    const double hi_ = (double)M[j], lo_ = (double)N[j];
-                    const double qj = qr[r][i];
-                    const double hi = qj >= 0.0 ? hi_ : lo_;
-                    const double lo = qj >= 0.0 ? lo_ : hi_;
-                    pu = fma(qj, hi, pu);
-                    pl = fma(qj, lo, pl);
-                    pa = fma(fabs(qj), fmax(fabs(hi_), fabs(lo_)), pa);
+                for (int r = 0; r < G; ++r) {
+                    const int g = lane + 32 * r;
+                    if (4 * g < d) {
+                        double hv[4], lv[4];
+                        if (d % 4 == 0) {
+                            Elem<AT>::load4(M + 4 * g, hv);
+                            Elem<AT>::load4(N + 4 * g, lv);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                hv[i] = 4 * g + i < d ? (double)M[4 * g + i] : 0.0;
+                                lv[i] = 4 * g + i < d ? (double)N[4 * g + i] : 0.0;
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            if (4 * g + i < d) {
+                                const double qj = qr[r][i];
+                                const double hi = qj >= 0.0 ? hv[i] : lv[i];
+                                const double lo = qj >= 0.0 ? lv[i] : hv[i];
+                                pu[u] = fma(qj, hi, pu[u]);
+                                pl[u] = fma(qj, lo, pl[u]);
+                                pa[u] = fma(fabs(qj), fmax(fabs(hv[i]), fabs(lv[i])), pa[u]);
+                            }
+                        }
+                    }
                 }
             }
         }
-        double u = tree_allreduce(pu), l = tree_allreduce(pl), a = tree_allreduce(pa);
-        if (rows > 1) {
-            const double slack = a * fac;
-            u = u + slack;
-            l = l - slack;
-        }
-        if (lane == 0) {
-            U[lane_i * bnd_stride + c] = u / sd;
-            L[lane_i * bnd_stride + c] = l / sd;
+        double u_ = tree_8tok(pu, lane), l_ = tree_8tok(pl, lane), a_ = tree_8tok(pa, lane);
+        const int t = (lane >> 2) & 7;
+        const int64_t c = c0 + t;
+        if ((lane & 3) == 0 && c < nl) {
+            int64_t rows;
+            if (ls) rows = ((c + 1 < nl) ? (int64_t)ls[c + 1] : n) - ls[c];
+            else rows = kvt::imin((int64_t)C, n - c * C);
+            if (rows > 1) {
+                const double slack = a_ * fac;
+                u_ = u_ + slack;
+                l_ = l_ - slack;
+            }
+            U[lane_i * bnd_stride + c] = u_ / sd;
+            L[lane_i * bnd_stride + c] = l_ / sd;
         }
     }
 }
@@ -294,7 +312,7 @@ template <typename QT, typename AT, int G>
 static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                           const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
                           double* U, double* L, int64_t bs, int64_t max_leaves, cudaStream_t st) {
-    int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 7) / 8, 1024));
+    int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 63) / 64, 1024));
     // keep ~8 CTAs per SM in total when lanes are few
     dim3 grid(gx, (unsigned)n_lanes);
     bounds_kernel<QT, AT, G><<<grid, 256, 0, st>>>((const QT*)q, d, n, C, ls, nl, lstr, (const AT*)amax,

@@ -61,7 +61,7 @@ struct LayerWs {
     int32_t *items, *n_items, *n_cand;
     double* cand_score;
     int32_t* cand_tok;
-    double* attn_part;
+    char* attn_part;
     size_t bytes;
 };
 
@@ -76,7 +76,7 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     w.n_cand = c.take<int32_t>((size_t)n_lanes);
     w.cand_score = c.take<double>((size_t)(n_lanes * n));
     w.cand_tok = c.take<int32_t>((size_t)(n_lanes * n));
-    w.attn_part = c.take<double>((size_t)(n_lanes * MAX_SPLITS * (d + 2)));
+    w.attn_part = c.take<char>(kvt_attn_workspace_bytes(n_lanes, d, MAX_SPLITS));  // tickets + partials
     w.bytes = c.used;
     return w;
 }
@@ -123,14 +123,9 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     rc = kvt_cand_score(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items, item_cap,
                         w.n_items, w.cand_score, w.cand_tok, a->n, blocks, stream);
     if (rc) return rc;
-    rc = kvt_topk_select(w.cand_score, w.cand_tok, w.n_cand, a->n, a->n_lanes, a->k, a->sel_tok, a->sel_score, a->k,
-                         a->n_sel, stream);
+    rc = kvt_topk_select_runs(w.cand_score, w.cand_tok, w.n_cand, a->n, a->n_lanes, a->k, a->sel_tok, a->sel_score,
+                              a->k, a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);  // K5 + fused K6
     if (rc) return rc;
-    if (a->run_start) {
-        rc = kvt_runs_scan(a->sel_tok, a->n_sel, a->k, a->n_lanes, a->n, a->run_start, a->run_len, a->k, a->n_runs,
-                           nullptr, nullptr, 0, nullptr, stream);
-        if (rc) return rc;
-    }
     if (a->out && a->values) {
         int splits = a->attn_splits;
         if (splits <= 0) {

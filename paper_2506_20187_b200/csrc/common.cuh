@@ -76,6 +76,11 @@ template <> struct Elem<__nv_bfloat16> {
 };
 template <> struct Elem<__half> {
     static constexpr int code = KVT_F16;
+    __device__ __forceinline__ static void unpack(uint2 u, float f[4]) {
+        __half2 a = *reinterpret_cast<__half2*>(&u.x), b = *reinterpret_cast<__half2*>(&u.y);
+        float2 fa = __half22float2(a), fb = __half22float2(b);
+        f[0] = fa.x; f[1] = fa.y; f[2] = fb.x; f[3] = fb.y;
+    }
     __device__ __forceinline__ static void load4(const __half* p, double v[4]) {
         uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
         __half2 a = *reinterpret_cast<__half2*>(&u.x), b = *reinterpret_cast<__half2*>(&u.y);
@@ -102,6 +107,29 @@ __device__ __forceinline__ void load_group(const T* row, int g, int d, double v[
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[i] = (j0 + i < d) ? Elem<T>::ld1(row + j0 + i) : 0.0;
     }
+}
+
+// Same, from shared memory (plain vector loads).
+template <typename T> __device__ __forceinline__ void lds4(const T* p, double v[4]);
+template <> __device__ __forceinline__ void lds4<float>(const float* p, double v[4]) {
+    float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+template <> __device__ __forceinline__ void lds4<double>(const double* p, double v[4]) {
+    double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <> __device__ __forceinline__ void lds4<__nv_bfloat16>(const __nv_bfloat16* p, double v[4]) {
+    uint2 u = *reinterpret_cast<const uint2*>(p);
+    float f[4];
+    Elem<__nv_bfloat16>::unpack(u, f);
+    v[0] = f[0]; v[1] = f[1]; v[2] = f[2]; v[3] = f[3];
+}
+template <> __device__ __forceinline__ void lds4<__half>(const __half* p, double v[4]) {
+    uint2 u = *reinterpret_cast<const uint2*>(p);
+    __half2 a = *reinterpret_cast<__half2*>(&u.x), b = *reinterpret_cast<__half2*>(&u.y);
+    float2 fa = __half22float2(a), fb = __half22float2(b);
+    v[0] = fa.x; v[1] = fa.y; v[2] = fb.x; v[3] = fb.y;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -162,6 +190,44 @@ __device__ __forceinline__ uint64_t ord_key(double s) {
 __device__ __forceinline__ double key_to_double(uint64_t k) {
     uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
     return __longlong_as_double((long long)b);
+}
+
+// ------------------------------------------------------------------------------------------
+// mbarrier + bulk async copy (TMA engine, cp.async.bulk) helpers
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (16 B aligned, bytes % 16 == 0), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 // ------------------------------------------------------------------------------------------

@@ -1,10 +1,13 @@
 // plan.cu -- lower-bound threshold tau and candidate work items (pruning half of
 // chunk_tree.py:233-338 select_top_k).
 //
-// tau = max{x : sum of rows over leaves with L >= x is >= k}: at least k tokens score
-// >= tau, so the k-th best score is >= tau and any leaf with U < tau holds no top-k token
-// (strictly below, ties included).  Found with an 8-pass weighted radix select over the
-// orderable 64-bit keys of L (one CTA per lane; histogram weights are row counts).
+// tau* = max{x : sum of rows over leaves with L >= x is >= k}: at least k tokens score
+// >= tau*, so the k-th best score is >= tau* and any leaf with U < tau* holds no top-k
+// token (strictly below, ties included).  A 3-pass weighted radix select over the top 24
+// bits of the orderable 64-bit keys of L (sign, exponent, 12 mantissa bits) finds the
+// bucket of tau*; tau = the smallest value of that bucket <= tau* is used, which prunes
+// within 2^-12 relative of the exact threshold and stays sound.  One CTA per lane; the
+// keys are staged in shared memory once; histogram weights are row counts.
 // Candidate leaves (U >= tau) are emitted in ascending token order as work items of
 // <= 64 tokens: (tok_start, count, out_pos), out_pos = exclusive prefix of candidate rows.
 #include "common.cuh"
@@ -29,7 +32,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
     int64_t n, int C, const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ n_leaves,
     int64_t leaf_stride, const double* __restrict__ U, const double* __restrict__ L, int64_t bnd_stride,
     int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
-    int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals) {
+    int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals, int stage_cap) {
+    extern __shared__ __align__(16) unsigned char plan_smem[];
+    uint64_t* kst = reinterpret_cast<uint64_t*>(plan_smem);  // staged keys (if they fit)
     __shared__ unsigned long long hist[256];
     __shared__ long long scan_sh[33];
     __shared__ unsigned long long s_prefix, s_mask;
@@ -42,11 +47,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
     const double* Ul = U + li * bnd_stride;
     const double* Ll = L + li * bnd_stride;
 
+    const bool staged = nl <= stage_cap;
+    if (staged)
+        for (int64_t c = tid; c < nl; c += PLAN_THREADS) kst[c] = ord_key(Ll[c]);
     if (tid == 0) { s_prefix = 0; s_mask = 0; s_remaining = k; s_done = (k <= 0); }
     __syncthreads();
 
-    // ---- weighted radix select: largest key T with W(key >= T) >= k ----
-    for (int shift = 56; shift >= 0 && !s_done; shift -= 8) {
+    // ---- weighted radix select on the top 24 key bits ----
+    for (int shift = 56; shift >= 40 && !s_done; shift -= 8) {
         for (int i = tid; i < 256; i += PLAN_THREADS) hist[i] = 0;
         __syncthreads();
         const unsigned long long prefix = s_prefix, mask = s_mask;
@@ -55,7 +63,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
             int digit = 256;
             unsigned long long w = 0;
             if (c < nl) {
-                const uint64_t key = ord_key(Ll[c]);
+                const uint64_t key = staged ? kst[c] : ord_key(Ll[c]);
                 if ((key & mask) == prefix) {
                     digit = (int)((key >> shift) & 0xff);
                     w = (unsigned long long)leaf_rows(ls, nl, c, n, C);
@@ -147,8 +155,16 @@ extern "C" int kvt_select_plan(int64_t n_lanes, int64_t n, int C, const int32_t*
     if (k < 0 || k > n) return KVT_ERR_K;
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
-    plan_kernel<<<(unsigned)n_lanes, PLAN_THREADS, 0, (cudaStream_t)stream>>>(
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+        if (e != cudaSuccess) return kvt_set_cuda_error(e);
+        configured = true;
+    }
+    const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
+    const int cap = (int)kvt::imin(max_leaves, 16384);
+    plan_kernel<<<(unsigned)n_lanes, PLAN_THREADS, (size_t)cap * 8, (cudaStream_t)stream>>>(
         n, C, leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand,
-        cand_leaf, evals);
+        cand_leaf, evals, cap);
     return kvt_check_launch();
 }

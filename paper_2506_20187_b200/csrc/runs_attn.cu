@@ -104,12 +104,62 @@ __device__ __forceinline__ void load_group_acc(const T* row, int g, int d, typen
     }
 }
 
+// Last-arriving split CTA of a lane merges all splits' (m, l, o) (threadFenceReduction
+// pattern: partial written -> __threadfence -> ticket; the last ticket holder reads all).
+// The per-lane ticket counter is reset to 0 by the merger, so the workspace stays valid
+// for the next call without a memset.
+__device__ __forceinline__ void attn_finish(double* __restrict__ part, int splits, int d, int64_t li,
+                                            unsigned int* __restrict__ tickets, float* __restrict__ out,
+                                            double* __restrict__ out64) {
+    __shared__ int s_last;
+    __shared__ double s_scale[64];
+    __shared__ double s_M, s_den;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(&tickets[li], 1u);
+        s_last = (t == (unsigned)splits - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double* P = part + li * splits * (int64_t)(d + 2);
+    if (threadIdx.x < 32) {
+        double M = -INFINITY;
+        for (int s = threadIdx.x; s < splits; s += 32)
+            if (__ldcg(P + s * (d + 2) + 1) > 0) M = fmax(M, __ldcg(P + s * (d + 2)));
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) M = fmax(M, __shfl_xor_sync(KVT_FULL, M, off));
+        double den = 0.0;
+        for (int s = threadIdx.x; s < splits; s += 32) {
+            const double ls = __ldcg(P + s * (d + 2) + 1);
+            const double sc = ls > 0 ? exp(__ldcg(P + s * (d + 2)) - M) : 0.0;
+            s_scale[s] = sc;
+            den += sc * ls;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(KVT_FULL, den, off);
+        if (threadIdx.x == 0) { s_M = M; s_den = den; }
+    }
+    __syncthreads();
+    const double den = s_den;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < splits; ++s) acc += s_scale[s] * __ldcg(P + s * (d + 2) + 2 + j);
+        const double r = den > 0 ? acc / den : 0.0;
+        if (out) out[li * d + j] = (float)r;
+        if (out64) out64[li * d + j] = r;
+    }
+    if (threadIdx.x == 0) tickets[li] = 0;
+}
+
 // partial record per (lane, split): m (f64), l, o[d] (Acc); stored as doubles for simplicity
 template <typename T, int G, bool VEC>
 __global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
     const T* __restrict__ values, int64_t lane_stride, int d, const int32_t* __restrict__ sel_tok,
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits,
-    double* __restrict__ part) {
+    double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
+    double* __restrict__ out64) {
     using Acc = typename AccOf<T>::type;
     __shared__ double red_m[ATTN_WARPS];
     __shared__ Acc red_o[ATTN_WARPS][4 * 32 * G];
@@ -201,30 +251,111 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
         P[0] = m;
         P[1] = (double)ls;
     }
+    attn_finish(part, splits, d, li, tickets, out, out64);
 }
 
-__global__ void attn_merge_kernel(const double* __restrict__ part, int splits, int d, float* __restrict__ out,
-                                  double* __restrict__ out64) {
-    const int64_t li = blockIdx.x;
-    const double* P = part + (int64_t)li * splits * (d + 2);
-    double M = -INFINITY;
-    for (int s = 0; s < splits; ++s)
-        if (P[s * (d + 2) + 1] > 0) M = fmax(M, P[s * (d + 2)]);
-    double denom = 0.0;
-    for (int s = 0; s < splits; ++s) {
-        const double ls = P[s * (d + 2) + 1];
-        if (ls > 0) denom += exp(P[s * (d + 2)] - M) * ls;
-    }
-    for (int j = threadIdx.x; j < d; j += blockDim.x) {
-        double acc = 0.0;
-        for (int s = 0; s < splits; ++s) {
-            const double ls = P[s * (d + 2) + 1];
-            if (ls > 0) acc += exp(P[s * (d + 2)] - M) * P[s * (d + 2) + 2 + j];
+// Fast path: 16 B per lane per load, a row spans LPR = d*sizeof(T)/16 lanes, a warp
+// instruction covers RPW = 32/LPR rows, and U = 8 instructions are in flight per lane
+// (4 KB of V per warp for bf16 d=128).
+template <typename T, int LPR>
+__global__ void __launch_bounds__(ATTN_THREADS) attn_split16_kernel(
+    const T* __restrict__ values, int64_t lane_stride, int d, const int32_t* __restrict__ sel_tok,
+    const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits,
+    double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
+    double* __restrict__ out64) {
+    using Acc = typename AccOf<T>::type;
+    constexpr int VPL = 16 / sizeof(T);
+    constexpr int RPW = 32 / LPR;
+    constexpr int U = 8;
+    __shared__ double red_m[ATTN_WARPS];
+    __shared__ Acc red_o[ATTN_WARPS][32 * VPL];
+    __shared__ Acc red_l[ATTN_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / LPR, col = lane % LPR;
+    const int64_t li = blockIdx.y;
+    const int s = blockIdx.x;
+    const int64_t k = n_sel[li];
+    const int64_t per = (k + splits - 1) / splits;
+    const int64_t a = kvt::imin(k, s * per), b = kvt::imin(k, a + per);
+    const int32_t* tok = sel_tok + li * sel_stride;
+    const double* sc = sel_score + li * sel_stride;
+    const T* base = values + li * lane_stride + col * VPL;
+    double m = -INFINITY;
+    for (int64_t i = a + threadIdx.x; i < b; i += ATTN_THREADS) m = fmax(m, sc[i]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(KVT_FULL, m, off));
+    if (lane == 0) red_m[warp] = m;
+    __syncthreads();
+    m = red_m[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_WARPS; ++w) m = fmax(m, red_m[w]);
+
+    Acc o[VPL];
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) o[e] = 0;
+    Acc l = 0;
+    constexpr int STEP = ATTN_WARPS * RPW;  // rows per CTA instruction slot
+    for (int64_t i0 = a + warp * RPW + sub; i0 < b; i0 += (int64_t)U * STEP) {
+        uint4 raw[U];
+        Acc w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + (int64_t)u * STEP;
+            if (i < b) {
+                raw[u] = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)tok[i] * d));
+                w[u] = (Acc)exp(sc[i] - m);
+            } else {
+                raw[u] = make_uint4(0, 0, 0, 0);
+                w[u] = 0;
+            }
         }
-        const double r = denom > 0 ? acc / denom : 0.0;
-        if (out) out[li * d + j] = (float)r;
-        if (out64) out64[li * d + j] = r;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            Acc v[VPL];
+            const T* e = reinterpret_cast<const T*>(&raw[u]);
+            if constexpr (sizeof(T) == 2) {
+                float f[4];
+                Elem<T>::unpack(make_uint2(raw[u].x, raw[u].y), f);
+                v[0] = f[0]; v[1] = f[1]; v[2] = f[2]; v[3] = f[3];
+                Elem<T>::unpack(make_uint2(raw[u].z, raw[u].w), f);
+                v[4] = f[0]; v[5] = f[1]; v[6] = f[2]; v[7] = f[3];
+            } else {
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) v[q] = (Acc)e[q];
+            }
+            l += w[u];
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) o[q] = fma(w[u], v[q], o[q]);
+        }
     }
+    // fold the RPW row groups of the warp onto lanes 0..LPR-1
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+        l += __shfl_xor_sync(KVT_FULL, l, off);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) o[q] += __shfl_xor_sync(KVT_FULL, o[q], off);
+    }
+    if (lane < LPR) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) red_o[warp][lane * VPL + q] = o[q];
+    }
+    if (lane == 0) red_l[warp] = l;
+    __syncthreads();
+    double* P = part + ((int64_t)li * splits + s) * (d + 2);
+    for (int j = threadIdx.x; j < d; j += ATTN_THREADS) {
+        Acc acc = 0;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) acc += red_o[w][j];
+        P[2 + j] = (double)acc;
+    }
+    if (threadIdx.x == 0) {
+        Acc ls = 0;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) ls += red_l[w];
+        P[0] = m;
+        P[1] = (double)ls;
+    }
+    attn_finish(part, splits, d, li, tickets, out, out64);
 }
 
 }  // namespace kvt
@@ -244,8 +375,14 @@ extern "C" int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64
     return kvt_check_launch();
 }
 
+// Workspace: one ticket counter per lane (first, 256 B aligned region), then the partials
+// [n_lanes][splits][d + 2] f64.  The caller zero-fills it once; every call leaves the
+// counters at zero again.
+static inline size_t ticket_bytes(int64_t n_lanes) { return ((size_t)n_lanes * 4 + 255) & ~(size_t)255; }
 extern "C" size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits) {
-    return (size_t)n_lanes * (size_t)(splits < 1 ? 1 : splits) * (size_t)(d + 2) * sizeof(double);
+    if (splits < 1) splits = 1;
+    if (splits > 64) splits = 64;
+    return ticket_bytes(n_lanes) + (size_t)n_lanes * (size_t)splits * (size_t)(d + 2) * sizeof(double);
 }
 
 static inline int agroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <= 512 ? 4 : 0; }
@@ -253,24 +390,38 @@ static inline int agroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <=
 template <typename T, int G, bool VEC>
 static void launch_attn(const void* values, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* sel_tok,
                         const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, double* part,
-                        cudaStream_t st) {
+                        unsigned int* tickets, float* out, double* out64, cudaStream_t st) {
     dim3 grid(splits, (unsigned)n_lanes);
     attn_split_kernel<T, G, VEC><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score,
-                                                                n_sel, sel_stride, splits, part);
+                                                                n_sel, sel_stride, splits, part, tickets, out, out64);
 }
 
 template <typename T>
 static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* sel_tok,
                          const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, double* part,
-                         cudaStream_t st) {
+                         unsigned int* tickets, float* out, double* out64, cudaStream_t st) {
+    const int64_t row = (int64_t)d * sizeof(T);
+    const bool fast = ((uintptr_t)values % 16 == 0) && (lane_stride * (int64_t)sizeof(T)) % 16 == 0 &&
+                      (row == 128 || row == 256 || row == 512);
+    if (fast) {
+        dim3 grid(splits, (unsigned)n_lanes);
+        const int lpr = (int)(row / 16);
+        if (lpr == 8)
+            attn_split16_kernel<T, 8><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64);
+        else if (lpr == 16)
+            attn_split16_kernel<T, 16><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64);
+        else
+            attn_split16_kernel<T, 32><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64);
+        return kvt_check_launch();
+    }
     const bool vec = ((uintptr_t)values % (4 * sizeof(T)) == 0) && d % 4 == 0 && lane_stride % 4 == 0;
     switch (agroups_for(d)) {
 #define KVT_CASE(GG)                                                                                                   \
     case GG:                                                                                                           \
         if (vec) launch_attn<T, GG, true>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride,     \
-                                          splits, part, st);                                                           \
+                                          splits, part, tickets, out, out64, st);                                      \
         else launch_attn<T, GG, false>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, \
-                                       part, st);                                                                      \
+                                       part, tickets, out, out64, st);                                                 \
         break;
         KVT_CASE(1) KVT_CASE(2) KVT_CASE(4)
 #undef KVT_CASE
@@ -288,17 +439,17 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 65535) return KVT_ERR_ARG;
     if (splits < 1) splits = 1;
+    if (splits > 64) splits = 64;
     cudaStream_t st = (cudaStream_t)stream;
-    double* part = (double*)ws;
+    unsigned int* tickets = (unsigned int*)ws;
+    double* part = (double*)((char*)ws + ticket_bytes(n_lanes));
     int rc;
     switch (v_dtype) {
-        case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
-        case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
-        case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
-        case KVT_F16: rc = dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, st); break;
+        case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
+        case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
+        case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
+        case KVT_F16: rc = dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
         default: return KVT_ERR_DTYPE;
     }
-    if (rc != KVT_OK) return rc;
-    attn_merge_kernel<<<(unsigned)n_lanes, 128, 0, st>>>(part, splits, d, out, out64);
-    return kvt_check_launch();
+    return rc;
 }

@@ -79,11 +79,184 @@ __global__ void __launch_bounds__(SCORE_THREADS) score_kernel(
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// TMA-pipelined variant (sm_100a): persistent CTAs walk the flattened (lane, item) list;
+// one producer thread streams each 64-token item (a contiguous run of key rows) into a
+// shared-memory ring with cp.async.bulk + mbarrier transaction counts, 8 consumer warps
+// score 8 tokens each per item straight from shared memory.  Bytes in flight per CTA =
+// stages x tile (64 KB for bf16 d=128), independent of the consumers' dependency chains.
+// ------------------------------------------------------------------------------------------
+
+constexpr int TS_CONSUMERS = 8;
+constexpr int TS_THREADS = (TS_CONSUMERS + 1) * 32;
+
+template <typename QT, typename T, int G, bool IMPLICIT>
+__global__ void __launch_bounds__(TS_THREADS) score_tma_kernel(
+    const QT* __restrict__ q, const T* __restrict__ keys, int64_t lane_stride, int d, int n_lanes,
+    const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items, int64_t n_implicit,
+    double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride, int stages,
+    int tile_bytes) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ long long scan_sh[33];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * tile_bytes);
+    uint64_t* empty = full + stages;
+    int4* meta = reinterpret_cast<int4*>(empty + stages);  // per stage: lane, t0, cnt, pos0
+    int32_t* lane_off = reinterpret_cast<int32_t*>(meta + stages);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // prefix of per-lane item counts (the flattened work list)
+    long long carry = 0;
+    for (int base = 0; base < n_lanes; base += TS_THREADS) {
+        const int i = base + tid;
+        long long v = 0;
+        if (i < n_lanes) v = IMPLICIT ? (n_implicit + 63) / 64 : (long long)n_items[i];
+        long long tot;
+        const long long ex = block_excl_scan<long long>(v, scan_sh, tot);
+        if (i < n_lanes) lane_off[i] = (int32_t)(carry + ex);
+        carry += tot;
+    }
+    if (tid == 0) {
+        lane_off[n_lanes] = (int32_t)carry;
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TS_CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t total = lane_off[n_lanes];
+    // contiguous block of the flattened list per CTA: the lane (and its query) changes rarely
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t g_begin = kvt::imin(total, (int64_t)blockIdx.x * per);
+    const int64_t g_end = kvt::imin(total, g_begin + per);
+
+    if (warp == TS_CONSUMERS) {  // ---- producer ----
+        if (lane == 0) {
+            int cur = 0;
+            int64_t i = 0;
+            for (int64_t g = g_begin; g < g_end; ++g, ++i) {
+                while (g >= lane_off[cur + 1]) ++cur;
+                const int64_t it = g - lane_off[cur];
+                int64_t t0, cnt;
+                if (IMPLICIT) { t0 = it * 64; cnt = kvt::imin(64, n_implicit - t0); }
+                else { const int32_t* m = items + ((int64_t)cur * item_stride + it) * 3; t0 = m[0]; cnt = m[1]; }
+                const int s = (int)(i % stages);
+                const int64_t r = i / stages;
+                if (r > 0) mbar_wait(&empty[s], (uint32_t)((r - 1) & 1));
+                const uint32_t bytes = (uint32_t)(cnt * d * (int64_t)sizeof(T));
+                int pos0;
+                if (IMPLICIT) pos0 = (int)t0;
+                else pos0 = items[((int64_t)cur * item_stride + it) * 3 + 2];
+                meta[s] = make_int4(cur, (int)t0, (int)cnt, pos0);
+                mbar_arrive_expect_tx(&full[s], bytes);
+                bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)cur * lane_stride + t0 * d, bytes, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---- consumers ----
+    const double sd = sqrt((double)d);
+    int cur = -1;
+    double qr[G][4];
+    int64_t i = 0;
+    for (int64_t g = g_begin; g < g_end; ++g, ++i) {
+        const int s = (int)(i % stages);
+        mbar_wait(&full[s], (uint32_t)((i / stages) & 1));
+        const int4 mt = meta[s];
+        if (mt.x != cur) {
+            cur = mt.x;
+#pragma unroll
+            for (int r = 0; r < G; ++r)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = 4 * (lane + 32 * r) + e;
+                    qr[r][e] = j < d ? (double)q[(int64_t)cur * d + j] : 0.0;
+                }
+        }
+        const int64_t t0 = mt.y, cnt = mt.z, pos0 = mt.w;
+        const T* tile = reinterpret_cast<const T*>(smem + (size_t)s * tile_bytes);
+        const int base_t = 8 * warp;
+        if (base_t < cnt) {
+            double p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                double acc = 0.0;
+                if (base_t + u < cnt) {
+                    const T* row = tile + (int64_t)(base_t + u) * d;
+#pragma unroll
+                    for (int r = 0; r < G; ++r) {
+                        const int gg = lane + 32 * r;
+                        if (4 * gg < d) {
+                            double v[4];
+                            lds4<T>(row + 4 * gg, v);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (4 * gg + e < d) acc = fma(qr[r][e], v[e], acc);
+                        }
+                    }
+                }
+                p[u] = acc;
+            }
+            const double dot = tree_8tok(p, lane);
+            const int t = (lane >> 2) & 7;
+            if ((lane & 3) == 0 && base_t + t < cnt) {
+                double* os = out_score + (int64_t)cur * out_stride;
+                os[pos0 + base_t + t] = dot / sd;
+                if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + base_t + t] = (int32_t)(t0 + base_t + t);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
 }  // namespace kvt
 
 using namespace kvt;
 
 static inline int sgroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <= 512 ? 4 : d <= 1024 ? 8 : 0; }
+
+static int g_sms = 0;
+static int sm_count() {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_sms <= 0)
+            g_sms = 148;
+    }
+    return g_sms;
+}
+
+// TMA path eligibility: whole-row bulk copies need 16 B aligned rows and lane bases.
+template <typename T>
+static bool tma_ok(const void* keys, int64_t lane_stride, int d, int64_t n_lanes) {
+    const int64_t row = (int64_t)d * sizeof(T);
+    return d % 4 == 0 && d <= 1024 && row % 16 == 0 && ((uintptr_t)keys % 16) == 0 &&
+           (lane_stride * (int64_t)sizeof(T)) % 16 == 0 && 64 * row * 2 <= 160 * 1024 && n_lanes <= 16384;
+}
+
+template <typename QT, typename T, int G, bool IMPL>
+static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
+                            const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
+                            double* os, int32_t* ot, int64_t ostr, cudaStream_t st) {
+    const int tile = 64 * d * (int)sizeof(T);
+    int stages = (int)kvt::imin(4, (160 * 1024) / tile);
+    if (stages < 2) stages = 2;
+    const size_t smem = (size_t)stages * tile + 32 * (size_t)stages + 4 * (size_t)(n_lanes + 1) + 16;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(score_tma_kernel<QT, T, G, IMPL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return kvt_set_cuda_error(e);
+        configured = 200 * 1024;
+    }
+    const int grid = sm_count() * (smem <= 100 * 1024 ? 2 : 1);
+    score_tma_kernel<QT, T, G, IMPL><<<grid, TS_THREADS, smem, st>>>(
+        (const QT*)q, (const T*)keys, lane_stride, d, (int)n_lanes, items, item_stride, n_items, n_impl, os, ot,
+        ostr, stages, tile);
+    return kvt_check_launch();
+}
 
 template <typename QT, typename T, int G, bool VEC, bool IMPL>
 static void launch_score(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
@@ -98,6 +271,13 @@ template <typename QT, typename T, bool IMPL>
 static int dispatch_score_t(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
                             const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
                             double* os, int32_t* ot, int64_t ostr, int blocks, cudaStream_t st) {
+    if (tma_ok<T>(keys, lane_stride, d, n_lanes)) {
+        switch (sgroups_for(d)) {
+            case 1: return launch_score_tma<QT, T, 1, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, st);
+            case 2: return launch_score_tma<QT, T, 2, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, st);
+            default: break;
+        }
+    }
     const bool vec = ((uintptr_t)keys % (4 * sizeof(T)) == 0) && d % 4 == 0 && lane_stride % 4 == 0;
     switch (sgroups_for(d)) {
 #define KVT_CASE(GG)                                                                                                  \

@@ -23,7 +23,8 @@ constexpr int SEL_MAX_CLUSTER = 8;
 
 struct SelShared {
     unsigned int hist[2][256];
-    unsigned int cnt_gt, cnt_eq;  // per-CTA counts published to the cluster
+    unsigned int tot[256];
+    unsigned int cnt_gt, cnt_eq, cnt_heads;  // per-CTA counts published to the cluster
     long long scan_sh[33];
     unsigned long long prefix, mask;
     unsigned int remaining;
@@ -33,7 +34,8 @@ struct SelShared {
 __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
     const double* __restrict__ cand_score, const int32_t* __restrict__ cand_tok, const int32_t* __restrict__ n_cand,
     int64_t cand_stride, int64_t k, int32_t* __restrict__ sel_tok, double* __restrict__ sel_score, int64_t sel_stride,
-    int32_t* __restrict__ n_sel, int slice_cap) {
+    int32_t* __restrict__ n_sel, int slice_cap, int32_t* __restrict__ run_start, int32_t* __restrict__ run_len,
+    int64_t run_stride, int32_t* __restrict__ n_runs) {
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ SelShared S;
     cg::cluster_group cluster = cg::this_cluster();
@@ -76,20 +78,20 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
             if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&h[digit], (unsigned)__popc(peers));
         }
         cluster.sync();
-        // every CTA sums all CTAs' histograms (DSMEM) and picks the same digit
+        // every CTA sums all CTAs' histograms (DSMEM): one bin per thread, CL remote loads each
+        for (int b = tid; b < 256; b += SEL_THREADS) {
+            unsigned int acc = 0;
+            for (unsigned r = 0; r < CL; ++r) acc += cluster.map_shared_rank(S.hist[buf], r)[b];
+            S.tot[b] = acc;
+        }
+        __syncthreads();
         if (tid < 32) {
             unsigned int loc[8];
             unsigned int lsum = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int b = 255 - 8 * lane - i;
-                unsigned int s = 0;
-                for (unsigned r = 0; r < CL; ++r) {
-                    const unsigned int* rh = cluster.map_shared_rank(S.hist[buf], r);
-                    s += rh[b];
-                }
-                loc[i] = s;
-                lsum += s;
+                loc[i] = S.tot[255 - 8 * lane - i];
+                lsum += loc[i];
             }
             const unsigned int inc = warp_incl_scan(lsum, lane);
             const unsigned int exc = inc - lsum;
@@ -161,6 +163,46 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
         }
     }
     if (rank == 0 && tid == 0) n_sel[li] = (int32_t)kk;
+    if (run_start && any) {
+        // ---- fused K6: runs of consecutive selected tokens (engine.py:176-183) ----
+        // this thread's output positions are [p0, p1) (its selected elements, in order)
+        int32_t* otok = sel_tok + li * sel_stride;
+        const long long p0 = out_base + ex_gt + min(ex_eq, eq_take);
+        long long taken_eq = max(0LL, min(ex_eq + neq, eq_take) - min(ex_eq, eq_take));
+        const long long p1 = p0 + ngt + taken_eq;
+        cluster.sync();  // every selected token of the lane is now visible (cluster-scope acq/rel)
+        long long heads = 0;
+        for (long long p = p0; p < p1; ++p) heads += (p == 0 || otok[p] != otok[p - 1] + 1);
+        long long tot_h;
+        const long long ex_h = block_excl_scan<long long>(heads, S.scan_sh, tot_h);
+        if (tid == 0) S.cnt_heads = (unsigned)tot_h;
+        cluster.sync();
+        long long run_base = 0, all_runs = 0;
+        for (unsigned r = 0; r < CL; ++r) {
+            const long long h = cluster.map_shared_rank(&S, r)->cnt_heads;
+            if (r < rank) run_base += h;
+            all_runs += h;
+        }
+        int32_t* rs = run_start + li * run_stride;
+        int32_t* rl = run_len + li * run_stride;
+        long long ridx = run_base + ex_h - 1;
+        for (long long p = p0; p < p1; ++p) {
+            if (p == 0 || otok[p] != otok[p - 1] + 1) {
+                ++ridx;
+                rs[ridx] = otok[p];
+                rl[ridx] = (int32_t)p;  // first position; turned into a length below
+            }
+        }
+        cluster.sync();
+        ridx = run_base + ex_h - 1;
+        for (long long p = p0; p < p1; ++p) {
+            if (p == 0 || otok[p] != otok[p - 1] + 1) ++ridx;
+            if (p == kk - 1 || otok[p + 1] != otok[p] + 1) rl[ridx] = (int32_t)(p + 1 - rl[ridx]);
+        }
+        if (rank == 0 && tid == 0) n_runs[li] = (int32_t)all_runs;
+    } else if (run_start && rank == 0 && tid == 0) {
+        n_runs[li] = 0;
+    }
     cluster.sync();  // keep this CTA's shared memory alive until all DSMEM reads are done
 }
 
@@ -171,9 +213,10 @@ using namespace kvt;
 static int g_sel_smem_cap_set = 0;
 constexpr int SEL_SLICE_CAP = 20480;  // 160 KB of staged keys per CTA
 
-extern "C" int kvt_topk_select(const double* cand_score, const int32_t* cand_tok, const int32_t* n_cand,
-                               int64_t cand_stride, int64_t n_lanes, int64_t k, int32_t* sel_tok, double* sel_score,
-                               int64_t sel_stride, int32_t* n_sel, void* stream) {
+extern "C" int kvt_topk_select_runs(const double* cand_score, const int32_t* cand_tok, const int32_t* n_cand,
+                         int64_t cand_stride, int64_t n_lanes, int64_t k, int32_t* sel_tok, double* sel_score,
+                         int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len, int64_t run_stride,
+                         int32_t* n_runs, void* stream) {
     if (!cand_score || !cand_tok || !n_cand || !sel_tok || !sel_score || !n_sel || n_lanes < 0) return KVT_ERR_ARG;
     if (k < 0) return KVT_ERR_K;
     if (n_lanes == 0) return KVT_OK;
@@ -202,7 +245,14 @@ extern "C" int kvt_topk_select(const double* cand_score, const int32_t* cand_tok
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, topk_select_kernel, cand_score, cand_tok, n_cand, cand_stride, k, sel_tok,
-                                       sel_score, sel_stride, n_sel, cap);
+                                       sel_score, sel_stride, n_sel, cap, run_start, run_len, run_stride, n_runs);
     if (e != cudaSuccess) return kvt_set_cuda_error(e);
     return kvt_check_launch();
+}
+
+extern "C" int kvt_topk_select(const double* cand_score, const int32_t* cand_tok, const int32_t* n_cand,
+                               int64_t cand_stride, int64_t n_lanes, int64_t k, int32_t* sel_tok, double* sel_score,
+                               int64_t sel_stride, int32_t* n_sel, void* stream) {
+    return kvt_topk_select_runs(cand_score, cand_tok, n_cand, cand_stride, n_lanes, k, sel_tok, sel_score, sel_stride,
+                                n_sel, nullptr, nullptr, 0, nullptr, stream);
 }

@@ -176,15 +176,25 @@ def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_p
     return cs, ct
 
 
-def topk_select(cs: torch.Tensor, ct: torch.Tensor, n_cand: torch.Tensor, k: int):
-    """Exact top-k (score desc, token asc) -> (sel_tok i32 [n_lanes,k] ascending, sel_score f64, n_sel)."""
+def topk_select(cs: torch.Tensor, ct: torch.Tensor, n_cand: torch.Tensor, k: int, want_runs: bool = False):
+    """Exact top-k (score desc, token asc) -> (sel_tok i32 [n_lanes,k] ascending, sel_score f64, n_sel)
+    [+ dict(run_start, run_len, n_runs) from the fused run scan]."""
     nl = cs.shape[0]
     dev = cs.device
     st = torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev)
     ss = torch.empty((nl, max(k, 1)), dtype=torch.float64, device=dev)
     ns = torch.empty(nl, dtype=torch.int32, device=dev)
-    L.check(L.kvt_topk_select(cs.data_ptr(), ct.data_ptr(), n_cand.data_ptr(), cs.stride(0), nl, k, st.data_ptr(),
-                              ss.data_ptr(), st.stride(0), ns.data_ptr(), _stream()), "topk_select")
+    runs = None
+    if want_runs:
+        runs = {"run_start": torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev),
+                "run_len": torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev),
+                "n_runs": torch.empty(nl, dtype=torch.int32, device=dev)}
+    L.check(L.kvt_topk_select_runs(cs.data_ptr(), ct.data_ptr(), n_cand.data_ptr(), cs.stride(0), nl, k,
+                                   st.data_ptr(), ss.data_ptr(), st.stride(0), ns.data_ptr(),
+                                   _p(runs["run_start"]) if runs else None, _p(runs["run_len"]) if runs else None,
+                                   st.stride(0), _p(runs["n_runs"]) if runs else None, _stream()), "topk_select")
+    if want_runs:
+        return st[:, :k], ss[:, :k], ns, runs
     return st[:, :k], ss[:, :k], ns
 
 
@@ -223,7 +233,7 @@ def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: t
     k = sel_tok.shape[1]
     if splits <= 0:
         splits = auto_splits(nl, k)
-    ws = torch.empty(max(1, L.kvt_attn_workspace_bytes(nl, d, splits)), dtype=torch.uint8, device=values.device)
+    ws = torch.zeros(max(1, L.kvt_attn_workspace_bytes(nl, d, splits)), dtype=torch.uint8, device=values.device)
     out = torch.empty((nl, d), dtype=torch.float32, device=values.device)
     out64 = torch.empty((nl, d), dtype=torch.float64, device=values.device) if want_f64 else None
     st = _nz(sel_tok)
@@ -243,7 +253,7 @@ class LayerWorkspace:
 
     def __init__(self, n_lanes: int, n_cap: int, max_leaves: int, d: int, device):
         self.bytes = int(L.kvt_layer_workspace_bytes(n_lanes, n_cap, max_leaves, d))
-        self.buf = torch.empty(self.bytes, dtype=torch.uint8, device=device)
+        self.buf = torch.zeros(self.bytes, dtype=torch.uint8, device=device)  # attn tickets start at 0
         self.key = (n_lanes, n_cap, max_leaves, d)
 
 
