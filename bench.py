@@ -47,7 +47,7 @@ N_LAYERS, N_HEADS, HEAD_DIM = 32, 32, 128  # LLaMA-7B attention shape
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--batch", type=int, default=1, help="batch rows per GPU")
@@ -128,7 +128,7 @@ def make_queries(torch, u, steps, data, gen):
 
 
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -139,11 +139,16 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(1.0)  # let the sampler come up before the timed region starts
         except OSError:
             self.p = None
         return self
+
+    def mark(self, tag):
+        """Timestamps bracketing the timed region; samples outside are discarded."""
+        setattr(self, tag, time.time())
 
     def __exit__(self, *a):
         self.lines = []
@@ -157,22 +162,31 @@ class ClockSampler:
             self.lines = [x for x in out.splitlines() if x.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        """Median SM clock and active throttle reasons over the samples taken inside
+        [t0, t1] (the timed region, host wall clock); all samples if none fall inside."""
+        import datetime as _dt
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in getattr(self, "lines", []):
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                ts = _dt.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        inside = [r for r in rows if t0 is not None and t0 - 0.05 <= r[0] <= t1 + 0.05]
+        use = inside or rows
+        reasons = set()
+        for r in use:
+            for nm, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = [r[1] for r in use]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": use[0][2] if use else None,
+                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside)}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -328,6 +342,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
+        clk.mark("t0")
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for s in range(args.steps):
@@ -336,6 +351,7 @@ def run_ours(args):
             ev1.record(stream)
         ev1.synchronize()
         torch.cuda.synchronize()
+        clk.mark("t1")
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     clocks = clk.summary()
@@ -404,7 +420,7 @@ def run_ours(args):
                 elif name == "select":
                     ops.topk_select(cs, ct, plan["n_cand"], k, want_runs=True)
                 elif name == "attn":
-                    ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)
+                    ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)  # logit_scale 1/sqrt(d): raw dots
         return run
 
     st_ms = {}

@@ -74,11 +74,13 @@ KVT_API int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_str
  * Leaves of lane i: if leaf_start == NULL the uniform grid of size C over [0, n)
  * (n_leaves = ceil(n/C)); otherwise leaf j = [leaf_start[i*leaf_stride + j],
  * leaf_start[i*leaf_stride + j + 1]) for j < n_leaves[i] (the last end is n).
- * q: [n_lanes][d] of q_dtype (F32 or F64).  U/L: float64 at U + i*bnd_stride + j. */
+ * q: [n_lanes][d] of q_dtype (F32 or F64).  U/L: float64 at U + i*bnd_stride + j.
+ * scaled != 0: bounds on the logits fl(q.k)/fl(sqrt d) (the importance.py form);
+ * scaled == 0: bounds on the raw canonical dots (what the pipeline prunes with). */
 KVT_API int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int d, int64_t n, int C,
                      const int32_t* leaf_start, const int32_t* n_leaves, int64_t leaf_stride,
                      const void* amax, const void* amin, int abs_dtype, int64_t abs_lane_stride,
-                     double* U, double* L, int64_t bnd_stride, void* stream);
+                     double* U, double* L, int64_t bnd_stride, int scaled, void* stream);
 
 /* ---- K4 (brute force): canonical token logits -----------------------------------------
  * Replaces importance.py:27-33 attention_logits / :46-53 score_tokens (logit mode) for
@@ -101,9 +103,11 @@ KVT_API int kvt_select_plan(int64_t n_lanes, int64_t n, int C, const int32_t* le
                     void* stream);
 
 /* ---- K4: candidate scoring -------------------------------------------------------------
- * Canonical float64 logits of every candidate token (the exact-score half of
- * select_top_k: singleton bounds, chunk_tree.py:291-296,321).  Writes cand_score
- * [i*cand_stride + pos] and cand_tok (token index) for pos < n_cand[i]. */
+ * Raw canonical float64 dots q.k of every candidate token (the exact-score half of
+ * select_top_k: singleton bounds, chunk_tree.py:291-296,321; logit = dot / sqrt d is a
+ * monotone map, so the order is the reference's).  Writes cand_score [i*cand_stride + pos]
+ * and cand_tok (token index) for pos < n_cand[i].  Items are streamed through a
+ * cp.async.bulk (TMA engine) shared-memory ring by persistent CTAs. */
 KVT_API int kvt_cand_score(const void* q, int q_dtype, const void* keys, int key_dtype,
                    int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,
                    int64_t item_stride, const int32_t* n_items, double* cand_score,
@@ -139,7 +143,9 @@ KVT_API int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t 
 
 /* ---- K7: sparse decode attention -----------------------------------------------------------
  * engine.py:145-154 attention_output over the selected set: softmax(sel_score) @ V[sel].
- * sel_score are the canonical logits from K5 (keys are not re-read).  Split over
+ * sel_score are the scores from K5 (keys are not re-read); the softmax logit of token i is
+ * (sel_score_i - max) * logit_scale, i.e. logit_scale = 1/sqrt(d) for raw dots and 1 for
+ * logits.  Split over
  * `splits` blocks per lane with an online-softmax (m, l, o) merge.  out: float32
  * [n_lanes][d] (out64: optional float64 copy).  ws: workspace of
  * kvt_attn_workspace_bytes(n_lanes, d, splits) bytes, zero-filled once by the caller (the
@@ -148,8 +154,8 @@ KVT_API int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t 
 KVT_API size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits);
 KVT_API int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride,
                            int d, const int32_t* sel_tok, const double* sel_score,
-                           const int32_t* n_sel, int64_t sel_stride, int splits, void* ws,
-                           float* out, double* out64, void* stream);
+                           const int32_t* n_sel, int64_t sel_stride, double logit_scale, int splits,
+                           void* ws, float* out, double* out64, void* stream);
 
 /* ---- fused per-layer pipeline -----------------------------------------------------------------
  * K3 -> plan -> K4 -> K5 -> K6 -> K7 for n_lanes lanes on the uniform grid C (or the

@@ -67,6 +67,12 @@ ORA_API double ora_dot(const double* q, const double* k, int d) {
 
 ORA_API double ora_sqrt_d(int d) { return sqrt((double)d); }
 
+/* Raw canonical dots: the selection key of the B200 pipeline (a positive scale does not
+ * change the order; the logit fl(dot)/fl(sqrt d) is only formed for the softmax). */
+ORA_API void ora_dots(const double* q, const double* keys, int64_t n, int d, double* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = ora_dot(q, keys + i * (int64_t)d, d);
+}
+
 /* importance.py:27-33 attention_logits, canonical order */
 ORA_API void ora_scores(const double* q, const double* keys, int64_t n, int d, double* out) {
     double s = sqrt((double)d);
@@ -92,8 +98,8 @@ ORA_API double ora_bound_slack_factor(int d) { return (double)(2 * chain_len(d) 
 
 /* importance.py:108-137 bound_chunk / bound_chunks_batch (logit mode), sound canonical form.
  * rows[i] = number of real tokens summarised by abstract i (1 => exact, no widening). */
-ORA_API void ora_bounds(const double* q, const double* mx, const double* mn, int64_t m, int d,
-                        const int64_t* rows, double* U, double* L) {
+ORA_API void ora_bounds2(const double* q, const double* mx, const double* mn, int64_t m, int d,
+                         const int64_t* rows, double* U, double* L, int scaled) {
     double s = sqrt((double)d);
     double fac = ora_bound_slack_factor(d);
     for (int64_t c = 0; c < m; ++c) {
@@ -116,9 +122,14 @@ ORA_API void ora_bounds(const double* q, const double* mx, const double* mn, int
             u = u + slack;
             lo = lo - slack;
         }
-        U[c] = u / s;
-        L[c] = lo / s;
+        U[c] = scaled ? u / s : u;
+        L[c] = scaled ? lo / s : lo;
     }
+}
+
+ORA_API void ora_bounds(const double* q, const double* mx, const double* mn, int64_t m, int d,
+                        const int64_t* rows, double* U, double* L) {
+    ora_bounds2(q, mx, mn, m, d, rows, U, L, 1);
 }
 
 /* ------------------------------------------------------------------------------------ */

@@ -50,6 +50,8 @@ def lib():
         L.ora_dot.restype = ctypes.c_double
         L.ora_dot.argtypes = [_dp, _dp, ctypes.c_int]
         L.ora_scores.argtypes = [_dp, _dp, _i64, ctypes.c_int, _dp]
+        L.ora_dots.argtypes = [_dp, _dp, _i64, ctypes.c_int, _dp]
+        L.ora_bounds2.argtypes = [_dp, _dp, _dp, _i64, ctypes.c_int, _ip, _dp, _dp, ctypes.c_int]
         L.ora_abstract.argtypes = [_dp, ctypes.c_int, _i64, _i64, _dp, _dp]
         L.ora_bound_slack_factor.restype = ctypes.c_double
         L.ora_bound_slack_factor.argtypes = [ctypes.c_int]
@@ -102,6 +104,16 @@ def scores(query, keys) -> np.ndarray:
     return out
 
 
+def dots(query, keys) -> np.ndarray:
+    """Raw canonical dots q.k (the B200 pipeline's selection key; logits = dots / sqrt d)."""
+    q, k = _f64(query), _f64(keys)
+    if k.ndim != 2 or q.ndim != 1 or k.shape[1] != q.shape[0]:
+        raise ValueError(f"shape mismatch: keys {k.shape} vs query {q.shape}")
+    out = np.empty(k.shape[0], dtype=np.float64)
+    lib().ora_dots(_p(q), _p(k), k.shape[0], q.shape[0], _p(out))
+    return out
+
+
 def abstract(keys, start: int = 0, end: int | None = None) -> tuple[np.ndarray, np.ndarray]:
     """(max_key, min_key) of keys[start:end) (importance.py:80-87)."""
     k = _f64(keys)
@@ -114,15 +126,16 @@ def abstract(keys, start: int = 0, end: int | None = None) -> tuple[np.ndarray, 
     return mx, mn
 
 
-def bounds(query, max_keys, min_keys, rows=None) -> tuple[np.ndarray, np.ndarray]:
-    """Sound canonical (U, L) per abstract row (importance.py:108-137)."""
+def bounds(query, max_keys, min_keys, rows=None, scaled: bool = True) -> tuple[np.ndarray, np.ndarray]:
+    """Sound canonical (U, L) per abstract row (importance.py:108-137); scaled=False gives the
+    raw (unscaled) bounds the B200 pipeline prunes with."""
     q, M, N = _f64(query), _f64(max_keys), _f64(min_keys)
     if M.ndim == 1:
         M, N = M[None, :], N[None, :]
     m, d = M.shape
     U, L = np.empty(m), np.empty(m)
     r = None if rows is None else np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
-    lib().ora_bounds(_p(q), _p(M), _p(N), m, d, None if r is None else _p(r, _ip), _p(U), _p(L))
+    lib().ora_bounds2(_p(q), _p(M), _p(N), m, d, None if r is None else _p(r, _ip), _p(U), _p(L), int(scaled))
     return U, L
 
 
@@ -155,8 +168,8 @@ def topk(score_vec, k: int) -> np.ndarray:
 
 
 def select(query, keys, k: int) -> np.ndarray:
-    """Brute-force exact top-k (canonical scores), ascending indices."""
-    return topk(scores(query, keys), k)
+    """Brute-force exact top-k by canonical dot (score desc, index asc), ascending indices."""
+    return topk(dots(query, keys), k)
 
 
 def runs(sel) -> list[tuple[int, int]]:

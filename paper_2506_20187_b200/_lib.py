@@ -65,7 +65,7 @@ kvt_abstract_build = _sig("kvt_abstract_build", ctypes.c_int, _vp, _i32, _i64, _
 kvt_abstract_spans = _sig("kvt_abstract_spans", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _vp,
                           _vp)
 kvt_chunk_bounds = _sig("kvt_chunk_bounds", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _i32, _vp, _vp, _i64, _vp,
-                        _vp, _i32, _i64, _vp, _vp, _i64, _vp)
+                        _vp, _i32, _i64, _vp, _vp, _i64, _i32, _vp)
 kvt_token_scores = _sig("kvt_token_scores", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i64,
                         _vp)
 kvt_select_plan = _sig("kvt_select_plan", ctypes.c_int, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
@@ -79,7 +79,7 @@ kvt_runs_scan = _sig("kvt_runs_scan", ctypes.c_int, _vp, _vp, _i64, _i64, _i64, 
                      _vp, _vp)
 kvt_attn_workspace_bytes = _sig("kvt_attn_workspace_bytes", _sz, _i64, _i32, _i32)
 kvt_sparse_decode_attn = _sig("kvt_sparse_decode_attn", ctypes.c_int, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp,
-                              _i64, _i32, _vp, _vp, _vp, _vp)
+                              _i64, ctypes.c_double, _i32, _vp, _vp, _vp, _vp)
 kvt_layer_workspace_bytes = _sig("kvt_layer_workspace_bytes", _sz, _i64, _i64, _i64, _i32)
 kvt_select_attend = _sig("kvt_select_attend", ctypes.c_int, ctypes.POINTER(KvtLayerArgs), _vp, _sz, _vp)
 

@@ -269,9 +269,11 @@ def select_top_k(partition: Partition, query: np.ndarray, k: int, store: ChunkSo
     U, L, plan = _bounds_plan(q, amax_a, amin_a, starts_a, n, k)
     result.eval_count += len(live)
     cand_a = plan["cand_leaf"][0, :len(live)].cpu().numpy().astype(bool)
+    # the pipeline prunes on raw dots; the leaf attributes keep kvtier's logit scale
+    sd = math.sqrt(q.shape[0])
     Uh, Lh = U[0, :len(live)].cpu().numpy(), L[0, :len(live)].cpu().numpy()
     for c, u, l in zip(live, Uh, Lh):
-        c.upper, c.lower = float(u), float(l)
+        c.upper, c.lower = float(u) / sd, float(l) / sd
 
     # ---- level B: refine wide candidate leaves on the base grid ----
     bs = dev["base_size"]
@@ -358,7 +360,7 @@ def _rebuild(partition: Partition, sel_tok, sel_score, n_sel, k: int) -> None:
     # per-leaf score bounds of important runs: exact extremes of their logits
     nr = int(runs["n_runs"][0].item())
     rlen = runs["run_len"][0, :nr].cpu().numpy().astype(np.int64)
-    sc = sel_score[0].cpu().numpy()
+    sc = sel_score[0].cpu().numpy() / math.sqrt(dev["base_max"].shape[1])  # raw dots -> logits
     run_hi, run_lo, pos = [], [], 0
     for ln in rlen:
         seg = sc[pos:pos + ln]

@@ -130,17 +130,18 @@ __global__ void __launch_bounds__(256) abstract_spans_kernel(
 // ------------------------------------------------------------------------------------------
 
 template <typename QT, typename AT, int G>
-__global__ void __launch_bounds__(256) bounds_kernel(
+__global__ void __launch_bounds__(256, 3) bounds_kernel(
     const QT* __restrict__ q, int d, int64_t n, int C, const int32_t* __restrict__ leaf_start,
     const int32_t* __restrict__ n_leaves, int64_t leaf_stride, const AT* __restrict__ amax,
     const AT* __restrict__ amin, int64_t abs_lane_stride, double* __restrict__ U,
-    double* __restrict__ L, int64_t bnd_stride) {
-    // 8 chunks per warp step: 16 independent 16 B abstract loads in flight per lane, then
-    // three reduce-scatter trees (U, L, A) leave chunk (lane >> 2) & 7 on each lane quad.
+    double* __restrict__ L, int64_t bnd_stride, int scaled) {
+    // 4 chunks per warp step: 8 independent 16 B abstract loads in flight per lane, then
+    // three reduce-scatter trees (U, L, A) leave chunk (lane >> 3) & 3 on each lane octet.
+    // Outputs are raw (unscaled) bounds unless `scaled` (the importance.py API form).
     const int lane = threadIdx.x & 31;
     const int64_t lane_i = blockIdx.y;
     const int64_t nl = leaf_start ? (int64_t)n_leaves[lane_i] : (n + C - 1) / C;
-    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5) * 8;
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5) * 4;
     double qr[G][4];
 #pragma unroll
     for (int r = 0; r < G; ++r)
@@ -154,10 +155,10 @@ __global__ void __launch_bounds__(256) bounds_kernel(
     const AT* mxb = amax + lane_i * abs_lane_stride;
     const AT* mnb = amin + lane_i * abs_lane_stride;
     const int32_t* ls = leaf_start ? leaf_start + lane_i * leaf_stride : nullptr;
-    for (int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; c0 < nl; c0 += wstride) {
-        double pu[8], pl[8], pa[8];
+    for (int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; c0 < nl; c0 += wstride) {
+        double pu[4], pl[4], pa[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
             pu[u] = 0.0; pl[u] = 0.0; pa[u] = 0.0;
             const int64_t c = c0 + u;
             if (c < nl) {
@@ -193,10 +194,10 @@ __global__ void __launch_bounds__(256) bounds_kernel(
                 }
             }
         }
-        double u_ = tree_8tok(pu, lane), l_ = tree_8tok(pl, lane), a_ = tree_8tok(pa, lane);
-        const int t = (lane >> 2) & 7;
+        double u_ = tree_4tok(pu, lane), l_ = tree_4tok(pl, lane), a_ = tree_4tok(pa, lane);
+        const int t = (lane >> 3) & 3;
         const int64_t c = c0 + t;
-        if ((lane & 3) == 0 && c < nl) {
+        if ((lane & 7) == 0 && c < nl) {
             int64_t rows;
             if (ls) rows = ((c + 1 < nl) ? (int64_t)ls[c + 1] : n) - ls[c];
             else rows = kvt::imin((int64_t)C, n - c * C);
@@ -205,8 +206,8 @@ __global__ void __launch_bounds__(256) bounds_kernel(
                 u_ = u_ + slack;
                 l_ = l_ - slack;
             }
-            U[lane_i * bnd_stride + c] = u_ / sd;
-            L[lane_i * bnd_stride + c] = l_ / sd;
+            U[lane_i * bnd_stride + c] = scaled ? u_ / sd : u_;
+            L[lane_i * bnd_stride + c] = scaled ? l_ / sd : l_;
         }
     }
 }
@@ -311,21 +312,21 @@ extern "C" int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_
 template <typename QT, typename AT, int G>
 static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                           const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
-                          double* U, double* L, int64_t bs, int64_t max_leaves, cudaStream_t st) {
-    int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 63) / 64, 1024));
+                          double* U, double* L, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
+    int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 31) / 32, 1024));
     // keep ~8 CTAs per SM in total when lanes are few
     dim3 grid(gx, (unsigned)n_lanes);
     bounds_kernel<QT, AT, G><<<grid, 256, 0, st>>>((const QT*)q, d, n, C, ls, nl, lstr, (const AT*)amax,
-                                                   (const AT*)amin, als, U, L, bs);
+                                                   (const AT*)amin, als, U, L, bs, scaled);
 }
 
 template <typename QT, typename AT>
 static int dispatch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                            const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
-                           double* U, double* L, int64_t bs, int64_t max_leaves, cudaStream_t st) {
+                           double* U, double* L, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
     switch (groups_for(d)) {
 #define KVT_CASE(GG) \
-    case GG: launch_bounds<QT, AT, GG>(q, n_lanes, d, n, C, ls, nl, lstr, amax, amin, als, U, L, bs, max_leaves, st); break;
+    case GG: launch_bounds<QT, AT, GG>(q, n_lanes, d, n, C, ls, nl, lstr, amax, amin, als, U, L, bs, max_leaves, scaled, st); break;
         KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
 #undef KVT_CASE
         default: return KVT_ERR_SHAPE;
@@ -336,7 +337,7 @@ static int dispatch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int
 extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int d, int64_t n, int C,
                                 const int32_t* leaf_start, const int32_t* n_leaves, int64_t leaf_stride,
                                 const void* amax, const void* amin, int abs_dtype, int64_t abs_lane_stride, double* U,
-                                double* L, int64_t bnd_stride, void* stream) {
+                                double* L, int64_t bnd_stride, int scaled, void* stream) {
     if (!q || !amax || !amin || !U || !L || d < 1 || n < 0 || n_lanes < 0) return KVT_ERR_ARG;
     if (!leaf_start && C < 1) return KVT_ERR_ARG;
     if (leaf_start && !n_leaves) return KVT_ERR_ARG;
@@ -345,12 +346,12 @@ extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
     cudaStream_t st = (cudaStream_t)stream;
     if (q_dtype == KVT_F32 && abs_dtype == KVT_F32)
-        return dispatch_bounds<float, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+        return dispatch_bounds<float, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F64 && abs_dtype == KVT_F32)
-        return dispatch_bounds<double, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+        return dispatch_bounds<double, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F32 && abs_dtype == KVT_F64)
-        return dispatch_bounds<float, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+        return dispatch_bounds<float, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F64 && abs_dtype == KVT_F64)
-        return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, st);
+        return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
     return KVT_ERR_DTYPE;
 }

@@ -108,7 +108,7 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     const int64_t item_cap = (a->n + ITEM_TOKENS - 1) / ITEM_TOKENS + max_leaves;
     int rc;
     rc = kvt_chunk_bounds(a->q, a->q_dtype, a->n_lanes, a->d, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride,
-                          a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L, max_leaves, stream);
+                          a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L, max_leaves, 0, stream);
     if (rc) return rc;
     rc = kvt_select_plan(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L, max_leaves,
                          a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals, stream);
@@ -129,14 +129,15 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     if (a->out && a->values) {
         int splits = a->attn_splits;
         if (splits <= 0) {
-            const int64_t target = (int64_t)num_sms() * 6;
+            const int64_t target = (int64_t)num_sms() * 3;  // one wave of 3 CTAs per SM
             const int64_t per_lane = (target + a->n_lanes - 1) / a->n_lanes;
             const int64_t need = (a->k + 255) / 256;
             splits = (int)kvt::imax(1, kvt::imin(kvt::imin(per_lane, need), MAX_SPLITS));
         }
         if (splits > MAX_SPLITS) splits = MAX_SPLITS;
         rc = kvt_sparse_decode_attn(a->values, a->v_dtype, a->n_lanes, a->lane_stride, a->d, a->sel_tok, a->sel_score,
-                                    a->n_sel, a->k, splits, w.attn_part, a->out, nullptr, stream);
+                                    a->n_sel, a->k, 1.0 / sqrt((double)a->d), splits, w.attn_part, a->out, nullptr,
+                                    stream);
         if (rc) return rc;
     }
     return KVT_OK;

@@ -175,6 +175,30 @@ __device__ __forceinline__ double tree_8tok(double p[8], int lane) {
     return v;
 }
 
+// Same for 4 partials: lane L ends with the full dot of item (L >> 3) & 3.
+__device__ __forceinline__ double tree_4tok(double p[4], int lane) {
+    {
+        const bool b = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            double send = b ? p[i] : p[2 + i];
+            double keep = b ? p[2 + i] : p[i];
+            p[i] = keep + __shfl_xor_sync(KVT_FULL, send, 16);
+        }
+    }
+    {
+        const bool b = lane & 8;
+        double send = b ? p[0] : p[1];
+        double keep = b ? p[1] : p[0];
+        p[0] = keep + __shfl_xor_sync(KVT_FULL, send, 8);
+    }
+    double v = p[0];
+    v = v + __shfl_xor_sync(KVT_FULL, v, 4);
+    v = v + __shfl_xor_sync(KVT_FULL, v, 2);
+    v = v + __shfl_xor_sync(KVT_FULL, v, 1);
+    return v;
+}
+
 // Chain length (<= 4*ceil(d/128)) + tree depth; the soundness widening factor.
 __host__ __device__ __forceinline__ int chain_len(int d) { return 4 * ((d + 127) / 128) + 5; }
 __host__ __device__ __forceinline__ double slack_factor(int d) {

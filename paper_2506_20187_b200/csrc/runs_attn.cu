@@ -10,7 +10,8 @@
 // the selected tokens are gathered (ascending token order => runs are contiguous rows and
 // each 128-dim bf16 row is one coalesced 256 B warp load).  Flash-decoding split: each CTA
 // reduces a slice of the selected set to (m, l, o[d]) with f32 accumulation (f64 for f64
-// values), a merge kernel rescales and combines the slices.  HBM-bound on k*d*s_V.
+// values); the last split CTA of each lane (atomic ticket) rescales and combines the
+// slices, so attention is one launch.  HBM-bound on k*d*s_V.
 #include "common.cuh"
 
 namespace kvt {
@@ -93,6 +94,13 @@ constexpr int ATTN_WARPS = ATTN_THREADS / 32;
 template <typename T> struct AccOf { using type = float; };
 template <> struct AccOf<double> { using type = double; };
 
+// softmax weight exp(x) of a (scaled, <= 0) logit difference, in the accumulation precision
+template <typename Acc> __device__ __forceinline__ Acc softmax_w(double x);
+template <> __device__ __forceinline__ float softmax_w<float>(double x) {
+    return exp2f((float)(x * 1.4426950408889634));
+}
+template <> __device__ __forceinline__ double softmax_w<double>(double x) { return exp(x); }
+
 template <typename T, bool VEC>
 __device__ __forceinline__ void load_group_acc(const T* row, int g, int d, typename AccOf<T>::type v[4]) {
     const int j0 = 4 * g;
@@ -110,7 +118,7 @@ __device__ __forceinline__ void load_group_acc(const T* row, int g, int d, typen
 // for the next call without a memset.
 __device__ __forceinline__ void attn_finish(double* __restrict__ part, int splits, int d, int64_t li,
                                             unsigned int* __restrict__ tickets, float* __restrict__ out,
-                                            double* __restrict__ out64) {
+                                            double* __restrict__ out64, double scale) {
     __shared__ int s_last;
     __shared__ double s_scale[64];
     __shared__ double s_M, s_den;
@@ -133,7 +141,7 @@ __device__ __forceinline__ void attn_finish(double* __restrict__ part, int split
         double den = 0.0;
         for (int s = threadIdx.x; s < splits; s += 32) {
             const double ls = __ldcg(P + s * (d + 2) + 1);
-            const double sc = ls > 0 ? exp(__ldcg(P + s * (d + 2)) - M) : 0.0;
+            const double sc = ls > 0 ? exp((__ldcg(P + s * (d + 2)) - M) * scale) : 0.0;
             s_scale[s] = sc;
             den += sc * ls;
         }
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
     const T* __restrict__ values, int64_t lane_stride, int d, const int32_t* __restrict__ sel_tok,
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
-    double* __restrict__ out64) {
+    double* __restrict__ out64, double scale) {
     using Acc = typename AccOf<T>::type;
     __shared__ double red_m[ATTN_WARPS];
     __shared__ Acc red_o[ATTN_WARPS][4 * 32 * G];
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
                 if (4 * g < d) load_group_acc<T, VEC>(row, g, d, v[u][r]);
                 else { v[u][r][0] = v[u][r][1] = v[u][r][2] = v[u][r][3] = 0; }
             }
-            w[u] = (Acc)exp(sc[ii] - m);
+            w[u] = softmax_w<Acc>((sc[ii] - m) * scale);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
     }
     for (; i < b; i += ATTN_WARPS) {
         const T* row = base + (int64_t)tok[i] * d;
-        const Acc w = (Acc)exp(sc[i] - m);
+        const Acc w = softmax_w<Acc>((sc[i] - m) * scale);
         l += w;
 #pragma unroll
         for (int r = 0; r < G; ++r) {
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split_kernel(
         P[0] = m;
         P[1] = (double)ls;
     }
-    attn_finish(part, splits, d, li, tickets, out, out64);
+    attn_finish(part, splits, d, li, tickets, out, out64, scale);
 }
 
 // Fast path: 16 B per lane per load, a row spans LPR = d*sizeof(T)/16 lanes, a warp
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split16_kernel(
     const T* __restrict__ values, int64_t lane_stride, int d, const int32_t* __restrict__ sel_tok,
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
-    double* __restrict__ out64) {
+    double* __restrict__ out64, double scale) {
     using Acc = typename AccOf<T>::type;
     constexpr int VPL = 16 / sizeof(T);
     constexpr int RPW = 32 / LPR;
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split16_kernel(
             const int64_t i = i0 + (int64_t)u * STEP;
             if (i < b) {
                 raw[u] = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)tok[i] * d));
-                w[u] = (Acc)exp(sc[i] - m);
+                w[u] = softmax_w<Acc>((sc[i] - m) * scale);
             } else {
                 raw[u] = make_uint4(0, 0, 0, 0);
                 w[u] = 0;
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split16_kernel(
         P[0] = m;
         P[1] = (double)ls;
     }
-    attn_finish(part, splits, d, li, tickets, out, out64);
+    attn_finish(part, splits, d, li, tickets, out, out64, scale);
 }
 
 }  // namespace kvt
@@ -390,16 +398,16 @@ static inline int agroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <=
 template <typename T, int G, bool VEC>
 static void launch_attn(const void* values, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* sel_tok,
                         const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, double* part,
-                        unsigned int* tickets, float* out, double* out64, cudaStream_t st) {
+                        unsigned int* tickets, float* out, double* out64, double scale, cudaStream_t st) {
     dim3 grid(splits, (unsigned)n_lanes);
     attn_split_kernel<T, G, VEC><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score,
-                                                                n_sel, sel_stride, splits, part, tickets, out, out64);
+                                                                n_sel, sel_stride, splits, part, tickets, out, out64, scale);
 }
 
 template <typename T>
 static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* sel_tok,
                          const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, double* part,
-                         unsigned int* tickets, float* out, double* out64, cudaStream_t st) {
+                         unsigned int* tickets, float* out, double* out64, double scale, cudaStream_t st) {
     const int64_t row = (int64_t)d * sizeof(T);
     const bool fast = ((uintptr_t)values % 16 == 0) && (lane_stride * (int64_t)sizeof(T)) % 16 == 0 &&
                       (row == 128 || row == 256 || row == 512);
@@ -407,11 +415,11 @@ static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_strid
         dim3 grid(splits, (unsigned)n_lanes);
         const int lpr = (int)(row / 16);
         if (lpr == 8)
-            attn_split16_kernel<T, 8><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64);
+            attn_split16_kernel<T, 8><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, scale);
         else if (lpr == 16)
-            attn_split16_kernel<T, 16><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64);
+            attn_split16_kernel<T, 16><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, scale);
         else
-            attn_split16_kernel<T, 32><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64);
+            attn_split16_kernel<T, 32><<<grid, ATTN_THREADS, 0, st>>>((const T*)values, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, scale);
         return kvt_check_launch();
     }
     const bool vec = ((uintptr_t)values % (4 * sizeof(T)) == 0) && d % 4 == 0 && lane_stride % 4 == 0;
@@ -419,9 +427,9 @@ static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_strid
 #define KVT_CASE(GG)                                                                                                   \
     case GG:                                                                                                           \
         if (vec) launch_attn<T, GG, true>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride,     \
-                                          splits, part, tickets, out, out64, st);                                      \
+                                          splits, part, tickets, out, out64, scale, st);                               \
         else launch_attn<T, GG, false>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, \
-                                       part, tickets, out, out64, st);                                                 \
+                                       part, tickets, out, out64, scale, st);                                          \
         break;
         KVT_CASE(1) KVT_CASE(2) KVT_CASE(4)
 #undef KVT_CASE
@@ -432,8 +440,8 @@ static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_strid
 
 extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride, int d,
                                       const int32_t* sel_tok, const double* sel_score, const int32_t* n_sel,
-                                      int64_t sel_stride, int splits, void* ws, float* out, double* out64,
-                                      void* stream) {
+                                      int64_t sel_stride, double logit_scale, int splits, void* ws, float* out,
+                                      double* out64, void* stream) {
     if (!values || !sel_tok || !sel_score || !n_sel || !ws || (!out && !out64) || d < 1 || n_lanes < 0)
         return KVT_ERR_ARG;
     if (n_lanes == 0) return KVT_OK;
@@ -445,10 +453,10 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
     double* part = (double*)((char*)ws + ticket_bytes(n_lanes));
     int rc;
     switch (v_dtype) {
-        case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
-        case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
-        case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
-        case KVT_F16: rc = dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, st); break;
+        case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
+        case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
+        case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
+        case KVT_F16: rc = dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
         default: return KVT_ERR_DTYPE;
     }
     return rc;

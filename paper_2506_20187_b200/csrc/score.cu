@@ -1,7 +1,8 @@
 // score.cu -- K4 canonical float64 token logits (candidate tokens, or all tokens).
 //
 // Replaces importance.py:27-33 attention_logits (k.q / sqrt d) for the tokens the plan
-// kept.  A warp scores 8 tokens per step: each lane loads its 4-dim group of the 8 rows
+// kept.  The pipeline keeps raw canonical dots (the 1/sqrt d scale does not change the
+// order and is applied inside the softmax of K7); kvt_token_scores returns fl(dot)/fl(sqrt d).  A warp scores 8 tokens per step: each lane loads its 4-dim group of the 8 rows
 // (8 independent 64/128-bit loads in flight per lane; a 128-dim bf16 row is one coalesced
 // 256 B warp access), runs its f64 fma chains, and a reduce-scatter butterfly
 // (tree_8tok: 9 f64 shuffles per 8 tokens instead of 40) yields the canonical dot of
@@ -16,7 +17,8 @@ template <typename QT, typename T, int G, bool VEC, bool IMPLICIT>
 __global__ void __launch_bounds__(SCORE_THREADS) score_kernel(
     const QT* __restrict__ q, const T* __restrict__ keys, int64_t lane_stride, int d,
     const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items,
-    int64_t n_implicit, double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride) {
+    int64_t n_implicit, double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride,
+    int scaled) {
     const int lane = threadIdx.x & 31;
     const int64_t li = blockIdx.y;
     double qr[G][4];
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(SCORE_THREADS) score_kernel(
             const double dot = tree_8tok(p, lane);
             const int t = (lane >> 2) & 7;
             if ((lane & 3) == 0 && g8 + t < cnt) {
-                os[pos0 + g8 + t] = dot / sd;
+                os[pos0 + g8 + t] = scaled ? dot / sd : dot;
                 if (ot) ot[pos0 + g8 + t] = (int32_t)(t0 + g8 + t);
             }
         }
@@ -91,11 +93,11 @@ constexpr int TS_CONSUMERS = 8;
 constexpr int TS_THREADS = (TS_CONSUMERS + 1) * 32;
 
 template <typename QT, typename T, int G, bool IMPLICIT>
-__global__ void __launch_bounds__(TS_THREADS) score_tma_kernel(
+__global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const QT* __restrict__ q, const T* __restrict__ keys, int64_t lane_stride, int d, int n_lanes,
     const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items, int64_t n_implicit,
     double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride, int stages,
-    int tile_bytes) {
+    int tile_bytes, int scaled) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ long long scan_sh[33];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * tile_bytes);
@@ -179,30 +181,47 @@ __global__ void __launch_bounds__(TS_THREADS) score_tma_kernel(
         const int base_t = 8 * warp;
         if (base_t < cnt) {
             double p[8];
+            const T* rows = tile + (int64_t)base_t * d;
+            if (base_t + 8 <= cnt && d == 128 * G) {
+                // full group of 8 tokens, d a multiple of 128: no bounds checks
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                double acc = 0.0;
-                if (base_t + u < cnt) {
-                    const T* row = tile + (int64_t)(base_t + u) * d;
+                for (int u = 0; u < 8; ++u) {
+                    double acc = 0.0;
 #pragma unroll
                     for (int r = 0; r < G; ++r) {
-                        const int gg = lane + 32 * r;
-                        if (4 * gg < d) {
-                            double v[4];
-                            lds4<T>(row + 4 * gg, v);
+                        double v[4];
+                        lds4<T>(rows + (int64_t)u * d + 4 * (lane + 32 * r), v);
 #pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                if (4 * gg + e < d) acc = fma(qr[r][e], v[e], acc);
+                        for (int e = 0; e < 4; ++e) acc = fma(qr[r][e], v[e], acc);
+                    }
+                    p[u] = acc;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    double acc = 0.0;
+                    if (base_t + u < cnt) {
+                        const T* row = rows + (int64_t)u * d;
+#pragma unroll
+                        for (int r = 0; r < G; ++r) {
+                            const int gg = lane + 32 * r;
+                            if (4 * gg < d) {
+                                double v[4];
+                                lds4<T>(row + 4 * gg, v);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    if (4 * gg + e < d) acc = fma(qr[r][e], v[e], acc);
+                            }
                         }
                     }
+                    p[u] = acc;
                 }
-                p[u] = acc;
             }
             const double dot = tree_8tok(p, lane);
             const int t = (lane >> 2) & 7;
             if ((lane & 3) == 0 && base_t + t < cnt) {
                 double* os = out_score + (int64_t)cur * out_stride;
-                os[pos0 + base_t + t] = dot / sd;
+                os[pos0 + base_t + t] = scaled ? dot / sd : dot;
                 if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + base_t + t] = (int32_t)(t0 + base_t + t);
             }
         }
@@ -239,9 +258,9 @@ static bool tma_ok(const void* keys, int64_t lane_stride, int d, int64_t n_lanes
 template <typename QT, typename T, int G, bool IMPL>
 static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
                             const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
-                            double* os, int32_t* ot, int64_t ostr, cudaStream_t st) {
+                            double* os, int32_t* ot, int64_t ostr, int scaled, cudaStream_t st) {
     const int tile = 64 * d * (int)sizeof(T);
-    int stages = (int)kvt::imin(4, (160 * 1024) / tile);
+    int stages = (int)kvt::imin(3, (150 * 1024) / tile);
     if (stages < 2) stages = 2;
     const size_t smem = (size_t)stages * tile + 32 * (size_t)stages + 4 * (size_t)(n_lanes + 1) + 16;
     static size_t configured = 0;
@@ -251,30 +270,31 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = 200 * 1024;
     }
-    const int grid = sm_count() * (smem <= 100 * 1024 ? 2 : 1);
+    const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
+    const int grid = sm_count() * per_sm;
     score_tma_kernel<QT, T, G, IMPL><<<grid, TS_THREADS, smem, st>>>(
         (const QT*)q, (const T*)keys, lane_stride, d, (int)n_lanes, items, item_stride, n_items, n_impl, os, ot,
-        ostr, stages, tile);
+        ostr, stages, tile, scaled);
     return kvt_check_launch();
 }
 
 template <typename QT, typename T, int G, bool VEC, bool IMPL>
 static void launch_score(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
                          const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
-                         double* os, int32_t* ot, int64_t ostr, int blocks, cudaStream_t st) {
+                         double* os, int32_t* ot, int64_t ostr, int blocks, int scaled, cudaStream_t st) {
     dim3 grid(blocks, (unsigned)n_lanes);
     score_kernel<QT, T, G, VEC, IMPL><<<grid, SCORE_THREADS, 0, st>>>(
-        (const QT*)q, (const T*)keys, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr);
+        (const QT*)q, (const T*)keys, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled);
 }
 
 template <typename QT, typename T, bool IMPL>
 static int dispatch_score_t(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
                             const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
-                            double* os, int32_t* ot, int64_t ostr, int blocks, cudaStream_t st) {
+                            double* os, int32_t* ot, int64_t ostr, int blocks, int scaled, cudaStream_t st) {
     if (tma_ok<T>(keys, lane_stride, d, n_lanes)) {
         switch (sgroups_for(d)) {
-            case 1: return launch_score_tma<QT, T, 1, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, st);
-            case 2: return launch_score_tma<QT, T, 2, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, st);
+            case 1: return launch_score_tma<QT, T, 1, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled, st);
+            case 2: return launch_score_tma<QT, T, 2, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled, st);
             default: break;
         }
     }
@@ -283,9 +303,9 @@ static int dispatch_score_t(const void* q, const void* keys, int64_t n_lanes, in
 #define KVT_CASE(GG)                                                                                                  \
     case GG:                                                                                                          \
         if (vec) launch_score<QT, T, GG, true, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items,  \
-                                                     n_impl, os, ot, ostr, blocks, st);                                \
+                                                     n_impl, os, ot, ostr, blocks, scaled, st);                                \
         else launch_score<QT, T, GG, false, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items,     \
-                                                  n_impl, os, ot, ostr, blocks, st);                                   \
+                                                  n_impl, os, ot, ostr, blocks, scaled, st);                                   \
         break;
         KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
 #undef KVT_CASE
@@ -298,9 +318,9 @@ template <bool IMPL>
 static int dispatch_score(const void* q, int q_dtype, const void* keys, int key_dtype, int64_t n_lanes,
                           int64_t lane_stride, int d, const int32_t* items, int64_t item_stride,
                           const int32_t* n_items, int64_t n_impl, double* os, int32_t* ot, int64_t ostr, int blocks,
-                          cudaStream_t st) {
+                          int scaled, cudaStream_t st) {
 #define KVT_K(QT, TT) \
-    return dispatch_score_t<QT, TT, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, blocks, st)
+    return dispatch_score_t<QT, TT, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, blocks, scaled, st)
     if (q_dtype == KVT_F32) {
         switch (key_dtype) {
             case KVT_F32: KVT_K(float, float);
@@ -329,7 +349,7 @@ extern "C" int kvt_cand_score(const void* q, int q_dtype, const void* keys, int 
     if (n_lanes > 65535) return KVT_ERR_ARG;
     if (blocks_per_lane < 1) blocks_per_lane = 1;
     return dispatch_score<false>(q, q_dtype, keys, key_dtype, n_lanes, lane_stride, d, items, item_stride, n_items,
-                                 0, cand_score, cand_tok, cand_stride, blocks_per_lane, (cudaStream_t)stream);
+                                 0, cand_score, cand_tok, cand_stride, blocks_per_lane, 0, (cudaStream_t)stream);
 }
 
 extern "C" int kvt_token_scores(const void* q, int q_dtype, const void* keys, int key_dtype, int64_t n_lanes,
@@ -341,5 +361,5 @@ extern "C" int kvt_token_scores(const void* q, int q_dtype, const void* keys, in
     int blocks = (int)kvt::imin((items + 7) / 8, kvt::imax(1, 2048 / n_lanes));
     if (blocks < 1) blocks = 1;
     return dispatch_score<true>(q, q_dtype, keys, key_dtype, n_lanes, lane_stride, d, nullptr, 0, nullptr, n, out,
-                                nullptr, out_stride, blocks, (cudaStream_t)stream);
+                                nullptr, out_stride, blocks, 1, (cudaStream_t)stream);
 }

@@ -21,7 +21,12 @@ namespace kvt {
 constexpr int SEL_THREADS = 512;
 constexpr int SEL_MAX_CLUSTER = 8;
 
+constexpr int SEL_LIST_CAP = 4096;  // survivors of the first 3 passes, scanned instead of the slice
+
 struct SelShared {
+    unsigned short list[SEL_LIST_CAP];
+    unsigned int list_n;
+    int list_ok;
     unsigned int hist[2][256];
     unsigned int tot[256];
     unsigned int cnt_gt, cnt_eq, cnt_heads;  // per-CTA counts published to the cluster
@@ -55,7 +60,7 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
 
     if (staged)
         for (int64_t i = tid; i < cnt; i += SEL_THREADS) keys[i] = ord_key(sc[i]);
-    if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)kk; S.done = (kk <= 0); }
+    if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)kk; S.done = (kk <= 0); S.list_ok = 0; S.list_n = 0; }
     __syncthreads();
 
     auto key_at = [&](int64_t i) -> uint64_t { return staged ? keys[i] : ord_key(sc[i]); };
@@ -67,10 +72,13 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
         for (int i = tid; i < 256; i += SEL_THREADS) h[i] = 0;
         __syncthreads();
         const unsigned long long prefix = S.prefix, mask = S.mask;
-        for (int64_t base = 0; base < cnt; base += SEL_THREADS) {
-            const int64_t i = base + tid;
+        const bool use_list = S.list_ok;
+        const int64_t span = use_list ? (int64_t)S.list_n : cnt;
+        for (int64_t base = 0; base < span; base += SEL_THREADS) {
+            const int64_t j = base + tid;
             int digit = 256;
-            if (i < cnt) {
+            if (j < span) {
+                const int64_t i = use_list ? (int64_t)S.list[j] : j;
                 const uint64_t key = key_at(i);
                 if ((key & mask) == prefix) digit = (int)((key >> shift) & 0xff);
             }
@@ -114,6 +122,25 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
         }
         __syncthreads();
         buf ^= 1;
+        // after the 3rd pass the surviving bucket is small: gather its members once
+        if (shift == 40 && !S.done && staged && cnt <= 65535) {
+            const unsigned long long pf = S.prefix, mk = S.mask;
+            for (int64_t base = 0; base < cnt; base += SEL_THREADS) {
+                const int64_t i = base + tid;
+                const bool m = i < cnt && (keys[i] & mk) == pf;
+                const unsigned ballot = __ballot_sync(KVT_FULL, m);
+                unsigned wbase = 0;
+                if (lane == 0 && ballot) wbase = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
+                wbase = __shfl_sync(KVT_FULL, wbase, 0);
+                if (m) {
+                    const unsigned slot = wbase + __popc(ballot & ((1u << lane) - 1));
+                    if (slot < SEL_LIST_CAP) S.list[slot] = (unsigned short)i;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) S.list_ok = S.list_n <= SEL_LIST_CAP;
+            __syncthreads();
+        }
     }
 
     // ---- compaction: key&mask > prefix, or == prefix and among the first `remaining` ----

@@ -42,7 +42,7 @@ def attention_output(query: np.ndarray, keys: np.ndarray, values: np.ndarray) ->
     logits = ops.token_scores(qd, kd, n)                                   # K4
     sel = torch.arange(n, dtype=torch.int32, device=qd.device)[None]
     ns = torch.tensor([n], dtype=torch.int32, device=qd.device)
-    out, out64 = ops.sparse_decode_attn(vd, sel, logits.contiguous(), ns, want_f64=True)   # K7
+    out, out64 = ops.sparse_decode_attn(vd, sel, logits.contiguous(), ns, want_f64=True, logit_scale=1.0)  # K7
     return out64[0].cpu().numpy()
 
 

@@ -105,8 +105,10 @@ def abstract_spans(keys: torch.Tensor, lane_of: torch.Tensor, starts: torch.Tens
 
 
 def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int, C: int = 0,
-                 leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None):
-    """Sound canonical (U, L) per leaf (importance.py:108-137) -> float64 [n_lanes, max_leaves]."""
+                 leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
+                 scaled: bool = False):
+    """Sound canonical (U, L) per leaf (importance.py:108-137) -> float64 [n_lanes, max_leaves].
+    scaled=False: bounds on raw dots (pipeline); scaled=True: on logits dot/sqrt(d) (API)."""
     require_cuda(q, amax, amin)
     nl, d = q.shape
     if leaf_start is not None:
@@ -119,7 +121,7 @@ def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int
     Lo = torch.empty_like(U)
     L.check(L.kvt_chunk_bounds(q.data_ptr(), dtype_code(q), nl, d, n, C, _p(leaf_start), _p(n_leaves), lstride,
                                amax.data_ptr(), amin.data_ptr(), dtype_code(amax), amax.stride(0), U.data_ptr(),
-                               Lo.data_ptr(), U.stride(0), _stream()), "chunk_bounds")
+                               Lo.data_ptr(), U.stride(0), int(scaled), _stream()), "chunk_bounds")
     return U, Lo
 
 
@@ -162,7 +164,7 @@ def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
 
 
 def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_per_lane: int = 0):
-    """Canonical logits of candidate tokens -> (cand_score f64 [n_lanes, n], cand_tok i32)."""
+    """Raw canonical dots of candidate tokens -> (cand_score f64 [n_lanes, n], cand_tok i32)."""
     require_cuda(q, keys)
     ls, d = _lanes(keys)
     nl = keys.shape[0]
@@ -220,13 +222,14 @@ def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition
 
 
 def auto_splits(n_lanes: int, k: int) -> int:
-    target = 148 * 6
+    target = 148 * 3
     return max(1, min((target + n_lanes - 1) // n_lanes, (k + 255) // 256, 64))
 
 
 def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor,
-                       splits: int = 0, want_f64: bool = False):
-    """softmax(sel_score) @ V[sel] (engine.py:145-154) -> out f32 [n_lanes, d] (and f64)."""
+                       splits: int = 0, want_f64: bool = False, logit_scale: float | None = None):
+    """softmax(sel_score * logit_scale) @ V[sel] (engine.py:145-154) -> out f32 [n_lanes, d] (and f64).
+    logit_scale defaults to 1/sqrt(d) (sel_score = raw dots from K4/K5); pass 1.0 for logits."""
     require_cuda(values)
     ls, d = _lanes(values)
     nl = values.shape[0]
@@ -239,9 +242,11 @@ def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: t
     st = _nz(sel_tok)
     ss = _nz(sel_score)
     sstride = sel_tok.shape[1] if k > 0 else 1
+    if logit_scale is None:
+        logit_scale = 1.0 / math.sqrt(d)
     L.check(L.kvt_sparse_decode_attn(values.data_ptr(), dtype_code(values), nl, ls, d, st.data_ptr(), ss.data_ptr(),
-                                     n_sel.data_ptr(), sstride, splits, ws.data_ptr(), out.data_ptr(), _p(out64),
-                                     _stream()), "sparse_decode_attn")
+                                     n_sel.data_ptr(), sstride, float(logit_scale), splits, ws.data_ptr(),
+                                     out.data_ptr(), _p(out64), _stream()), "sparse_decode_attn")
     return (out, out64) if want_f64 else out
 
 

@@ -57,7 +57,8 @@ def test_abstracts_and_bounds_bitexact(ops, dt, d, C):
     q = rng.normal(size=(lanes, d)) * rng.choice([0.1, 1.0, 10.0])
     q[:, 0] = 0.0
     amax, amin = ops.abstract_build(kt, n, C)
-    U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, n, C)
+    U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, n, C, scaled=True)
+    Ur_raw, Lr_raw = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, n, C)
     m = ops.n_grid_leaves(n, C)
     for i in range(lanes):
         mx = np.stack([kh[i, c * C:(c + 1) * C].max(0) for c in range(m)])
@@ -72,6 +73,13 @@ def test_abstracts_and_bounds_bitexact(ops, dt, d, C):
         for c in range(m):
             seg = s[c * C:(c + 1) * C]
             assert Lr[c] <= seg.min() and seg.max() <= Ur[c]  # sound for canonical logits
+        Ur2, Lr2 = O.bounds(q[i], mx, mn, rows, scaled=False)
+        assert np.array_equal(Ur_raw[i, :m].cpu().numpy(), Ur2)
+        assert np.array_equal(Lr_raw[i, :m].cpu().numpy(), Lr2)
+        dd = O.dots(q[i], kh[i])
+        for c in range(m):
+            seg = dd[c * C:(c + 1) * C]
+            assert Lr2[c] <= seg.min() and seg.max() <= Ur2[c]  # sound for raw canonical dots
 
 
 def test_bound_soundness_c02(ops):
@@ -86,7 +94,7 @@ def test_bound_soundness_c02(ops):
         q[rng.random(lanes) < 0.05] = 0.0
         kt = torch.from_numpy(k).cuda()
         amax, amin = ops.abstract_build(kt, C, C)
-        U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, C, C)
+        U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, C, C, scaled=True)
         s = ops.token_scores(torch.from_numpy(q).cuda(), kt, C).cpu().numpy()
         assert np.all(L[:, 0].cpu().numpy() <= s.min(1))
         assert np.all(s.max(1) <= U[:, 0].cpu().numpy())
@@ -137,7 +145,7 @@ def test_fused_select_attend_matches_oracle(ops, kind, dt, n, C, rate):
     Vh = vt.double().cpu().numpy()
     tol = 2e-3 if dt == "f32" else 1e-2
     for i in range(lanes):
-        s = O.scores(Q[i], Kh[i])
+        s = O.dots(Q[i], Kh[i])
         ref = O.topk(s, k)
         got = out["sel_tok"][i].cpu().numpy().astype(np.int64)
         assert np.array_equal(got, ref), (kind, dt, n, i)
