@@ -53,7 +53,8 @@ def parse():
     p.add_argument("--batch", type=int, default=1, help="batch rows per GPU")
     p.add_argument("--ctx", type=int, default=65536)
     p.add_argument("--data", choices=["planted", "random"], default="planted")
-    p.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
+    p.add_argument("--dtype", choices=["bf16", "f32", "int4"], default="bf16",
+                   help="KV storage: bf16/f32 rows or INT4 records (K8 compression, config 3)")
     p.add_argument("--layers", type=int, default=N_LAYERS)
     p.add_argument("--cpu-lanes", type=int, default=16, help="lanes in the CPU baseline sample")
     p.add_argument("--cpu-steps", type=int, default=2)
@@ -297,15 +298,33 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    dt = {"bf16": torch.bfloat16, "f32": torch.float32, "int4": ops.I4}[args.dtype]
     L = args.layers
     dec = SparseDecoder(L, args.batch, N_HEADS, HEAD_DIM, args.ctx, dtype=dt, device=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * args.seed + rank)
     rng = np.random.default_rng([args.seed, rank])
     u = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
-    for l in range(L):
-        fill_layer(torch, dec.K[l], dec.V[l], args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
+    quant_ms = None
+    if args.dtype == "int4":
+        # generate each layer in bf16, then compress it with K8 (timed: prefill compression)
+        kb = torch.empty((dec.lanes, args.ctx, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+        vb = torch.empty_like(kb)
+        qt = 0.0
+        for l in range(L):
+            fill_layer(torch, kb, vb, args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dec.load_layer(l, kb, vb)
+            e1.record()
+            e1.synchronize()
+            qt += e0.elapsed_time(e1)
+        quant_ms = qt
+        del kb, vb
+        torch.cuda.empty_cache()
+    else:
+        for l in range(L):
+            fill_layer(torch, dec.K[l], dec.V[l], args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
     dec.set_length(args.ctx)
     steps_total = args.warmup + args.steps
     Q = make_queries(torch, u, steps_total, args.data, gen)
@@ -457,7 +476,7 @@ def run_ours(args):
         "metric": "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if True else args.dtype,
+        "dtype": "f64",
         "kv_dtype": args.dtype,
         "data": f"synthetic {args.data} KV generated on device (trace.py:270-315 model); no model weights",
         "config": workload_config(args, world),
@@ -470,6 +489,10 @@ def run_ours(args):
         "selection_gather_frac": sel_gather_bytes / (ms_max / 1e3) / 1e9 / hbm_peak,
         "per_kernel": per_kernel,
         "candidate_fraction": float(np.sum(n_cand) / (L * dec.lanes * dec.n)),
+        "kv_compression": None if quant_ms is None else {
+            "codec": "INT4 group-32, fp16 (scale, min), 80 B/token/head vs 256 B bf16",
+            "prefill_quant_ms": quant_ms,
+            "prefill_quant_gbs": (2 * L * dec.lanes * args.ctx * (HEAD_DIM * 2 + 80)) / (quant_ms / 1e3) / 1e9},
         "gpu_launches": launches_per_layer * L * args.steps,
         "clocks": clocks,
         "e2e": e2e,

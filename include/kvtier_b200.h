@@ -44,7 +44,11 @@ typedef enum {
     KVT_ERR_ARG = -7         /* other invalid argument (ValueError) */
 } kvt_status;
 
-typedef enum { KVT_F32 = 0, KVT_F64 = 1, KVT_BF16 = 2, KVT_F16 = 3 } kvt_dtype;
+/* KVT_I4: INT4 KV records produced by kvt_kv_quant -- per token d/2 code bytes (dim 2j in
+ * the low nibble, 2j+1 in the high nibble) then d/32 (scale, min) fp16 pairs; dequantised
+ * value fmaf(code, scale, min).  For KVT_I4 operands lane strides are in BYTES and d must
+ * be a multiple of 128.  Accepted wherever keys/values are read (K1, K4, K7). */
+typedef enum { KVT_F32 = 0, KVT_F64 = 1, KVT_BF16 = 2, KVT_F16 = 3, KVT_I4 = 4 } kvt_dtype;
 
 /* Library version (major*10000 + minor*100 + patch) and status text. */
 KVT_API int kvt_version(void);
@@ -68,6 +72,18 @@ KVT_API int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lanes,
 KVT_API int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_stride, int d,
                        int64_t n_spans, const int32_t* lane_of, const int32_t* starts,
                        const int32_t* ends, void* amax, void* amin, void* stream);
+
+/* ---- K8: INT4 KV compression ------------------------------------------------------------
+ * North-star item 4 (the reference only models compression, pipeline.py:35-57 delta = 0.25,
+ * and has no quantizer): quantise tokens [t_begin, t_end) of every lane from src
+ * (F32/BF16/F16, [n_lanes] x src_lane_stride elements) into INT4 records at
+ * dst + i*dst_lane_stride (bytes) + t*(d/2 + d/8).  Group 32: scale = fp16((max-min)/15),
+ * min = fp16(min), code = clamp(rint((x - min)/scale), 0, 15).  Used at prefill (bulk) and
+ * for every appended token. */
+KVT_API int kvt_kv_quant(const void* src, int src_dtype, int64_t n_lanes, int64_t src_lane_stride,
+                         int64_t t_begin, int64_t t_end, int d, void* dst, int64_t dst_lane_stride,
+                         void* stream);
+KVT_API int kvt_i4_row_bytes(int d);
 
 /* ---- K3: query-vs-abstract bounds ----------------------------------------------------
  * Replaces importance.py:108-137 bound_chunk / bound_chunks_batch (logit mode).

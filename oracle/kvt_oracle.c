@@ -183,6 +183,73 @@ ORA_API void ora_bounds_ref(const double* q, const double* mx, const double* mn,
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* INT4 KV codec (north-star item 4; the reference has no quantizer -- parity of the codes */
+/* is against this definition)                                         */
+/* ------------------------------------------------------------------------------------ */
+/* Record per token: d/2 code bytes (dim 2j in the low nibble, 2j+1 in the high nibble),
+ * then d/32 (scale, min) fp16 pairs.  Per group of 32 dims:
+ *   lo, hi = min, max;  s = fp16(fl32((hi - lo) / 15));  m = fp16(lo)
+ *   code = s == 0 ? 0 : clamp(rint(fl32(fl32(x - m) / s)), 0, 15)
+ *   x^   = fmaf(code, s, m)                                  (one f32 rounding)
+ * Inputs are clamped to the fp16 range first. */
+
+ORA_API int ora_i4_record_bytes(int d) { return d / 2 + (d / 32) * 4; }
+
+static float clamp_h(float x) { return x > 65504.0f ? 65504.0f : (x < -65504.0f ? -65504.0f : x); }
+
+ORA_API void ora_i4_quant(const float* x, int64_t n, int d, uint8_t* rec) {
+    const int rb = ora_i4_record_bytes(d);
+    for (int64_t t = 0; t < n; ++t) {
+        const float* xt = x + t * d;
+        uint8_t* r = rec + t * rb;
+        memset(r, 0, (size_t)rb);
+        for (int g = 0; g < d / 32; ++g) {
+            float lo = clamp_h(xt[32 * g]), hi = lo;
+            for (int j = 1; j < 32; ++j) {
+                float v = clamp_h(xt[32 * g + j]);
+                if (v < lo) lo = v;
+                if (v > hi) hi = v;
+            }
+            volatile float diff = hi - lo;
+            volatile float sf = diff / 15.0f;
+            _Float16 sh = (_Float16)sf, mh = (_Float16)lo;
+            float sc = (float)sh, mn = (float)mh;
+            for (int j = 0; j < 32; ++j) {
+                int c = 0;
+                if (sc != 0.0f) {
+                    volatile float num = clamp_h(xt[32 * g + j]) - mn;
+                    volatile float q = num / sc;
+                    float rq = rintf(q);
+                    c = rq < 0.0f ? 0 : (rq > 15.0f ? 15 : (int)rq);
+                }
+                int dim = 32 * g + j;
+                r[dim >> 1] |= (uint8_t)(c << ((dim & 1) * 4));
+            }
+            memcpy(r + d / 2 + 4 * g, &sh, 2);
+            memcpy(r + d / 2 + 4 * g + 2, &mh, 2);
+        }
+    }
+}
+
+ORA_API void ora_i4_dequant(const uint8_t* rec, int64_t n, int d, float* x) {
+    const int rb = ora_i4_record_bytes(d);
+    for (int64_t t = 0; t < n; ++t) {
+        const uint8_t* r = rec + t * rb;
+        for (int g = 0; g < d / 32; ++g) {
+            _Float16 sh, mh;
+            memcpy(&sh, r + d / 2 + 4 * g, 2);
+            memcpy(&mh, r + d / 2 + 4 * g + 2, 2);
+            float sc = (float)sh, mn = (float)mh;
+            for (int j = 0; j < 32; ++j) {
+                int dim = 32 * g + j;
+                int c = (r[dim >> 1] >> ((dim & 1) * 4)) & 15;
+                x[t * d + dim] = fmaf((float)c, sc, mn);
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* exact top-k (score desc, index asc)                                                   */
 /* ------------------------------------------------------------------------------------ */
 

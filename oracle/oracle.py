@@ -59,6 +59,10 @@ def lib():
         L.ora_np_sum.restype = ctypes.c_double
         L.ora_np_sum.argtypes = [_dp, _i64]
         L.ora_bounds_ref.argtypes = [_dp, _dp, _dp, _i64, ctypes.c_int, _dp, _dp]
+        L.ora_i4_record_bytes.restype = ctypes.c_int
+        L.ora_i4_record_bytes.argtypes = [ctypes.c_int]
+        L.ora_i4_quant.argtypes = [_fp, _i64, ctypes.c_int, ctypes.c_void_p]
+        L.ora_i4_dequant.argtypes = [ctypes.c_void_p, _i64, ctypes.c_int, _fp]
         L.ora_topk.restype = _i64
         L.ora_topk.argtypes = [_dp, _i64, _i64, _ip]
         L.ora_runs.restype = _i64
@@ -157,6 +161,29 @@ def np_sum(a) -> float:
 
 def slack_factor(d: int) -> float:
     return lib().ora_bound_slack_factor(d)
+
+
+def i4_record_bytes(d: int) -> int:
+    return lib().ora_i4_record_bytes(d)
+
+
+def i4_quant(x) -> np.ndarray:
+    """INT4 records [n, d/2 + d/8] (uint8) of f32 rows x [n, d] (DESIGN.md sec. 2 codec)."""
+    X = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    n, d = X.shape
+    if d % 32:
+        raise ValueError("d must be a multiple of 32")
+    rec = np.zeros((n, i4_record_bytes(d)), dtype=np.uint8)
+    lib().ora_i4_quant(_p(X, _fp), n, d, rec.ctypes.data_as(ctypes.c_void_p))
+    return rec
+
+
+def i4_dequant(rec, d: int) -> np.ndarray:
+    R = np.ascontiguousarray(np.asarray(rec, dtype=np.uint8))
+    n = R.shape[0]
+    x = np.empty((n, d), dtype=np.float32)
+    lib().ora_i4_dequant(R.ctypes.data_as(ctypes.c_void_p), n, d, _p(x, _fp))
+    return x
 
 
 def topk(score_vec, k: int) -> np.ndarray:

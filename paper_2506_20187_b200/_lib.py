@@ -27,7 +27,7 @@ _L = ctypes.CDLL(str(LIB_PATH))
 # status codes (kvt_status)
 OK, ERR_SHAPE, ERR_K, ERR_COLD, ERR_OOM, ERR_CUDA, ERR_DTYPE, ERR_ARG = 0, -1, -2, -3, -4, -5, -6, -7
 # dtype codes (kvt_dtype)
-F32, F64, BF16, F16 = 0, 1, 2, 3
+F32, F64, BF16, F16, I4 = 0, 1, 2, 3, 4
 
 _i64, _i32, _vp, _dp, _fp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p
 _sz = ctypes.c_size_t
@@ -80,6 +80,8 @@ kvt_runs_scan = _sig("kvt_runs_scan", ctypes.c_int, _vp, _vp, _i64, _i64, _i64, 
 kvt_attn_workspace_bytes = _sig("kvt_attn_workspace_bytes", _sz, _i64, _i32, _i32)
 kvt_sparse_decode_attn = _sig("kvt_sparse_decode_attn", ctypes.c_int, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp,
                               _i64, ctypes.c_double, _i32, _vp, _vp, _vp, _vp)
+kvt_kv_quant = _sig("kvt_kv_quant", ctypes.c_int, _vp, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _vp)
+kvt_i4_row_bytes = _sig("kvt_i4_row_bytes", ctypes.c_int, _i32)
 kvt_layer_workspace_bytes = _sig("kvt_layer_workspace_bytes", _sz, _i64, _i64, _i64, _i32)
 kvt_select_attend = _sig("kvt_select_attend", ctypes.c_int, ctypes.POINTER(KvtLayerArgs), _vp, _sz, _vp)
 
@@ -88,7 +90,7 @@ EXPORTED = [
     "kvt_chunk_bounds", "kvt_token_scores", "kvt_select_plan", "kvt_cand_score", "kvt_topk_select",
     "kvt_topk_select_runs",
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
-    "kvt_select_attend",
+    "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes",
 ]
 
 

@@ -260,6 +260,7 @@ extern "C" int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lan
     if (n_lanes > 65535) return KVT_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     switch (key_dtype) {
+        case KVT_I4: return kvt_abstract_build_i4(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
         case KVT_F32: return dispatch_abs_grid<float>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
         case KVT_F64: return dispatch_abs_grid<double>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
         case KVT_BF16: return dispatch_abs_grid<__nv_bfloat16>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);

@@ -133,6 +133,41 @@ template <> __device__ __forceinline__ void lds4<__half>(const __half* p, double
 }
 
 // ------------------------------------------------------------------------------------------
+// INT4 KV records (kvt_kv_quant): per token d/2 code bytes (dim 2j low nibble, 2j+1 high
+// nibble) followed by d/32 (scale, min) fp16 pairs; x^ = fmaf(code, scale, min).
+// ------------------------------------------------------------------------------------------
+
+struct I4 {};  // storage tag
+
+__host__ __device__ __forceinline__ int i4_row_bytes(int d) { return d / 2 + (d / 32) * 4; }
+
+__device__ __forceinline__ void i4_dequant4(uint32_t c16, __half2 p, float f[4]) {
+    const float s = __low2float(p), m = __high2float(p);
+    f[0] = __fmaf_rn((float)(c16 & 15u), s, m);
+    f[1] = __fmaf_rn((float)((c16 >> 4) & 15u), s, m);
+    f[2] = __fmaf_rn((float)((c16 >> 8) & 15u), s, m);
+    f[3] = __fmaf_rn((float)((c16 >> 12) & 15u), s, m);
+}
+
+// Row loaders on byte-addressed rows (shared or global memory): dims 4g..4g+3 as f64.
+template <typename T> struct RowLd {
+    __host__ __device__ static int row_bytes(int d) { return d * (int)sizeof(T); }
+    __device__ __forceinline__ static void load(const unsigned char* row, int g, int d, double v[4]) {
+        lds4<T>(reinterpret_cast<const T*>(row) + 4 * g, v);
+    }
+};
+template <> struct RowLd<I4> {
+    __host__ __device__ static int row_bytes(int d) { return i4_row_bytes(d); }
+    __device__ __forceinline__ static void load(const unsigned char* row, int g, int d, double v[4]) {
+        const uint32_t c = *reinterpret_cast<const unsigned short*>(row + 2 * g);
+        const __half2 p = *reinterpret_cast<const __half2*>(row + d / 2 + 4 * (g >> 3));
+        float f[4];
+        i4_dequant4(c, p, f);
+        v[0] = f[0]; v[1] = f[1]; v[2] = f[2]; v[3] = f[3];
+    }
+};
+
+// ------------------------------------------------------------------------------------------
 // canonical reductions
 // ------------------------------------------------------------------------------------------
 
@@ -290,6 +325,11 @@ __device__ __forceinline__ V block_excl_scan(V v, V* sh, V& total) {
 }
 
 }  // namespace kvt
+
+// INT4 K1 (quant.cu)
+int kvt_abstract_build_i4(const void* keys, int64_t n_lanes, int64_t lane_stride_b, int64_t n, int d, int C,
+                          int64_t c_begin, int64_t c_end, void* amax, void* amin, int64_t abs_lane_stride,
+                          cudaStream_t st);
 
 // status plumbing (api.cu)
 int kvt_set_cuda_error(cudaError_t e);

@@ -366,6 +366,107 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_split16_kernel(
     attn_finish(part, splits, d, li, tickets, out, out64, scale);
 }
 
+// INT4 values: a row (record) spans LPR = d/32 lanes, each lane dequantises one 32-dim
+// group (16 B of codes + its (scale, min)) per row; RPW = 32/LPR rows per warp load.
+template <int LPR>
+__global__ void __launch_bounds__(ATTN_THREADS) attn_i4_kernel(
+    const unsigned char* __restrict__ values, int64_t lane_stride_b, int d, const int32_t* __restrict__ sel_tok,
+    const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits,
+    double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
+    double* __restrict__ out64, double scale) {
+    constexpr int RPW = 32 / LPR;
+    constexpr int U = 4;
+    __shared__ double red_m[ATTN_WARPS];
+    __shared__ float red_o[ATTN_WARPS][32 * LPR];
+    __shared__ float red_l[ATTN_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / LPR, grp = lane % LPR;
+    const int rb = i4_row_bytes(d);
+    const int64_t li = blockIdx.y;
+    const int s = blockIdx.x;
+    const int64_t k = n_sel[li];
+    const int64_t per = (k + splits - 1) / splits;
+    const int64_t a = kvt::imin(k, s * per), b = kvt::imin(k, a + per);
+    const int32_t* tok = sel_tok + li * sel_stride;
+    const double* sc = sel_score + li * sel_stride;
+    const unsigned char* base = values + li * lane_stride_b;
+    double m = -INFINITY;
+    for (int64_t i = a + threadIdx.x; i < b; i += ATTN_THREADS) m = fmax(m, sc[i]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(KVT_FULL, m, off));
+    if (lane == 0) red_m[warp] = m;
+    __syncthreads();
+    m = red_m[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_WARPS; ++w) m = fmax(m, red_m[w]);
+
+    float o[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) o[e] = 0.f;
+    float l = 0.f;
+    constexpr int STEP = ATTN_WARPS * RPW;
+    for (int64_t i0 = a + warp * RPW + sub; i0 < b; i0 += (int64_t)U * STEP) {
+        uint4 cw[U];
+        uint32_t pw[U];
+        float w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + (int64_t)u * STEP;
+            if (i < b) {
+                const unsigned char* row = base + (int64_t)tok[i] * rb;
+                cw[u] = __ldg(reinterpret_cast<const uint4*>(row + 16 * grp));
+                pw[u] = __ldg(reinterpret_cast<const unsigned int*>(row + d / 2 + 4 * grp));
+                w[u] = softmax_w<float>((sc[i] - m) * scale);
+            } else {
+                cw[u] = make_uint4(0, 0, 0, 0);
+                pw[u] = 0;
+                w[u] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const __half2 p = *reinterpret_cast<const __half2*>(&pw[u]);
+            const float sc_ = __low2float(p), mn = __high2float(p);
+            const uint32_t words[4] = {cw[u].x, cw[u].y, cw[u].z, cw[u].w};
+            l += w[u];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float x = __fmaf_rn((float)((words[q] >> (4 * e)) & 15u), sc_, mn);
+                    o[8 * q + e] = fmaf(w[u], x, o[8 * q + e]);
+                }
+        }
+    }
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+        l += __shfl_xor_sync(KVT_FULL, l, off);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] += __shfl_xor_sync(KVT_FULL, o[e], off);
+    }
+    if (lane < LPR) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) red_o[warp][32 * grp + e] = o[e];
+    }
+    if (lane == 0) red_l[warp] = l;
+    __syncthreads();
+    double* P = part + ((int64_t)li * splits + s) * (d + 2);
+    for (int j = threadIdx.x; j < d; j += ATTN_THREADS) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) acc += red_o[w][j];
+        P[2 + j] = (double)acc;
+    }
+    if (threadIdx.x == 0) {
+        float ls = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) ls += red_l[w];
+        P[0] = m;
+        P[1] = (double)ls;
+    }
+    attn_finish(part, splits, d, li, tickets, out, out64, scale);
+}
+
 }  // namespace kvt
 
 using namespace kvt;
@@ -453,6 +554,20 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
     double* part = (double*)((char*)ws + ticket_bytes(n_lanes));
     int rc;
     switch (v_dtype) {
+        case KVT_I4: {
+            if ((d != 128 && d != 256) || ((uintptr_t)values % 16) || (lane_stride % 16)) return KVT_ERR_SHAPE;
+            dim3 grid(splits, (unsigned)n_lanes);
+            if (d == 128)
+                attn_i4_kernel<4><<<grid, ATTN_THREADS, 0, st>>>((const unsigned char*)values, lane_stride, d, sel_tok,
+                                                                  sel_score, n_sel, sel_stride, splits, part, tickets,
+                                                                  out, out64, logit_scale);
+            else
+                attn_i4_kernel<8><<<grid, ATTN_THREADS, 0, st>>>((const unsigned char*)values, lane_stride, d, sel_tok,
+                                                                  sel_score, n_sel, sel_stride, splits, part, tickets,
+                                                                  out, out64, logit_scale);
+            rc = kvt_check_launch();
+            break;
+        }
         case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
         case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
         case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;

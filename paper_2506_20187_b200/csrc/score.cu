@@ -7,6 +7,8 @@
 // 256 B warp access), runs its f64 fma chains, and a reduce-scatter butterfly
 // (tree_8tok: 9 f64 shuffles per 8 tokens instead of 40) yields the canonical dot of
 // token (lane>>2) on every quad.  HBM-bound: n_cand*d*s_K read, n_cand*12 B written.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace kvt {
@@ -94,10 +96,10 @@ constexpr int TS_THREADS = (TS_CONSUMERS + 1) * 32;
 
 template <typename QT, typename T, int G, bool IMPLICIT>
 __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
-    const QT* __restrict__ q, const T* __restrict__ keys, int64_t lane_stride, int d, int n_lanes,
-    const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items, int64_t n_implicit,
-    double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride, int stages,
-    int tile_bytes, int scaled) {
+    const QT* __restrict__ q, const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d,
+    int n_lanes, const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items,
+    int64_t n_implicit, double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride,
+    int stages, int tile_bytes, int scaled) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ long long scan_sh[33];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * tile_bytes);
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const int64_t g_begin = kvt::imin(total, (int64_t)blockIdx.x * per);
     const int64_t g_end = kvt::imin(total, g_begin + per);
 
-    if (warp == TS_CONSUMERS) {  // ---- producer ----
+    if (warp == TS_CONSUMERS) {  // ---- producer: one elected thread drives the bulk-copy engine ----
         if (lane == 0) {
             int cur = 0;
             int64_t i = 0;
@@ -140,24 +142,26 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
                 while (g >= lane_off[cur + 1]) ++cur;
                 const int64_t it = g - lane_off[cur];
                 int64_t t0, cnt;
-                if (IMPLICIT) { t0 = it * 64; cnt = kvt::imin(64, n_implicit - t0); }
-                else { const int32_t* m = items + ((int64_t)cur * item_stride + it) * 3; t0 = m[0]; cnt = m[1]; }
+                int pos0;
+                if (IMPLICIT) { t0 = it * 64; cnt = kvt::imin(64, n_implicit - t0); pos0 = (int)t0; }
+                else {
+                    const int32_t* m = items + ((int64_t)cur * item_stride + it) * 3;
+                    t0 = m[0]; cnt = m[1]; pos0 = m[2];
+                }
                 const int s = (int)(i % stages);
                 const int64_t r = i / stages;
                 if (r > 0) mbar_wait(&empty[s], (uint32_t)((r - 1) & 1));
-                const uint32_t bytes = (uint32_t)(cnt * d * (int64_t)sizeof(T));
-                int pos0;
-                if (IMPLICIT) pos0 = (int)t0;
-                else pos0 = items[((int64_t)cur * item_stride + it) * 3 + 2];
+                const uint32_t bytes = (uint32_t)(cnt * row_b);
                 meta[s] = make_int4(cur, (int)t0, (int)cnt, pos0);
                 mbar_arrive_expect_tx(&full[s], bytes);
-                bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)cur * lane_stride + t0 * d, bytes, &full[s]);
+                bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)cur * lane_stride_b + t0 * row_b, bytes,
+                         &full[s]);
             }
         }
         return;
     }
 
-    // ---- consumers ----
+    // ---- consumers: 8 warps x 8 tokens per 64-token item ----
     const double sd = sqrt((double)d);
     int cur = -1;
     double qr[G][4];
@@ -177,11 +181,11 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
                 }
         }
         const int64_t t0 = mt.y, cnt = mt.z, pos0 = mt.w;
-        const T* tile = reinterpret_cast<const T*>(smem + (size_t)s * tile_bytes);
+        const unsigned char* tile = smem + (size_t)s * tile_bytes;
         const int base_t = 8 * warp;
         if (base_t < cnt) {
             double p[8];
-            const T* rows = tile + (int64_t)base_t * d;
+            const unsigned char* rows = tile + (int64_t)base_t * row_b;
             if (base_t + 8 <= cnt && d == 128 * G) {
                 // full group of 8 tokens, d a multiple of 128: no bounds checks
 #pragma unroll
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
 #pragma unroll
                     for (int r = 0; r < G; ++r) {
                         double v[4];
-                        lds4<T>(rows + (int64_t)u * d + 4 * (lane + 32 * r), v);
+                        RowLd<T>::load(rows + (int64_t)u * row_b, lane + 32 * r, d, v);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) acc = fma(qr[r][e], v[e], acc);
                     }
@@ -201,13 +205,13 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
                 for (int u = 0; u < 8; ++u) {
                     double acc = 0.0;
                     if (base_t + u < cnt) {
-                        const T* row = rows + (int64_t)u * d;
+                        const unsigned char* row = rows + (int64_t)u * row_b;
 #pragma unroll
                         for (int r = 0; r < G; ++r) {
                             const int gg = lane + 32 * r;
                             if (4 * gg < d) {
                                 double v[4];
-                                lds4<T>(row + 4 * gg, v);
+                                RowLd<T>::load(row, gg, d, v);
 #pragma unroll
                                 for (int e = 0; e < 4; ++e)
                                     if (4 * gg + e < d) acc = fma(qr[r][e], v[e], acc);
@@ -248,19 +252,23 @@ static int sm_count() {
 }
 
 // TMA path eligibility: whole-row bulk copies need 16 B aligned rows and lane bases.
+// lane_stride is in elements (bytes for I4).
 template <typename T>
 static bool tma_ok(const void* keys, int64_t lane_stride, int d, int64_t n_lanes) {
-    const int64_t row = (int64_t)d * sizeof(T);
-    return d % 4 == 0 && d <= 1024 && row % 16 == 0 && ((uintptr_t)keys % 16) == 0 &&
-           (lane_stride * (int64_t)sizeof(T)) % 16 == 0 && 64 * row * 2 <= 160 * 1024 && n_lanes <= 16384;
+    const int64_t row = RowLd<T>::row_bytes(d);
+    const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
+    return d % 4 == 0 && d <= 1024 && row % 16 == 0 && ((uintptr_t)keys % 16) == 0 && ls_b % 16 == 0 &&
+           64 * row * 2 <= 160 * 1024 && n_lanes <= 16384;
 }
 
 template <typename QT, typename T, int G, bool IMPL>
 static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
                             const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
                             double* os, int32_t* ot, int64_t ostr, int scaled, cudaStream_t st) {
-    const int tile = 64 * d * (int)sizeof(T);
-    int stages = (int)kvt::imin(3, (150 * 1024) / tile);
+    const int row_b = RowLd<T>::row_bytes(d);
+    const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
+    const int tile = 64 * row_b;
+    int stages = (int)kvt::imin(std::is_same<T, I4>::value ? 6 : 3, (150 * 1024) / tile);
     if (stages < 2) stages = 2;
     const size_t smem = (size_t)stages * tile + 32 * (size_t)stages + 4 * (size_t)(n_lanes + 1) + 16;
     static size_t configured = 0;
@@ -273,8 +281,8 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
     const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
     const int grid = sm_count() * per_sm;
     score_tma_kernel<QT, T, G, IMPL><<<grid, TS_THREADS, smem, st>>>(
-        (const QT*)q, (const T*)keys, lane_stride, d, (int)n_lanes, items, item_stride, n_items, n_impl, os, ot,
-        ostr, stages, tile, scaled);
+        (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, (int)n_lanes, items, item_stride, n_items, n_impl,
+        os, ot, ostr, stages, tile, scaled);
     return kvt_check_launch();
 }
 
@@ -321,6 +329,17 @@ static int dispatch_score(const void* q, int q_dtype, const void* keys, int key_
                           int scaled, cudaStream_t st) {
 #define KVT_K(QT, TT) \
     return dispatch_score_t<QT, TT, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, blocks, scaled, st)
+    if (key_dtype == KVT_I4) {
+        if ((d != 128 && d != 256) || !tma_ok<I4>(keys, lane_stride, d, n_lanes)) return KVT_ERR_SHAPE;
+        if (q_dtype != KVT_F32 && q_dtype != KVT_F64) return KVT_ERR_DTYPE;
+        if (d == 128)
+            return q_dtype == KVT_F32
+                ? launch_score_tma<float, I4, 1, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled, st)
+                : launch_score_tma<double, I4, 1, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled, st);
+        return q_dtype == KVT_F32
+            ? launch_score_tma<float, I4, 2, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled, st)
+            : launch_score_tma<double, I4, 2, IMPL>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, n_impl, os, ot, ostr, scaled, st);
+    }
     if (q_dtype == KVT_F32) {
         switch (key_dtype) {
             case KVT_F32: KVT_K(float, float);

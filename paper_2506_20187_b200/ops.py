@@ -15,16 +15,62 @@ from . import _lib as L
 
 ITEM_TOKENS = 64
 _DT = {torch.float32: L.F32, torch.float64: L.F64, torch.bfloat16: L.BF16, torch.float16: L.F16}
+I4 = "int4"
 
 
-def dtype_code(t: torch.Tensor) -> int:
+class I4KV:
+    """INT4-compressed KV rows (kvt_kv_quant records): `data` is uint8 [n_lanes, N_cap, d/2 + d/8]
+    (lane stride in bytes), `d` the logical head dim.  Dequantised value fmaf(code, scale, min)."""
+
+    def __init__(self, data: torch.Tensor, d: int):
+        if data.dtype != torch.uint8 or data.dim() < 3 or data.shape[-1] != row_bytes_i4(d):
+            raise ValueError("I4KV data must be uint8 [..., n_lanes, N_cap, d/2 + d/8]")
+        self.data, self.d = data, d
+        self.dtype = I4
+
+    @classmethod
+    def empty(cls, n_lanes: int, n_cap: int, d: int, device) -> "I4KV":
+        return cls(torch.empty((n_lanes, n_cap, row_bytes_i4(d)), dtype=torch.uint8, device=device), d)
+
+    @property
+    def shape(self):
+        return tuple(self.data.shape[:-1]) + (self.d,)
+
+    @property
+    def device(self):
+        return self.data.device
+
+    @property
+    def is_cuda(self):
+        return self.data.is_cuda
+
+    def data_ptr(self):
+        return self.data.data_ptr()
+
+    def stride(self, i):
+        return self.data.stride(i)
+
+    def __getitem__(self, idx):
+        return I4KV(self.data[idx], self.d)
+
+    def element_size(self):
+        return row_bytes_i4(self.d) / self.d
+
+
+def row_bytes_i4(d: int) -> int:
+    return d // 2 + (d // 32) * 4
+
+
+def dtype_code(t) -> int:
+    if isinstance(t, I4KV):
+        return L.I4
     try:
         return _DT[t.dtype]
     except KeyError:
         raise ValueError(f"unsupported dtype {t.dtype}") from None
 
 
-def abs_dtype_for(key_dtype: torch.dtype) -> torch.dtype:
+def abs_dtype_for(key_dtype) -> torch.dtype:
     """Abstract storage dtype: f64 for f64 keys, f32 otherwise (importance.py:75-77 wire f32)."""
     return torch.float64 if key_dtype == torch.float64 else torch.float32
 
@@ -50,8 +96,12 @@ def require_cuda(*ts: torch.Tensor) -> None:
             raise RuntimeError("paper_2506_20187_b200 runs on CUDA (sm_100a) only; got a CPU tensor")
 
 
-def _lanes(t: torch.Tensor) -> tuple[int, int]:
-    """(lane_stride, d) of a [n_lanes, N, d] tensor with contiguous rows."""
+def _lanes(t) -> tuple[int, int]:
+    """(lane_stride, d) of a [n_lanes, N, d] tensor with contiguous rows (bytes for I4KV)."""
+    if isinstance(t, I4KV):
+        if t.data.stride(2) != 1 or t.data.stride(1) != t.data.shape[2]:
+            raise ValueError("I4KV rows must be contiguous")
+        return t.data.stride(0), t.d
     if t.dim() != 3 or t.stride(2) != 1 or t.stride(1) != t.shape[2]:
         raise ValueError(f"expected [n_lanes, N, d] with contiguous rows, got shape {tuple(t.shape)} strides {t.stride()}")
     return t.stride(0), t.shape[2]
@@ -59,6 +109,21 @@ def _lanes(t: torch.Tensor) -> tuple[int, int]:
 
 def n_grid_leaves(n: int, C: int) -> int:
     return (n + C - 1) // C
+
+
+# -- K8 ----------------------------------------------------------------------------------------
+
+
+def kv_quant(src: torch.Tensor, dst: I4KV, t_begin: int = 0, t_end: int | None = None) -> I4KV:
+    """INT4-compress rows [t_begin, t_end) of every lane of src [n_lanes, N, d] into dst (K8)."""
+    require_cuda(src)
+    ls, d = _lanes(src)
+    t_end = src.shape[1] if t_end is None else t_end
+    if dst.d != d or dst.shape[0] != src.shape[0] or dst.shape[1] < t_end:
+        raise ValueError("kv_quant: destination shape mismatch")
+    L.check(L.kvt_kv_quant(src.data_ptr(), dtype_code(src), src.shape[0], ls, t_begin, t_end, d, dst.data_ptr(),
+                           dst.stride(0), _stream()), "kv_quant")
+    return dst
 
 
 # -- K1 ----------------------------------------------------------------------------------------

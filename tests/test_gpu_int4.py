@@ -1,0 +1,102 @@
+"""INT4 KV compression (K8) and the INT4 paths of K1/K4/K5/K7 against the C oracle.
+
+The reference has no quantizer (parity of the codes is against the codec defined in
+oracle/kvt_oracle.c, itself checked against an independent numpy formulation in
+tests/test_host_cpu.py); selection, logits and attention on the dequantised values are
+held to the same bar as bf16: bit-exact sets/dots, attention within 1e-2."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from oracle import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_20187_b200 import ops as _ops
+    return _ops
+
+
+@pytest.mark.parametrize("src_dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d", [128, 256])
+def test_kv_quant_codes_bitexact(ops, src_dt, d):
+    rng = np.random.default_rng(d)
+    lanes, n = 3, 777
+    x = (rng.normal(size=(lanes, n, d)) * rng.choice([0.01, 1.0, 30.0], size=(lanes, 1, 1))).astype(np.float32)
+    x[0, 5] = 0.0          # constant group -> scale 0
+    x[1, 7, :32] = 3.25    # constant group with nonzero value
+    xt = torch.from_numpy(x).to(src_dt).cuda()
+    dst = ops.I4KV.empty(lanes, n + 5, d, xt.device)
+    ops.kv_quant(xt, dst, 0, n)
+    got = dst.data[:, :n].cpu().numpy()
+    xs = xt.float().cpu().numpy()
+    for i in range(lanes):
+        ref = O.i4_quant(xs[i])
+        assert np.array_equal(got[i], ref), i
+
+
+def _i4_lanes(ops, kind, lanes, n, d, seed):
+    if kind == "random":
+        rng = np.random.default_rng(seed)
+        K = rng.normal(size=(lanes, n, d)).astype(np.float32)
+        V = rng.normal(size=(lanes, n, d)).astype(np.float32)
+        Q = rng.normal(size=(lanes, d)).astype(np.float32)
+    else:
+        K = np.empty((lanes, n, d), np.float32)
+        V = np.empty_like(K)
+        Q = np.empty((lanes, d), np.float32)
+        for i in range(lanes):
+            k, q, v, _ = synth.lane(synth.Profile(0.7, 3, 1.0, seed), 0, i, n, d, 1)
+            K[i], V[i], Q[i] = k, v, q[0]
+    kt = ops.I4KV.empty(lanes, n, d, "cuda")
+    vt = ops.I4KV.empty(lanes, n, d, "cuda")
+    ops.kv_quant(torch.from_numpy(K).to(torch.bfloat16).cuda(), kt)
+    ops.kv_quant(torch.from_numpy(V).to(torch.bfloat16).cuda(), vt)
+    Kd = np.stack([O.i4_dequant(kt.data[i].cpu().numpy(), d) for i in range(lanes)]).astype(np.float64)
+    Vd = np.stack([O.i4_dequant(vt.data[i].cpu().numpy(), d) for i in range(lanes)]).astype(np.float64)
+    return kt, vt, Kd, Vd, Q
+
+
+@pytest.mark.parametrize("kind", ["random", "planted"])
+@pytest.mark.parametrize("n,C,rate", [(4096, 64, 0.1), (2000, 8, 0.5), (65536, 64, 0.1)])
+def test_int4_select_attend_matches_oracle(ops, kind, n, C, rate):
+    lanes, d = (3 if n <= 4096 else 2), 128
+    kt, vt, Kd, Vd, Q = _i4_lanes(ops, kind, lanes, n, d, seed=n)
+    k = math.ceil(rate * n)
+    qt = torch.from_numpy(Q).cuda()
+    amax, amin = ops.abstract_build(kt, n, C)
+    m = ops.n_grid_leaves(n, C)
+    for i in range(lanes):
+        mx = np.stack([Kd[i, c * C:(c + 1) * C].max(0) for c in range(m)])
+        assert np.array_equal(amax[i, :m].double().cpu().numpy(), mx)
+    ws = ops.LayerWorkspace(lanes, n, m, d, qt.device)
+    out = {"sel_tok": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "sel_score": torch.empty((lanes, k), dtype=torch.float64, device="cuda"),
+           "n_sel": torch.empty(lanes, dtype=torch.int32, device="cuda"),
+           "run_start": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "run_len": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "n_runs": torch.empty(lanes, dtype=torch.int32, device="cuda"),
+           "out": torch.empty((lanes, d), dtype=torch.float32, device="cuda"),
+           "evals": torch.empty(lanes, dtype=torch.int64, device="cuda")}
+    ops.select_attend(qt, kt, vt, amax, amin, n, k, C, ws, out)
+    torch.cuda.synchronize()
+    logits = ops.token_scores(qt.double(), kt, n).cpu().numpy()
+    for i in range(lanes):
+        dd = O.dots(Q[i], Kd[i])
+        ref = O.topk(dd, k)
+        assert np.array_equal(out["sel_tok"][i].cpu().numpy().astype(np.int64), ref)
+        assert np.array_equal(out["sel_score"][i].cpu().numpy(), dd[ref])
+        assert np.array_equal(logits[i], O.scores(Q[i], Kd[i]))
+        att = O.attention(Q[i], Kd[i], Vd[i], ref)
+        err = np.linalg.norm(out["out"][i].cpu().numpy() - att) / np.linalg.norm(att)
+        assert err <= 1e-2, err

@@ -80,3 +80,26 @@ def test_shard_blocks_cover_disjointly():
             toks = [token_block(n * 64 + 3, w, r) for r in range(w)]
             assert toks[0][0] == 0 and toks[-1][1] == n * 64 + 3
             assert all(a[1] == b[0] and (a[1] % 64 == 0 or a[1] == n * 64 + 3) for a, b in zip(toks, toks[1:]))
+
+
+def test_int4_codec_oracle_matches_numpy_definition():
+    """The C oracle's INT4 codec equals an independent numpy statement of DESIGN.md sec. 2."""
+    import numpy as np
+    from oracle import oracle as O
+    rng = np.random.default_rng(0)
+    x = (rng.normal(size=(500, 128)) * rng.choice([0.001, 1.0, 100.0], size=(500, 1))).astype(np.float32)
+    x[3] = 1.5
+    rec = O.i4_quant(x)
+    g = x.reshape(500, 4, 32)
+    lo, hi = g.min(2), g.max(2)
+    sf = ((hi - lo).astype(np.float32) / np.float32(15)).astype(np.float32)
+    sh, mh = sf.astype(np.float16), lo.astype(np.float16)
+    s, m = sh.astype(np.float32), mh.astype(np.float32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        qv = ((g - m[..., None]).astype(np.float32) / s[..., None]).astype(np.float32)
+    c = np.where(s[..., None] == 0, 0, np.clip(np.rint(qv), 0, 15)).astype(np.uint8).reshape(500, 128)
+    assert np.array_equal(rec[:, :64], (c[:, 0::2] | (c[:, 1::2] << 4)).astype(np.uint8))
+    assert np.array_equal(rec[:, 64:], np.stack([sh, mh], -1).reshape(500, 8).view(np.uint8))
+    deq = O.i4_dequant(rec, 128)
+    ref = (c.astype(np.float32).reshape(500, 4, 32) * s[..., None] + m[..., None]).reshape(500, 128)
+    assert np.abs(deq - ref).max() <= 1e-6 * np.abs(ref).max()
