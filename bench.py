@@ -417,27 +417,27 @@ def run_ours(args):
         q_static.copy_(Q[args.warmup])
         for l in range(L):
             C, n, k = dec.C[l], dec.n, dec.k_for(l)
-            U, Lo = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C)
-            plan = ops.select_plan(U, Lo, n, k, C)
-            cs, ct = ops.cand_score(q_static[l], dec.K[l], plan, n)
-            st_, ss_, ns_, _ = ops.topk_select(cs, ct, plan["n_cand"], k, want_runs=True)
-            inter.append((U, Lo, plan, cs, ct, st_, ss_, ns_))
+            U, Lo, A = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
+            plan = ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
+            cs, ct = ops.cand_score_f32(q_static[l], dec.K[l], plan, n)
+            st_, ss_, ns_, _ = ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
+            inter.append((U, Lo, A, plan, cs, ct, st_, ss_, ns_))
         stream.synchronize()
-    n_cand = [x[2]["n_cand"].cpu().tolist() for x in inter]
+    n_cand = [x[3]["n_cand"].cpu().tolist() for x in inter]
 
     def stage_fn(name):
         def run():
             for l in range(L):
                 C, n, k = dec.C[l], dec.n, dec.k_for(l)
-                U, Lo, plan, cs, ct, st_, ss_, ns_ = inter[l]
+                U, Lo, A, plan, cs, ct, st_, ss_, ns_ = inter[l]
                 if name == "bounds":
-                    ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C)
+                    ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
                 elif name == "plan":
-                    ops.select_plan(U, Lo, n, k, C)
+                    ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
                 elif name == "score":
-                    ops.cand_score(q_static[l], dec.K[l], plan, n)
+                    ops.cand_score_f32(q_static[l], dec.K[l], plan, n)
                 elif name == "select":
-                    ops.topk_select(cs, ct, plan["n_cand"], k, want_runs=True)
+                    ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
                 elif name == "attn":
                     ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)  # logit_scale 1/sqrt(d): raw dots
         return run

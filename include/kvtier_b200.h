@@ -84,6 +84,12 @@ KVT_API int kvt_kv_quant(const void* src, int src_dtype, int64_t n_lanes, int64_
                          int64_t t_begin, int64_t t_end, int d, void* dst, int64_t dst_lane_stride,
                          void* stream);
 KVT_API int kvt_i4_row_bytes(int d);
+/* Expand INT4 records (src lane stride in bytes) of tokens [t_begin, t_end) into rows of
+ * dst_dtype (F32/BF16/F16): the device half of a compressed host->HBM tier transfer
+ * (pipeline.py:79-103 decompress_rate is this kernel's throughput). */
+KVT_API int kvt_kv_dequant(const void* src, int64_t src_lane_stride, int64_t n_lanes, int64_t t_begin,
+                           int64_t t_end, int d, void* dst, int dst_dtype, int64_t dst_lane_stride,
+                           void* stream);
 
 /* ---- K3: query-vs-abstract bounds ----------------------------------------------------
  * Replaces importance.py:108-137 bound_chunk / bound_chunks_batch (logit mode).
@@ -92,11 +98,13 @@ KVT_API int kvt_i4_row_bytes(int d);
  * leaf_start[i*leaf_stride + j + 1]) for j < n_leaves[i] (the last end is n).
  * q: [n_lanes][d] of q_dtype (F32 or F64).  U/L: float64 at U + i*bnd_stride + j.
  * scaled != 0: bounds on the logits fl(q.k)/fl(sqrt d) (the importance.py form);
- * scaled == 0: bounds on the raw canonical dots (what the pipeline prunes with). */
+ * scaled == 0: bounds on the raw canonical dots (what the pipeline prunes with).
+ * A (optional): sum_j |q_j| max(|max_j|, |min_j|) per chunk, a bound on sum_j |q_j k_j| for
+ * every token of the chunk (feeds the f32 scoring error bound). */
 KVT_API int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int d, int64_t n, int C,
                      const int32_t* leaf_start, const int32_t* n_leaves, int64_t leaf_stride,
                      const void* amax, const void* amin, int abs_dtype, int64_t abs_lane_stride,
-                     double* U, double* L, int64_t bnd_stride, int scaled, void* stream);
+                     double* U, double* L, double* A, int64_t bnd_stride, int scaled, void* stream);
 
 /* ---- K4 (brute force): canonical token logits -----------------------------------------
  * Replaces importance.py:27-33 attention_logits / :46-53 score_tokens (logit mode) for
@@ -128,6 +136,31 @@ KVT_API int kvt_cand_score(const void* q, int q_dtype, const void* keys, int key
                    int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,
                    int64_t item_stride, const int32_t* n_items, double* cand_score,
                    int32_t* cand_tok, int64_t cand_stride, int blocks_per_lane, void* stream);
+
+/* ---- fast scoring: f32 estimates + exact band re-scoring ---------------------------------
+ * kvt_select_plan2 = kvt_select_plan that also writes err[i] = a rigorous bound on
+ * |f32 estimate - canonical f64 dot| over lane i's candidates (from the chunks' A of
+ * kvt_chunk_bounds; d is the head dim).  kvt_cand_score_f32 writes the f32 estimates
+ * (TMA pipeline, any key dtype but F64).  kvt_topk_select_band selects the exact canonical
+ * top-k from them: 32-bit radix select for the k-th estimate T, tokens above T + 2 err are
+ * in, below T - 2 err out, and the band in between is re-scored canonically in f64 from the
+ * key rows (q: [n_lanes][d]); a wide band (ties) falls back to full canonical re-scoring.
+ * Output as kvt_topk_select_runs (sel_score: estimate for sure tokens, exact for the band). */
+KVT_API int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start,
+                    const int32_t* n_leaves, int64_t leaf_stride, const double* U, const double* L,
+                    int64_t bnd_stride, int64_t k, int32_t* items, int64_t item_stride,
+                    int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf, int64_t* evals,
+                    const double* A, double* err, int d, void* stream);
+KVT_API int kvt_cand_score_f32(const void* q, int q_dtype, const void* keys, int key_dtype,
+                    int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,
+                    int64_t item_stride, const int32_t* n_items, float* cand_score32,
+                    int32_t* cand_tok, int64_t cand_stride, void* stream);
+KVT_API int kvt_topk_select_band(const float* cand_score32, const int32_t* cand_tok,
+                    const int32_t* n_cand, int64_t cand_stride, const double* err, int64_t n_lanes,
+                    int64_t k, const void* q, int q_dtype, const void* keys, int key_dtype,
+                    int64_t lane_stride, int d, int32_t* sel_tok, double* sel_score,
+                    int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len,
+                    int64_t run_stride, int32_t* n_runs, void* stream);
 
 /* ---- K5: exact top-k ---------------------------------------------------------------------
  * Result contract of select_top_k (chunk_tree.py:233-338) / brute force
@@ -202,6 +235,7 @@ typedef struct {
     int64_t* evals;             /* [n_lanes] (may be NULL) */
     int attn_splits;            /* 0 = auto */
     int score_blocks;           /* 0 = auto */
+    int exact_scores;           /* 1: canonical f64 scoring of every candidate (no f32 band path) */
 } kvt_layer_args;
 
 KVT_API size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d);

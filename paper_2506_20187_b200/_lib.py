@@ -46,7 +46,7 @@ class KvtLayerArgs(ctypes.Structure):
         ("sel_tok", _vp), ("sel_score", _vp), ("n_sel", _vp),
         ("run_start", _vp), ("run_len", _vp), ("n_runs", _vp),
         ("out", _vp), ("evals", _vp),
-        ("attn_splits", _i32), ("score_blocks", _i32),
+        ("attn_splits", _i32), ("score_blocks", _i32), ("exact_scores", _i32),
     ]
 
 
@@ -65,7 +65,13 @@ kvt_abstract_build = _sig("kvt_abstract_build", ctypes.c_int, _vp, _i32, _i64, _
 kvt_abstract_spans = _sig("kvt_abstract_spans", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _vp,
                           _vp)
 kvt_chunk_bounds = _sig("kvt_chunk_bounds", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _i32, _vp, _vp, _i64, _vp,
-                        _vp, _i32, _i64, _vp, _vp, _i64, _i32, _vp)
+                        _vp, _i32, _i64, _vp, _vp, _vp, _i64, _i32, _vp)
+kvt_select_plan2 = _sig("kvt_select_plan2", ctypes.c_int, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
+                        _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp)
+kvt_cand_score_f32 = _sig("kvt_cand_score_f32", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _vp,
+                          _vp, _vp, _i64, _vp)
+kvt_topk_select_band = _sig("kvt_topk_select_band", ctypes.c_int, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i32,
+                            _vp, _i32, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp)
 kvt_token_scores = _sig("kvt_token_scores", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i64,
                         _vp)
 kvt_select_plan = _sig("kvt_select_plan", ctypes.c_int, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
@@ -82,6 +88,7 @@ kvt_sparse_decode_attn = _sig("kvt_sparse_decode_attn", ctypes.c_int, _vp, _i32,
                               _i64, ctypes.c_double, _i32, _vp, _vp, _vp, _vp)
 kvt_kv_quant = _sig("kvt_kv_quant", ctypes.c_int, _vp, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _vp)
 kvt_i4_row_bytes = _sig("kvt_i4_row_bytes", ctypes.c_int, _i32)
+kvt_kv_dequant = _sig("kvt_kv_dequant", ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _i32, _i64, _vp)
 kvt_layer_workspace_bytes = _sig("kvt_layer_workspace_bytes", _sz, _i64, _i64, _i64, _i32)
 kvt_select_attend = _sig("kvt_select_attend", ctypes.c_int, ctypes.POINTER(KvtLayerArgs), _vp, _sz, _vp)
 
@@ -90,7 +97,8 @@ EXPORTED = [
     "kvt_chunk_bounds", "kvt_token_scores", "kvt_select_plan", "kvt_cand_score", "kvt_topk_select",
     "kvt_topk_select_runs",
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
-    "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes",
+    "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_select_plan2", "kvt_cand_score_f32",
+    "kvt_topk_select_band", "kvt_kv_dequant",
 ]
 
 

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256, 3) bounds_kernel(
     const QT* __restrict__ q, int d, int64_t n, int C, const int32_t* __restrict__ leaf_start,
     const int32_t* __restrict__ n_leaves, int64_t leaf_stride, const AT* __restrict__ amax,
     const AT* __restrict__ amin, int64_t abs_lane_stride, double* __restrict__ U,
-    double* __restrict__ L, int64_t bnd_stride, int scaled) {
+    double* __restrict__ L, double* __restrict__ A, int64_t bnd_stride, int scaled) {
     // 4 chunks per warp step: 8 independent 16 B abstract loads in flight per lane, then
     // three reduce-scatter trees (U, L, A) leave chunk (lane >> 3) & 3 on each lane octet.
     // Outputs are raw (unscaled) bounds unless `scaled` (the importance.py API form).
@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(256, 3) bounds_kernel(
             }
             U[lane_i * bnd_stride + c] = scaled ? u_ / sd : u_;
             L[lane_i * bnd_stride + c] = scaled ? l_ / sd : l_;
+            if (A) A[lane_i * bnd_stride + c] = a_;  // sum |q| max(|max|,|min|): bounds sum |q.k| in the chunk
         }
     }
 }
@@ -313,21 +314,21 @@ extern "C" int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_
 template <typename QT, typename AT, int G>
 static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                           const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
-                          double* U, double* L, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
+                          double* U, double* L, double* A, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
     int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 31) / 32, 1024));
     // keep ~8 CTAs per SM in total when lanes are few
     dim3 grid(gx, (unsigned)n_lanes);
     bounds_kernel<QT, AT, G><<<grid, 256, 0, st>>>((const QT*)q, d, n, C, ls, nl, lstr, (const AT*)amax,
-                                                   (const AT*)amin, als, U, L, bs, scaled);
+                                                   (const AT*)amin, als, U, L, A, bs, scaled);
 }
 
 template <typename QT, typename AT>
 static int dispatch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                            const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
-                           double* U, double* L, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
+                           double* U, double* L, double* A, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
     switch (groups_for(d)) {
 #define KVT_CASE(GG) \
-    case GG: launch_bounds<QT, AT, GG>(q, n_lanes, d, n, C, ls, nl, lstr, amax, amin, als, U, L, bs, max_leaves, scaled, st); break;
+    case GG: launch_bounds<QT, AT, GG>(q, n_lanes, d, n, C, ls, nl, lstr, amax, amin, als, U, L, A, bs, max_leaves, scaled, st); break;
         KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
 #undef KVT_CASE
         default: return KVT_ERR_SHAPE;
@@ -338,7 +339,7 @@ static int dispatch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int
 extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int d, int64_t n, int C,
                                 const int32_t* leaf_start, const int32_t* n_leaves, int64_t leaf_stride,
                                 const void* amax, const void* amin, int abs_dtype, int64_t abs_lane_stride, double* U,
-                                double* L, int64_t bnd_stride, int scaled, void* stream) {
+                                double* L, double* A, int64_t bnd_stride, int scaled, void* stream) {
     if (!q || !amax || !amin || !U || !L || d < 1 || n < 0 || n_lanes < 0) return KVT_ERR_ARG;
     if (!leaf_start && C < 1) return KVT_ERR_ARG;
     if (leaf_start && !n_leaves) return KVT_ERR_ARG;
@@ -347,12 +348,12 @@ extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
     cudaStream_t st = (cudaStream_t)stream;
     if (q_dtype == KVT_F32 && abs_dtype == KVT_F32)
-        return dispatch_bounds<float, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
+        return dispatch_bounds<float, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F64 && abs_dtype == KVT_F32)
-        return dispatch_bounds<double, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
+        return dispatch_bounds<double, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F32 && abs_dtype == KVT_F64)
-        return dispatch_bounds<float, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
+        return dispatch_bounds<float, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F64 && abs_dtype == KVT_F64)
-        return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, bnd_stride, max_leaves, scaled, st);
+        return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     return KVT_ERR_DTYPE;
 }

@@ -57,7 +57,7 @@ struct Carve {
 };
 
 struct LayerWs {
-    double *U, *L;
+    double *U, *L, *A, *err;
     int32_t *items, *n_items, *n_cand;
     double* cand_score;
     int32_t* cand_tok;
@@ -71,6 +71,8 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     const int64_t item_cap = (n + ITEM_TOKENS - 1) / ITEM_TOKENS + max_leaves;
     w.U = c.take<double>((size_t)(n_lanes * max_leaves));
     w.L = c.take<double>((size_t)(n_lanes * max_leaves));
+    w.A = c.take<double>((size_t)(n_lanes * max_leaves));
+    w.err = c.take<double>((size_t)n_lanes);
     w.items = c.take<int32_t>((size_t)(n_lanes * item_cap * 3));
     w.n_items = c.take<int32_t>((size_t)n_lanes);
     w.n_cand = c.take<int32_t>((size_t)n_lanes);
@@ -107,25 +109,42 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     if (w.bytes > ws_bytes) return KVT_ERR_OOM;
     const int64_t item_cap = (a->n + ITEM_TOKENS - 1) / ITEM_TOKENS + max_leaves;
     int rc;
+    // fast path: f32 estimates + exact band re-scoring (any key dtype but f64, d = 128/256)
+    const bool fast = kvt_fast_ok(a->key_dtype, a->d) && !a->exact_scores;
     rc = kvt_chunk_bounds(a->q, a->q_dtype, a->n_lanes, a->d, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride,
-                          a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L, max_leaves, 0, stream);
+                          a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L, fast ? w.A : nullptr,
+                          max_leaves, 0, stream);
     if (rc) return rc;
-    rc = kvt_select_plan(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L, max_leaves,
-                         a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals, stream);
+    rc = kvt_select_plan2(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L, max_leaves,
+                          a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals, fast ? w.A : nullptr,
+                          fast ? w.err : nullptr, a->d, stream);
     if (rc) return rc;
-    int blocks = a->score_blocks;
-    if (blocks <= 0) {
-        const int64_t target = (int64_t)num_sms() * 8;  // 8 CTAs of 256 threads per SM
-        const int64_t per_lane = (target + a->n_lanes - 1) / a->n_lanes;
-        const int64_t need = (item_cap + 7) / 8;
-        blocks = (int)kvt::imax(1, kvt::imin(per_lane, need));
+    if (fast) {
+        float* cs32 = reinterpret_cast<float*>(w.cand_score);
+        rc = kvt_cand_score_f32(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items,
+                                item_cap, w.n_items, cs32, w.cand_tok, a->n, stream);
+        if (rc) return rc;
+        rc = kvt_topk_select_band(cs32, w.cand_tok, w.n_cand, a->n, w.err, a->n_lanes, a->k, a->q, a->q_dtype,
+                                  a->keys, a->key_dtype, a->lane_stride, a->d, a->sel_tok, a->sel_score, a->k,
+                                  a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);
+        if (rc) return rc;
+    } else {
+
+        int blocks = a->score_blocks;
+        if (blocks <= 0) {
+            const int64_t target = (int64_t)num_sms() * 8;  // 8 CTAs of 256 threads per SM
+            const int64_t per_lane = (target + a->n_lanes - 1) / a->n_lanes;
+            const int64_t need = (item_cap + 7) / 8;
+            blocks = (int)kvt::imax(1, kvt::imin(per_lane, need));
+        }
+        rc = kvt_cand_score(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items, item_cap,
+                            w.n_items, w.cand_score, w.cand_tok, a->n, blocks, stream);
+        if (rc) return rc;
+        rc = kvt_topk_select_runs(w.cand_score, w.cand_tok, w.n_cand, a->n, a->n_lanes, a->k, a->sel_tok, a->sel_score,
+                                  a->k, a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);  // K5 + fused K6
+        if (rc) return rc;
+
     }
-    rc = kvt_cand_score(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items, item_cap,
-                        w.n_items, w.cand_score, w.cand_tok, a->n, blocks, stream);
-    if (rc) return rc;
-    rc = kvt_topk_select_runs(w.cand_score, w.cand_tok, w.n_cand, a->n, a->n_lanes, a->k, a->sel_tok, a->sel_score,
-                              a->k, a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);  // K5 + fused K6
-    if (rc) return rc;
     if (a->out && a->values) {
         int splits = a->attn_splits;
         if (splits <= 0) {

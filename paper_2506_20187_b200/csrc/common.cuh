@@ -155,6 +155,15 @@ template <typename T> struct RowLd {
     __device__ __forceinline__ static void load(const unsigned char* row, int g, int d, double v[4]) {
         lds4<T>(reinterpret_cast<const T*>(row) + 4 * g, v);
     }
+    __device__ __forceinline__ static void loadf(const unsigned char* row, int g, int d, float v[4]) {
+        const T* p = reinterpret_cast<const T*>(row) + 4 * g;
+        if constexpr (sizeof(T) == 4) {
+            const float4 x = *reinterpret_cast<const float4*>(p);
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+            Elem<T>::unpack(*reinterpret_cast<const uint2*>(p), v);
+        }
+    }
 };
 template <> struct RowLd<I4> {
     __host__ __device__ static int row_bytes(int d) { return i4_row_bytes(d); }
@@ -165,7 +174,23 @@ template <> struct RowLd<I4> {
         i4_dequant4(c, p, f);
         v[0] = f[0]; v[1] = f[1]; v[2] = f[2]; v[3] = f[3];
     }
+    __device__ __forceinline__ static void loadf(const unsigned char* row, int g, int d, float v[4]) {
+        const uint32_t c = *reinterpret_cast<const unsigned short*>(row + 2 * g);
+        const __half2 p = *reinterpret_cast<const __half2*>(row + d / 2 + 4 * (g >> 3));
+        i4_dequant4(c, p, v);
+    }
 };
+
+// Orderable 32-bit key of a finite float (larger value -> larger key); -0 == +0.
+__device__ __forceinline__ uint32_t ord_key32(float s) {
+    if (s == 0.0f) s = 0.0f;
+    const uint32_t b = __float_as_uint(s);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key32_to_float(uint32_t k) {
+    const uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return __uint_as_float(b);
+}
 
 // ------------------------------------------------------------------------------------------
 // canonical reductions
@@ -179,13 +204,14 @@ __device__ __forceinline__ double tree_allreduce(double v) {
 
 // Reduce-scatter of 8 per-lane partials (tokens 0..7) with the canonical tree; on return
 // lane L holds the full dot of token (L >> 2) & 7 (same value on the 4 lanes of a quad).
-__device__ __forceinline__ double tree_8tok(double p[8], int lane) {
+template <typename V>
+__device__ __forceinline__ V tree_8tok(V p[8], int lane) {
     {
         const bool b = lane & 16;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            double send = b ? p[i] : p[4 + i];
-            double keep = b ? p[4 + i] : p[i];
+            V send = b ? p[i] : p[4 + i];
+            V keep = b ? p[4 + i] : p[i];
             p[i] = keep + __shfl_xor_sync(KVT_FULL, send, 16);
         }
     }
@@ -193,18 +219,18 @@ __device__ __forceinline__ double tree_8tok(double p[8], int lane) {
         const bool b = lane & 8;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            double send = b ? p[i] : p[2 + i];
-            double keep = b ? p[2 + i] : p[i];
+            V send = b ? p[i] : p[2 + i];
+            V keep = b ? p[2 + i] : p[i];
             p[i] = keep + __shfl_xor_sync(KVT_FULL, send, 8);
         }
     }
     {
         const bool b = lane & 4;
-        double send = b ? p[0] : p[1];
-        double keep = b ? p[1] : p[0];
+        V send = b ? p[0] : p[1];
+        V keep = b ? p[1] : p[0];
         p[0] = keep + __shfl_xor_sync(KVT_FULL, send, 4);
     }
-    double v = p[0];
+    V v = p[0];
     v = v + __shfl_xor_sync(KVT_FULL, v, 2);
     v = v + __shfl_xor_sync(KVT_FULL, v, 1);
     return v;
@@ -325,6 +351,8 @@ __device__ __forceinline__ V block_excl_scan(V v, V* sh, V& total) {
 }
 
 }  // namespace kvt
+
+bool kvt_fast_ok(int key_dtype, int d);
 
 // INT4 K1 (quant.cu)
 int kvt_abstract_build_i4(const void* keys, int64_t n_lanes, int64_t lane_stride_b, int64_t n, int d, int C,

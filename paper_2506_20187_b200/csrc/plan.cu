@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
     int64_t n, int C, const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ n_leaves,
     int64_t leaf_stride, const double* __restrict__ U, const double* __restrict__ L, int64_t bnd_stride,
     int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
-    int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals, int stage_cap) {
+    int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals, int stage_cap,
+    const double* __restrict__ A, double* __restrict__ err, double err_factor) {
     extern __shared__ __align__(16) unsigned char plan_smem[];
     uint64_t* kst = reinterpret_cast<uint64_t*>(plan_smem);  // staged keys (if they fit)
     __shared__ unsigned long long hist[256];
@@ -106,8 +107,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
     }
     const double tau = (k <= 0) ? INFINITY : key_to_double(s_prefix);
 
-    // ---- candidate compaction -> items ----
+    // ---- candidate compaction -> items (+ max A over candidates for the f32 error bound) ----
     long long carry_items = 0, carry_tok = 0;
+    double amax_c = 0.0;
     for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
         const int64_t c = base + tid;
         long long it = 0, tk = 0;
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
             rows = leaf_rows(ls, nl, c, n, C);
             cand = Ul[c] >= tau;
             if (cand) { tk = rows; it = (rows + ITEM_TOKENS - 1) / ITEM_TOKENS; }
+            if (cand && A) amax_c = fmax(amax_c, A[li * bnd_stride + c]);
             if (cand_leaf) cand_leaf[li * leaf_stride + c] = cand ? 1 : 0;
         }
         long long tot_it, tot_tk;
@@ -135,6 +138,20 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
         carry_items += tot_it;
         carry_tok += tot_tk;
     }
+    if (err) {
+        // block max of amax_c (reuse hist as scratch)
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) amax_c = fmax(amax_c, __shfl_xor_sync(KVT_FULL, amax_c, off));
+        __syncthreads();
+        double* red = reinterpret_cast<double*>(hist);
+        if (lane == 0) red[tid >> 5] = amax_c;
+        __syncthreads();
+        if (tid == 0) {
+            double m = 0.0;
+            for (int w = 0; w < PLAN_THREADS / 32; ++w) m = fmax(m, red[w]);
+            err[li] = m * err_factor;  // |f32 estimate - canonical dot| <= err for every candidate
+        }
+    }
     if (tid == 0) {
         n_items[li] = (int32_t)carry_items;
         n_cand[li] = (int32_t)carry_tok;
@@ -146,10 +163,26 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
 
 using namespace kvt;
 
+// Rigorous bound on |f32 estimate - canonical f64 dot| relative to A = sum |q_j| |k_j|:
+// the f32 path (q rounded to f32: 1 unit; fma chain + tree: n = chain_len(d) units of
+// 2^-24, gamma_n) plus the canonical f64 path's own error (n units of 2^-53), with slack.
+static double f32_err_factor(int d) {
+    const int n = chain_len(d);
+    return ((double)(n + 2) * 0x1p-24) * (1.0 + 0x1p-10) + (double)(n + 2) * 0x1p-52;
+}
+
 extern "C" int kvt_select_plan(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start, const int32_t* n_leaves,
                                int64_t leaf_stride, const double* U, const double* L, int64_t bnd_stride, int64_t k,
                                int32_t* items, int64_t item_stride, int32_t* n_items, int32_t* n_cand,
                                int8_t* cand_leaf, int64_t* evals, void* stream) {
+    return kvt_select_plan2(n_lanes, n, C, leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items,
+                               item_stride, n_items, n_cand, cand_leaf, evals, nullptr, nullptr, 0, stream);
+}
+
+extern "C" int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start, const int32_t* n_leaves,
+                        int64_t leaf_stride, const double* U, const double* L, int64_t bnd_stride, int64_t k,
+                        int32_t* items, int64_t item_stride, int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf,
+                        int64_t* evals, const double* A, double* err, int d, void* stream) {
     if (!U || !L || !items || !n_items || !n_cand || n_lanes < 0 || n < 0) return KVT_ERR_ARG;
     if (!leaf_start && C < 1) return KVT_ERR_ARG;
     if (k < 0 || k > n) return KVT_ERR_K;
@@ -165,6 +198,6 @@ extern "C" int kvt_select_plan(int64_t n_lanes, int64_t n, int C, const int32_t*
     const int cap = (int)kvt::imin(max_leaves, 16384);
     plan_kernel<<<(unsigned)n_lanes, PLAN_THREADS, (size_t)cap * 8, (cudaStream_t)stream>>>(
         n, C, leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand,
-        cand_leaf, evals, cap);
+        cand_leaf, evals, cap, A, err, f32_err_factor(d));
     return kvt_check_launch();
 }

@@ -94,12 +94,15 @@ __global__ void __launch_bounds__(SCORE_THREADS) score_kernel(
 constexpr int TS_CONSUMERS = 8;
 constexpr int TS_THREADS = (TS_CONSUMERS + 1) * 32;
 
-template <typename QT, typename T, int G, bool IMPLICIT>
+// AccT = double: canonical f64 dots (the exact definition); AccT = float: the fast f32
+// estimate written to out32 (select2.cu brackets it with a rigorous error bound and
+// re-scores the few tokens near the k-th value in f64, so the selected set stays exact).
+template <typename QT, typename T, int G, bool IMPLICIT, typename AccT>
 __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const QT* __restrict__ q, const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d,
     int n_lanes, const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items,
-    int64_t n_implicit, double* __restrict__ out_score, int32_t* __restrict__ out_tok, int64_t out_stride,
-    int stages, int tile_bytes, int scaled) {
+    int64_t n_implicit, double* __restrict__ out_score, float* __restrict__ out32, int32_t* __restrict__ out_tok,
+    int64_t out_stride, int stages, int tile_bytes, int scaled) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ long long scan_sh[33];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * tile_bytes);
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     // ---- consumers: 8 warps x 8 tokens per 64-token item ----
     const double sd = sqrt((double)d);
     int cur = -1;
-    double qr[G][4];
+    AccT qr[G][4];
     int64_t i = 0;
     for (int64_t g = g_begin; g < g_end; ++g, ++i) {
         const int s = (int)(i % stages);
@@ -177,24 +180,25 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int j = 4 * (lane + 32 * r) + e;
-                    qr[r][e] = j < d ? (double)q[(int64_t)cur * d + j] : 0.0;
+                    qr[r][e] = j < d ? (AccT)q[(int64_t)cur * d + j] : (AccT)0;
                 }
         }
         const int64_t t0 = mt.y, cnt = mt.z, pos0 = mt.w;
         const unsigned char* tile = smem + (size_t)s * tile_bytes;
         const int base_t = 8 * warp;
         if (base_t < cnt) {
-            double p[8];
+            AccT p[8];
             const unsigned char* rows = tile + (int64_t)base_t * row_b;
             if (base_t + 8 <= cnt && d == 128 * G) {
                 // full group of 8 tokens, d a multiple of 128: no bounds checks
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    double acc = 0.0;
+                    AccT acc = 0;
 #pragma unroll
                     for (int r = 0; r < G; ++r) {
-                        double v[4];
-                        RowLd<T>::load(rows + (int64_t)u * row_b, lane + 32 * r, d, v);
+                        AccT v[4];
+                        if constexpr (sizeof(AccT) == 8) RowLd<T>::load(rows + (int64_t)u * row_b, lane + 32 * r, d, v);
+                        else RowLd<T>::loadf(rows + (int64_t)u * row_b, lane + 32 * r, d, v);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) acc = fma(qr[r][e], v[e], acc);
                     }
@@ -203,15 +207,16 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    double acc = 0.0;
+                    AccT acc = 0;
                     if (base_t + u < cnt) {
                         const unsigned char* row = rows + (int64_t)u * row_b;
 #pragma unroll
                         for (int r = 0; r < G; ++r) {
                             const int gg = lane + 32 * r;
                             if (4 * gg < d) {
-                                double v[4];
-                                RowLd<T>::load(row, gg, d, v);
+                                AccT v[4];
+                                if constexpr (sizeof(AccT) == 8) RowLd<T>::load(row, gg, d, v);
+                                else RowLd<T>::loadf(row, gg, d, v);
 #pragma unroll
                                 for (int e = 0; e < 4; ++e)
                                     if (4 * gg + e < d) acc = fma(qr[r][e], v[e], acc);
@@ -221,11 +226,15 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
                     p[u] = acc;
                 }
             }
-            const double dot = tree_8tok(p, lane);
+            const AccT dot = tree_8tok<AccT>(p, lane);
             const int t = (lane >> 2) & 7;
             if ((lane & 3) == 0 && base_t + t < cnt) {
-                double* os = out_score + (int64_t)cur * out_stride;
-                os[pos0 + base_t + t] = scaled ? dot / sd : dot;
+                if constexpr (sizeof(AccT) == 8) {
+                    double* os = out_score + (int64_t)cur * out_stride;
+                    os[pos0 + base_t + t] = scaled ? dot / sd : dot;
+                } else {
+                    out32[(int64_t)cur * out_stride + pos0 + base_t + t] = dot;
+                }
                 if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + base_t + t] = (int32_t)(t0 + base_t + t);
             }
         }
@@ -261,10 +270,10 @@ static bool tma_ok(const void* keys, int64_t lane_stride, int d, int64_t n_lanes
            64 * row * 2 <= 160 * 1024 && n_lanes <= 16384;
 }
 
-template <typename QT, typename T, int G, bool IMPL>
+template <typename QT, typename T, int G, bool IMPL, typename AccT = double>
 static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d,
                             const int32_t* items, int64_t item_stride, const int32_t* n_items, int64_t n_impl,
-                            double* os, int32_t* ot, int64_t ostr, int scaled, cudaStream_t st) {
+                            double* os, int32_t* ot, int64_t ostr, int scaled, cudaStream_t st, float* os32 = nullptr) {
     const int row_b = RowLd<T>::row_bytes(d);
     const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
     const int tile = 64 * row_b;
@@ -273,16 +282,16 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
     const size_t smem = (size_t)stages * tile + 32 * (size_t)stages + 4 * (size_t)(n_lanes + 1) + 16;
     static size_t configured = 0;
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(score_tma_kernel<QT, T, G, IMPL>,
+        cudaError_t e = cudaFuncSetAttribute(score_tma_kernel<QT, T, G, IMPL, AccT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = 200 * 1024;
     }
     const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
     const int grid = sm_count() * per_sm;
-    score_tma_kernel<QT, T, G, IMPL><<<grid, TS_THREADS, smem, st>>>(
+    score_tma_kernel<QT, T, G, IMPL, AccT><<<grid, TS_THREADS, smem, st>>>(
         (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, (int)n_lanes, items, item_stride, n_items, n_impl,
-        os, ot, ostr, stages, tile, scaled);
+        os, os32, ot, ostr, stages, tile, scaled);
     return kvt_check_launch();
 }
 
@@ -382,3 +391,47 @@ extern "C" int kvt_token_scores(const void* q, int q_dtype, const void* keys, in
     return dispatch_score<true>(q, q_dtype, keys, key_dtype, n_lanes, lane_stride, d, nullptr, 0, nullptr, n, out,
                                 nullptr, out_stride, blocks, 1, (cudaStream_t)stream);
 }
+
+// Fast f32 candidate scores (select2.cu pairs them with an error bound): float keys of
+// every dtype except f64; requires the TMA path.
+template <typename QT, typename T>
+static int fast_t(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,
+                  int64_t item_stride, const int32_t* n_items, float* cs32, int32_t* ct, int64_t cstride,
+                  cudaStream_t st) {
+    if (!tma_ok<T>(keys, lane_stride, d, n_lanes)) return KVT_ERR_SHAPE;
+    if (d == 128)
+        return launch_score_tma<QT, T, 1, false, float>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items,
+                                                        0, nullptr, ct, cstride, 0, st, cs32);
+    if (d == 256)
+        return launch_score_tma<QT, T, 2, false, float>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items,
+                                                        0, nullptr, ct, cstride, 0, st, cs32);
+    return KVT_ERR_SHAPE;
+}
+
+extern "C" int kvt_cand_score_f32(const void* q, int q_dtype, const void* keys, int key_dtype, int64_t n_lanes,
+                                  int64_t lane_stride, int d, const int32_t* items, int64_t item_stride,
+                                  const int32_t* n_items, float* cs32, int32_t* ct, int64_t cstride, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!q || !keys || !items || !n_items || !cs32 || !ct || n_lanes < 0) return KVT_ERR_ARG;
+    if (n_lanes == 0) return KVT_OK;
+#define KVT_F(QT, TT) return fast_t<QT, TT>(q, keys, n_lanes, lane_stride, d, items, item_stride, n_items, cs32, ct, cstride, st)
+    if (q_dtype == KVT_F32) {
+        switch (key_dtype) {
+            case KVT_F32: KVT_F(float, float);
+            case KVT_BF16: KVT_F(float, __nv_bfloat16);
+            case KVT_F16: KVT_F(float, __half);
+            case KVT_I4: KVT_F(float, I4);
+        }
+    } else if (q_dtype == KVT_F64) {
+        switch (key_dtype) {
+            case KVT_F32: KVT_F(double, float);
+            case KVT_BF16: KVT_F(double, __nv_bfloat16);
+            case KVT_F16: KVT_F(double, __half);
+            case KVT_I4: KVT_F(double, I4);
+        }
+    }
+#undef KVT_F
+    return KVT_ERR_DTYPE;
+}
+
+bool kvt_fast_ok(int key_dtype, int d) { return key_dtype != KVT_F64 && (d == 128 || d == 256); }

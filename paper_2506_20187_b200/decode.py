@@ -140,9 +140,9 @@ class SparseDecoder:
             m = ops.n_grid_leaves(self.n, self.C[l])
             k = self.k_for(l)
             nc = sum(n_cand[l])
-            out["bounds"] += self.lanes * (m * 2 * d * sA + d * 8 + m * 16)
-            out["plan"] += self.lanes * m * 16 + nc // 64 * 12
-            out["score"] += nc * (d * sK + 12)
+            out["bounds"] += self.lanes * (m * 2 * d * sA + d * 8 + m * 24)       # + U, L, A out
+            out["plan"] += self.lanes * m * 24 + nc // 64 * 12
+            out["score"] += nc * (d * sK + 8)                                      # f32 estimate + token
             out["select"] += nc * 8 + self.lanes * k * 12
             out["runs"] += self.lanes * k * 4 * 3
             out["attn"] += self.lanes * k * (d * sK + 4 + 8) + self.lanes * d * 4

@@ -171,7 +171,7 @@ def abstract_spans(keys: torch.Tensor, lane_of: torch.Tensor, starts: torch.Tens
 
 def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int, C: int = 0,
                  leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
-                 scaled: bool = False):
+                 scaled: bool = False, want_A: bool = False):
     """Sound canonical (U, L) per leaf (importance.py:108-137) -> float64 [n_lanes, max_leaves].
     scaled=False: bounds on raw dots (pipeline); scaled=True: on logits dot/sqrt(d) (API)."""
     require_cuda(q, amax, amin)
@@ -184,10 +184,11 @@ def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int
         maxl = n_grid_leaves(n, C)
     U = torch.empty((nl, max(maxl, 1)), dtype=torch.float64, device=q.device)
     Lo = torch.empty_like(U)
+    A = torch.empty_like(U) if want_A else None
     L.check(L.kvt_chunk_bounds(q.data_ptr(), dtype_code(q), nl, d, n, C, _p(leaf_start), _p(n_leaves), lstride,
                                amax.data_ptr(), amin.data_ptr(), dtype_code(amax), amax.stride(0), U.data_ptr(),
-                               Lo.data_ptr(), U.stride(0), int(scaled), _stream()), "chunk_bounds")
-    return U, Lo
+                               Lo.data_ptr(), _p(A), U.stride(0), int(scaled), _stream()), "chunk_bounds")
+    return (U, Lo, A) if want_A else (U, Lo)
 
 
 # -- K4 ----------------------------------------------------------------------------------------
@@ -209,8 +210,9 @@ def token_scores(q: torch.Tensor, keys: torch.Tensor, n: int | None = None) -> t
 
 def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
                 leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
-                want_cand_leaf: bool = False):
-    """tau + candidate items -> dict(items, n_items, n_cand, cand_leaf, evals)."""
+                want_cand_leaf: bool = False, A: torch.Tensor | None = None, d: int = 0):
+    """tau + candidate items -> dict(items, n_items, n_cand, cand_leaf, evals[, err]).
+    With A (from chunk_bounds(want_A=True)) and d, also the f32 scoring error bound err."""
     nl = U.shape[0]
     maxl = leaf_start.shape[1] if leaf_start is not None else n_grid_leaves(n, C)
     item_cap = (n + ITEM_TOKENS - 1) // ITEM_TOKENS + maxl
@@ -221,11 +223,12 @@ def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
     evals = torch.empty(nl, dtype=torch.int64, device=dev)
     cand_leaf = torch.zeros((nl, max(maxl, 1)), dtype=torch.int8, device=dev) if want_cand_leaf else None
     lstride = leaf_start.shape[1] if leaf_start is not None else maxl
-    L.check(L.kvt_select_plan(nl, n, C, _p(leaf_start), _p(n_leaves), lstride, U.data_ptr(), Lo.data_ptr(),
-                              U.stride(0), k, items.data_ptr(), item_cap, n_items.data_ptr(), n_cand.data_ptr(),
-                              _p(cand_leaf), evals.data_ptr(), _stream()), "select_plan")
+    err = torch.empty(nl, dtype=torch.float64, device=dev) if A is not None else None
+    L.check(L.kvt_select_plan2(nl, n, C, _p(leaf_start), _p(n_leaves), lstride, U.data_ptr(), Lo.data_ptr(),
+                               U.stride(0), k, items.data_ptr(), item_cap, n_items.data_ptr(), n_cand.data_ptr(),
+                               _p(cand_leaf), evals.data_ptr(), _p(A), _p(err), d, _stream()), "select_plan")
     return {"items": items, "n_items": n_items, "n_cand": n_cand, "cand_leaf": cand_leaf, "evals": evals,
-            "item_cap": item_cap}
+            "item_cap": item_cap, "err": err}
 
 
 def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_per_lane: int = 0):
@@ -241,6 +244,43 @@ def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_p
                              plan["items"].data_ptr(), plan["item_cap"], plan["n_items"].data_ptr(), cs.data_ptr(),
                              ct.data_ptr(), cs.stride(0), blocks_per_lane, _stream()), "cand_score")
     return cs, ct
+
+
+def cand_score_f32(q: torch.Tensor, keys, plan: dict, n: int):
+    """Fast f32 estimates of the candidate dots (|err| <= plan["err"]) -> (cs32 f32, cand_tok i32)."""
+    require_cuda(q, keys)
+    ls, d = _lanes(keys)
+    nl = keys.shape[0]
+    cs = torch.empty((nl, max(n, 1)), dtype=torch.float32, device=q.device)
+    ct = torch.empty((nl, max(n, 1)), dtype=torch.int32, device=q.device)
+    L.check(L.kvt_cand_score_f32(q.data_ptr(), dtype_code(q), keys.data_ptr(), dtype_code(keys), nl, ls, d,
+                                 plan["items"].data_ptr(), plan["item_cap"], plan["n_items"].data_ptr(), cs.data_ptr(),
+                                 ct.data_ptr(), cs.stride(0), _stream()), "cand_score_f32")
+    return cs, ct
+
+
+def topk_select_band(cs32: torch.Tensor, ct: torch.Tensor, plan: dict, k: int, q: torch.Tensor, keys,
+                     want_runs: bool = True):
+    """Exact canonical top-k from f32 estimates (band re-scoring) -> (sel_tok, sel_score, n_sel[, runs])."""
+    ls, d = _lanes(keys)
+    nl = cs32.shape[0]
+    dev = cs32.device
+    st = torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev)
+    ss = torch.empty((nl, max(k, 1)), dtype=torch.float64, device=dev)
+    ns = torch.empty(nl, dtype=torch.int32, device=dev)
+    runs = None
+    if want_runs:
+        runs = {"run_start": torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev),
+                "run_len": torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev),
+                "n_runs": torch.empty(nl, dtype=torch.int32, device=dev)}
+    L.check(L.kvt_topk_select_band(cs32.data_ptr(), ct.data_ptr(), plan["n_cand"].data_ptr(), cs32.stride(0),
+                                   plan["err"].data_ptr(), nl, k, q.data_ptr(), dtype_code(q), keys.data_ptr(),
+                                   dtype_code(keys), ls, d, st.data_ptr(), ss.data_ptr(), st.stride(0), ns.data_ptr(),
+                                   _p(runs["run_start"]) if runs else None, _p(runs["run_len"]) if runs else None,
+                                   st.stride(0), _p(runs["n_runs"]) if runs else None, _stream()), "topk_select_band")
+    if want_runs:
+        return st[:, :k], ss[:, :k], ns, runs
+    return st[:, :k], ss[:, :k], ns
 
 
 def topk_select(cs: torch.Tensor, ct: torch.Tensor, n_cand: torch.Tensor, k: int, want_runs: bool = False):
@@ -327,9 +367,9 @@ class LayerWorkspace:
         self.key = (n_lanes, n_cap, max_leaves, d)
 
 
-def select_attend(q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor,
+def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch.Tensor,
                   n: int, k: int, C: int, ws: LayerWorkspace, out: dict, attn_splits: int = 0,
-                  score_blocks: int = 0) -> None:
+                  score_blocks: int = 0, exact_scores: bool = False) -> None:
     """One layer, all lanes: K3 -> plan -> K4 -> K5 -> K6 -> K7 into the caller's `out` buffers
     (sel_tok, sel_score, n_sel, run_start, run_len, n_runs, out, evals)."""
     ls, d = _lanes(keys)
@@ -347,7 +387,7 @@ def select_attend(q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, ama
     a.n_runs = _p(out.get("n_runs"))
     a.out = _p(out.get("out"))
     a.evals = _p(out.get("evals"))
-    a.attn_splits, a.score_blocks = attn_splits, score_blocks
+    a.attn_splits, a.score_blocks, a.exact_scores = attn_splits, score_blocks, int(exact_scores)
     L.check(L.kvt_select_attend(a, ws.buf.data_ptr(), ws.bytes, _stream()), "select_attend")
 
 

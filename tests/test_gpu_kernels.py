@@ -110,6 +110,16 @@ def _lane_data(kind, lanes, n, d, seed):
         K = np.ones((lanes, n, d), np.float32)
         K[:, ::7] = 2.0
         return K, rng.normal(size=(lanes, n, d)).astype(np.float32), np.ones((lanes, d), np.float32)
+    if kind == "neartie":
+        # many keys whose dots differ by a few f64 ulps only: the f32 estimates tie, the
+        # canonical f64 dots do not -> exercises the band re-scoring
+        rng = np.random.default_rng(seed)
+        K = rng.normal(size=(lanes, n, d)).astype(np.float32)
+        Q = np.ones((lanes, d), np.float32)
+        base = np.full(d, 0.25, np.float32)
+        K[:, : n // 3] = base
+        K[:, : n // 3, 0] += (np.arange(n // 3) % 97 * 2.0 ** -20).astype(np.float32)
+        return K, rng.normal(size=(lanes, n, d)).astype(np.float32), Q
     K = np.empty((lanes, n, d), np.float32)
     V = np.empty_like(K)
     Q = np.empty((lanes, d), np.float32)
@@ -119,10 +129,11 @@ def _lane_data(kind, lanes, n, d, seed):
     return K, V, Q
 
 
-@pytest.mark.parametrize("kind", ["random", "planted", "ties"])
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("kind", ["random", "planted", "ties", "neartie"])
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 @pytest.mark.parametrize("n,C,rate", [(4096, 64, 0.10), (1000, 8, 0.5), (65536, 64, 0.10), (33, 4, 0.1)])
-def test_fused_select_attend_matches_oracle(ops, kind, dt, n, C, rate):
+def test_fused_select_attend_matches_oracle(ops, kind, dt, n, C, rate, exact):
     lanes, d = (4 if n <= 4096 else 2), 128
     K, V, Q = _lane_data(kind, lanes, n, d, seed=n + C)
     k = math.ceil(rate * n)
@@ -139,7 +150,7 @@ def test_fused_select_attend_matches_oracle(ops, kind, dt, n, C, rate):
            "n_runs": torch.empty(lanes, dtype=torch.int32, device="cuda"),
            "out": torch.empty((lanes, d), dtype=torch.float32, device="cuda"),
            "evals": torch.empty(lanes, dtype=torch.int64, device="cuda")}
-    ops.select_attend(qt, kt, vt, amax, amin, n, k, C, ws, out)
+    ops.select_attend(qt, kt, vt, amax, amin, n, k, C, ws, out, exact_scores=exact)
     torch.cuda.synchronize()
     Kh = kt.double().cpu().numpy()
     Vh = vt.double().cpu().numpy()
@@ -149,7 +160,11 @@ def test_fused_select_attend_matches_oracle(ops, kind, dt, n, C, rate):
         ref = O.topk(s, k)
         got = out["sel_tok"][i].cpu().numpy().astype(np.int64)
         assert np.array_equal(got, ref), (kind, dt, n, i)
-        assert np.array_equal(out["sel_score"][i].cpu().numpy(), s[ref])
+        if exact:
+            assert np.array_equal(out["sel_score"][i].cpu().numpy(), s[ref])
+        else:  # f32 estimates for the sure tokens, canonical for the band
+            A = np.abs(Q[i]).astype(np.float64) @ np.abs(Kh[i]).max(0)
+            assert np.all(np.abs(out["sel_score"][i].cpu().numpy() - s[ref]) <= 1e-6 * A)
         runs = O.runs(ref)
         nr = int(out["n_runs"][i])
         assert nr == len(runs)

@@ -34,7 +34,7 @@ def test_abi_rejects_bad_arguments_without_gpu():
     """Argument validation happens before any CUDA call, so it is testable on CPU."""
     from paper_2506_20187_b200 import _lib as L
     assert L.kvt_select_plan(1, 10, 4, None, None, 0, 1, 1, 3, 11, 1, 1, 1, 1, None, None, None) == L.ERR_K
-    assert L.kvt_chunk_bounds(None, 0, 1, 4, 10, 4, None, None, 0, None, None, 0, 0, None, None, 0, 0, None) == L.ERR_ARG
+    assert L.kvt_chunk_bounds(None, 0, 1, 4, 10, 4, None, None, 0, None, None, 0, 0, None, None, None, 0, 0, None) == L.ERR_ARG
     assert L.kvt_topk_select(1, 1, 1, 1, 1, -1, 1, 1, 1, 1, None) == L.ERR_K
     with pytest.raises(ValueError):
         L.check(L.ERR_K, "x")
