@@ -138,14 +138,18 @@ KVT_API int kvt_cand_score(const void* q, int q_dtype, const void* keys, int key
                    int32_t* cand_tok, int64_t cand_stride, int blocks_per_lane, void* stream);
 
 /* ---- fast scoring: f32 estimates + exact band re-scoring ---------------------------------
- * kvt_select_plan2 = kvt_select_plan that also writes err[i] = a rigorous bound on
- * |f32 estimate - canonical f64 dot| over lane i's candidates (from the chunks' A of
- * kvt_chunk_bounds; d is the head dim).  kvt_cand_score_f32 writes the f32 estimates
- * (TMA pipeline, any key dtype but F64).  kvt_topk_select_band selects the exact canonical
- * top-k from them: 32-bit radix select for the k-th estimate T, tokens above T + 2 err are
- * in, below T - 2 err out, and the band in between is re-scored canonically in f64 from the
- * key rows (q: [n_lanes][d]); a wide band (ties) falls back to full canonical re-scoring.
- * Output as kvt_topk_select_runs (sel_score: estimate for sure tokens, exact for the band). */
+ * kvt_select_plan2 = kvt_select_plan that also writes a 4-double record per lane:
+ * err[4i] = E, a rigorous bound on |f32 estimate - canonical f64 dot| over lane i's
+ * candidates (from the chunks' A of kvt_chunk_bounds; d is the head dim), err[4i+1] = tau
+ * (<= the k-th canonical dot), err[4i+2] = max U over the candidates.
+ * kvt_cand_score_f32 writes the f32 estimates (TMA pipeline, any key dtype but F64).
+ * kvt_topk_select_band (one CTA per lane) selects the exact canonical top-k from them:
+ * linear-bucket histogram over [tau - 2E, Umax + 2E] + radix select inside the k-th bucket
+ * give the exact k-th estimate T; tokens above T + 2E are in, below T - 2E out, and the band
+ * in between is re-scored canonically in f64 from the key rows (q: [n_lanes][d]).  A wide
+ * band (ties) falls back to canonical re-scoring of every candidate into `scratch` (f64,
+ * cand_stride per lane).  Output as kvt_topk_select_runs (sel_score: the estimate for the
+ * sure tokens, exact for the band / fallback). */
 KVT_API int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start,
                     const int32_t* n_leaves, int64_t leaf_stride, const double* U, const double* L,
                     int64_t bnd_stride, int64_t k, int32_t* items, int64_t item_stride,
@@ -158,7 +162,7 @@ KVT_API int kvt_cand_score_f32(const void* q, int q_dtype, const void* keys, int
 KVT_API int kvt_topk_select_band(const float* cand_score32, const int32_t* cand_tok,
                     const int32_t* n_cand, int64_t cand_stride, const double* err, int64_t n_lanes,
                     int64_t k, const void* q, int q_dtype, const void* keys, int key_dtype,
-                    int64_t lane_stride, int d, int32_t* sel_tok, double* sel_score,
+                    int64_t lane_stride, int d, double* scratch, int32_t* sel_tok, double* sel_score,
                     int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len,
                     int64_t run_stride, int32_t* n_runs, void* stream);
 

@@ -71,7 +71,7 @@ kvt_select_plan2 = _sig("kvt_select_plan2", ctypes.c_int, _i64, _i64, _i32, _vp,
 kvt_cand_score_f32 = _sig("kvt_cand_score_f32", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _vp,
                           _vp, _vp, _i64, _vp)
 kvt_topk_select_band = _sig("kvt_topk_select_band", ctypes.c_int, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i32,
-                            _vp, _i32, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp)
+                            _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp)
 kvt_token_scores = _sig("kvt_token_scores", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i64,
                         _vp)
 kvt_select_plan = _sig("kvt_select_plan", ctypes.c_int, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp,

@@ -60,6 +60,7 @@ struct LayerWs {
     double *U, *L, *A, *err;
     int32_t *items, *n_items, *n_cand;
     double* cand_score;
+    float* cs32;
     int32_t* cand_tok;
     char* attn_part;
     size_t bytes;
@@ -72,12 +73,13 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     w.U = c.take<double>((size_t)(n_lanes * max_leaves));
     w.L = c.take<double>((size_t)(n_lanes * max_leaves));
     w.A = c.take<double>((size_t)(n_lanes * max_leaves));
-    w.err = c.take<double>((size_t)n_lanes);
+    w.err = c.take<double>((size_t)(n_lanes * 4));
     w.items = c.take<int32_t>((size_t)(n_lanes * item_cap * 3));
     w.n_items = c.take<int32_t>((size_t)n_lanes);
     w.n_cand = c.take<int32_t>((size_t)n_lanes);
     w.cand_score = c.take<double>((size_t)(n_lanes * n));
     w.cand_tok = c.take<int32_t>((size_t)(n_lanes * n));
+    w.cs32 = c.take<float>((size_t)(n_lanes * n));
     w.attn_part = c.take<char>(kvt_attn_workspace_bytes(n_lanes, d, MAX_SPLITS));  // tickets + partials
     w.bytes = c.used;
     return w;
@@ -120,13 +122,12 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
                           fast ? w.err : nullptr, a->d, stream);
     if (rc) return rc;
     if (fast) {
-        float* cs32 = reinterpret_cast<float*>(w.cand_score);
         rc = kvt_cand_score_f32(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items,
-                                item_cap, w.n_items, cs32, w.cand_tok, a->n, stream);
+                                item_cap, w.n_items, w.cs32, w.cand_tok, a->n, stream);
         if (rc) return rc;
-        rc = kvt_topk_select_band(cs32, w.cand_tok, w.n_cand, a->n, w.err, a->n_lanes, a->k, a->q, a->q_dtype,
-                                  a->keys, a->key_dtype, a->lane_stride, a->d, a->sel_tok, a->sel_score, a->k,
-                                  a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);
+        rc = kvt_topk_select_band(w.cs32, w.cand_tok, w.n_cand, a->n, w.err, a->n_lanes, a->k, a->q, a->q_dtype,
+                                  a->keys, a->key_dtype, a->lane_stride, a->d, w.cand_score, a->sel_tok,
+                                  a->sel_score, a->k, a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);
         if (rc) return rc;
     } else {
 

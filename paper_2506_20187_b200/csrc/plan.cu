@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
 
     // ---- candidate compaction -> items (+ max A over candidates for the f32 error bound) ----
     long long carry_items = 0, carry_tok = 0;
-    double amax_c = 0.0;
+    double amax_c = 0.0, umax_c = -INFINITY;
     for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
         const int64_t c = base + tid;
         long long it = 0, tk = 0;
@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
             cand = Ul[c] >= tau;
             if (cand) { tk = rows; it = (rows + ITEM_TOKENS - 1) / ITEM_TOKENS; }
             if (cand && A) amax_c = fmax(amax_c, A[li * bnd_stride + c]);
+            if (cand) umax_c = fmax(umax_c, Ul[c]);
             if (cand_leaf) cand_leaf[li * leaf_stride + c] = cand ? 1 : 0;
         }
         long long tot_it, tot_tk;
@@ -139,17 +140,23 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
         carry_tok += tot_tk;
     }
     if (err) {
-        // block max of amax_c (reuse hist as scratch)
+        // err record per lane: [bound on |f32 estimate - canonical dot|, tau, max U over candidates, 0]
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) amax_c = fmax(amax_c, __shfl_xor_sync(KVT_FULL, amax_c, off));
+        for (int off = 16; off >= 1; off >>= 1) {
+            amax_c = fmax(amax_c, __shfl_xor_sync(KVT_FULL, amax_c, off));
+            umax_c = fmax(umax_c, __shfl_xor_sync(KVT_FULL, umax_c, off));
+        }
         __syncthreads();
         double* red = reinterpret_cast<double*>(hist);
-        if (lane == 0) red[tid >> 5] = amax_c;
+        if (lane == 0) { red[tid >> 5] = amax_c; red[32 + (tid >> 5)] = umax_c; }
         __syncthreads();
         if (tid == 0) {
-            double m = 0.0;
-            for (int w = 0; w < PLAN_THREADS / 32; ++w) m = fmax(m, red[w]);
-            err[li] = m * err_factor;  // |f32 estimate - canonical dot| <= err for every candidate
+            double m = 0.0, um = -INFINITY;
+            for (int w = 0; w < PLAN_THREADS / 32; ++w) { m = fmax(m, red[w]); um = fmax(um, red[32 + w]); }
+            err[li * 4 + 0] = m * err_factor;
+            err[li * 4 + 1] = tau;
+            err[li * 4 + 2] = um;
+            err[li * 4 + 3] = 0.0;
         }
     }
     if (tid == 0) {

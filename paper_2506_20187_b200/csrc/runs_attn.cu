@@ -121,7 +121,7 @@ __device__ __forceinline__ void attn_finish(double* __restrict__ part, int split
                                             double* __restrict__ out64, double scale) {
     __shared__ int s_last;
     __shared__ double s_scale[64];
-    __shared__ double s_M, s_den;
+    __shared__ double s_den;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -147,7 +147,7 @@ __device__ __forceinline__ void attn_finish(double* __restrict__ part, int split
         }
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(KVT_FULL, den, off);
-        if (threadIdx.x == 0) { s_M = M; s_den = den; }
+        if (threadIdx.x == 0) s_den = den;
     }
     __syncthreads();
     const double den = s_den;

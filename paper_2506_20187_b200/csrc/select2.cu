@@ -1,4 +1,5 @@
-// select2.cu -- K5 on fast f32 scores, exact by construction.
+// select2.cu -- K5 on fast f32 scores, exact by construction; the cluster-per-lane variant
+// used when there are too few lanes to fill the GPU with one CTA each (select3.cu).
 //
 // K4's f32 estimate s of each candidate's canonical f64 dot c satisfies |s - c| <= E, a
 // rigorous per-lane bound computed by the plan (E = err_factor * max A over candidates,
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(S2_THREADS) topk_select2_kernel(
             if (shift == 16) build_list<uint32_t>(S, k32, cnt);
         }
         const double Tk = (double)key32_to_float((uint32_t)S.prefix);
-        const double E = err[li];
+        const double E = err[li * 4];  // plan record: [E, tau, Umax, 0]
         hi = Tk + 2.0 * E;
         lo_ = Tk - 2.0 * E;
         // ---- count sure tokens and the band ----
@@ -455,7 +456,7 @@ static int launch_select2(const float* cs32, const int32_t* ctok, const int32_t*
     return kvt_check_launch();
 }
 
-extern "C" int kvt_topk_select_band(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
+int kvt_topk_select_band_cluster(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
                          const double* err, int64_t n_lanes, int64_t k, const void* q, int q_dtype, const void* keys,
                          int key_dtype, int64_t lane_stride, int d, int32_t* sel_tok, double* sel_score,
                          int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len, int64_t run_stride,

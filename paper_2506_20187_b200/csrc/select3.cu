@@ -1,0 +1,527 @@
+// select3.cu -- K5 (fast path): exact canonical top-k from K4's f32 estimates, one CTA per lane.
+//
+// The plan supplies, per lane, E (a rigorous bound on |f32 estimate s - canonical f64 dot c|
+// for every candidate), tau (<= the k-th canonical dot) and Umax (>= every candidate's c).
+// 1. Histogram the estimates into 4096 linear buckets over [tau - 2E, Umax + 2E] (the range
+//    adapts to the lane's score spread); the bucket holding the k-th estimate is found by a
+//    block scan, its members gathered into shared memory and radix-selected (32-bit keys) to
+//    get the exact k-th largest estimate T.
+// 2. s > T + 2E  =>  c > S_k (selected);  s < T - 2E  =>  c < S_k (not selected): only the
+//    band [T - 2E, T + 2E] -- typically a handful of tokens -- is re-scored canonically in
+//    f64 from the key rows and ranked by (c desc, token asc) to fill the remaining slots.
+// 3. Stable warp-ballot compaction writes the set in ascending token order; the run scan
+//    (engine.py:176-183) is fused.
+// A wide band or an overfull bucket (heavy ties) takes the exact fallback: canonical f64
+// re-scoring of every candidate into `scratch` and a 64-bit radix select over it.  The
+// result is always the oracle's canonical top-k set (score desc, index asc).
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace kvt {
+
+constexpr int S3_THREADS = 1024;
+constexpr int S3_WARPS = S3_THREADS / 32;
+constexpr int S3_BINS = 4096;
+constexpr int S3_LIST_CAP = 8192;
+constexpr int S3_BAND_CAP = 1024;
+
+struct S3Shared {
+    unsigned int hist[S3_BINS];
+    double band_c[S3_BAND_CAP];
+    int band_t[S3_BAND_CAP];
+    unsigned char band_sel[S3_BAND_CAP];
+    unsigned int rh[256];
+    long long scan_sh[33];
+    long long warp_cnt[S3_WARPS];
+    unsigned long long prefix, mask;
+    unsigned int list_n, remaining;
+    int bstar;
+    long long above;
+};
+
+__device__ __forceinline__ int s3_bucket(double s, double lo, double inv) {
+    if (s < lo) return -1;
+    const double x = (s - lo) * inv;
+    return x >= (double)(S3_BINS - 1) ? S3_BINS - 1 : (int)x;
+}
+
+// Block-wide: find the digit bin of `hist` (nb bins, descending order) where the running
+// count from the top reaches `want`; returns (bin, count strictly above it) via S.
+__device__ __forceinline__ void s3_find_bin(S3Shared& S, const unsigned int* hist, int nb, long long want) {
+    const int tid = threadIdx.x;
+    const int per = (nb + S3_THREADS - 1) / S3_THREADS;
+    long long loc = 0;
+    for (int j = 0; j < per; ++j) {
+        const int b = nb - 1 - (tid * per + j);
+        if (b >= 0) loc += hist[b];
+    }
+    long long tot;
+    const long long ex = block_excl_scan<long long>(loc, S.scan_sh, tot);
+    if (ex < want && want <= ex + loc) {
+        long long run = ex;
+        for (int j = 0; j < per; ++j) {
+            const int b = nb - 1 - (tid * per + j);
+            if (b < 0) break;
+            if (run + hist[b] >= want) {
+                S.bstar = b;
+                S.above = run;
+                break;
+            }
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+}
+
+// Radix select on the shared list of 32-bit keys: exact key of the `want`-th largest.
+__device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* keys, int n, long long want) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)want; }
+    __syncthreads();
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += S3_THREADS) S.rh[i] = 0;
+        __syncthreads();
+        const uint32_t pf = (uint32_t)S.prefix, mk = (uint32_t)S.mask;
+        for (int base = 0; base < n; base += S3_THREADS) {
+            const int i = base + tid;
+            int dg = 256;
+            if (i < n && (keys[i] & mk) == pf) dg = (keys[i] >> shift) & 0xff;
+            const unsigned peers = __match_any_sync(KVT_FULL, dg);
+            if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&S.rh[dg], (unsigned)__popc(peers));
+        }
+        __syncthreads();
+        if (tid < 32) {
+            unsigned loc[8], ls = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { loc[i] = S.rh[255 - 8 * lane - i]; ls += loc[i]; }
+            const unsigned inc = warp_incl_scan(ls, lane), exc = inc - ls, rem = S.remaining;
+            if (exc < rem && rem <= inc) {
+                unsigned run = exc;
+                for (int i = 0; i < 8; ++i) {
+                    if (run + loc[i] >= rem) {
+                        const int b = 255 - 8 * lane - i;
+                        S.prefix = pf | ((uint32_t)b << shift);
+                        S.mask = mk | (0xffu << shift);
+                        S.remaining = rem - run;
+                        break;
+                    }
+                    run += loc[i];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    return (uint32_t)S.prefix;
+}
+
+// Stable warp-ballot compaction helper: warp w owns the contiguous range
+// [w*per, (w+1)*per) of [0, n) and walks it 32 elements at a time.
+struct WarpRange {
+    int64_t a, b;
+    __device__ WarpRange(int64_t n, int warp) {
+        const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 31) / 32 * 32;
+        a = kvt::imin(n, warp * per);
+        b = kvt::imin(n, a + per);
+    }
+};
+
+template <typename QT, typename T>
+__device__ __forceinline__ double s3_canon(const QT* q, const unsigned char* row, int d, int lane) {
+    double acc = 0.0;
+    for (int g = lane; 4 * g < d; g += 32) {
+        double v[4];
+        RowLd<T>::load(row, g, d, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (4 * g + e < d) acc = fma((double)q[4 * g + e], v[e], acc);
+    }
+    return tree_allreduce(acc);
+}
+
+template <typename QT, typename T>
+__global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
+    const float* __restrict__ cs32, const int32_t* __restrict__ ctok, const int32_t* __restrict__ n_cand,
+    int64_t cand_stride, const double* __restrict__ rec, int64_t k, const QT* __restrict__ q,
+    const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, double* __restrict__ scratch,
+    int32_t* __restrict__ sel_tok, double* __restrict__ sel_score, int64_t sel_stride, int32_t* __restrict__ n_sel,
+    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs) {
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    __shared__ S3Shared S;
+    uint32_t* lkey = reinterpret_cast<uint32_t*>(dyn_smem);
+    int32_t* lpos = reinterpret_cast<int32_t*>(lkey + S3_LIST_CAP);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t li = blockIdx.x;
+    const int64_t n = n_cand[li];
+    const int64_t kk = kvt::imin(k, n);
+    const float* sc = cs32 + li * cand_stride;
+    const int32_t* tk = ctok + li * cand_stride;
+    const QT* ql = q + li * d;
+    const unsigned char* kl = keys + li * lane_stride_b;
+    int32_t* otok = sel_tok + li * sel_stride;
+    double* osc = sel_score + li * sel_stride;
+    if (kk <= 0) {
+        if (tid == 0) { n_sel[li] = 0; if (run_start) n_runs[li] = 0; }
+        return;
+    }
+    const double E = rec[li * 4 + 0];
+    const double lo = rec[li * 4 + 1] - 2.0 * E;
+    const double hi = rec[li * 4 + 2] + 2.0 * E;
+    const double inv = hi > lo ? (double)S3_BINS / (hi - lo) : 0.0;
+
+    // ---- 1. bucket histogram of the estimates ----
+    for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
+    if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; }
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += S3_THREADS) {
+        const int64_t i = base + tid;
+        const int b = i < n ? s3_bucket((double)sc[i], lo, inv) : -1;
+        const unsigned peers = __match_any_sync(KVT_FULL, b);
+        if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    s3_find_bin(S, S.hist, S3_BINS, kk);
+    const int bstar = S.bstar;
+    const long long need_in_bucket = kk - S.above;
+    // gather the bucket
+    for (int64_t base = 0; base < n; base += S3_THREADS) {
+        const int64_t i = base + tid;
+        const bool m = i < n && s3_bucket((double)sc[i], lo, inv) == bstar;
+        const unsigned ballot = __ballot_sync(KVT_FULL, m);
+        unsigned wb = 0;
+        if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
+        wb = __shfl_sync(KVT_FULL, wb, 0);
+        if (m) {
+            const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
+            if (slot < S3_LIST_CAP) { lkey[slot] = ord_key32(sc[i]); lpos[slot] = (int32_t)i; }
+        }
+    }
+    __syncthreads();
+    bool fallback = bstar < 0 || S.list_n > S3_LIST_CAP;
+    double hb = 0.0, lb = 0.0;
+    long long need = 0;
+    const WarpRange wr(n, warp);
+    if (!fallback) {
+        const uint32_t T32 = s3_list_select(S, lkey, (int)S.list_n, need_in_bucket);
+        const double Tk = (double)key32_to_float(T32);
+        hb = Tk + 2.0 * E;
+        lb = Tk - 2.0 * E;
+        // ---- 2. sure tokens and the band (stable order per warp range) ----
+        long long nsure = 0, nband = 0;
+        for (int64_t base = wr.a; base < wr.b; base += 32) {
+            const int64_t i = base + lane;
+            const double s = i < wr.b ? (double)sc[i] : -INFINITY;
+            nsure += __popc(__ballot_sync(KVT_FULL, i < wr.b && s > hb));
+            nband += __popc(__ballot_sync(KVT_FULL, i < wr.b && s >= lb && s <= hb));
+        }
+        if (lane == 0) S.warp_cnt[warp] = nband;
+        long long tot_sure;
+        block_excl_scan<long long>(lane == 0 ? nsure : 0, S.scan_sh, tot_sure);
+        long long band_base = 0, tot_band = 0;
+        for (int w = 0; w < S3_WARPS; ++w) {
+            if (w < warp) band_base += S.warp_cnt[w];
+            tot_band += S.warp_cnt[w];
+        }
+        need = kk - tot_sure;
+        if (tot_band > S3_BAND_CAP) {
+            fallback = true;
+        } else {
+            long long pos = band_base;
+            for (int64_t base = wr.a; base < wr.b; base += 32) {
+                const int64_t i = base + lane;
+                const double s = i < wr.b ? (double)sc[i] : -INFINITY;
+                const bool m = i < wr.b && s >= lb && s <= hb;
+                const unsigned ballot = __ballot_sync(KVT_FULL, m);
+                if (m) S.band_t[pos + __popc(ballot & ((1u << lane) - 1))] = tk[i];
+                pos += __popc(ballot);
+            }
+            __syncthreads();
+            for (int j = warp; j < (int)tot_band; j += S3_WARPS) {
+                const double c = s3_canon<QT, T>(ql, kl + (int64_t)S.band_t[j] * row_b, d, lane);
+                if (lane == 0) S.band_c[j] = c;
+            }
+            __syncthreads();
+            for (int j = tid; j < (int)tot_band; j += S3_THREADS) {
+                const double cj = S.band_c[j];
+                const int tj = S.band_t[j];
+                long long better = 0;
+                for (int f = 0; f < (int)tot_band; ++f) {
+                    const double cf = S.band_c[f];
+                    better += (cf > cj) || (cf == cj && S.band_t[f] < tj);
+                }
+                S.band_sel[j] = better < need ? 1 : 0;
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+
+    unsigned long long fpref = 0, fmask = 0;
+    long long eq_take_total = 0;
+    if (fallback) {
+        // ---- exact fallback: canonical f64 for every candidate, 64-bit radix select ----
+        double* sc64 = scratch + li * cand_stride;
+        for (int64_t base = (int64_t)warp * 8; base < n; base += (int64_t)S3_WARPS * 8) {
+            double p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                double acc = 0.0;
+                if (base + u < n) {
+                    const unsigned char* row = kl + (int64_t)tk[base + u] * row_b;
+                    for (int g = lane; 4 * g < d; g += 32) {
+                        double v[4];
+                        RowLd<T>::load(row, g, d, v);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (4 * g + e < d) acc = fma((double)ql[4 * g + e], v[e], acc);
+                    }
+                }
+                p[u] = acc;
+            }
+            const double dot = tree_8tok<double>(p, lane);
+            const int t = (lane >> 2) & 7;
+            if ((lane & 3) == 0 && base + t < n) sc64[base + t] = dot;
+        }
+        __syncthreads();
+        if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)kk; }
+        __syncthreads();
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int i = tid; i < 256; i += S3_THREADS) S.rh[i] = 0;
+            __syncthreads();
+            const unsigned long long pf = S.prefix, mk = S.mask;
+            for (int64_t base = 0; base < n; base += S3_THREADS) {
+                const int64_t i = base + tid;
+                int dg = 256;
+                if (i < n) {
+                    const uint64_t key = ord_key(sc64[i]);
+                    if ((key & mk) == pf) dg = (int)((key >> shift) & 0xff);
+                }
+                const unsigned peers = __match_any_sync(KVT_FULL, dg);
+                if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&S.rh[dg], (unsigned)__popc(peers));
+            }
+            __syncthreads();
+            if (tid < 32) {
+                unsigned loc[8], ls = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { loc[i] = S.rh[255 - 8 * lane - i]; ls += loc[i]; }
+                const unsigned inc = warp_incl_scan(ls, lane), exc = inc - ls, rem = S.remaining;
+                if (exc < rem && rem <= inc) {
+                    unsigned run = exc;
+                    for (int i = 0; i < 8; ++i) {
+                        if (run + loc[i] >= rem) {
+                            const int b = 255 - 8 * lane - i;
+                            S.prefix = pf | ((unsigned long long)b << shift);
+                            S.mask = mk | (0xffull << shift);
+                            S.remaining = rem - run;
+                            break;
+                        }
+                        run += loc[i];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        fpref = S.prefix;
+        fmask = S.mask;
+        eq_take_total = S.remaining;
+    }
+
+    // ---- 3. stable compaction, ascending token order ----
+    auto is_sel = [&](int64_t i, long long& band_idx, long long& eq_seen, double& score) -> bool {
+        if (!fallback) {
+            const double s = (double)sc[i];
+            score = s;
+            if (s > hb) return true;
+            if (s >= lb) {
+                const long long j = band_idx++;
+                score = S.band_c[j];
+                return S.band_sel[j] != 0;
+            }
+            return false;
+        }
+        const double c = scratch[li * cand_stride + i];
+        score = c;
+        const uint64_t key = ord_key(c);
+        if (key > fpref) return true;  // fmask is all ones after 8 passes
+        if (key == fpref) return eq_seen++ < eq_take_total;
+        return false;
+    };
+    (void)fmask;
+    // count per warp (band / tie order follows the same warp-range order)
+    long long cnt_sel = 0, cnt_band = 0, cnt_eq = 0;
+    for (int64_t base = wr.a; base < wr.b; base += 32) {
+        const int64_t i = base + lane;
+        bool m = false;
+        if (i < wr.b) {
+            if (!fallback) {
+                const double s = (double)sc[i];
+                m = s > hb;
+                const bool bd = !m && s >= lb;
+                cnt_band += __popc(__ballot_sync(KVT_FULL, bd));
+                (void)bd;
+            } else {
+                const uint64_t key = ord_key(scratch[li * cand_stride + i]);
+                m = key > fpref;
+                cnt_eq += __popc(__ballot_sync(KVT_FULL, key == fpref));
+            }
+        } else {
+            if (!fallback) cnt_band += __popc(__ballot_sync(KVT_FULL, false));
+            else cnt_eq += __popc(__ballot_sync(KVT_FULL, false));
+        }
+        cnt_sel += __popc(__ballot_sync(KVT_FULL, m));
+    }
+    // band/eq members before this warp, and their selected counts
+    __shared__ long long w_band[S3_WARPS], w_eq[S3_WARPS], w_sel[S3_WARPS];
+    if (lane == 0) { w_band[warp] = cnt_band; w_eq[warp] = cnt_eq; w_sel[warp] = cnt_sel; }
+    __syncthreads();
+    long long band_before = 0, eq_before = 0;
+    for (int w = 0; w < warp; ++w) { band_before += w_band[w]; eq_before += w_eq[w]; }
+    long long extra = 0;  // band / tie members of this warp that are selected
+    if (!fallback) {
+        for (long long j = band_before; j < band_before + cnt_band; ++j) extra += S.band_sel[j];
+    } else {
+        extra = max(0LL, min(cnt_eq, eq_take_total - eq_before));
+    }
+    __syncthreads();
+    if (lane == 0) w_sel[warp] = cnt_sel + extra;
+    __syncthreads();
+    long long out_base = 0;
+    for (int w = 0; w < warp; ++w) out_base += w_sel[w];
+    long long pos = out_base;
+    const long long p_begin = pos;
+    long long band_idx = band_before, eq_seen = eq_before;
+    for (int64_t base = wr.a; base < wr.b; base += 32) {
+        // lanes resolve their element in order within the 32-wide window
+        bool m = false;
+        double score = 0.0;
+        const int64_t i = base + lane;
+        // band / tie counters must advance in element order: serialise the rare members
+        bool special = false;
+        if (i < wr.b) {
+            if (!fallback) { const double s = (double)sc[i]; special = !(s > hb) && s >= lb; }
+            else special = ord_key(scratch[li * cand_stride + i]) == fpref;
+        }
+        const unsigned sp = __ballot_sync(KVT_FULL, special);
+        if (i < wr.b) {
+            if (special) {
+                const int before = __popc(sp & ((1u << lane) - 1));
+                long long bi = band_idx + before, es = eq_seen + before;
+                m = is_sel(i, bi, es, score);
+            } else {
+                long long dummy1 = 0, dummy2 = 0;
+                m = is_sel(i, dummy1, dummy2, score);
+            }
+        }
+        band_idx += __popc(sp);
+        eq_seen += __popc(sp);
+        const unsigned ballot = __ballot_sync(KVT_FULL, m);
+        if (m) {
+            const long long p = pos + __popc(ballot & ((1u << lane) - 1));
+            otok[p] = tk[i];
+            osc[p] = score;
+        }
+        pos += __popc(ballot);
+    }
+    if (tid == 0) n_sel[li] = (int32_t)kk;
+    if (!run_start) return;
+
+    // ---- 4. fused run scan (engine.py:176-183); each lane takes a slice of its warp's output ----
+    const long long wlen = pos - p_begin;
+    const long long lper = (wlen + 31) / 32;
+    const long long p_lo = p_begin + kvt::imin(wlen, lane * lper);
+    const long long p_hi = p_begin + kvt::imin(wlen, (lane + 1) * lper);
+    __syncthreads();
+    long long heads = 0;
+    for (long long p = p_lo; p < p_hi; ++p) heads += (p == 0 || otok[p] != otok[p - 1] + 1);
+    long long tot_h;
+    const long long ex_h = block_excl_scan<long long>(heads, S.scan_sh, tot_h);
+    int32_t* rs = run_start + li * run_stride;
+    int32_t* rl = run_len + li * run_stride;
+    long long ridx = ex_h - 1;
+    for (long long p = p_lo; p < p_hi; ++p) {
+        if (p == 0 || otok[p] != otok[p - 1] + 1) {
+            ++ridx;
+            rs[ridx] = otok[p];
+            rl[ridx] = (int32_t)p;
+        }
+    }
+    __syncthreads();
+    ridx = ex_h - 1;
+    for (long long p = p_lo; p < p_hi; ++p) {
+        if (p == 0 || otok[p] != otok[p - 1] + 1) ++ridx;
+        if (p == kk - 1 || otok[p + 1] != otok[p] + 1) rl[ridx] = (int32_t)(p + 1 - rl[ridx]);
+    }
+    if (tid == 0) n_runs[li] = (int32_t)tot_h;
+}
+
+}  // namespace kvt
+
+using namespace kvt;
+
+int kvt_topk_select_band_cluster(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
+                                 const double* err, int64_t n_lanes, int64_t k, const void* q, int q_dtype,
+                                 const void* keys, int key_dtype, int64_t lane_stride, int d, int32_t* sel_tok,
+                                 double* sel_score, int64_t sel_stride, int32_t* n_sel, int32_t* run_start,
+                                 int32_t* run_len, int64_t run_stride, int32_t* n_runs, void* stream);
+
+template <typename QT, typename T>
+static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
+                          const double* rec, int64_t n_lanes, int64_t k, const void* q, const void* keys,
+                          int64_t lane_stride, int d, double* scratch, int32_t* sel_tok, double* sel_score,
+                          int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len,
+                          int64_t run_stride, int32_t* n_runs, cudaStream_t st) {
+    const int row_b = RowLd<T>::row_bytes(d);
+    const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
+    const size_t smem = (size_t)S3_LIST_CAP * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(topk_select3_kernel<QT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return kvt_set_cuda_error(e);
+        configured = true;
+    }
+    topk_select3_kernel<QT, T><<<(unsigned)n_lanes, S3_THREADS, smem, st>>>(
+        cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
+        sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs);
+    return kvt_check_launch();
+}
+
+extern "C" int kvt_topk_select_band(const float* cs32, const int32_t* ctok, const int32_t* n_cand,
+                                    int64_t cand_stride, const double* rec, int64_t n_lanes, int64_t k, const void* q,
+                                    int q_dtype, const void* keys, int key_dtype, int64_t lane_stride, int d,
+                                    double* scratch, int32_t* sel_tok, double* sel_score, int64_t sel_stride,
+                                    int32_t* n_sel, int32_t* run_start, int32_t* run_len, int64_t run_stride,
+                                    int32_t* n_runs, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!cs32 || !ctok || !n_cand || !rec || !q || !keys || !scratch || !sel_tok || !sel_score || !n_sel)
+        return KVT_ERR_ARG;
+    if (k < 0) return KVT_ERR_K;
+    if (n_lanes == 0) return KVT_OK;
+    if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
+    // few lanes: one CTA per lane would leave most SMs idle -> cluster of CTAs per lane
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (n_lanes < sms && cand_stride >= 8192 && cand_stride <= 8 * 20480 && n_lanes <= 65535)
+        return kvt_topk_select_band_cluster(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, q_dtype, keys,
+                                            key_dtype, lane_stride, d, sel_tok, sel_score, sel_stride, n_sel,
+                                            run_start, run_len, run_stride, n_runs, stream);
+#define KVT_S(QT, TT) return launch_select3<QT, TT>(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, keys, lane_stride, d, scratch, sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, st)
+    if (q_dtype == KVT_F32) {
+        switch (key_dtype) {
+            case KVT_F32: KVT_S(float, float);
+            case KVT_BF16: KVT_S(float, __nv_bfloat16);
+            case KVT_F16: KVT_S(float, __half);
+            case KVT_I4: KVT_S(float, I4);
+        }
+    } else if (q_dtype == KVT_F64) {
+        switch (key_dtype) {
+            case KVT_F32: KVT_S(double, float);
+            case KVT_BF16: KVT_S(double, __nv_bfloat16);
+            case KVT_F16: KVT_S(double, __half);
+            case KVT_I4: KVT_S(double, I4);
+        }
+    }
+#undef KVT_S
+    return KVT_ERR_DTYPE;
+}

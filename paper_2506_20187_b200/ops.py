@@ -223,7 +223,7 @@ def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
     evals = torch.empty(nl, dtype=torch.int64, device=dev)
     cand_leaf = torch.zeros((nl, max(maxl, 1)), dtype=torch.int8, device=dev) if want_cand_leaf else None
     lstride = leaf_start.shape[1] if leaf_start is not None else maxl
-    err = torch.empty(nl, dtype=torch.float64, device=dev) if A is not None else None
+    err = torch.empty((nl, 4), dtype=torch.float64, device=dev) if A is not None else None
     L.check(L.kvt_select_plan2(nl, n, C, _p(leaf_start), _p(n_leaves), lstride, U.data_ptr(), Lo.data_ptr(),
                                U.stride(0), k, items.data_ptr(), item_cap, n_items.data_ptr(), n_cand.data_ptr(),
                                _p(cand_leaf), evals.data_ptr(), _p(A), _p(err), d, _stream()), "select_plan")
@@ -268,6 +268,9 @@ def topk_select_band(cs32: torch.Tensor, ct: torch.Tensor, plan: dict, k: int, q
     st = torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev)
     ss = torch.empty((nl, max(k, 1)), dtype=torch.float64, device=dev)
     ns = torch.empty(nl, dtype=torch.int32, device=dev)
+    scratch = plan.get("scratch")
+    if scratch is None or scratch.shape != cs32.shape:
+        scratch = plan["scratch"] = torch.empty(cs32.shape, dtype=torch.float64, device=dev)
     runs = None
     if want_runs:
         runs = {"run_start": torch.empty((nl, max(k, 1)), dtype=torch.int32, device=dev),
@@ -275,7 +278,8 @@ def topk_select_band(cs32: torch.Tensor, ct: torch.Tensor, plan: dict, k: int, q
                 "n_runs": torch.empty(nl, dtype=torch.int32, device=dev)}
     L.check(L.kvt_topk_select_band(cs32.data_ptr(), ct.data_ptr(), plan["n_cand"].data_ptr(), cs32.stride(0),
                                    plan["err"].data_ptr(), nl, k, q.data_ptr(), dtype_code(q), keys.data_ptr(),
-                                   dtype_code(keys), ls, d, st.data_ptr(), ss.data_ptr(), st.stride(0), ns.data_ptr(),
+                                   dtype_code(keys), ls, d, scratch.data_ptr(), st.data_ptr(), ss.data_ptr(),
+                                   st.stride(0), ns.data_ptr(),
                                    _p(runs["run_start"]) if runs else None, _p(runs["run_len"]) if runs else None,
                                    st.stride(0), _p(runs["n_runs"]) if runs else None, _stream()), "topk_select_band")
     if want_runs:
