@@ -50,10 +50,10 @@ def parse():
     p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--batch", type=int, default=1, help="batch rows per GPU")
+    p.add_argument("--batch", type=int, default=8, help="batch rows per GPU (config 3: 8)")
     p.add_argument("--ctx", type=int, default=65536)
     p.add_argument("--data", choices=["planted", "random"], default="planted")
-    p.add_argument("--dtype", choices=["bf16", "f32", "int4"], default="bf16",
+    p.add_argument("--dtype", choices=["bf16", "f32", "int4"], default="int4",
                    help="KV storage: bf16/f32 rows or INT4 records (K8 compression, config 3)")
     p.add_argument("--layers", type=int, default=N_LAYERS)
     p.add_argument("--cpu-lanes", type=int, default=16, help="lanes in the CPU baseline sample")

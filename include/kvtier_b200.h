@@ -60,11 +60,12 @@ KVT_API const char* kvt_last_error(void);
  * Replaces importance.py:80-87 make_abstract (and the per-leaf loop of chunk_tree.py:
  * 199-208 build_partition).  Uniform grid: chunk c of lane i covers tokens
  * [c*C, min((c+1)*C, n)); chunks [c_begin, c_end) are (re)built.  Outputs are the
- * element-wise max / min key rows, dtype F32 for F32/BF16/F16 keys and F64 for F64 keys,
- * at amax + i*abs_lane_stride + c*d. */
+ * element-wise max / min key rows at amax + i*abs_lane_stride + c*d, in abs_dtype: F32 for
+ * F32/BF16/F16/I4 keys and F64 for F64 keys (exact), or BF16 for any keys (rounded outward:
+ * max up, min down -- half the bytes, still a sound summary). */
 KVT_API int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lanes, int64_t lane_stride,
                        int64_t n, int d, int C, int64_t c_begin, int64_t c_end,
-                       void* amax, void* amin, int64_t abs_lane_stride, void* stream);
+                       void* amax, void* amin, int abs_dtype, int64_t abs_lane_stride, void* stream);
 
 /* Arbitrary spans (exact abstracts of keys[start:end) of lane lane_of[j]); used for
  * partition leaves and merged desert runs (importance.py:90-100 merge_abstracts,

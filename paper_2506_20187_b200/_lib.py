@@ -61,7 +61,7 @@ kvt_version = _sig("kvt_version", ctypes.c_int)
 kvt_status_string = _sig("kvt_status_string", ctypes.c_char_p, ctypes.c_int)
 kvt_last_error = _sig("kvt_last_error", ctypes.c_char_p)
 kvt_abstract_build = _sig("kvt_abstract_build", ctypes.c_int, _vp, _i32, _i64, _i64, _i64, _i32, _i32, _i64, _i64,
-                          _vp, _vp, _i64, _vp)
+                          _vp, _vp, _i32, _i64, _vp)
 kvt_abstract_spans = _sig("kvt_abstract_spans", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _vp,
                           _vp)
 kvt_chunk_bounds = _sig("kvt_chunk_bounds", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _i32, _vp, _vp, _i64, _vp,

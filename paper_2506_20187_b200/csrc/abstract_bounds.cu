@@ -17,12 +17,22 @@ namespace kvt {
 template <typename T> struct AbsOf { using type = float; };
 template <> struct AbsOf<double> { using type = double; };
 
-template <typename T, int G, bool VEC>
+// Abstract stores.  bf16 abstracts (the decoder's compact form, half the bytes of f32) are
+// rounded OUTWARD -- max up, min down -- so they still bound every key and the bounds stay
+// sound; f32/f64 stores are exact (f32/bf16/f16 keys are exact in f32).
+template <typename A> __device__ __forceinline__ void st_max(A* p, double v) { *p = (A)v; }
+template <typename A> __device__ __forceinline__ void st_min(A* p, double v) { *p = (A)v; }
+template <> __device__ __forceinline__ void st_max<__nv_bfloat16>(__nv_bfloat16* p, double v) {
+    *p = __float2bfloat16_ru((float)v);
+}
+template <> __device__ __forceinline__ void st_min<__nv_bfloat16>(__nv_bfloat16* p, double v) {
+    *p = __float2bfloat16_rd((float)v);
+}
+
+template <typename T, int G, bool VEC, typename A>
 __global__ void __launch_bounds__(256) abstract_grid_kernel(
     const T* __restrict__ keys, int64_t lane_stride, int64_t n, int d, int C, int64_t c_begin,
-    int64_t c_end, typename AbsOf<T>::type* __restrict__ amax,
-    typename AbsOf<T>::type* __restrict__ amin, int64_t abs_lane_stride) {
-    using A = typename AbsOf<T>::type;
+    int64_t c_end, A* __restrict__ amax, A* __restrict__ amin, int64_t abs_lane_stride) {
     const int lane = threadIdx.x & 31;
     const int64_t lane_i = blockIdx.y;
     const int64_t nchunks = c_end - c_begin;
@@ -76,7 +86,7 @@ __global__ void __launch_bounds__(256) abstract_grid_kernel(
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int j = 4 * g + i;
-                if (j < d) { omx[j] = (A)mx[r][i]; omn[j] = (A)mn[r][i]; }
+                if (j < d) { st_max<A>(omx + j, mx[r][i]); st_min<A>(omn + j, mn[r][i]); }
             }
         }
     }
@@ -213,6 +223,125 @@ __global__ void __launch_bounds__(256, 3) bounds_kernel(
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// K3, TMA-staged variant for the uniform grid (the decoder's case): persistent CTAs walk the
+// flattened (lane, 64-chunk block) list; one producer thread bulk-copies each block's max
+// rows and min rows (contiguous, 2 x 64 x d x s_A bytes) into a shared-memory ring, eight
+// consumer warps bound eight chunks each straight from shared memory.  Same arithmetic as
+// bounds_kernel (canonical order, outward slack), different data movement.
+// ------------------------------------------------------------------------------------------
+
+constexpr int BT_CONSUMERS = 8;
+constexpr int BT_THREADS = (BT_CONSUMERS + 1) * 32;
+
+template <typename QT, typename AT, int G>
+__global__ void __launch_bounds__(BT_THREADS, 2) bounds_tma_kernel(
+    const QT* __restrict__ q, int d, int64_t n, int C, int n_lanes, const AT* __restrict__ amax,
+    const AT* __restrict__ amin, int64_t abs_lane_stride, double* __restrict__ U, double* __restrict__ L,
+    double* __restrict__ A, int64_t bnd_stride, int scaled, int stages) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tile = 2 * 64 * d * (int)sizeof(AT);  // max rows then min rows
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * tile);
+    uint64_t* empty = full + stages;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m = (n + C - 1) / C;
+    const int64_t per_lane = (m + 63) / 64;
+    const int64_t total = per_lane * n_lanes;
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BT_CONSUMERS); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t g0 = kvt::imin(total, (int64_t)blockIdx.x * per), g1 = kvt::imin(total, g0 + per);
+    if (warp == BT_CONSUMERS) {
+        if (lane == 0) {
+            int64_t i = 0;
+            int ps = 0, pr = 0;
+            for (int64_t g = g0; g < g1; ++g, ++i) {
+                const int64_t li = g / per_lane, c0 = (g % per_lane) * 64;
+                const int64_t cnt = kvt::imin(64, m - c0);
+                // ring position without integer division: stage ps, fill round pr
+                const int s = ps;
+                if (pr > 0) mbar_wait(&empty[s], (uint32_t)((pr - 1) & 1));
+                if (++ps == stages) { ps = 0; ++pr; }
+                const uint32_t half = (uint32_t)(cnt * d * sizeof(AT));
+                mbar_arrive_expect_tx(&full[s], 2 * half);
+                unsigned char* dst = smem + (size_t)s * tile;
+                bulk_g2s(dst, amax + li * abs_lane_stride + c0 * d, half, &full[s]);
+                bulk_g2s(dst + tile / 2, amin + li * abs_lane_stride + c0 * d, half, &full[s]);
+            }
+        }
+        return;
+    }
+    const double sd = sqrt((double)d);
+    const double fac = slack_factor(d);
+    int64_t cur = -1;
+    double qr[G][4];
+    int64_t i = 0;
+    int cs = 0, cr = 0;
+    for (int64_t g = g0; g < g1; ++g, ++i) {
+        const int64_t li = g / per_lane, c0 = (g % per_lane) * 64;
+        const int64_t cnt = kvt::imin(64, m - c0);
+        if (li != cur) {
+            cur = li;
+#pragma unroll
+            for (int r = 0; r < G; ++r)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = 4 * (lane + 32 * r) + e;
+                    qr[r][e] = j < d ? (double)q[li * d + j] : 0.0;
+                }
+        }
+        const int s = cs;
+        mbar_wait(&full[s], (uint32_t)(cr & 1));
+        if (++cs == stages) { cs = 0; ++cr; }
+        const AT* Mx = reinterpret_cast<const AT*>(smem + (size_t)s * tile);
+        const AT* Mn = Mx + 64 * d;
+        const int base = 8 * warp;
+        if (base < cnt) {
+            double pu[8], pl[8], pa[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                pu[u] = 0.0; pl[u] = 0.0; pa[u] = 0.0;
+                if (base + u < cnt) {
+#pragma unroll
+                    for (int r = 0; r < G; ++r) {
+                        double hv[4], lv[4];
+                        lds4<AT>(Mx + (int64_t)(base + u) * d + 4 * (lane + 32 * r), hv);
+                        lds4<AT>(Mn + (int64_t)(base + u) * d + 4 * (lane + 32 * r), lv);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const double qj = qr[r][e];
+                            const double hi = qj >= 0.0 ? hv[e] : lv[e];
+                            const double lo = qj >= 0.0 ? lv[e] : hv[e];
+                            pu[u] = fma(qj, hi, pu[u]);
+                            pl[u] = fma(qj, lo, pl[u]);
+                            pa[u] = fma(fabs(qj), fmax(fabs(hv[e]), fabs(lv[e])), pa[u]);
+                        }
+                    }
+                }
+            }
+            double u_ = tree_8tok<double>(pu, lane), l_ = tree_8tok<double>(pl, lane), a_ = tree_8tok<double>(pa, lane);
+            const int t = (lane >> 2) & 7;
+            const int64_t c = c0 + base + t;
+            if ((lane & 3) == 0 && base + t < cnt) {
+                const int64_t rows = kvt::imin((int64_t)C, n - c * C);
+                if (rows > 1) {
+                    const double slack = a_ * fac;
+                    u_ = u_ + slack;
+                    l_ = l_ - slack;
+                }
+                U[li * bnd_stride + c] = scaled ? u_ / sd : u_;
+                L[li * bnd_stride + c] = scaled ? l_ / sd : l_;
+                if (A) A[li * bnd_stride + c] = a_;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
 }  // namespace kvt
 
 using namespace kvt;
@@ -225,25 +354,30 @@ static inline bool aligned16(const void* p, int64_t elem_bytes, int64_t lane_str
 
 template <typename T, int G, bool VEC>
 static void launch_abs_grid(const void* keys, int64_t n_lanes, int64_t lane_stride, int64_t n, int d, int C,
-                            int64_t cb, int64_t ce, void* amax, void* amin, int64_t als, cudaStream_t st) {
+                            int64_t cb, int64_t ce, void* amax, void* amin, int64_t als, bool bf16_abs,
+                            cudaStream_t st) {
     using A = typename AbsOf<T>::type;
     const int64_t nch = ce - cb;
     int gx = (int)kvt::imin((nch + 7) / 8, 4096);
     if (gx < 1) gx = 1;
     dim3 grid(gx, (unsigned)n_lanes);
-    abstract_grid_kernel<T, G, VEC><<<grid, 256, 0, st>>>((const T*)keys, lane_stride, n, d, C, cb, ce, (A*)amax,
-                                                          (A*)amin, als);
+    if (bf16_abs)
+        abstract_grid_kernel<T, G, VEC, __nv_bfloat16><<<grid, 256, 0, st>>>(
+            (const T*)keys, lane_stride, n, d, C, cb, ce, (__nv_bfloat16*)amax, (__nv_bfloat16*)amin, als);
+    else
+        abstract_grid_kernel<T, G, VEC, A><<<grid, 256, 0, st>>>((const T*)keys, lane_stride, n, d, C, cb, ce,
+                                                                 (A*)amax, (A*)amin, als);
 }
 
 template <typename T>
 static int dispatch_abs_grid(const void* keys, int64_t n_lanes, int64_t lane_stride, int64_t n, int d, int C,
-                             int64_t cb, int64_t ce, void* amax, void* amin, int64_t als, cudaStream_t st) {
+                             int64_t cb, int64_t ce, void* amax, void* amin, int64_t als, bool bf, cudaStream_t st) {
     const bool vec = aligned16(keys, sizeof(T), lane_stride, d);
     switch (groups_for(d)) {
 #define KVT_CASE(GG)                                                                                        \
     case GG:                                                                                                \
-        if (vec) launch_abs_grid<T, GG, true>(keys, n_lanes, lane_stride, n, d, C, cb, ce, amax, amin, als, st); \
-        else launch_abs_grid<T, GG, false>(keys, n_lanes, lane_stride, n, d, C, cb, ce, amax, amin, als, st);   \
+        if (vec) launch_abs_grid<T, GG, true>(keys, n_lanes, lane_stride, n, d, C, cb, ce, amax, amin, als, bf, st); \
+        else launch_abs_grid<T, GG, false>(keys, n_lanes, lane_stride, n, d, C, cb, ce, amax, amin, als, bf, st);   \
         break;
         KVT_CASE(1) KVT_CASE(2) KVT_CASE(4) KVT_CASE(8)
 #undef KVT_CASE
@@ -254,18 +388,21 @@ static int dispatch_abs_grid(const void* keys, int64_t n_lanes, int64_t lane_str
 
 extern "C" int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lanes, int64_t lane_stride, int64_t n,
                                   int d, int C, int64_t c_begin, int64_t c_end, void* amax, void* amin,
-                                  int64_t abs_lane_stride, void* stream) {
+                                  int abs_dtype, int64_t abs_lane_stride, void* stream) {
     if (!keys || !amax || !amin || n_lanes < 0 || n < 0 || d < 1 || C < 1) return KVT_ERR_ARG;
     if (c_begin < 0 || c_end < c_begin || c_end > (n + C - 1) / C) return KVT_ERR_SHAPE;
     if (n_lanes == 0 || c_end == c_begin) return KVT_OK;
     if (n_lanes > 65535) return KVT_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
+    const bool bf = abs_dtype == KVT_BF16;
+    const int natural = key_dtype == KVT_F64 ? KVT_F64 : KVT_F32;
+    if (!bf && abs_dtype != natural) return KVT_ERR_DTYPE;
     switch (key_dtype) {
-        case KVT_I4: return kvt_abstract_build_i4(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
-        case KVT_F32: return dispatch_abs_grid<float>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
-        case KVT_F64: return dispatch_abs_grid<double>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
-        case KVT_BF16: return dispatch_abs_grid<__nv_bfloat16>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
-        case KVT_F16: return dispatch_abs_grid<__half>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, st);
+        case KVT_I4: return kvt_abstract_build_i4(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, bf, st);
+        case KVT_F32: return dispatch_abs_grid<float>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, bf, st);
+        case KVT_F64: return dispatch_abs_grid<double>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, bf, st);
+        case KVT_BF16: return dispatch_abs_grid<__nv_bfloat16>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, bf, st);
+        case KVT_F16: return dispatch_abs_grid<__half>(keys, n_lanes, lane_stride, n, d, C, c_begin, c_end, amax, amin, abs_lane_stride, bf, st);
         default: return KVT_ERR_DTYPE;
     }
 }
@@ -311,10 +448,34 @@ extern "C" int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_
     }
 }
 
+static int g_bt_sms = 0;
+
 template <typename QT, typename AT, int G>
 static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                           const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
                           double* U, double* L, double* A, int64_t bs, int64_t max_leaves, int scaled, cudaStream_t st) {
+    // uniform grid, vector-aligned rows, d = 128 G: the TMA-staged kernel
+    const int64_t row = (int64_t)d * sizeof(AT);
+    if (!ls && sizeof(AT) <= 4 && d == 128 * G && G <= 2 && row % 16 == 0 && ((uintptr_t)amax % 16) == 0 && ((uintptr_t)amin % 16) == 0 &&
+        (als * (int64_t)sizeof(AT)) % 16 == 0 && n_lanes <= 2147483647LL) {
+        const int tile = (int)(2 * 64 * row);
+        const int stages = (int)kvt::imax(2, kvt::imin(4, (100 * 1024) / tile));
+        const size_t smem = (size_t)stages * tile + 16 * (size_t)stages + 16;
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(bounds_tma_kernel<QT, AT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            configured = true;
+        }
+        if (!g_bt_sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&g_bt_sms, cudaDevAttrMultiProcessorCount, dev);
+            if (g_bt_sms <= 0) g_bt_sms = 148;
+        }
+        bounds_tma_kernel<QT, AT, G><<<g_bt_sms * (smem <= 110 * 1024 ? 2 : 1), BT_THREADS, smem, st>>>(
+            (const QT*)q, d, n, C, (int)n_lanes, (const AT*)amax, (const AT*)amin, als, U, L, A, bs, scaled, stages);
+        return;
+    }
     int gx = (int)kvt::imax(1, kvt::imin((max_leaves + 31) / 32, 1024));
     // keep ~8 CTAs per SM in total when lanes are few
     dim3 grid(gx, (unsigned)n_lanes);
@@ -353,6 +514,10 @@ extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int
         return dispatch_bounds<double, float>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F32 && abs_dtype == KVT_F64)
         return dispatch_bounds<float, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
+    if (q_dtype == KVT_F32 && abs_dtype == KVT_BF16)
+        return dispatch_bounds<float, __nv_bfloat16>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
+    if (q_dtype == KVT_F64 && abs_dtype == KVT_BF16)
+        return dispatch_bounds<double, __nv_bfloat16>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     if (q_dtype == KVT_F64 && abs_dtype == KVT_F64)
         return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     return KVT_ERR_DTYPE;

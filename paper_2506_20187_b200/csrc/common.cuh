@@ -356,7 +356,7 @@ bool kvt_fast_ok(int key_dtype, int d);
 
 // INT4 K1 (quant.cu)
 int kvt_abstract_build_i4(const void* keys, int64_t n_lanes, int64_t lane_stride_b, int64_t n, int d, int C,
-                          int64_t c_begin, int64_t c_end, void* amax, void* amin, int64_t abs_lane_stride,
+                          int64_t c_begin, int64_t c_end, void* amax, void* amin, int64_t abs_lane_stride, bool bf,
                           cudaStream_t st);
 
 // status plumbing (api.cu)

@@ -173,8 +173,11 @@ using namespace kvt;
 // Rigorous bound on |f32 estimate - canonical f64 dot| relative to A = sum |q_j| |k_j|:
 // the f32 path (q rounded to f32: 1 unit; fma chain + tree: n = chain_len(d) units of
 // 2^-24, gamma_n) plus the canonical f64 path's own error (n units of 2^-53), with slack.
+// The f32 paths use at most chain_len(d) + 3 roundings per term: the row layout (4 dims per
+// lane, tree of 5) or the INT4 layout (32 dims per lane in 4 chains of 8, 2 pairwise adds,
+// <= 3 shuffle levels).
 static double f32_err_factor(int d) {
-    const int n = chain_len(d);
+    const int n = chain_len(d) + 3;
     return ((double)(n + 2) * 0x1p-24) * (1.0 + 0x1p-10) + (double)(n + 2) * 0x1p-52;
 }
 

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_i4_kernel(
     float o[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) o[e] = 0.f;
-    float l = 0.f;
+    float l = 0.f, om = 0.f;
     constexpr int STEP = ATTN_WARPS * RPW;
     for (int64_t i0 = a + warp * RPW + sub; i0 < b; i0 += (int64_t)U * STEP) {
         uint4 cw[U];
@@ -425,19 +425,28 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_i4_kernel(
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            // o += w * (c*scale + min) = (w*scale) * c + w*min: one FFMA per element, the
+            // min term once per row (om); codes -> float by byte permute (0x4B0000cc = 2^23 + c)
             const __half2 p = *reinterpret_cast<const __half2*>(&pw[u]);
-            const float sc_ = __low2float(p), mn = __high2float(p);
+            const float ws = w[u] * __low2float(p);
+            om = fmaf(w[u], __high2float(p), om);
             const uint32_t words[4] = {cw[u].x, cw[u].y, cw[u].z, cw[u].w};
             l += w[u];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t lo4 = words[q] & 0x0f0f0f0fu, hi4 = (words[q] >> 4) & 0x0f0f0f0fu;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float x = __fmaf_rn((float)((words[q] >> (4 * e)) & 15u), sc_, mn);
-                    o[8 * q + e] = fmaf(w[u], x, o[8 * q + e]);
+                for (int bb = 0; bb < 4; ++bb) {
+                    const float c0 = __uint_as_float(__byte_perm(lo4, 0x4B000000u, 0x7440 + bb)) - 8388608.0f;
+                    const float c1 = __uint_as_float(__byte_perm(hi4, 0x4B000000u, 0x7440 + bb)) - 8388608.0f;
+                    o[8 * q + 2 * bb] = fmaf(ws, c0, o[8 * q + 2 * bb]);
+                    o[8 * q + 2 * bb + 1] = fmaf(ws, c1, o[8 * q + 2 * bb + 1]);
                 }
+            }
         }
     }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) o[e] += om;
 #pragma unroll
     for (int off = LPR; off < 32; off <<= 1) {
         l += __shfl_xor_sync(KVT_FULL, l, off);

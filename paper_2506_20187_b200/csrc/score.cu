@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
         if (lane == 0) {
             int cur = 0;
             int64_t i = 0;
+            int ps = 0, pr = 0;
             for (int64_t g = g_begin; g < g_end; ++g, ++i) {
                 while (g >= lane_off[cur + 1]) ++cur;
                 const int64_t it = g - lane_off[cur];
@@ -151,9 +152,10 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
                     const int32_t* m = items + ((int64_t)cur * item_stride + it) * 3;
                     t0 = m[0]; cnt = m[1]; pos0 = m[2];
                 }
-                const int s = (int)(i % stages);
-                const int64_t r = i / stages;
-                if (r > 0) mbar_wait(&empty[s], (uint32_t)((r - 1) & 1));
+                // ring position without integer division: stage ps, fill round pr
+                const int s = ps;
+                if (pr > 0) mbar_wait(&empty[s], (uint32_t)((pr - 1) & 1));
+                if (++ps == stages) { ps = 0; ++pr; }
                 const uint32_t bytes = (uint32_t)(cnt * row_b);
                 meta[s] = make_int4(cur, (int)t0, (int)cnt, pos0);
                 mbar_arrive_expect_tx(&full[s], bytes);
@@ -168,10 +170,14 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const double sd = sqrt((double)d);
     int cur = -1;
     AccT qr[G][4];
+    float qg[std::is_same<T, I4>::value && sizeof(AccT) == 4 ? 32 : 1];  // INT4 fast path: a lane's 32-dim group of q
+    int qcur_i4 = -1;
     int64_t i = 0;
+    int cs = 0, cr = 0;
     for (int64_t g = g_begin; g < g_end; ++g, ++i) {
-        const int s = (int)(i % stages);
-        mbar_wait(&full[s], (uint32_t)((i / stages) & 1));
+        const int s = cs;
+        mbar_wait(&full[s], (uint32_t)(cr & 1));
+        if (++cs == stages) { cs = 0; ++cr; }
         const int4 mt = meta[s];
         if (mt.x != cur) {
             cur = mt.x;
@@ -186,7 +192,52 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
         const int64_t t0 = mt.y, cnt = mt.z, pos0 = mt.w;
         const unsigned char* tile = smem + (size_t)s * tile_bytes;
         const int base_t = 8 * warp;
-        if (base_t < cnt) {
+        if constexpr (std::is_same<T, I4>::value && sizeof(AccT) == 4) {
+            // INT4 fast estimate: a token's record is read by LPT = d/32 lanes, one 32-dim group
+            // each (16 B of codes + its (scale, min)), 4 independent fma chains of 8, then a
+            // shuffle reduction over the token's lanes.  (Any order is fine for the f32
+            // estimate: the plan's error bound covers <= chain_len(d) + 3 roundings.)
+            constexpr int LPT = 4 * G;        // lanes per token (d = 128 G)
+            constexpr int TPW = 32 / LPT;     // tokens per warp instruction
+            const int grp = lane % LPT, sub = lane / LPT;
+            if (cur != qcur_i4) {
+                qcur_i4 = cur;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) qg[e] = (float)q[(int64_t)cur * d + 32 * grp + e];
+            }
+#pragma unroll
+            for (int rep = 0; rep < 8 / TPW; ++rep) {
+                const int u = base_t + rep * TPW + sub;  // token within the item
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                if (u < cnt) {
+                    const unsigned char* row = tile + (int64_t)u * row_b;
+                    const uint4 cw = *reinterpret_cast<const uint4*>(row + 16 * grp);
+                    const __half2 pr = *reinterpret_cast<const __half2*>(row + d / 2 + 4 * grp);
+                    const float sc_ = __low2float(pr), mn = __high2float(pr);
+                    const uint32_t wv[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+                    for (int wi = 0; wi < 4; ++wi) {
+                        const uint32_t lo4 = wv[wi] & 0x0f0f0f0fu, hi4 = (wv[wi] >> 4) & 0x0f0f0f0fu;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            // code -> float without I2F: one byte permute builds 0x4B0000cc = 2^23 + c
+                            const float c0 = __uint_as_float(__byte_perm(lo4, 0x4B000000u, 0x7440 + b)) - 8388608.0f;
+                            const float c1 = __uint_as_float(__byte_perm(hi4, 0x4B000000u, 0x7440 + b)) - 8388608.0f;
+                            const int e = 8 * wi + 2 * b;
+                            acc[wi] = fmaf(qg[e], __fmaf_rn(c0, sc_, mn), acc[wi]);
+                            acc[wi] = fmaf(qg[e + 1], __fmaf_rn(c1, sc_, mn), acc[wi]);
+                        }
+                    }
+                }
+                float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+                for (int off = 1; off < LPT; off <<= 1) v += __shfl_xor_sync(KVT_FULL, v, off);
+                if (grp == 0 && u < cnt) {
+                    out32[(int64_t)cur * out_stride + pos0 + u] = v;
+                    if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + u] = (int32_t)(t0 + u);
+                }
+            }
+        } else if (base_t < cnt) {
             AccT p[8];
             const unsigned char* rows = tile + (int64_t)base_t * row_b;
             if (base_t + 8 <= cnt && d == 128 * G) {

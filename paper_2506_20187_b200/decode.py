@@ -4,7 +4,8 @@ engine.py:307-357, for every (batch row, head) lane of a layer at once).
 
 Layout in HBM:
   K, V       [L][B*H][N_cap][d]   key/value rows, lanes contiguous (bf16 by default)
-  amax/amin  per layer [B*H][ceil(N_cap/C_l)][d] f32 chunk abstracts (importance.py:56-87)
+  amax/amin  per layer [B*H][ceil(N_cap/C_l)][d] bf16 chunk abstracts rounded outward
+             (importance.py:56-87 summaries; exact f32 on request)
   C_l        ChunkPlanConfig: early layers use early_chunk_size, the rest default_chunk_size
              (chunk_tree.py:111-123, steady state after the early steps)
   k_l        ceil(rate_l * n), rate 0.5 for layers < early_layers else 0.1 (engine.py:83-86,312)
@@ -23,7 +24,8 @@ from .chunk_tree import ChunkPlanConfig
 class SparseDecoder:
     def __init__(self, n_layers: int, batch: int, n_heads: int, head_dim: int, n_cap: int,
                  dtype: torch.dtype = torch.bfloat16, plan: ChunkPlanConfig | None = None,
-                 importance_rate: float = 0.10, early_layer_rate: float = 0.50, device=None):
+                 importance_rate: float = 0.10, early_layer_rate: float = 0.50, device=None,
+                 abstract_dtype: torch.dtype = torch.bfloat16):
         if not torch.cuda.is_available():
             raise RuntimeError("SparseDecoder needs a CUDA device (B200, sm_100a)")
         self.L, self.B, self.H, self.d = n_layers, batch, n_heads, head_dim
@@ -42,7 +44,8 @@ class SparseDecoder:
         else:
             self.K = torch.empty((n_layers, self.lanes, n_cap, head_dim), dtype=dtype, device=self.device)
             self.V = torch.empty_like(self.K)
-        adt = ops.abs_dtype_for(dtype)
+        # bf16 abstracts rounded outward (max up, min down): half the bound-pass bytes, still sound
+        adt = abstract_dtype if abstract_dtype is not None else ops.abs_dtype_for(dtype)
         self.amax = [torch.empty((self.lanes, ops.n_grid_leaves(n_cap, C), head_dim), dtype=adt, device=self.device)
                      for C in self.C]
         self.amin = [torch.empty_like(a) for a in self.amax]

@@ -129,22 +129,27 @@ def kv_quant(src: torch.Tensor, dst: I4KV, t_begin: int = 0, t_end: int | None =
 # -- K1 ----------------------------------------------------------------------------------------
 
 
-def abstract_build(keys: torch.Tensor, n: int, C: int, amax: torch.Tensor | None = None,
-                   amin: torch.Tensor | None = None, c_begin: int = 0, c_end: int | None = None):
-    """Uniform-grid chunk abstracts (importance.py:80-87) -> (amax, amin) [n_lanes, m_cap, d]."""
+def abstract_build(keys, n: int, C: int, amax: torch.Tensor | None = None,
+                   amin: torch.Tensor | None = None, c_begin: int = 0, c_end: int | None = None,
+                   abs_dtype: torch.dtype | None = None):
+    """Uniform-grid chunk abstracts (importance.py:80-87) -> (amax, amin) [n_lanes, m_cap, d].
+    abs_dtype: exact f32/f64 (default) or torch.bfloat16 (rounded outward, half the bytes)."""
     require_cuda(keys)
     ls, d = _lanes(keys)
     nl = keys.shape[0]
     m = n_grid_leaves(n, C)
     c_end = m if c_end is None else c_end
-    adt = abs_dtype_for(keys.dtype)
+    if amax is not None:
+        abs_dtype = amax.dtype
+    adt = abs_dtype or abs_dtype_for(keys.dtype)
     if amax is None:
         amax = torch.empty((nl, m, d), dtype=adt, device=keys.device)
         amin = torch.empty_like(amax)
-    if amax.dtype != adt or amin.dtype != adt or amax.stride(2) != 1:
+    if amin.dtype != adt or amax.stride(2) != 1:
         raise ValueError("abstract buffers must be contiguous rows of the abstract dtype")
     L.check(L.kvt_abstract_build(keys.data_ptr(), dtype_code(keys), nl, ls, n, d, C, c_begin, c_end,
-                                 amax.data_ptr(), amin.data_ptr(), amax.stride(0), _stream()), "abstract_build")
+                                 amax.data_ptr(), amin.data_ptr(), dtype_code(amax), amax.stride(0), _stream()),
+            "abstract_build")
     return amax, amin
 
 

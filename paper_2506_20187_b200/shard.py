@@ -61,6 +61,57 @@ def allgather_lse_merge(m: torch.Tensor, l: torch.Tensor, o: torch.Tensor, group
     return lse_merge(out[..., 0], out[..., 1], out[..., 2:])
 
 
+_MIN64 = -(2 ** 63)
+
+
+def _ord_keys(scores: torch.Tensor) -> torch.Tensor:
+    """Bit patterns (held in int64) of the unsigned orderable keys of float64 scores:
+    larger score -> larger unsigned key; -0 == +0."""
+    s = torch.where(scores == 0, torch.zeros_like(scores), scores)
+    b = s.view(torch.int64)
+    return torch.where(b < 0, ~b, b | torch.tensor(_MIN64, dtype=torch.int64, device=b.device))
+
+
+def global_topk_mask(scores: torch.Tensor, k: int, group=None) -> torch.Tensor:
+    """Exact top-k across a sequence-sharded lane.
+
+    Every rank holds the canonical scores of its contiguous token shard (rank order = token
+    order).  An 8-round radix select over the 64-bit orderable keys, each round an
+    all-reduce of a 256-bin histogram (the "global threshold exchange"), finds the exact
+    k-th key T; ties at T go to the lowest token indices, i.e. to lower ranks first (one
+    all-gather of the per-rank tie counts).  Returns this rank's boolean selection mask.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    keys = _ord_keys(scores.double())
+    dev = keys.device
+    prefix = torch.zeros((), dtype=torch.int64, device=dev)
+    mask = torch.zeros((), dtype=torch.int64, device=dev)
+    remaining = int(k)
+    for shift in range(56, -8, -8):
+        sel = (keys & mask) == prefix
+        digits = ((keys >> shift) & 0xFF)[sel]
+        hist = torch.bincount(digits, minlength=256).to(torch.int64)
+        dist.all_reduce(hist, group=group)
+        h = hist.flip(0).cumsum(0)  # counts from the top digit down
+        idx = int(torch.searchsorted(h, torch.tensor(remaining, device=dev)).item())
+        b = 255 - idx
+        above = int(h[idx - 1].item()) if idx > 0 else 0
+        prefix = prefix | (torch.tensor(b, dtype=torch.int64, device=dev) << shift)
+        mask = mask | (torch.tensor(0xFF, dtype=torch.int64, device=dev) << shift)
+        remaining -= above
+    # unsigned comparison through the sign flip; ties share the key `prefix`
+    flip = torch.tensor(_MIN64, dtype=torch.int64, device=dev)
+    gt = (keys ^ flip) > (prefix ^ flip)
+    eq = keys == prefix
+    eq_counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(eq_counts, eq.sum().reshape(1), group=group)
+    before = int(sum(int(c.item()) for c in eq_counts[:rank]))
+    take = max(0, min(int(eq.sum().item()), remaining - before))
+    eq_rank = torch.cumsum(eq.to(torch.int64), 0) - 1
+    return gt | (eq & (eq_rank < take))
+
+
 def max_over_ranks(x: float, device=None, group=None) -> float:
     """Max of a per-rank scalar (multi-GPU timing is the slowest rank)."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:

@@ -61,8 +61,25 @@ def _worker(rank, world, port, ret):
     full = np.concatenate([x[2] for x in sorted(sizes, key=lambda x: x[0])])
     err_lane = float(np.abs(full - ref).max())
     t = max_over_ranks(float(rank + 1))
+    # --- exact global top-k threshold exchange over sequence shards (incl. heavy ties) ---
+    from paper_2506_20187_b200.shard import global_topk_mask
+    ok_topk = True
+    for trial in range(4):
+        rng2 = np.random.default_rng(100 + trial)
+        full_scores = rng2.normal(size=1000)
+        if trial >= 2:
+            full_scores = np.round(full_scores, 1)  # many exact ties across shard boundaries
+        t0, t1 = token_block(1000, world, rank, align=1)
+        for kk in (1, 37, 500, 1000):
+            m = global_topk_mask(torch.tensor(full_scores[t0:t1]), kk).numpy()
+            got = np.nonzero(m)[0] + t0
+            gathered = [None] * world
+            dist.all_gather_object(gathered, got.tolist())
+            allsel = sorted(x for g in gathered for x in g)
+            ref = O.topk(full_scores, kk).tolist()
+            ok_topk &= allsel == ref
     if rank == 0:
-        ret.put((err_seq, err_lane, t))
+        ret.put((err_seq, err_lane, t, ok_topk))
     dist.destroy_process_group()
 
 
@@ -74,8 +91,9 @@ def test_gloo_sharding(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    err_seq, err_lane, t = q.get(timeout=120)
+    err_seq, err_lane, t, ok_topk = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert err_seq < 1e-12 and err_lane == 0.0 and t == float(world)
+    assert ok_topk

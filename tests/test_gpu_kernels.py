@@ -82,6 +82,34 @@ def test_abstracts_and_bounds_bitexact(ops, dt, d, C):
             assert Lr2[c] <= seg.min() and seg.max() <= Ur2[c]  # sound for raw canonical dots
 
 
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_bf16_abstracts_outward_and_bounds_bitexact(ops, dt):
+    """bf16 abstracts round max up / min down; bounds over them are bit-exact vs the oracle
+    fed the same rounded abstracts, and sound for every canonical dot."""
+    rng = np.random.default_rng(11)
+    lanes, n, d, C = 3, 1000, 128, 64
+    kt, kh = _keys(rng, lanes, n, d, dt)
+    q = rng.normal(size=(lanes, d))
+    amax, amin = ops.abstract_build(kt, n, C, abs_dtype=torch.bfloat16)
+    U, L = ops.chunk_bounds(torch.from_numpy(q).cuda(), amax, amin, n, C)
+    m = ops.n_grid_leaves(n, C)
+    for i in range(lanes):
+        mx = np.stack([kh[i, c * C:(c + 1) * C].max(0) for c in range(m)])
+        mn = np.stack([kh[i, c * C:(c + 1) * C].min(0) for c in range(m)])
+        bmx = amax[i, :m].double().cpu().numpy()
+        bmn = amin[i, :m].double().cpu().numpy()
+        assert np.all(bmx >= mx) and np.all(bmn <= mn)
+        rt = lambda a: torch.from_numpy(a).float().to(torch.bfloat16).double().numpy()
+        assert np.all(bmx <= np.nextafter(rt(mx) + np.abs(rt(mx)) * 2 ** -7, np.inf))
+        rows = [min(C, n - c * C) for c in range(m)]
+        Ur, Lr = O.bounds(q[i], bmx, bmn, rows, scaled=False)
+        assert np.array_equal(U[i, :m].cpu().numpy(), Ur) and np.array_equal(L[i, :m].cpu().numpy(), Lr)
+        dd = O.dots(q[i], kh[i])
+        for c in range(m):
+            seg = dd[c * C:(c + 1) * C]
+            assert Lr[c] <= seg.min() and seg.max() <= Ur[c]
+
+
 def test_bound_soundness_c02(ops):
     """test_acceptance.py:101-123 criterion 2, on canonical logits (no tolerance)."""
     rng = np.random.default_rng(2024)
