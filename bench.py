@@ -411,6 +411,9 @@ def run_ours(args):
     # own CUDA graph and replayed between CUDA events on the launching stream, so each
     # number is the device time of that kernel alone (no host gaps), averaged over reps.
     stages = ["bounds", "plan", "score", "select", "attn"]
+    is_i4 = isinstance(dec.K, ops.I4KV)
+    # INT4 keys: estimates from exact int32 inner products on the tensor cores (+ qprep launch)
+    score_fn = ops.cand_score_i4mma if is_i4 else ops.cand_score_f32
     inter = []
     n_cand = []
     with torch.cuda.stream(stream):
@@ -419,7 +422,7 @@ def run_ours(args):
             C, n, k = dec.C[l], dec.n, dec.k_for(l)
             U, Lo, A = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
             plan = ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
-            cs, ct = ops.cand_score_f32(q_static[l], dec.K[l], plan, n)
+            cs, ct = score_fn(q_static[l], dec.K[l], plan, n)
             st_, ss_, ns_, _ = ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
             inter.append((U, Lo, A, plan, cs, ct, st_, ss_, ns_))
         stream.synchronize()
@@ -435,7 +438,7 @@ def run_ours(args):
                 elif name == "plan":
                     ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
                 elif name == "score":
-                    ops.cand_score_f32(q_static[l], dec.K[l], plan, n)
+                    score_fn(q_static[l], dec.K[l], plan, n)
                 elif name == "select":
                     ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
                 elif name == "attn":
@@ -469,7 +472,8 @@ def run_ours(args):
     per_kernel = {s: {"ms_per_step": st_ms[s], "algo_bytes": algo[s],
                       "gbs": algo[s] / (st_ms[s] / 1e3) / 1e9 if st_ms[s] > 0 else None} for s in stages}
     staged_total = sum(st_ms.values())
-    launches_per_layer = 5  # bounds, plan, score (TMA), select+runs (cluster), attn (split + ticket merge)
+    # bounds, plan, [INT4: qprep,] score (TMA), select+runs, attn (split + ticket merge)
+    launches_per_layer = 6 if is_i4 else 5
     sel_gather_bytes = algo["bounds"] + algo["score"] + algo["select"] + algo["attn"]
     frac_of = "measured" if "hbm_gbs" in peaks else "fallback"
     line = {

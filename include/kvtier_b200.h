@@ -167,6 +167,22 @@ KVT_API int kvt_topk_select_band(const float* cand_score32, const int32_t* cand_
                     int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len,
                     int64_t run_stride, int32_t* n_runs, void* stream);
 
+/* ---- INT4 keys: fast estimates on the integer tensor cores ------------------------------
+ * kvt_i4_qprep writes, per lane, the query as 4 signed 8-bit digits on power-of-two scales
+ * laid out as m16n8k32 B fragments in the INT4 nibble order, plus per-group error weights
+ * (kvt_i4_qprep_bytes(n_lanes, d) bytes, 16 B aligned; d = 128 or 256).
+ * kvt_cand_score_i4mma = kvt_cand_score_f32 for KVT_I4 keys (records of kvt_kv_quant) with
+ * the inner products done exactly in int32 by MMA; it also max-es a rigorous per-lane bound
+ * on |estimate - canonical f64 dot| into err[4 i + 3] (the kvt_select_plan2 record, which
+ * must be written first), which kvt_topk_select_band then uses as E.  Runs kvt_i4_qprep
+ * into qprep_ws itself. */
+KVT_API size_t kvt_i4_qprep_bytes(int64_t n_lanes, int d);
+KVT_API int kvt_i4_qprep(const void* q, int q_dtype, int64_t n_lanes, int d, void* out, void* stream);
+KVT_API int kvt_cand_score_i4mma(const void* q, int q_dtype, const void* keys, int64_t n_lanes,
+                    int64_t lane_stride, int d, const int32_t* items, int64_t item_stride,
+                    const int32_t* n_items, float* cand_score32, int32_t* cand_tok,
+                    int64_t cand_stride, double* err, void* qprep_ws, void* stream);
+
 /* ---- K5: exact top-k ---------------------------------------------------------------------
  * Result contract of select_top_k (chunk_tree.py:233-338) / brute force
  * (engine.py:337-339): the k best candidates by (score desc, token asc).  One thread-

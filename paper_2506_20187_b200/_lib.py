@@ -70,6 +70,10 @@ kvt_select_plan2 = _sig("kvt_select_plan2", ctypes.c_int, _i64, _i64, _i32, _vp,
                         _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp)
 kvt_cand_score_f32 = _sig("kvt_cand_score_f32", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _vp,
                           _vp, _vp, _i64, _vp)
+kvt_i4_qprep_bytes = _sig("kvt_i4_qprep_bytes", _sz, _i64, _i32)
+kvt_i4_qprep = _sig("kvt_i4_qprep", ctypes.c_int, _vp, _i32, _i64, _i32, _vp, _vp)
+kvt_cand_score_i4mma = _sig("kvt_cand_score_i4mma", ctypes.c_int, _vp, _i32, _vp, _i64, _i64, _i32, _vp, _i64, _vp,
+                            _vp, _vp, _i64, _vp, _vp, _vp)
 kvt_topk_select_band = _sig("kvt_topk_select_band", ctypes.c_int, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i32,
                             _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp)
 kvt_token_scores = _sig("kvt_token_scores", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i64,
@@ -98,7 +102,7 @@ EXPORTED = [
     "kvt_topk_select_runs",
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
     "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_select_plan2", "kvt_cand_score_f32",
-    "kvt_topk_select_band", "kvt_kv_dequant",
+    "kvt_topk_select_band", "kvt_kv_dequant", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
 ]
 
 

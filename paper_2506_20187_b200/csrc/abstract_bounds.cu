@@ -457,7 +457,7 @@ static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int 
     // uniform grid, vector-aligned rows, d = 128 G: the TMA-staged kernel
     const int64_t row = (int64_t)d * sizeof(AT);
     if (!ls && sizeof(AT) <= 4 && d == 128 * G && G <= 2 && row % 16 == 0 && ((uintptr_t)amax % 16) == 0 && ((uintptr_t)amin % 16) == 0 &&
-        (als * (int64_t)sizeof(AT)) % 16 == 0 && n_lanes <= 2147483647LL) {
+        (als * (int64_t)sizeof(AT)) % 16 == 0 && n_lanes <= 2147483647LL && 2 * (2 * 64 * row) <= 200 * 1024) {
         const int tile = (int)(2 * 64 * row);
         const int stages = (int)kvt::imax(2, kvt::imin(4, (100 * 1024) / tile));
         const size_t smem = (size_t)stages * tile + 16 * (size_t)stages + 16;

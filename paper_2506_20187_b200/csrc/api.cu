@@ -63,6 +63,7 @@ struct LayerWs {
     float* cs32;
     int32_t* cand_tok;
     char* attn_part;
+    unsigned char* qprep;
     size_t bytes;
 };
 
@@ -81,6 +82,7 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     w.cand_tok = c.take<int32_t>((size_t)(n_lanes * n));
     w.cs32 = c.take<float>((size_t)(n_lanes * n));
     w.attn_part = c.take<char>(kvt_attn_workspace_bytes(n_lanes, d, MAX_SPLITS));  // tickets + partials
+    w.qprep = c.take<unsigned char>(kvt_i4_qprep_bytes(n_lanes, d));              // INT4 query digits
     w.bytes = c.used;
     return w;
 }
@@ -122,8 +124,12 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
                           fast ? w.err : nullptr, a->d, stream);
     if (rc) return rc;
     if (fast) {
-        rc = kvt_cand_score_f32(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items,
-                                item_cap, w.n_items, w.cs32, w.cand_tok, a->n, stream);
+        if (a->key_dtype == KVT_I4)  // exact int32 inner products on the tensor cores + per-lane bound
+            rc = kvt_cand_score_i4mma(a->q, a->q_dtype, a->keys, a->n_lanes, a->lane_stride, a->d, w.items, item_cap,
+                                      w.n_items, w.cs32, w.cand_tok, a->n, w.err, w.qprep, stream);
+        else
+            rc = kvt_cand_score_f32(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items,
+                                    item_cap, w.n_items, w.cs32, w.cand_tok, a->n, stream);
         if (rc) return rc;
         rc = kvt_topk_select_band(w.cs32, w.cand_tok, w.n_cand, a->n, w.err, a->n_lanes, a->k, a->q, a->q_dtype,
                                   a->keys, a->key_dtype, a->lane_stride, a->d, w.cand_score, a->sel_tok,

@@ -112,15 +112,20 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     // prefix of per-lane item counts (the flattened work list)
+    // one block scan: thread t owns a contiguous run of lanes (independent loads, one latency)
     long long carry = 0;
-    for (int base = 0; base < n_lanes; base += TS_THREADS) {
-        const int i = base + tid;
+    {
+        const int per = (n_lanes + TS_THREADS - 1) / TS_THREADS;
+        const int a = min(n_lanes, tid * per), b = min(n_lanes, a + per);
         long long v = 0;
-        if (i < n_lanes) v = IMPLICIT ? (n_implicit + 63) / 64 : (long long)n_items[i];
+        for (int i = a; i < b; ++i) v += IMPLICIT ? (n_implicit + 63) / 64 : (long long)n_items[i];
         long long tot;
-        const long long ex = block_excl_scan<long long>(v, scan_sh, tot);
-        if (i < n_lanes) lane_off[i] = (int32_t)(carry + ex);
-        carry += tot;
+        long long run = block_excl_scan<long long>(v, scan_sh, tot);
+        for (int i = a; i < b; ++i) {
+            lane_off[i] = (int32_t)run;
+            run += IMPLICIT ? (n_implicit + 63) / 64 : (long long)n_items[i];
+        }
+        carry = tot;
     }
     if (tid == 0) {
         lane_off[n_lanes] = (int32_t)carry;
@@ -137,31 +142,50 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const int64_t g_begin = kvt::imin(total, (int64_t)blockIdx.x * per);
     const int64_t g_end = kvt::imin(total, g_begin + per);
 
-    if (warp == TS_CONSUMERS) {  // ---- producer: one elected thread drives the bulk-copy engine ----
-        if (lane == 0) {
-            int cur = 0;
-            int64_t i = 0;
-            int ps = 0, pr = 0;
-            for (int64_t g = g_begin; g < g_end; ++g, ++i) {
-                while (g >= lane_off[cur + 1]) ++cur;
-                const int64_t it = g - lane_off[cur];
+    if (warp == TS_CONSUMERS) {  // ---- producer warp: lane 0 drives the bulk-copy engine ----
+        // explicit item lists are read 32 items at a time (one load per lane, shuffled to
+        // lane 0): one memory latency per batch instead of per item
+        int cur = 0;
+        {  // binary search: last lane with lane_off[lane] <= g_begin
+            int lo = 0, hi = n_lanes - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (lane_off[mid] <= g_begin) lo = mid; else hi = mid - 1;
+            }
+            cur = lo;
+        }
+        int ps = 0, pr = 0;
+        int64_t g = g_begin;
+        while (g < g_end) {
+            while (g >= lane_off[cur + 1]) ++cur;
+            const int64_t it0 = g - lane_off[cur];
+            const int nb = (int)kvt::imin((int64_t)32, kvt::imin((int64_t)lane_off[cur + 1] - g, g_end - g));
+            int m0 = 0, m1 = 0, m2 = 0;
+            if (!IMPLICIT && lane < nb) {
+                const int32_t* m = items + ((int64_t)cur * item_stride + it0 + lane) * 3;
+                m0 = m[0]; m1 = m[1]; m2 = m[2];
+            }
+            for (int j = 0; j < nb; ++j) {
                 int64_t t0, cnt;
                 int pos0;
-                if (IMPLICIT) { t0 = it * 64; cnt = kvt::imin(64, n_implicit - t0); pos0 = (int)t0; }
+                if (IMPLICIT) { t0 = (it0 + j) * 64; cnt = kvt::imin((int64_t)64, n_implicit - t0); pos0 = (int)t0; }
                 else {
-                    const int32_t* m = items + ((int64_t)cur * item_stride + it) * 3;
-                    t0 = m[0]; cnt = m[1]; pos0 = m[2];
+                    t0 = __shfl_sync(KVT_FULL, m0, j);
+                    cnt = __shfl_sync(KVT_FULL, m1, j);
+                    pos0 = __shfl_sync(KVT_FULL, m2, j);
                 }
-                // ring position without integer division: stage ps, fill round pr
                 const int s = ps;
-                if (pr > 0) mbar_wait(&empty[s], (uint32_t)((pr - 1) & 1));
+                if (lane == 0) {
+                    if (pr > 0) mbar_wait(&empty[s], (uint32_t)((pr - 1) & 1));
+                    const uint32_t bytes = (uint32_t)(cnt * row_b);
+                    meta[s] = make_int4(cur, (int)t0, (int)cnt, pos0);
+                    mbar_arrive_expect_tx(&full[s], bytes);
+                    bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)cur * lane_stride_b + t0 * row_b, bytes,
+                             &full[s]);
+                }
                 if (++ps == stages) { ps = 0; ++pr; }
-                const uint32_t bytes = (uint32_t)(cnt * row_b);
-                meta[s] = make_int4(cur, (int)t0, (int)cnt, pos0);
-                mbar_arrive_expect_tx(&full[s], bytes);
-                bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)cur * lane_stride_b + t0 * row_b, bytes,
-                         &full[s]);
             }
+            g += nb;
         }
         return;
     }

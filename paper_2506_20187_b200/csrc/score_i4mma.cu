@@ -1,0 +1,396 @@
+// score_i4mma.cu -- K4 fast estimates for INT4 key records on the integer tensor cores.
+//
+// The candidate logits of importance.py:27-33 over INT4 records (quant.cu) are estimated as
+//     est(t) = sum_g [ s_g(t) * inner_g(t) + m_g(t) * Qt_g ],   inner_g = sum_{j in g} c_j(t) qt_j
+// with c_j the 4-bit codes, (s_g, m_g) the group's fp16 (scale, min) and qt a decomposition of
+// the query into P = 4 signed 8-bit digits on power-of-two scales,
+//     qt_j = sum_p s_p qi_{p,j},   s_p = s_0 2^-7p,   |qi| <= 127.
+// inner_g is then an exact integer combination: one m16n8k32 s8 MMA per (8 dims of each of 4
+// groups) x 16 tokens sums c_j qi_{p,j} exactly in int32, the record's nibbles become MMA
+// operands with one mask (lo) or shift+mask (hi) per 4 codes -- the K order is permuted to the
+// nibble order and the query digits are laid out to match (kvt_i4_qprep).  The epilogue is a
+// few f64 fmas per (token, group): inner_g is exact in f64 (<= 37 significant bits), and so
+// are s_g * inner_g and m_g * Qt_g, so est(t) carries only a handful of f64 roundings before
+// the final rounding to f32.  A rigorous per-token bound
+//     |est32(t) - canonical f64 dot(t)| <= e(t) = 1.001 [u |est32(t)| + sum_g (15|s_g| + |m_g|) w_g(t)]
+// (u = 2^-24) covers the final f32 rounding, the f64 roundings, the digit residual q - qt, the
+// canonical dot's own f64 rounding and -- only for groups where fmaf(c, s, m) is not exact in
+// f32 for some code c (a test on the fp16 exponents of s and m) -- the fp32 rounding of the
+// dequantised element the canonical dot sees; w_g per lane and group comes from
+// kvt_i4_qprep.  The per-lane max of e(t) is atomically max-ed into err[4 lane + 3], where
+// the band select (select2/select3) takes it as E: the band is then a few ulps wide and the
+// selected set stays the exact canonical top-k.
+//
+// Dataflow: the persistent TMA ring of score.cu (one producer thread issuing cp.async.bulk
+// of 64-token items, plus the lane's 560 B digit block on a lane change), 4 consumer warps,
+// warp w owning tokens 16w..16w+15 of the item.  Per 16 tokens and 128 dims a warp issues
+// 2 LDS.128 of codes, 8 MMAs and ~40 f32 ops -- a few instructions per token instead of the
+// ~4 per dim of CUDA-core dequantisation, so the kernel streams at HBM rate.
+#include <cfloat>
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace kvt {
+
+constexpr int QM_CONSUMERS = 4;
+constexpr int QM_THREADS = (QM_CONSUMERS + 1) * 32;
+constexpr int QM_STAGES = 8;
+
+__host__ __device__ __forceinline__ int qprep_bytes(int d) { return (d / 32) * 144 + 16; }
+
+// ---- query digits: one warp per lane ---------------------------------------------------------
+// Block layout per lane: [G][4 parts][4 i][b0, b1] (G*128 B) | [G](Qt_g f64, w0_g, w1_g f32) |
+// s_0..s_3 f32.
+// b0 byte j = qi_p[32g + 8i + 2j], b1 byte j = qi_p[32g + 8i + 2j + 1] (the nibble order).
+template <typename QT>
+__global__ void qprep_kernel(const QT* __restrict__ q, int64_t n_lanes, int d, unsigned char* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t li = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (li >= n_lanes) return;
+    const int G = d / 32;
+    const QT* ql = q + li * d;
+    unsigned char* blk = out + li * (int64_t)qprep_bytes(d);
+    double mx = 0.0;
+    for (int g = 0; g < G; ++g) mx = fmax(mx, fabs((double)ql[32 * g + lane]));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(KVT_FULL, mx, off));
+    double s0 = 1.0;
+    if (mx > 0.0) {
+        int e;
+        frexp(mx / 127.0, &e);
+        s0 = ldexp(1.0, e);
+    }
+    // canonical dot rounding depth n = 4 ceil(d / 128) + 5 (plan.cu, oracle.bounds)
+    const double n_can = 4.0 * ((d + 127) / 128) + 5.0;
+    const double u = 0x1p-24;
+    unsigned char* cst = blk + G * 128;
+    for (int g = 0; g < G; ++g) {
+        const int e = lane;  // element within the group
+        const double qv = (double)ql[32 * g + e];
+        double r = qv, qt = 0.0, qd = 0.0;
+        const int off = 8 * (e >> 3) + 4 * (e & 1) + ((e & 7) >> 1);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const double sp = ldexp(s0, -7 * p);
+            double di = rint(r / sp);
+            di = fmin(127.0, fmax(-127.0, di));
+            blk[g * 128 + p * 32 + off] = (unsigned char)(signed char)(int)di;
+            qt += di * sp;  // exact: few significant bits
+            qd += fabs(di) * sp;
+            r = qv - qt;
+        }
+        double qabs = fabs(qv), r1 = fabs(r), qts = qt;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            qabs += __shfl_xor_sync(KVT_FULL, qabs, o);
+            r1 += __shfl_xor_sync(KVT_FULL, r1, o);
+            qd += __shfl_xor_sync(KVT_FULL, qd, o);
+            qts += __shfl_xor_sync(KVT_FULL, qts, o);  // exact: multiples of s_3, < 2^40 s_3
+        }
+        if (lane == 0) {
+            // w0_g (always): canonical f64 ((2n+4) 2^-53) on sum|q|, the digit residual, and
+            // (G + 3) 2^-53 on sum_p s_p|qi| for the f64 epilogue.  w1_g (groups whose
+            // dequantisation rounds): u on sum|q|.  1% slack for the f64 evaluation here.
+            const double w0 = 1.01 * (qabs * (2.0 * n_can + 4.0) * 0x1p-53 + r1 * (1.0 + 0x1p-40) +
+                                      (G + 3.0) * 0x1p-53 * qd) + DBL_MIN;
+            const double w1 = 1.01 * u * qabs;
+            float f0 = (float)w0, f1 = (float)w1;
+            if ((double)f0 < w0) f0 = nextafterf(f0, INFINITY);
+            if ((double)f1 < w1) f1 = nextafterf(f1, INFINITY);
+            *reinterpret_cast<double*>(cst + 16 * g) = qts;
+            reinterpret_cast<float*>(cst + 16 * g)[2] = f0;
+            reinterpret_cast<float*>(cst + 16 * g)[3] = f1;
+        }
+    }
+    if (lane < 4) reinterpret_cast<float*>(blk + G * 144)[lane] = (float)ldexp(s0, -7 * lane);
+}
+
+// fmaf(c, s, m) is exact in f32 for every code c in 0..15 when s and m (fp16) are multiples
+// of 2^L and 15|s| + |m| < 2^(L + 24); L from the fp16 exponent fields (lsb of the format).
+__device__ __forceinline__ bool i4_group_exact(uint32_t hm2, float sc, float mn) {
+    const uint32_t hs = hm2 & 0xffffu, hmn = hm2 >> 16;
+    const int es = (int)((hs >> 10) & 31u), em = (int)((hmn >> 10) & 31u);
+    const int ls = (es ? es : 1) - 25, lm = (em ? em : 1) - 25;
+    const bool zs = (hs & 0x7fffu) == 0u, zm = (hmn & 0x7fffu) == 0u;
+    const int L = zs ? lm : (zm ? ls : min(ls, lm));
+    return __fmaf_rn(15.f, fabsf(sc), fabsf(mn)) < __int_as_float((L + 24 + 127) << 23);
+}
+
+__device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// ---- the scoring kernel --------------------------------------------------------------------
+template <int R>  // R = d / 128 rounds of 4 groups
+__global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
+    const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
+    int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
+    float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err) {
+    constexpr int d = 128 * R;
+    constexpr int G = 4 * R;
+    constexpr int row_b = d / 2 + G * 4;
+    constexpr int tile_b = 64 * row_b;
+    constexpr int qb = G * 144 + 16;
+    constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t full[QM_STAGES], empty[QM_STAGES];
+    __shared__ int4 meta[QM_STAGES];
+    __shared__ long long scan_sh[33];
+    __shared__ long long start_info[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // flattened item list: find the first lane of this CTA's contiguous range (one block scan)
+    long long total;
+    {
+        const int per = (n_lanes + QM_THREADS - 1) / QM_THREADS;
+        const int a = min(n_lanes, tid * per), b = min(n_lanes, a + per);
+        long long v = 0;
+        for (int i = a; i < b; ++i) v += n_items[i];
+        long long run = block_excl_scan<long long>(v, scan_sh, total);
+        const long long per_cta = (total + gridDim.x - 1) / gridDim.x;
+        const long long g0 = min(total, (long long)blockIdx.x * per_cta);
+        for (int i = a; i < b; ++i) {
+            const long long c = n_items[i];
+            if (c > 0 && g0 >= run && g0 < run + c) { start_info[0] = i; start_info[1] = g0 - run; }
+            run += c;
+        }
+        if (tid == 0) {
+            for (int s = 0; s < QM_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], QM_CONSUMERS); }
+            fence_mbar_init();
+        }
+    }
+    __syncthreads();
+    const long long per_cta = (total + gridDim.x - 1) / gridDim.x;
+    const long long g_begin = min(total, (long long)blockIdx.x * per_cta);
+    const long long g_end = min(total, g_begin + per_cta);
+    const long long n_my = g_end - g_begin;
+
+    if (warp == QM_CONSUMERS) {  // ---- producer warp: lane 0 drives the bulk-copy engine ----
+        // Item metadata is fetched 32 items at a time (one coalesced load per lane, handed to
+        // lane 0 by shuffles), so the issue loop pays one memory latency per batch, not per item.
+        if (n_my > 0) {
+            int cur = (int)start_info[0];
+            long long it = start_info[1];
+            long long cnt_cur = n_items[cur];
+            long long cnt_next = cur + 1 < n_lanes ? n_items[cur + 1] : 0;
+            int prev = -1;
+            int ps = 0, pr = 0;
+            long long g = 0;
+            while (g < n_my) {
+                while (it >= cnt_cur) {
+                    ++cur;
+                    it = 0;
+                    cnt_cur = cnt_next;
+                    cnt_next = cur + 1 < n_lanes ? n_items[cur + 1] : 0;
+                }
+                const int nb = (int)min(32LL, min(cnt_cur - it, n_my - g));
+                int m0 = 0, m1 = 0, m2 = 0;
+                if (lane < nb) {
+                    const int32_t* m = items + ((int64_t)cur * item_stride + it + lane) * 3;
+                    m0 = m[0]; m1 = m[1]; m2 = m[2];
+                }
+                for (int j = 0; j < nb; ++j) {
+                    const int t0 = __shfl_sync(KVT_FULL, m0, j), cnt = __shfl_sync(KVT_FULL, m1, j);
+                    const int pos0 = __shfl_sync(KVT_FULL, m2, j);
+                    const int s = ps;
+                    const bool newq = cur != prev;
+                    if (lane == 0) {
+                        if (pr > 0) mbar_wait(&empty[s], (uint32_t)((pr - 1) & 1));
+                        const uint32_t bytes = (uint32_t)(cnt * row_b) + (newq ? (uint32_t)qb : 0u);
+                        meta[s] = make_int4(cur, t0, cnt, pos0);
+                        mbar_arrive_expect_tx(&full[s], bytes);
+                        unsigned char* st = smem + (size_t)s * stage_b;
+                        bulk_g2s(st, keys + (int64_t)cur * lane_stride_b + (int64_t)t0 * row_b,
+                                 (uint32_t)(cnt * row_b), &full[s]);
+                        if (newq) bulk_g2s(st + tile_b, qprep + (int64_t)cur * qb, (uint32_t)qb, &full[s]);
+                    }
+                    prev = cur;
+                    if (++ps == QM_STAGES) { ps = 0; ++pr; }
+                }
+                it += nb;
+                g += nb;
+            }
+        }
+        return;
+    }
+
+    // ---- consumers ----
+    const int gid = lane >> 2, tig = lane & 3;
+    uint32_t B[R][2][4][2];
+    double qt[R], sp[4];
+    float w0[R], w1[R];
+    int cur = -1;
+    float emax = 0.f;
+    int cs = 0, cr = 0;
+    for (long long g = 0; g < n_my; ++g) {
+        const int s = cs;
+        mbar_wait(&full[s], (uint32_t)(cr & 1));
+        if (++cs == QM_STAGES) { cs = 0; ++cr; }
+        const int4 mt = meta[s];
+        const unsigned char* st = smem + (size_t)s * stage_b;
+        if (mt.x != cur) {
+            // flush the finished lane's error max, then load the new lane's digits
+            float e = emax;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) e = fmaxf(e, __shfl_xor_sync(KVT_FULL, e, o));
+            if (lane == 0 && cur >= 0 && e > 0.f)
+                atomicMax(reinterpret_cast<unsigned long long*>(err + (int64_t)cur * 4 + 3),
+                          (unsigned long long)__double_as_longlong((double)e));
+            emax = 0.f;
+            cur = mt.x;
+            const unsigned char* qs = st + tile_b;
+            const bool role = (gid >> 1) == tig;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int gq = 4 * r + tig;
+#pragma unroll
+                for (int S = 0; S < 2; ++S) {
+                    const int p = 2 * S + (gid & 1);
+                    if (role) {
+                        const uint4 x0 = *reinterpret_cast<const uint4*>(qs + gq * 128 + p * 32);
+                        const uint4 x1 = *reinterpret_cast<const uint4*>(qs + gq * 128 + p * 32 + 16);
+                        B[r][S][0][0] = x0.x; B[r][S][0][1] = x0.y; B[r][S][1][0] = x0.z; B[r][S][1][1] = x0.w;
+                        B[r][S][2][0] = x1.x; B[r][S][2][1] = x1.y; B[r][S][3][0] = x1.z; B[r][S][3][1] = x1.w;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) B[r][S][i][0] = B[r][S][i][1] = 0u;
+                    }
+                }
+                qt[r] = *reinterpret_cast<const double*>(qs + G * 128 + 16 * gq);
+                const float2 c2 = *reinterpret_cast<const float2*>(qs + G * 128 + 16 * gq + 8);
+                w0[r] = c2.x;
+                w1[r] = c2.y;
+            }
+            const float4 s4 = *reinterpret_cast<const float4*>(qs + G * 144);
+            sp[0] = s4.x; sp[1] = s4.y; sp[2] = s4.z; sp[3] = s4.w;
+        }
+        const int cnt = mt.z, pos0 = mt.w, t0 = mt.y;
+        if (16 * warp < cnt) {
+            const int row0 = 16 * warp + gid, row1 = row0 + 8;
+            double est0 = 0.0, est1 = 0.0;
+            float er0 = 0.f, er1 = 0.f;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int gq = 4 * r + tig;
+                const uint4 A0 = *reinterpret_cast<const uint4*>(st + row0 * row_b + 16 * gq);
+                const uint4 A1 = *reinterpret_cast<const uint4*>(st + row1 * row_b + 16 * gq);
+                const uint32_t w0v[4] = {A0.x, A0.y, A0.z, A0.w}, w1v[4] = {A1.x, A1.y, A1.z, A1.w};
+                int c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t a0 = w0v[i] & 0x0f0f0f0fu, a2 = (w0v[i] >> 4) & 0x0f0f0f0fu;
+                    const uint32_t a1 = w1v[i] & 0x0f0f0f0fu, a3 = (w1v[i] >> 4) & 0x0f0f0f0fu;
+                    mma_s8(c0, a0, a1, a2, a3, B[r][0][i][0], B[r][0][i][1]);
+                    mma_s8(c1, a0, a1, a2, a3, B[r][1][i][0], B[r][1][i][1]);
+                }
+                // c0: parts 0,1 / c1: parts 2,3 of group gq; [0],[1] row0, [2],[3] row1.
+                // inner = sum_p s_p D_p exactly (multiples of s_3 below 2^40 s_3)
+                const double in0 =
+                    fma(sp[3], (double)c1[1], fma(sp[2], (double)c1[0], fma(sp[1], (double)c0[1], sp[0] * (double)c0[0])));
+                const double in1 =
+                    fma(sp[3], (double)c1[3], fma(sp[2], (double)c1[2], fma(sp[1], (double)c0[3], sp[0] * (double)c0[2])));
+                const uint32_t h0 = *reinterpret_cast<const uint32_t*>(st + row0 * row_b + d / 2 + 4 * gq);
+                const uint32_t h1 = *reinterpret_cast<const uint32_t*>(st + row1 * row_b + d / 2 + 4 * gq);
+                const __half2 p0 = *reinterpret_cast<const __half2*>(&h0), p1 = *reinterpret_cast<const __half2*>(&h1);
+                const float sc0 = __low2float(p0), mn0 = __high2float(p0);
+                const float sc1 = __low2float(p1), mn1 = __high2float(p1);
+                est0 += fma((double)sc0, in0, (double)mn0 * qt[r]);  // products exact, one rounding
+                est1 += fma((double)sc1, in1, (double)mn1 * qt[r]);
+                er0 += __fmaf_rn(15.f, fabsf(sc0), fabsf(mn0)) * (i4_group_exact(h0, sc0, mn0) ? w0[r] : w0[r] + w1[r]);
+                er1 += __fmaf_rn(15.f, fabsf(sc1), fabsf(mn1)) * (i4_group_exact(h1, sc1, mn1) ? w0[r] : w0[r] + w1[r]);
+            }
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                est0 += __shfl_xor_sync(KVT_FULL, est0, o);
+                est1 += __shfl_xor_sync(KVT_FULL, est1, o);
+                er0 += __shfl_xor_sync(KVT_FULL, er0, o);
+                er1 += __shfl_xor_sync(KVT_FULL, er1, o);
+            }
+            const int row = tig == 0 ? row0 : row1;
+            const float est = (float)(tig == 0 ? est0 : est1);
+            const float er = 1.001f * __fmaf_rn(0x1p-24f, fabsf(est), tig == 0 ? er0 : er1);
+            if (tig < 2 && row < cnt) {
+                out32[(int64_t)cur * out_stride + pos0 + row] = est;
+                if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + row] = t0 + row;
+                emax = fmaxf(emax, er);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    float e = emax;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) e = fmaxf(e, __shfl_xor_sync(KVT_FULL, e, o));
+    if (lane == 0 && cur >= 0 && e > 0.f)
+        atomicMax(reinterpret_cast<unsigned long long*>(err + (int64_t)cur * 4 + 3),
+                  (unsigned long long)__double_as_longlong((double)e));
+}
+
+}  // namespace kvt
+
+using namespace kvt;
+
+extern "C" size_t kvt_i4_qprep_bytes(int64_t n_lanes, int d) {
+    if (d != 128 && d != 256) return 0;
+    return (size_t)n_lanes * (size_t)qprep_bytes(d);
+}
+
+extern "C" int kvt_i4_qprep(const void* q, int q_dtype, int64_t n_lanes, int d, void* out, void* stream) {
+    if (d != 128 && d != 256) return KVT_ERR_SHAPE;
+    if (n_lanes <= 0) return n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
+    if (!q || !out || ((uintptr_t)out % 16)) return KVT_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int wpb = 8;
+    const unsigned grid = (unsigned)((n_lanes + wpb - 1) / wpb);
+    if (q_dtype == KVT_F32) qprep_kernel<float><<<grid, 32 * wpb, 0, st>>>((const float*)q, n_lanes, d, (unsigned char*)out);
+    else if (q_dtype == KVT_F64) qprep_kernel<double><<<grid, 32 * wpb, 0, st>>>((const double*)q, n_lanes, d, (unsigned char*)out);
+    else return KVT_ERR_DTYPE;
+    return kvt_check_launch();
+}
+
+template <int R>
+static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const int32_t* items, int64_t item_stride,
+                        const int32_t* n_items, const void* qprep, float* os, int32_t* ot, int64_t ostr, double* err,
+                        cudaStream_t st) {
+    constexpr int d = 128 * R, G = 4 * R, row_b = d / 2 + G * 4, tile_b = 64 * row_b, qb = G * 144 + 16;
+    constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
+    const size_t smem = (size_t)QM_STAGES * stage_b;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(score_i4mma_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return kvt_set_cuda_error(e);
+        configured = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = (int)std::min<size_t>(4, (200 * 1024) / (smem + 2048));
+    score_i4mma_kernel<R><<<sms * std::max(per_sm, 1), QM_THREADS, smem, st>>>(
+        (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
+        ostr, err);
+    return kvt_check_launch();
+}
+
+extern "C" int kvt_cand_score_i4mma(const void* q, int q_dtype, const void* keys, int64_t n_lanes, int64_t lane_stride,
+                                    int d, const int32_t* items, int64_t item_stride, const int32_t* n_items,
+                                    float* cand_score32, int32_t* cand_tok, int64_t cand_stride, double* err,
+                                    void* qprep_ws, void* stream) {
+    if (d != 128 && d != 256) return KVT_ERR_SHAPE;
+    if (n_lanes <= 0) return n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
+    if (!keys || !items || !n_items || !cand_score32 || !err || !qprep_ws) return KVT_ERR_ARG;
+    if (((uintptr_t)keys % 16) || (lane_stride % 16) || n_lanes > INT32_MAX) return KVT_ERR_SHAPE;
+    int rc = kvt_i4_qprep(q, q_dtype, n_lanes, d, qprep_ws, stream);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    return d == 128 ? launch_i4mma<1>(keys, n_lanes, lane_stride, items, item_stride, n_items, qprep_ws, cand_score32,
+                                      cand_tok, cand_stride, err, st)
+                    : launch_i4mma<2>(keys, n_lanes, lane_stride, items, item_stride, n_items, qprep_ws, cand_score32,
+                                      cand_tok, cand_stride, err, st);
+}

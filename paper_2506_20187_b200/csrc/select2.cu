@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(S2_THREADS) topk_select2_kernel(
             if (shift == 16) build_list<uint32_t>(S, k32, cnt);
         }
         const double Tk = (double)key32_to_float((uint32_t)S.prefix);
-        const double E = err[li * 4];  // plan record: [E, tau, Umax, 0]
+        const double E = err[li * 4 + 3] > 0.0 ? err[li * 4 + 3] : err[li * 4];  // [E, tau, Umax, E_i4mma]
         hi = Tk + 2.0 * E;
         lo_ = Tk - 2.0 * E;
         // ---- count sure tokens and the band ----

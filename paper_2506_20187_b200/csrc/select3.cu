@@ -139,6 +139,27 @@ __device__ __forceinline__ double s3_canon(const QT* q, const unsigned char* row
     return tree_allreduce(acc);
 }
 
+// Per-warp contiguous ranges in units of 128 elements (32 lanes x float4), so a warp's
+// iteration covers 128 consecutive candidates and lane l owns elements 4l..4l+3 of it.
+struct WarpRange4 {
+    int64_t a, b;
+    __device__ WarpRange4(int64_t n, int warp) {
+        const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128;
+        a = kvt::imin(n, warp * per);
+        b = kvt::imin(n, a + per);
+    }
+};
+
+__device__ __forceinline__ void load4s(const float* sc, int64_t i, int64_t end, bool vec, float v[4]) {
+    if (vec && i + 4 <= end) {
+        const float4 x = *reinterpret_cast<const float4*>(sc + i);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (i + e < end) ? sc[i + e] : -INFINITY;
+    }
+}
+
 template <typename QT, typename T>
 __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
     const float* __restrict__ cs32, const int32_t* __restrict__ ctok, const int32_t* __restrict__ n_cand,
@@ -148,8 +169,9 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
     int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs) {
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ S3Shared S;
+    __shared__ long long w_sel[S3_WARPS];
+    __shared__ int band_pos[S3_BAND_CAP];
     uint32_t* lkey = reinterpret_cast<uint32_t*>(dyn_smem);
-    int32_t* lpos = reinterpret_cast<int32_t*>(lkey + S3_LIST_CAP);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t li = blockIdx.x;
     const int64_t n = n_cand[li];
@@ -160,92 +182,106 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
     const unsigned char* kl = keys + li * lane_stride_b;
     int32_t* otok = sel_tok + li * sel_stride;
     double* osc = sel_score + li * sel_stride;
+    const bool vec = ((uintptr_t)sc % 16) == 0;
     if (kk <= 0) {
         if (tid == 0) { n_sel[li] = 0; if (run_start) n_runs[li] = 0; }
         return;
     }
-    const double E = rec[li * 4 + 0];
+    const double E = rec[li * 4 + 3] > 0.0 ? rec[li * 4 + 3] : rec[li * 4 + 0];  // K4-i4mma bound if set
     const double lo = rec[li * 4 + 1] - 2.0 * E;
     const double hi = rec[li * 4 + 2] + 2.0 * E;
     const double inv = hi > lo ? (double)S3_BINS / (hi - lo) : 0.0;
 
-    // ---- 1. bucket histogram of the estimates ----
+    // ---- 1. bucket histogram of the estimates (4 per thread per iteration) ----
     for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
-    if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; }
+    if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; S.remaining = 0; }
     __syncthreads();
-    for (int64_t base = 0; base < n; base += S3_THREADS) {
-        const int64_t i = base + tid;
-        const int b = i < n ? s3_bucket((double)sc[i], lo, inv) : -1;
-        const unsigned peers = __match_any_sync(KVT_FULL, b);
-        if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (unsigned)__popc(peers));
+    for (int64_t base = 0; base < n; base += 4 * S3_THREADS) {
+        const int64_t i = base + 4 * tid;
+        float v[4];
+        load4s(sc, i, n, vec, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int bkt = i + e < n ? s3_bucket((double)v[e], lo, inv) : -1;
+            const unsigned peers = __match_any_sync(KVT_FULL, bkt);
+            if (bkt >= 0 && lane == __ffs(peers) - 1) atomicAdd(&S.hist[bkt], (unsigned)__popc(peers));
+        }
     }
     __syncthreads();
     s3_find_bin(S, S.hist, S3_BINS, kk);
     const int bstar = S.bstar;
     const long long need_in_bucket = kk - S.above;
-    // gather the bucket
-    for (int64_t base = 0; base < n; base += S3_THREADS) {
-        const int64_t i = base + tid;
-        const bool m = i < n && s3_bucket((double)sc[i], lo, inv) == bstar;
-        const unsigned ballot = __ballot_sync(KVT_FULL, m);
-        unsigned wb = 0;
-        if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
-        wb = __shfl_sync(KVT_FULL, wb, 0);
-        if (m) {
-            const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
-            if (slot < S3_LIST_CAP) { lkey[slot] = ord_key32(sc[i]); lpos[slot] = (int32_t)i; }
+    // ---- 2. gather the k-th bucket (unordered) ----
+    for (int64_t base = 0; base < n; base += 4 * S3_THREADS) {
+        const int64_t i = base + 4 * tid;
+        float v[4];
+        load4s(sc, i, n, vec, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const bool m = i + e < n && s3_bucket((double)v[e], lo, inv) == bstar;
+            const unsigned ballot = __ballot_sync(KVT_FULL, m);
+            unsigned wb = 0;
+            if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
+            wb = __shfl_sync(KVT_FULL, wb, 0);
+            if (m) {
+                const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
+                if (slot < S3_LIST_CAP) lkey[slot] = ord_key32(v[e]);
+            }
         }
     }
     __syncthreads();
     bool fallback = bstar < 0 || S.list_n > S3_LIST_CAP;
     double hb = 0.0, lb = 0.0;
-    long long need = 0;
-    const WarpRange wr(n, warp);
+    const WarpRange4 wr(n, warp);
+    long long nsure = 0;
+    unsigned int nband_total = 0;
     if (!fallback) {
         const uint32_t T32 = s3_list_select(S, lkey, (int)S.list_n, need_in_bucket);
         const double Tk = (double)key32_to_float(T32);
         hb = Tk + 2.0 * E;
         lb = Tk - 2.0 * E;
-        // ---- 2. sure tokens and the band (stable order per warp range) ----
-        long long nsure = 0, nband = 0;
-        for (int64_t base = wr.a; base < wr.b; base += 32) {
-            const int64_t i = base + lane;
-            const double s = i < wr.b ? (double)sc[i] : -INFINITY;
-            nsure += __popc(__ballot_sync(KVT_FULL, i < wr.b && s > hb));
-            nband += __popc(__ballot_sync(KVT_FULL, i < wr.b && s >= lb && s <= hb));
+        // ---- 3. per-warp sure counts + band members (appended, unordered) ----
+        if (tid == 0) S.list_n = 0;  // reused as the band counter
+        __syncthreads();
+        for (int64_t base = wr.a; base < wr.b; base += 128) {
+            const int64_t i = base + 4 * lane;
+            float v[4];
+            load4s(sc, i, wr.b, vec, v);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double sv = (double)v[e];
+                const bool in = i + e < wr.b;
+                nsure += __popc(__ballot_sync(KVT_FULL, in && sv > hb));
+                const bool bd = in && sv <= hb && sv >= lb;
+                const unsigned ballot = __ballot_sync(KVT_FULL, bd);
+                unsigned wb = 0;
+                if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
+                wb = __shfl_sync(KVT_FULL, wb, 0);
+                if (bd) {
+                    const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
+                    if (slot < S3_BAND_CAP) { S.band_t[slot] = tk[i + e]; band_pos[slot] = (int)(i + e); }
+                }
+            }
         }
-        if (lane == 0) S.warp_cnt[warp] = nband;
-        long long tot_sure;
-        block_excl_scan<long long>(lane == 0 ? nsure : 0, S.scan_sh, tot_sure);
-        long long band_base = 0, tot_band = 0;
-        for (int w = 0; w < S3_WARPS; ++w) {
-            if (w < warp) band_base += S.warp_cnt[w];
-            tot_band += S.warp_cnt[w];
-        }
-        need = kk - tot_sure;
-        if (tot_band > S3_BAND_CAP) {
+        if (lane == 0) w_sel[warp] = nsure;
+        __syncthreads();
+        nband_total = S.list_n;
+        long long tot_sure = 0;
+        for (int w = 0; w < S3_WARPS; ++w) tot_sure += w_sel[w];
+        const long long need = kk - tot_sure;
+        if (nband_total > (unsigned)S3_BAND_CAP) {
             fallback = true;
         } else {
-            long long pos = band_base;
-            for (int64_t base = wr.a; base < wr.b; base += 32) {
-                const int64_t i = base + lane;
-                const double s = i < wr.b ? (double)sc[i] : -INFINITY;
-                const bool m = i < wr.b && s >= lb && s <= hb;
-                const unsigned ballot = __ballot_sync(KVT_FULL, m);
-                if (m) S.band_t[pos + __popc(ballot & ((1u << lane) - 1))] = tk[i];
-                pos += __popc(ballot);
-            }
-            __syncthreads();
-            for (int j = warp; j < (int)tot_band; j += S3_WARPS) {
+            for (int j = warp; j < (int)nband_total; j += S3_WARPS) {
                 const double c = s3_canon<QT, T>(ql, kl + (int64_t)S.band_t[j] * row_b, d, lane);
                 if (lane == 0) S.band_c[j] = c;
             }
             __syncthreads();
-            for (int j = tid; j < (int)tot_band; j += S3_THREADS) {
+            for (int j = tid; j < (int)nband_total; j += S3_THREADS) {
                 const double cj = S.band_c[j];
                 const int tj = S.band_t[j];
                 long long better = 0;
-                for (int f = 0; f < (int)tot_band; ++f) {
+                for (int f = 0; f < (int)nband_total; ++f) {
                     const double cf = S.band_c[f];
                     better += (cf > cj) || (cf == cj && S.band_t[f] < tj);
                 }
@@ -255,10 +291,48 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
         }
     }
     __syncthreads();
-
-    unsigned long long fpref = 0, fmask = 0;
-    long long eq_take_total = 0;
-    if (fallback) {
+    if (!fallback) {
+        // ---- 4. stable compaction: per-warp offsets, lane-level scan inside each window ----
+        long long extra = 0;  // selected band members inside this warp's range
+        for (int j = lane; j < (int)nband_total; j += 32)
+            extra += (band_pos[j] >= wr.a && band_pos[j] < wr.b) ? S.band_sel[j] : 0;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) extra += __shfl_xor_sync(KVT_FULL, extra, off);
+        __syncthreads();
+        if (lane == 0) w_sel[warp] = nsure + extra;
+        __syncthreads();
+        long long pos = 0;
+        for (int w = 0; w < warp; ++w) pos += w_sel[w];
+        for (int64_t base = wr.a; base < wr.b; base += 128) {
+            const int64_t i = base + 4 * lane;
+            float v[4];
+            load4s(sc, i, wr.b, vec, v);
+            bool m[4];
+            double scr[4];
+            int cnt = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double sv = (double)v[e];
+                m[e] = false;
+                scr[e] = sv;
+                if (i + e < wr.b) {
+                    if (sv > hb) m[e] = true;
+                    else if (sv >= lb) {
+                        for (int j = 0; j < (int)nband_total; ++j)
+                            if (band_pos[j] == (int)(i + e)) { m[e] = S.band_sel[j] != 0; scr[e] = S.band_c[j]; break; }
+                    }
+                }
+                cnt += m[e];
+            }
+            const int inc = warp_incl_scan(cnt, lane);
+            long long p = pos + inc - cnt;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (m[e]) { otok[p] = tk[i + e]; osc[p] = scr[e]; ++p; }
+            pos += __shfl_sync(KVT_FULL, inc, 31);
+        }
+        w_sel[warp] = w_sel[warp];  // (no-op: keeps the per-warp totals for the run scan below)
+    } else {
         // ---- exact fallback: canonical f64 for every candidate, 64-bit radix select ----
         double* sc64 = scratch + li * cand_stride;
         for (int64_t base = (int64_t)warp * 8; base < n; base += (int64_t)S3_WARPS * 8) {
@@ -269,11 +343,11 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
                 if (base + u < n) {
                     const unsigned char* row = kl + (int64_t)tk[base + u] * row_b;
                     for (int g = lane; 4 * g < d; g += 32) {
-                        double v[4];
-                        RowLd<T>::load(row, g, d, v);
+                        double vv[4];
+                        RowLd<T>::load(row, g, d, vv);
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
-                            if (4 * g + e < d) acc = fma((double)ql[4 * g + e], v[e], acc);
+                            if (4 * g + e < d) acc = fma((double)ql[4 * g + e], vv[e], acc);
                     }
                 }
                 p[u] = acc;
@@ -309,8 +383,8 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
                     unsigned run = exc;
                     for (int i = 0; i < 8; ++i) {
                         if (run + loc[i] >= rem) {
-                            const int b = 255 - 8 * lane - i;
-                            S.prefix = pf | ((unsigned long long)b << shift);
+                            const int bb = 255 - 8 * lane - i;
+                            S.prefix = pf | ((unsigned long long)bb << shift);
                             S.mask = mk | (0xffull << shift);
                             S.remaining = rem - run;
                             break;
@@ -321,116 +395,53 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
             }
             __syncthreads();
         }
-        fpref = S.prefix;
-        fmask = S.mask;
-        eq_take_total = S.remaining;
-    }
-
-    // ---- 3. stable compaction, ascending token order ----
-    auto is_sel = [&](int64_t i, long long& band_idx, long long& eq_seen, double& score) -> bool {
-        if (!fallback) {
-            const double s = (double)sc[i];
-            score = s;
-            if (s > hb) return true;
-            if (s >= lb) {
-                const long long j = band_idx++;
-                score = S.band_c[j];
-                return S.band_sel[j] != 0;
+        const uint64_t T64 = S.prefix;
+        const long long eq_take_total = S.remaining;
+        // per-warp counts of (key > T) and ties, in warp-range order
+        const WarpRange w1(n, warp);
+        long long c_gt = 0, c_eq = 0;
+        for (int64_t base = w1.a; base < w1.b; base += 32) {
+            const int64_t i = base + lane;
+            uint64_t key = 0;
+            if (i < w1.b) key = ord_key(sc64[i]);
+            c_gt += __popc(__ballot_sync(KVT_FULL, i < w1.b && key > T64));
+            c_eq += __popc(__ballot_sync(KVT_FULL, i < w1.b && key == T64));
+        }
+        __shared__ long long w_eq[S3_WARPS], w_gt[S3_WARPS];
+        if (lane == 0) { w_eq[warp] = c_eq; w_gt[warp] = c_gt; }
+        __syncthreads();
+        long long eq_before = 0, pos = 0;
+        for (int w = 0; w < warp; ++w) {
+            const long long take = max(0LL, min(w_eq[w], eq_take_total - eq_before));
+            pos += w_gt[w] + take;
+            eq_before += w_eq[w];
+        }
+        long long eq_seen = eq_before;
+        for (int64_t base = w1.a; base < w1.b; base += 32) {
+            const int64_t i = base + lane;
+            uint64_t key = 0;
+            if (i < w1.b) key = ord_key(sc64[i]);
+            const bool is_eq = i < w1.b && key == T64;
+            const unsigned eqb = __ballot_sync(KVT_FULL, is_eq);
+            const long long my_eq = eq_seen + __popc(eqb & ((1u << lane) - 1));
+            const bool m = i < w1.b && (key > T64 || (is_eq && my_eq < eq_take_total));
+            const unsigned ballot = __ballot_sync(KVT_FULL, m);
+            if (m) {
+                const long long p = pos + __popc(ballot & ((1u << lane) - 1));
+                otok[p] = tk[i];
+                osc[p] = sc64[i];
             }
-            return false;
+            pos += __popc(ballot);
+            eq_seen += __popc(eqb);
         }
-        const double c = scratch[li * cand_stride + i];
-        score = c;
-        const uint64_t key = ord_key(c);
-        if (key > fpref) return true;  // fmask is all ones after 8 passes
-        if (key == fpref) return eq_seen++ < eq_take_total;
-        return false;
-    };
-    (void)fmask;
-    // count per warp (band / tie order follows the same warp-range order)
-    long long cnt_sel = 0, cnt_band = 0, cnt_eq = 0;
-    for (int64_t base = wr.a; base < wr.b; base += 32) {
-        const int64_t i = base + lane;
-        bool m = false;
-        if (i < wr.b) {
-            if (!fallback) {
-                const double s = (double)sc[i];
-                m = s > hb;
-                const bool bd = !m && s >= lb;
-                cnt_band += __popc(__ballot_sync(KVT_FULL, bd));
-                (void)bd;
-            } else {
-                const uint64_t key = ord_key(scratch[li * cand_stride + i]);
-                m = key > fpref;
-                cnt_eq += __popc(__ballot_sync(KVT_FULL, key == fpref));
-            }
-        } else {
-            if (!fallback) cnt_band += __popc(__ballot_sync(KVT_FULL, false));
-            else cnt_eq += __popc(__ballot_sync(KVT_FULL, false));
-        }
-        cnt_sel += __popc(__ballot_sync(KVT_FULL, m));
-    }
-    // band/eq members before this warp, and their selected counts
-    __shared__ long long w_band[S3_WARPS], w_eq[S3_WARPS], w_sel[S3_WARPS];
-    if (lane == 0) { w_band[warp] = cnt_band; w_eq[warp] = cnt_eq; w_sel[warp] = cnt_sel; }
-    __syncthreads();
-    long long band_before = 0, eq_before = 0;
-    for (int w = 0; w < warp; ++w) { band_before += w_band[w]; eq_before += w_eq[w]; }
-    long long extra = 0;  // band / tie members of this warp that are selected
-    if (!fallback) {
-        for (long long j = band_before; j < band_before + cnt_band; ++j) extra += S.band_sel[j];
-    } else {
-        extra = max(0LL, min(cnt_eq, eq_take_total - eq_before));
-    }
-    __syncthreads();
-    if (lane == 0) w_sel[warp] = cnt_sel + extra;
-    __syncthreads();
-    long long out_base = 0;
-    for (int w = 0; w < warp; ++w) out_base += w_sel[w];
-    long long pos = out_base;
-    const long long p_begin = pos;
-    long long band_idx = band_before, eq_seen = eq_before;
-    for (int64_t base = wr.a; base < wr.b; base += 32) {
-        // lanes resolve their element in order within the 32-wide window
-        bool m = false;
-        double score = 0.0;
-        const int64_t i = base + lane;
-        // band / tie counters must advance in element order: serialise the rare members
-        bool special = false;
-        if (i < wr.b) {
-            if (!fallback) { const double s = (double)sc[i]; special = !(s > hb) && s >= lb; }
-            else special = ord_key(scratch[li * cand_stride + i]) == fpref;
-        }
-        const unsigned sp = __ballot_sync(KVT_FULL, special);
-        if (i < wr.b) {
-            if (special) {
-                const int before = __popc(sp & ((1u << lane) - 1));
-                long long bi = band_idx + before, es = eq_seen + before;
-                m = is_sel(i, bi, es, score);
-            } else {
-                long long dummy1 = 0, dummy2 = 0;
-                m = is_sel(i, dummy1, dummy2, score);
-            }
-        }
-        band_idx += __popc(sp);
-        eq_seen += __popc(sp);
-        const unsigned ballot = __ballot_sync(KVT_FULL, m);
-        if (m) {
-            const long long p = pos + __popc(ballot & ((1u << lane) - 1));
-            otok[p] = tk[i];
-            osc[p] = score;
-        }
-        pos += __popc(ballot);
     }
     if (tid == 0) n_sel[li] = (int32_t)kk;
     if (!run_start) return;
 
-    // ---- 4. fused run scan (engine.py:176-183); each lane takes a slice of its warp's output ----
-    const long long wlen = pos - p_begin;
-    const long long lper = (wlen + 31) / 32;
-    const long long p_lo = p_begin + kvt::imin(wlen, lane * lper);
-    const long long p_hi = p_begin + kvt::imin(wlen, (lane + 1) * lper);
+    // ---- 5. fused run scan (engine.py:176-183) over the k outputs ----
     __syncthreads();
+    const long long per_t = (kk + S3_THREADS - 1) / S3_THREADS;
+    const long long p_lo = kvt::imin(kk, tid * per_t), p_hi = kvt::imin(kk, p_lo + per_t);
     long long heads = 0;
     for (long long p = p_lo; p < p_hi; ++p) heads += (p == 0 || otok[p] != otok[p - 1] + 1);
     long long tot_h;
@@ -472,7 +483,7 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
                           int64_t run_stride, int32_t* n_runs, cudaStream_t st) {
     const int row_b = RowLd<T>::row_bytes(d);
     const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
-    const size_t smem = (size_t)S3_LIST_CAP * 8;
+    const size_t smem = (size_t)S3_LIST_CAP * 4;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(topk_select3_kernel<QT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,

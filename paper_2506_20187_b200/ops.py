@@ -264,6 +264,22 @@ def cand_score_f32(q: torch.Tensor, keys, plan: dict, n: int):
     return cs, ct
 
 
+def cand_score_i4mma(q: torch.Tensor, keys: "I4KV", plan: dict, n: int):
+    """INT4 keys: estimates with exact int32 inner products on the tensor cores.  Also max-es
+    the per-lane bound on |estimate - canonical dot| into plan["err"][:, 3] (used as E by
+    topk_select_band) -> (cs32 f32, cand_tok i32)."""
+    require_cuda(q, keys)
+    ls, d = _lanes(keys)
+    nl = keys.shape[0]
+    cs = torch.empty((nl, max(n, 1)), dtype=torch.float32, device=q.device)
+    ct = torch.empty((nl, max(n, 1)), dtype=torch.int32, device=q.device)
+    ws = torch.empty(max(int(L.kvt_i4_qprep_bytes(nl, d)), 16), dtype=torch.uint8, device=q.device)
+    L.check(L.kvt_cand_score_i4mma(q.data_ptr(), dtype_code(q), keys.data_ptr(), nl, ls, d, plan["items"].data_ptr(),
+                                   plan["item_cap"], plan["n_items"].data_ptr(), cs.data_ptr(), ct.data_ptr(),
+                                   cs.stride(0), plan["err"].data_ptr(), ws.data_ptr(), _stream()), "cand_score_i4mma")
+    return cs, ct
+
+
 def topk_select_band(cs32: torch.Tensor, ct: torch.Tensor, plan: dict, k: int, q: torch.Tensor, keys,
                      want_runs: bool = True):
     """Exact canonical top-k from f32 estimates (band re-scoring) -> (sel_tok, sel_score, n_sel[, runs])."""

@@ -105,3 +105,45 @@ def test_int4_select_attend_matches_oracle(ops, kind, n, C, rate, exact):
         att = O.attention(Q[i], Kd[i], Vd[i], ref)
         err = np.linalg.norm(out["out"][i].cpu().numpy() - att) / np.linalg.norm(att)
         assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("qkind", ["normal", "wide", "f64"])
+@pytest.mark.parametrize("kind", ["random", "planted"])
+@pytest.mark.parametrize("d,C", [(128, 64), (128, 8), (256, 64)])
+def test_i4mma_estimates_within_bound(ops, kind, qkind, d, C):
+    """K4 on the integer tensor cores: every candidate's estimate lies within the per-lane
+    bound err[:, 3] of its canonical f64 dot, the candidate list equals the CUDA-core f32
+    path's, and the bound is tight enough to keep the re-scoring band narrow."""
+    lanes, n = 5, 3000
+    kt, vt, Kd, Vd, Q = _i4_lanes(ops, kind, lanes, n, d, seed=d + C)
+    rng = np.random.default_rng(7)
+    if qkind == "wide":  # dims spanning 10 decades: exercises the digit residual
+        Q = (Q * 10.0 ** rng.uniform(-8, 2, size=Q.shape)).astype(np.float32)
+    Q[lanes - 1] = 0.0   # a zero query: every estimate exact
+    qt = torch.from_numpy(Q).cuda()
+    if qkind == "f64":
+        qt = qt.double()
+    k = math.ceil(0.1 * n)
+    amax, amin = ops.abstract_build(kt, n, C)
+    U, Lo, A = ops.chunk_bounds(qt, amax, amin, n, C, want_A=True)
+    plan = ops.select_plan(U, Lo, n, k, C, A=A, d=d)
+    cs32, ct32 = ops.cand_score_f32(qt, kt, plan, n)
+    cs, ct = ops.cand_score_i4mma(qt, kt, plan, n)
+    torch.cuda.synchronize()
+    nc = plan["n_cand"].cpu().numpy()
+    err = plan["err"].cpu().numpy()
+    for i in range(lanes):
+        m = int(nc[i])
+        toks = ct[i, :m].cpu().numpy()
+        assert np.array_equal(toks, ct32[i, :m].cpu().numpy())
+        dd = O.dots(Q[i].astype(np.float64) if qkind == "f64" else Q[i], Kd[i])
+        est = cs[i, :m].double().cpu().numpy()
+        e = err[i, 3]
+        gap = np.abs(est - dd[toks]).max() if m else 0.0
+        assert gap <= e, (i, gap, e)
+        if i == lanes - 1:
+            assert gap == 0.0
+        else:
+            Amax = np.abs(Q[i]).astype(np.float64) @ np.abs(Kd[i]).max(0)
+            assert 0 < e <= 2e-5 * Amax, (e, Amax)
+            assert e <= err[i, 0]  # no looser than the CUDA-core f32 bound
