@@ -187,18 +187,47 @@ ORA_API void ora_bounds_ref(const double* q, const double* mx, const double* mn,
 /* is against this definition)                                         */
 /* ------------------------------------------------------------------------------------ */
 /* Record per token: d/2 code bytes (dim 2j in the low nibble, 2j+1 in the high nibble),
- * then d/32 (scale, min) fp16 pairs.  Per group of 32 dims:
- *   lo, hi = min, max;  s = fp16(fl32((hi - lo) / 15));  m = fp16(lo)
- *   code = s == 0 ? 0 : clamp(rint(fl32(fl32(x - m) / s)), 0, 15)
+ * then d/32 (scale, min) fp16 pairs.  Per group of 32 dims (GPU: quant.cu kv_quant_kernel):
+ *   lo, hi = min, max of the inputs clamped to the fp16 range
+ *   m   = fp16_rd(lo)
+ *   s   = fp16_ru(fl_ru(fl_ru(hi - m) * R15)),   R15 = fl_ru(1/15)
+ *   inv = fl32(1 / s)
+ *   code = s == 0 ? 0 : RN_int(fl32(x - m) * inv)            (ties to even, no clamp needed:
+ *          the outward rounding puts the product in [0, 15 (1 + 2^-24)])
  *   x^   = fmaf(code, s, m)                                  (one f32 rounding)
- * Inputs are clamped to the fp16 range first. */
+ * RN_int of the exact product is fmaf(a, inv, 1.5 * 2^23) - 1.5 * 2^23.  The directed
+ * roundings are built from round-to-nearest operations plus exact error terms, so this
+ * file needs no fenv. */
 
 ORA_API int ora_i4_record_bytes(int d) { return d / 2 + (d / 32) * 4; }
 
 static float clamp_h(float x) { return x > 65504.0f ? 65504.0f : (x < -65504.0f ? -65504.0f : x); }
 
+static float sub_ru(float a, float b) {  /* fl_ru(a - b) via TwoSum's exact error */
+    volatile float s = a - b;
+    volatile float bb = s - a;
+    volatile float err = (a - (s - bb)) + (-b - bb);
+    return err > 0.0f ? nextafterf(s, INFINITY) : s;
+}
+static float mul_ru(float a, float b) {  /* fl_ru(a * b): the fma residual is exact */
+    volatile float p = a * b;
+    float err = fmaf(a, b, -p);
+    return err > 0.0f ? nextafterf(p, INFINITY) : p;
+}
+static uint16_t h_bits(_Float16 h) { uint16_t u; memcpy(&u, &h, 2); return u; }
+static _Float16 h_from(uint16_t u) { _Float16 h; memcpy(&h, &u, 2); return h; }
+static _Float16 h_next(_Float16 h, int up) {  /* adjacent finite fp16 toward +inf (up) or -inf */
+    uint16_t u = h_bits(h);
+    if ((u & 0x7fff) == 0) return h_from(up ? 0x0001 : 0x8001);
+    int neg = u >> 15;
+    return h_from((uint16_t)((neg ^ up) ? u + 1 : u - 1));
+}
+static _Float16 h_rd(float x) { _Float16 h = (_Float16)x; return (float)h > x ? h_next(h, 0) : h; }
+static _Float16 h_ru(float x) { _Float16 h = (_Float16)x; return (float)h < x ? h_next(h, 1) : h; }
+
 ORA_API void ora_i4_quant(const float* x, int64_t n, int d, uint8_t* rec) {
     const int rb = ora_i4_record_bytes(d);
+    const float magic = 12582912.0f, r15 = 0.0666666701436042785645f;
     for (int64_t t = 0; t < n; ++t) {
         const float* xt = x + t * d;
         uint8_t* r = rec + t * rb;
@@ -210,17 +239,16 @@ ORA_API void ora_i4_quant(const float* x, int64_t n, int d, uint8_t* rec) {
                 if (v < lo) lo = v;
                 if (v > hi) hi = v;
             }
-            volatile float diff = hi - lo;
-            volatile float sf = diff / 15.0f;
-            _Float16 sh = (_Float16)sf, mh = (_Float16)lo;
-            float sc = (float)sh, mn = (float)mh;
+            _Float16 mh = h_rd(lo);
+            float mn = (float)mh;
+            _Float16 sh = h_ru(mul_ru(sub_ru(hi, mn), r15));
+            float sc = (float)sh;
+            volatile float inv = 1.0f / sc;
             for (int j = 0; j < 32; ++j) {
                 int c = 0;
                 if (sc != 0.0f) {
                     volatile float num = clamp_h(xt[32 * g + j]) - mn;
-                    volatile float q = num / sc;
-                    float rq = rintf(q);
-                    c = rq < 0.0f ? 0 : (rq > 15.0f ? 15 : (int)rq);
+                    c = (int)(fmaf(num, inv, magic) - magic);
                 }
                 int dim = 32 * g + j;
                 r[dim >> 1] |= (uint8_t)(c << ((dim & 1) * 4));

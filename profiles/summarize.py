@@ -1,6 +1,6 @@
 """Summarise ncu captures / launch lists into the markdown tables kept under profiles/.
 
-    python profiles/summarize.py raw   <report.ncu-rep>   > profiles/<name>.md
+    python profiles/summarize.py raw   <report.ncu-rep | raw.csv>   > profiles/<name>.md
     python profiles/summarize.py launches <launches.csv>  > profiles/<name>.md
 """
 
@@ -35,7 +35,11 @@ def short(name: str) -> str:
 
 
 def raw(path: str) -> None:
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # exported on the GPU box with `ncu -i … --page raw --csv`
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    out = out[out.index('"ID"'):]
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     print(f"ncu --set full summary of `{path}` (cold-cache, serialised replay; one launch per kernel)\n")
@@ -63,7 +67,9 @@ def raw(path: str) -> None:
 
 
 def launches(path: str) -> None:
-    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    import gzip
+    fh = gzip.open(path, "rt") if path.endswith(".gz") else open(path)
+    rows = [r for r in csv.reader(fh) if len(r) > 5]
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     tot, cnt = collections.defaultdict(float), collections.Counter()

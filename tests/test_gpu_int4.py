@@ -27,14 +27,20 @@ def ops():
     return _ops
 
 
-@pytest.mark.parametrize("src_dt", [torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("src_dt", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("d", [32, 96, 128, 256])
 def test_kv_quant_codes_bitexact(ops, src_dt, d):
     rng = np.random.default_rng(d)
     lanes, n = 3, 777
     x = (rng.normal(size=(lanes, n, d)) * rng.choice([0.01, 1.0, 30.0], size=(lanes, 1, 1))).astype(np.float32)
     x[0, 5] = 0.0          # constant group -> scale 0
     x[1, 7, :32] = 3.25    # constant group with nonzero value
+    x[2, 9, :32] = 1000.0 + rng.normal(size=32) * 1e-3   # narrow range at large magnitude
+    x[2, 10, :32] = rng.normal(size=32) * 1e-6            # fp16-subnormal scales
+    x[0, 11, :32] = 3e-41                                 # f32 subnormal inputs
+    if src_dt != torch.float16:
+        x[1, 12, :32] = rng.normal(size=32) * 1e5         # beyond the fp16 range: clamped
+        x[1, 13, 0] = -9e4
     xt = torch.from_numpy(x).to(src_dt).cuda()
     dst = ops.I4KV.empty(lanes, n + 5, d, xt.device)
     ops.kv_quant(xt, dst, 0, n)
@@ -43,6 +49,12 @@ def test_kv_quant_codes_bitexact(ops, src_dt, d):
     for i in range(lanes):
         ref = O.i4_quant(xs[i])
         assert np.array_equal(got[i], ref), i
+    # outward rounding: every dequantised value lies within half a step of its (clamped) input
+    deq = np.stack([O.i4_dequant(got[i], d) for i in range(lanes)])
+    scale = got[..., d // 2:].copy().view(np.float16).reshape(lanes, n, d // 32, 2)[..., 0].astype(np.float64)
+    step = np.repeat(scale, 32, axis=-1)
+    xc = np.clip(xs, -65504, 65504).astype(np.float64)
+    assert np.all(np.abs(deq - xc) <= 0.5 * step * (1 + 1e-6) + 1e-6 * np.abs(xc) + 1e-30)
 
 
 def _i4_lanes(ops, kind, lanes, n, d, seed):

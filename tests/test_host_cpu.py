@@ -92,12 +92,28 @@ def test_int4_codec_oracle_matches_numpy_definition():
     rec = O.i4_quant(x)
     g = x.reshape(500, 4, 32)
     lo, hi = g.min(2), g.max(2)
-    sf = ((hi - lo).astype(np.float32) / np.float32(15)).astype(np.float32)
-    sh, mh = sf.astype(np.float16), lo.astype(np.float16)
-    s, m = sh.astype(np.float32), mh.astype(np.float32)
+
+    def h_dir(v, up):  # fp16 rounded toward +inf (up) or -inf, from float32 v
+        h = v.astype(np.float16)
+        bad = (h.astype(np.float32) < v) if up else (h.astype(np.float32) > v)
+        return np.where(bad, np.nextafter(h, np.float16(np.inf if up else -np.inf)), h)
+
+    def f32_up(exact64):  # fl_ru of a value known exactly in f64
+        r = exact64.astype(np.float32)
+        return np.where(r.astype(np.float64) < exact64, np.nextafter(r, np.float32(np.inf)), r)
+
+    mh = h_dir(lo, False)
+    m = mh.astype(np.float32)
+    diff = f32_up(hi.astype(np.float64) - m.astype(np.float64))  # exact in f64 for these ranges
+    sh = h_dir(f32_up(diff.astype(np.float64) * np.float64(np.float32(0.0666666701436042785645))), True)
+    s = sh.astype(np.float32)
+    assert np.all(15 * s.astype(np.float64) >= hi.astype(np.float64) - m) and np.all(m <= lo)
     with np.errstate(divide="ignore", invalid="ignore"):
-        qv = ((g - m[..., None]).astype(np.float32) / s[..., None]).astype(np.float32)
-    c = np.where(s[..., None] == 0, 0, np.clip(np.rint(qv), 0, 15)).astype(np.uint8).reshape(500, 128)
+        inv = (np.float32(1) / s).astype(np.float32)
+        # fl32(x - m) * inv is exact in f64 (24 x 24 bits); np.rint = RN_int, ties to even
+        qv = (g - m[..., None]).astype(np.float32).astype(np.float64) * inv[..., None].astype(np.float64)
+    assert np.all(np.where(s[..., None] == 0, 0, qv) <= 15.5)
+    c = np.where(s[..., None] == 0, 0, np.rint(qv)).astype(np.uint8).reshape(500, 128)
     assert np.array_equal(rec[:, :64], (c[:, 0::2] | (c[:, 1::2] << 4)).astype(np.uint8))
     assert np.array_equal(rec[:, 64:], np.stack([sh, mh], -1).reshape(500, 8).view(np.uint8))
     deq = O.i4_dequant(rec, 128)
