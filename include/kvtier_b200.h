@@ -85,6 +85,9 @@ KVT_API int kvt_kv_quant(const void* src, int src_dtype, int64_t n_lanes, int64_
                          int64_t t_begin, int64_t t_end, int d, void* dst, int64_t dst_lane_stride,
                          void* stream);
 KVT_API int kvt_i4_row_bytes(int d);
+/* Test hook: counts (atomically, into *bad_dev) the positive finite fp16 scales s for which
+ * the codec's fast reciprocal differs from the correctly rounded fl32(1/s).  Expected: 0. */
+KVT_API int kvt_i4_recip_check(int* bad_dev, void* stream);
 /* Expand INT4 records (src lane stride in bytes) of tokens [t_begin, t_end) into rows of
  * dst_dtype (F32/BF16/F16): the device half of a compressed host->HBM tier transfer
  * (pipeline.py:79-103 decompress_rate is this kernel's throughput). */

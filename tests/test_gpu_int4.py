@@ -159,3 +159,30 @@ def test_i4mma_estimates_within_bound(ops, kind, qkind, d, C):
             Amax = np.abs(Q[i]).astype(np.float64) @ np.abs(Kd[i]).max(0)
             assert 0 < e <= 2e-5 * Amax, (e, Amax)
             assert e <= err[i, 0]  # no looser than the CUDA-core f32 bound
+
+
+@pytest.mark.parametrize("d", [32, 96, 128, 256])
+def test_kv_dequant_bitexact(ops, d):
+    """kvt_kv_dequant == the oracle's fmaf(code, scale, min) (f32 exactly; bf16/f16 = RN of it)."""
+    from paper_2506_20187_b200.tier import kv_dequant
+    rng = np.random.default_rng(100 + d)
+    lanes, n = 3, 533
+    x = (rng.normal(size=(lanes, n, d)) * 3.0).astype(np.float32)
+    rec = ops.I4KV.empty(lanes, n, d, "cuda")
+    ops.kv_quant(torch.from_numpy(x).cuda(), rec, 0, n)
+    ref = np.stack([O.i4_dequant(rec.data[i].cpu().numpy(), d) for i in range(lanes)])
+    for dt in (torch.float32, torch.bfloat16, torch.float16):
+        out = torch.full((lanes, n, d), 7.0, dtype=dt, device="cuda")
+        kv_dequant(rec, out, 5, n - 3)
+        got = out.float().cpu().numpy()
+        want = torch.from_numpy(ref).to(dt).float().numpy()
+        assert np.array_equal(got[:, 5:n - 3], want[:, 5:n - 3]), dt
+        assert np.all(got[:, :5] == 7.0) and np.all(got[:, n - 3:] == 7.0), dt
+
+
+def test_codec_reciprocal_exhaustive(ops):
+    """The codec's fast reciprocal equals fl32(1/s) for every positive finite fp16 scale."""
+    from paper_2506_20187_b200 import _lib as L
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L.check(L.kvt_i4_recip_check(bad.data_ptr(), torch.cuda.current_stream().cuda_stream), "recip_check")
+    assert int(bad.item()) == 0
