@@ -357,11 +357,16 @@ def run_ours(args):
             dist.barrier()
 
     # ---- timed region (device-resident inputs) ----
+    # KVT_PROFILE_RANGE=1: cudaProfilerStart/Stop around it, for `ncu --profile-from-start off`
+    # (launch lists and captures of the decode step only; never a bench number).
+    prof = os.environ.get("KVT_PROFILE_RANGE") == "1"
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
         clk.mark("t0")
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for s in range(args.steps):
@@ -370,6 +375,8 @@ def run_ours(args):
             ev1.record(stream)
         ev1.synchronize()
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
         clk.mark("t1")
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps

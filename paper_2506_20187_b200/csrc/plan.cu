@@ -10,6 +10,9 @@
 // keys are staged in shared memory once; histogram weights are row counts.
 // Candidate leaves (U >= tau) are emitted in ascending token order as work items of
 // <= 64 tokens: (tok_start, count, out_pos), out_pos = exclusive prefix of candidate rows.
+// Runs of adjacent candidate leaves are merged: items start at a run's first token and at
+// every multiple of 64 inside a run, and end at the next multiple of 64 or the run's end,
+// so small leaves (C = 8 in the early layers) still give full 64-token items.
 #include "common.cuh"
 
 namespace kvt {
@@ -107,18 +110,33 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
     }
     const double tau = (k <= 0) ? INFINITY : key_to_double(s_prefix);
 
+    // ---- candidate flags (staged over the keys, which are no longer needed) ----
+    int8_t* fl = reinterpret_cast<int8_t*>(plan_smem);
+    __syncthreads();
+    if (staged)
+        for (int64_t c = tid; c < nl; c += PLAN_THREADS) fl[c] = Ul[c] >= tau ? 1 : 0;
+    __syncthreads();
+    auto is_cand = [&](int64_t c) -> bool { return staged ? fl[c] != 0 : Ul[c] >= tau; };
+
     // ---- candidate compaction -> items (+ max A over candidates for the f32 error bound) ----
     long long carry_items = 0, carry_tok = 0;
     double amax_c = 0.0, umax_c = -INFINITY;
     for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
         const int64_t c = base + tid;
         long long it = 0, tk = 0;
-        int64_t rows = 0;
+        int64_t rows = 0, s = 0, first = 0;
         bool cand = false;
         if (c < nl) {
             rows = leaf_rows(ls, nl, c, n, C);
-            cand = Ul[c] >= tau;
-            if (cand) { tk = rows; it = (rows + ITEM_TOKENS - 1) / ITEM_TOKENS; }
+            s = leaf_begin(ls, c, C);
+            cand = is_cand(c);
+            if (cand) {
+                tk = rows;
+                const bool run_start = c == 0 || !is_cand(c - 1);
+                first = (run_start || s % ITEM_TOKENS == 0) ? s : (s / ITEM_TOKENS + 1) * ITEM_TOKENS;
+                const int64_t e = s + rows;
+                it = first < e ? 1 + ((e - 1) / ITEM_TOKENS - first / ITEM_TOKENS) : 0;
+            }
             if (cand && A) amax_c = fmax(amax_c, A[li * bnd_stride + c]);
             if (cand) umax_c = fmax(umax_c, Ul[c]);
             if (cand_leaf) cand_leaf[li * leaf_stride + c] = cand ? 1 : 0;
@@ -126,14 +144,23 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
         long long tot_it, tot_tk;
         const long long ex_it = block_excl_scan<long long>(it, scan_sh, tot_it);
         const long long ex_tk = block_excl_scan<long long>(tk, scan_sh, tot_tk);
-        if (cand) {
-            const int64_t s = leaf_begin(ls, c, C);
+        if (it > 0) {
+            const int64_t e = s + rows;
             int32_t* out = items + li * item_stride * 3;
+            int64_t t = first;
             for (long long j = 0; j < it; ++j) {
+                const int64_t nxt = (t / ITEM_TOKENS + 1) * ITEM_TOKENS;
+                int64_t end = nxt;
+                if (nxt > e) {  // the item may run on into the following candidate leaves
+                    int64_t cc = c + 1, ce = e;
+                    while (ce < nxt && cc < nl && is_cand(cc)) { ce += leaf_rows(ls, nl, cc, n, C); ++cc; }
+                    end = ce < nxt ? ce : nxt;
+                }
                 const int64_t pos = carry_items + ex_it + j;
-                out[pos * 3 + 0] = (int32_t)(s + j * ITEM_TOKENS);
-                out[pos * 3 + 1] = (int32_t)kvt::imin(ITEM_TOKENS, rows - j * ITEM_TOKENS);
-                out[pos * 3 + 2] = (int32_t)(carry_tok + ex_tk + j * ITEM_TOKENS);
+                out[pos * 3 + 0] = (int32_t)t;
+                out[pos * 3 + 1] = (int32_t)(end - t);
+                out[pos * 3 + 2] = (int32_t)(carry_tok + ex_tk + (t - s));
+                t = nxt;
             }
         }
         carry_items += tot_it;

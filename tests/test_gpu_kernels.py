@@ -232,3 +232,46 @@ def test_runs_partition(ops):
         got = [(int(a), int(b), "important" if c == 1 else "desert") for a, b, c in zip(ps, pe, pst)]
         ref = [x for x in O.canonical_partition(sel, n) if x[2] != "pad"]
         assert got == ref
+
+
+@pytest.mark.parametrize("C,n", [(8, 65536), (8, 1003), (4, 517), (64, 4096), (0, 3000)])
+def test_select_plan_items_merge_candidate_runs(ops, C, n):
+    """Items tile exactly the candidate tokens in ascending order (out_pos = stream index),
+    hold <= 64 tokens, and are cut only at run starts and multiples of 64."""
+    rng = np.random.default_rng(C * 7 + n)
+    lanes = 3
+    if C:
+        nl = ops.n_grid_leaves(n, C)
+        starts = [np.arange(nl) * C for _ in range(lanes)]
+        ls = nleaves = None
+    else:  # explicit partition with random leaf sizes
+        starts = []
+        for _ in range(lanes):
+            cuts = np.sort(rng.choice(np.arange(1, n), size=400, replace=False))
+            starts.append(np.concatenate([[0], cuts]))
+        nl = max(len(s) for s in starts)
+        ls = torch.zeros((lanes, nl), dtype=torch.int32)
+        for i, s in enumerate(starts):
+            ls[i, :len(s)] = torch.from_numpy(s.astype(np.int32))
+        ls = ls.cuda()
+        nleaves = torch.tensor([len(s) for s in starts], dtype=torch.int32, device="cuda")
+    U = torch.from_numpy(rng.normal(size=(lanes, nl))).cuda()
+    Lo = U - 1.0
+    k = max(1, n // 3)
+    plan = ops.select_plan(U, Lo, n, k, C, leaf_start=ls, n_leaves=nleaves, want_cand_leaf=True)
+    for i in range(lanes):
+        st = starts[i]
+        ends = np.append(st[1:], n)
+        cl = plan["cand_leaf"][i, :len(st)].cpu().numpy().astype(bool)
+        cand_tok = np.concatenate([np.arange(a, b) for a, b, c in zip(st, ends, cl) if c] or [np.zeros(0, int)])
+        ni = int(plan["n_items"][i])
+        it = plan["items"][i, :ni].cpu().numpy()
+        assert int(plan["n_cand"][i]) == len(cand_tok)
+        toks = np.concatenate([np.arange(t, t + c) for t, c, _ in it] or [np.zeros(0, int)])
+        assert np.array_equal(toks, cand_tok)
+        assert np.all(it[:, 1] >= 1) and np.all(it[:, 1] <= 64)
+        assert np.array_equal(it[:, 2], np.concatenate([[0], np.cumsum(it[:-1, 1])]) if ni else it[:, 2])
+        # maximal: an item boundary inside a run only at multiples of 64
+        for a, b in zip(it[:-1], it[1:]):
+            if a[0] + a[1] == b[0]:
+                assert b[0] % 64 == 0
