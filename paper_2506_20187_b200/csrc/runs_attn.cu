@@ -12,6 +12,8 @@
 // reduces a slice of the selected set to (m, l, o[d]) with f32 accumulation (f64 for f64
 // values); the last split CTA of each lane (atomic ticket) rescales and combines the
 // slices, so attention is one launch.  HBM-bound on k*d*s_V.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace kvt {
@@ -476,6 +478,223 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_i4_kernel(
     attn_finish(part, splits, d, li, tickets, out, out64, scale);
 }
 
+
+// ---- gather attention v2 (the decode-path kernel for INT4 and 2-byte rows) ------------------
+// Work unit = (lane, split) over <= R consecutive selected rows (R ~ 1024).  A row spans
+// LPR lanes (one 16 B piece each); U row loads are in flight per lane.  Accumulation is
+// packed f32x2 (sm_100a FFMA2/FADD2: two IEEE fmas per issue).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// INT4 records: lane = one 32-dim group (16 B of codes + its (scale, min)).
+// x^ = code * s + m, so sum_i w_i x^_ij = sum_i (w_i s_i) code_ij + sum_i w_i m_i: one packed
+// fma per two codes; code -> float by byte permute into 2^23 + code and a packed subtract.
+template <int D>
+struct FmtI4 {
+    static constexpr int LPR = D / 32, NE = 32;
+    struct Raw { uint4 c; uint32_t sm; };
+    __host__ __device__ static constexpr int row_bytes() { return D / 2 + D / 8; }
+    __device__ static Raw load(const unsigned char* row, int grp) {
+        Raw r;
+        r.c = __ldg(reinterpret_cast<const uint4*>(row + 16 * grp));
+        r.sm = __ldg(reinterpret_cast<const uint32_t*>(row + D / 2 + 4 * grp));
+        return r;
+    }
+    __device__ static Raw zero() { Raw r; r.c = make_uint4(0, 0, 0, 0); r.sm = 0; return r; }
+    __device__ static void acc(uint64_t (&o2)[NE / 2], const Raw& r, float w, float& om) {
+        const __half2 p = *reinterpret_cast<const __half2*>(&r.sm);
+        const float ws = w * __low2float(p);
+        om = fmaf(w, __high2float(p), om);
+        const uint64_t ws2 = f2_pack(ws, ws), neg = f2_pack(-8388608.0f, -8388608.0f);
+        const uint32_t words[4] = {r.c.x, r.c.y, r.c.z, r.c.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t lo4 = words[q] & 0x0f0f0f0fu, hi4 = (words[q] >> 4) & 0x0f0f0f0fu;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const uint64_t c2 = f2_add(f2_pack(__uint_as_float(__byte_perm(lo4, 0x4B000000u, 0x7440 + bb)),
+                                                   __uint_as_float(__byte_perm(hi4, 0x4B000000u, 0x7440 + bb))),
+                                           neg);
+                o2[4 * q + bb] = f2_fma(ws2, c2, o2[4 * q + bb]);
+            }
+        }
+    }
+    __device__ static float bias(float om) { return om; }
+};
+
+// 2-byte rows (bf16 / f16): lane = 8 consecutive dims (16 B).
+template <typename T, int D>
+struct Fmt16 {
+    static constexpr int LPR = D * 2 / 16, NE = 8;
+    using Raw = uint4;
+    __host__ __device__ static constexpr int row_bytes() { return D * 2; }
+    __device__ static Raw load(const unsigned char* row, int grp) {
+        return __ldg(reinterpret_cast<const uint4*>(row + 16 * grp));
+    }
+    __device__ static Raw zero() { return make_uint4(0, 0, 0, 0); }
+    __device__ static void acc(uint64_t (&o2)[NE / 2], const Raw& r, float w, float&) {
+        const uint64_t w2 = f2_pack(w, w);
+        const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint64_t v2;
+            if constexpr (std::is_same<T, __half>::value) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&words[i]));
+                v2 = f2_pack(f.x, f.y);
+            } else {
+                v2 = f2_pack(__uint_as_float(words[i] << 16), __uint_as_float(words[i] & 0xffff0000u));
+            }
+            o2[i] = f2_fma(w2, v2, o2[i]);
+        }
+    }
+    __device__ static float bias(float) { return 0.f; }
+};
+
+template <class F, int U>
+__global__ void __launch_bounds__(ATTN_THREADS) attn_gather_kernel(
+    const unsigned char* __restrict__ values, int64_t lane_stride_b, int d, const int32_t* __restrict__ sel_tok,
+    const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
+    double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
+    double* __restrict__ out64, double scale) {
+    // Each warp runs its own online softmax over rows warp*RPW + sub + u*STEP + it*U*STEP
+    // (no block barrier before the first row load); the next iteration's token ids and
+    // scores are fetched while the current rows are in flight.  Warps are combined in
+    // shared memory at the end, then splits by the last-arriving CTA of the lane.
+    constexpr int LPR = F::LPR, NE = F::NE, RPW = 32 / LPR, STEP = ATTN_WARPS * RPW;
+    __shared__ double red_m[ATTN_WARPS];
+    __shared__ float red_o[ATTN_WARPS][LPR * NE];
+    __shared__ float red_l[ATTN_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t li = blockIdx.y;
+    const int s = blockIdx.x;
+    const int64_t k = n_sel[li];
+    const int64_t a = kvt::imin(k, (int64_t)s * R), b = kvt::imin(k, a + R);
+    const int nr = (int)(b - a);
+    const int32_t* tok = sel_tok + li * sel_stride + a;
+    const double* sc = sel_score + li * sel_stride + a;
+    const int sub = lane / LPR, grp = lane % LPR;
+    const unsigned char* base = values + li * lane_stride_b;
+    const double sl2 = scale * 1.4426950408889634;
+
+    uint64_t o2[NE / 2];
+#pragma unroll
+    for (int e = 0; e < NE / 2; ++e) o2[e] = 0ull;
+    float l = 0.f, om = 0.f;
+    double m = -INFINITY;
+    int t_nx[U];
+    double s_nx[U];
+    const int i0 = warp * RPW + sub;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * STEP;
+        t_nx[u] = i < nr ? tok[i] : 0;
+        s_nx[u] = i < nr ? sc[i] : -INFINITY;
+    }
+    for (int it = 0; it * U * STEP < nr; ++it) {  // warp-uniform trip count
+        typename F::Raw raw[U];
+        double sv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + (it * U + u) * STEP;
+            raw[u] = i < nr ? F::load(base + (int64_t)t_nx[u] * F::row_bytes(), grp) : F::zero();
+            sv[u] = s_nx[u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {  // prefetch the next iteration's ids and scores
+            const int i = i0 + ((it + 1) * U + u) * STEP;
+            t_nx[u] = i < nr ? tok[i] : 0;
+            s_nx[u] = i < nr ? sc[i] : -INFINITY;
+        }
+        double mi = sv[0];
+#pragma unroll
+        for (int u = 1; u < U; ++u) mi = fmax(mi, sv[u]);
+#pragma unroll
+        for (int off = 16; off >= LPR; off >>= 1) mi = fmax(mi, __shfl_xor_sync(KVT_FULL, mi, off));
+        if (mi > m) {  // warp-uniform: rescale the running sums
+            const float r = m == -INFINITY ? 0.f : exp2f((float)((m - mi) * sl2));
+            const uint64_t r2 = f2_pack(r, r);
+#pragma unroll
+            for (int e = 0; e < NE / 2; ++e) o2[e] = f2_fma(o2[e], r2, 0ull);
+            l *= r;
+            om *= r;
+            m = mi;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float w = sv[u] == -INFINITY ? 0.f : exp2f((float)((sv[u] - m) * sl2));
+            F::acc(o2, raw[u], w, om);
+            l += w;
+        }
+    }
+    float o[NE];
+#pragma unroll
+    for (int e = 0; e < NE / 2; ++e) f2_unpack(o2[e], o[2 * e], o[2 * e + 1]);
+    const float bias = F::bias(om);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) o[e] += bias;
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+        l += __shfl_xor_sync(KVT_FULL, l, off);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) o[e] += __shfl_xor_sync(KVT_FULL, o[e], off);
+    }
+    if (lane < LPR) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) red_o[warp][NE * grp + e] = o[e];
+    }
+    if (lane == 0) { red_l[warp] = l; red_m[warp] = m; }
+    __syncthreads();
+    double M = red_m[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_WARPS; ++w) M = fmax(M, red_m[w]);
+    float wsc[ATTN_WARPS];
+#pragma unroll
+    for (int w = 0; w < ATTN_WARPS; ++w) wsc[w] = red_m[w] == -INFINITY ? 0.f : exp2f((float)((red_m[w] - M) * sl2));
+    double* P = part + ((int64_t)li * splits + s) * (d + 2);
+    for (int j = tid; j < d; j += ATTN_THREADS) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) acc = fmaf(wsc[w], red_o[w][j], acc);
+        P[2 + j] = (double)acc;
+    }
+    if (tid == 0) {
+        float ls = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) ls = fmaf(wsc[w], red_l[w], ls);
+        P[0] = M;
+        P[1] = (double)ls;
+    }
+    attn_finish(part, splits, d, li, tickets, out, out64, scale);
+}
+
+template <class F, int U>
+static int launch_gather(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, const int32_t* sel_tok,
+                         const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, int R,
+                         double* part, unsigned int* tickets, float* out, double* out64, double scale,
+                         cudaStream_t st) {
+    dim3 grid(splits, (unsigned)n_lanes);
+    attn_gather_kernel<F, U><<<grid, ATTN_THREADS, 0, st>>>((const unsigned char*)values, lane_stride_b, d, sel_tok,
+                                                               sel_score, n_sel, sel_stride, splits, R, part, tickets,
+                                                               out, out64, scale);
+    return kvt_check_launch();
+}
+
 }  // namespace kvt
 
 using namespace kvt;
@@ -562,25 +781,38 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
     unsigned int* tickets = (unsigned int*)ws;
     double* part = (double*)((char*)ws + ticket_bytes(n_lanes));
     int rc;
+    // rows per work unit: the whole selection in <= splits units
+    const int64_t kmax = sel_stride;
+    const int R = (int)kvt::imax(32, ((kmax + splits - 1) / splits + 31) / 32 * 32);
+    const bool aligned = ((uintptr_t)values % 16) == 0;
     switch (v_dtype) {
         case KVT_I4: {
-            if ((d != 128 && d != 256) || ((uintptr_t)values % 16) || (lane_stride % 16)) return KVT_ERR_SHAPE;
-            dim3 grid(splits, (unsigned)n_lanes);
-            if (d == 128)
-                attn_i4_kernel<4><<<grid, ATTN_THREADS, 0, st>>>((const unsigned char*)values, lane_stride, d, sel_tok,
-                                                                  sel_score, n_sel, sel_stride, splits, part, tickets,
-                                                                  out, out64, logit_scale);
-            else
-                attn_i4_kernel<8><<<grid, ATTN_THREADS, 0, st>>>((const unsigned char*)values, lane_stride, d, sel_tok,
-                                                                  sel_score, n_sel, sel_stride, splits, part, tickets,
-                                                                  out, out64, logit_scale);
-            rc = kvt_check_launch();
+            if ((d != 128 && d != 256) || !aligned || (lane_stride % 16)) return KVT_ERR_SHAPE;
+            rc = d == 128 ? launch_gather<FmtI4<128>, 4>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                                                         sel_stride, splits, R, part, tickets, out, out64, logit_scale, st)
+                          : launch_gather<FmtI4<256>, 2>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                                                         sel_stride, splits, R, part, tickets, out, out64, logit_scale, st);
             break;
         }
+        case KVT_BF16:
+        case KVT_F16:
+            if ((d == 128 || d == 256) && aligned && (lane_stride * 2) % 16 == 0) {
+                const int64_t lsb = lane_stride * 2;
+#define KVT_G(TT, DD) launch_gather<Fmt16<TT, DD>, 4>(values, n_lanes, lsb, d, sel_tok, sel_score, n_sel, sel_stride, \
+                                                      splits, R, part, tickets, out, out64, logit_scale, st)
+                if (v_dtype == KVT_BF16) rc = d == 128 ? KVT_G(__nv_bfloat16, 128) : KVT_G(__nv_bfloat16, 256);
+                else rc = d == 128 ? KVT_G(__half, 128) : KVT_G(__half, 256);
+#undef KVT_G
+                break;
+            }
+            rc = v_dtype == KVT_BF16
+                     ? dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride,
+                                                    splits, part, tickets, out, out64, logit_scale, st)
+                     : dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride,
+                                             splits, part, tickets, out, out64, logit_scale, st);
+            break;
         case KVT_F32: rc = dispatch_attn<float>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
         case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
-        case KVT_BF16: rc = dispatch_attn<__nv_bfloat16>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
-        case KVT_F16: rc = dispatch_attn<__half>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
         default: return KVT_ERR_DTYPE;
     }
     return rc;

@@ -20,7 +20,7 @@
 
 namespace kvt {
 
-constexpr int S3_THREADS = 1024;
+constexpr int S3_THREADS = 512;  // two CTAs per SM: a 256-lane layer is one wave
 constexpr int S3_WARPS = S3_THREADS / 32;
 constexpr int S3_BINS = 4096;
 constexpr int S3_LIST_CAP = 8192;
@@ -75,8 +75,24 @@ __device__ __forceinline__ void s3_find_bin(S3Shared& S, const unsigned int* his
 }
 
 // Radix select on the shared list of 32-bit keys: exact key of the `want`-th largest.
+// Short lists (the usual case: one of 4096 buckets) are ranked by counting instead: one
+// barrier instead of four radix rounds.
 __device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* keys, int n, long long want) {
     const int tid = threadIdx.x, lane = tid & 31;
+    if (n <= 1024) {
+        for (int j = tid; j < n; j += S3_THREADS) {
+            const uint32_t kj = keys[j];
+            int gt = 0, eq = 0;
+            for (int f = 0; f < n; ++f) {
+                const uint32_t kf = keys[f];
+                gt += kf > kj;
+                eq += kf == kj;
+            }
+            if (gt < want && want <= gt + eq) S.prefix = kj;  // every writer stores the same key
+        }
+        __syncthreads();
+        return (uint32_t)S.prefix;
+    }
     if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)want; }
     __syncthreads();
     for (int shift = 24; shift >= 0; shift -= 8) {
@@ -161,7 +177,7 @@ __device__ __forceinline__ void load4s(const float* sc, int64_t i, int64_t end, 
 }
 
 template <typename QT, typename T>
-__global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
+__global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const float* __restrict__ cs32, const int32_t* __restrict__ ctok, const int32_t* __restrict__ n_cand,
     int64_t cand_stride, const double* __restrict__ rec, int64_t k, const QT* __restrict__ q,
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, double* __restrict__ scratch,
@@ -203,8 +219,7 @@ __global__ void __launch_bounds__(S3_THREADS) topk_select3_kernel(
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int bkt = i + e < n ? s3_bucket((double)v[e], lo, inv) : -1;
-            const unsigned peers = __match_any_sync(KVT_FULL, bkt);
-            if (bkt >= 0 && lane == __ffs(peers) - 1) atomicAdd(&S.hist[bkt], (unsigned)__popc(peers));
+            if (bkt >= 0) atomicAdd(&S.hist[bkt], 1u);
         }
     }
     __syncthreads();
@@ -509,11 +524,11 @@ extern "C" int kvt_topk_select_band(const float* cs32, const int32_t* ctok, cons
     if (k < 0) return KVT_ERR_K;
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
-    // few lanes: one CTA per lane would leave most SMs idle -> cluster of CTAs per lane
+    // very few lanes: one CTA per lane would leave most SMs idle -> cluster of CTAs per lane
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (n_lanes < sms && cand_stride >= 8192 && cand_stride <= 8 * 20480 && n_lanes <= 65535)
+    if (n_lanes * 4 < sms && cand_stride >= 8192 && cand_stride <= 8 * 20480 && n_lanes <= 65535)
         return kvt_topk_select_band_cluster(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, q_dtype, keys,
                                             key_dtype, lane_stride, d, sel_tok, sel_score, sel_stride, n_sel,
                                             run_start, run_len, run_stride, n_runs, stream);

@@ -352,8 +352,10 @@ def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition
 
 
 def auto_splits(n_lanes: int, k: int) -> int:
-    target = 148 * 3
-    return max(1, min((target + n_lanes - 1) // n_lanes, (k + 255) // 256, 64))
+    """Same rule as kvt_select_attend (api.cu): ~1024-row units, >= 6 CTAs per SM overall."""
+    by_rows = (k + 1023) // 1024
+    by_sms = (148 * 6 + n_lanes - 1) // max(n_lanes, 1)
+    return max(1, min(max(by_rows, by_sms), 64, max(1, (k + 31) // 32)))
 
 
 def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor,
