@@ -423,11 +423,17 @@ def run_ours(args):
     score_fn = ops.cand_score_i4mma if is_i4 else ops.cand_score_f32
     inter = []
     n_cand = []
+
+    def bounds_fn(l, n, C):  # the K3 variant select_attend runs (fast f32 when absmag is kept)
+        if dec.absmag is not None:
+            return ops.chunk_bounds_fast(q_static[l], dec.amax[l], dec.amin[l], n, C, dec.absmag[l])
+        return ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
+
     with torch.cuda.stream(stream):
         q_static.copy_(Q[args.warmup])
         for l in range(L):
             C, n, k = dec.C[l], dec.n, dec.k_for(l)
-            U, Lo, A = ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
+            U, Lo, A = bounds_fn(l, n, C)
             plan = ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
             cs, ct = score_fn(q_static[l], dec.K[l], plan, n)
             st_, ss_, ns_, _ = ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
@@ -441,7 +447,7 @@ def run_ours(args):
                 C, n, k = dec.C[l], dec.n, dec.k_for(l)
                 U, Lo, A, plan, cs, ct, st_, ss_, ns_ = inter[l]
                 if name == "bounds":
-                    ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
+                    bounds_fn(l, n, C)
                 elif name == "plan":
                     ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
                 elif name == "score":

@@ -260,7 +260,19 @@ typedef struct {
     int attn_splits;            /* 0 = auto */
     int score_blocks;           /* 0 = auto */
     int exact_scores;           /* 1: canonical f64 scoring of every candidate (no f32 band path) */
+    const float* abs_mag;       /* [n_lanes][d] per-lane max |key| over all chunks, or NULL.  With bf16
+                                   abstracts, f32 q, a uniform grid and d = 128/256 it selects the
+                                   directed-rounding f32 bounds (kvt_chunk_bounds_fast) */
 } kvt_layer_args;
+
+/* K3 for the decode path (bounds_fast.cu): sound f32 bounds of raw dots over bf16 abstracts on a
+ * uniform grid C, every fma/add rounded outward (U toward +inf, L toward -inf); A[c] = one
+ * per-lane upper bound RU(sum_j |q_j| mag_j) on every chunk's sum |q||k|.  Replaces the
+ * canonical kvt_chunk_bounds inside kvt_select_attend when abs_mag is given; the selected set
+ * does not depend on it (pruning only needs soundness).  d = 128 or 256; U, L, A f64. */
+KVT_API int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int64_t n, int C, const void* amax,
+                                  const void* amin, int64_t abs_lane_stride, const float* mag, double* U,
+                                  double* L, double* A, int64_t bnd_stride, void* stream);
 
 KVT_API size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d);
 KVT_API int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream);

@@ -47,6 +47,7 @@ class KvtLayerArgs(ctypes.Structure):
         ("run_start", _vp), ("run_len", _vp), ("n_runs", _vp),
         ("out", _vp), ("evals", _vp),
         ("attn_splits", _i32), ("score_blocks", _i32), ("exact_scores", _i32),
+        ("abs_mag", _vp),
     ]
 
 
@@ -66,6 +67,8 @@ kvt_abstract_spans = _sig("kvt_abstract_spans", ctypes.c_int, _vp, _i32, _i64, _
                           _vp)
 kvt_chunk_bounds = _sig("kvt_chunk_bounds", ctypes.c_int, _vp, _i32, _i64, _i32, _i64, _i32, _vp, _vp, _i64, _vp,
                         _vp, _i32, _i64, _vp, _vp, _vp, _i64, _i32, _vp)
+kvt_chunk_bounds_fast = _sig("kvt_chunk_bounds_fast", ctypes.c_int, _vp, _i64, _i32, _i64, _i32, _vp, _vp, _i64,
+                             _vp, _vp, _vp, _vp, _i64, _vp)
 kvt_select_plan2 = _sig("kvt_select_plan2", ctypes.c_int, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
                         _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp)
 kvt_cand_score_f32 = _sig("kvt_cand_score_f32", ctypes.c_int, _vp, _i32, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _vp,
@@ -103,7 +106,7 @@ EXPORTED = [
     "kvt_topk_select_runs",
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
     "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_i4_recip_check", "kvt_select_plan2", "kvt_cand_score_f32",
-    "kvt_topk_select_band", "kvt_kv_dequant", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
+    "kvt_topk_select_band", "kvt_kv_dequant", "kvt_chunk_bounds_fast", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
 ]
 
 

@@ -115,9 +115,15 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     int rc;
     // fast path: f32 estimates + exact band re-scoring (any key dtype but f64, d = 128/256)
     const bool fast = kvt_fast_ok(a->key_dtype, a->d) && !a->exact_scores;
-    rc = kvt_chunk_bounds(a->q, a->q_dtype, a->n_lanes, a->d, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride,
-                          a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L, fast ? w.A : nullptr,
-                          max_leaves, 0, stream);
+    const bool fast_bounds = fast && a->abs_mag && a->abs_dtype == KVT_BF16 && a->q_dtype == KVT_F32 &&
+                             !a->leaf_start && (a->d == 128 || a->d == 256);
+    if (fast_bounds)  // sound f32 directed-rounding bounds (bounds_fast.cu)
+        rc = kvt_chunk_bounds_fast((const float*)a->q, a->n_lanes, a->d, a->n, a->C, a->amax, a->amin,
+                                   a->abs_lane_stride, a->abs_mag, w.U, w.L, w.A, max_leaves, stream);
+    else
+        rc = kvt_chunk_bounds(a->q, a->q_dtype, a->n_lanes, a->d, a->n, a->C, a->leaf_start, a->n_leaves,
+                              a->leaf_stride, a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L,
+                              fast ? w.A : nullptr, max_leaves, 0, stream);
     if (rc) return rc;
     rc = kvt_select_plan2(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L, max_leaves,
                           a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals, fast ? w.A : nullptr,

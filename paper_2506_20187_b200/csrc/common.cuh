@@ -359,6 +359,18 @@ int kvt_abstract_build_i4(const void* keys, int64_t n_lanes, int64_t lane_stride
                           int64_t c_begin, int64_t c_end, void* amax, void* amin, int64_t abs_lane_stride, bool bf,
                           cudaStream_t st);
 
+// Resident CTAs per SM of `kernel` at this block size / dynamic smem (occupancy API), so
+// persistent grids are exactly one wave.  Falls back to `fallback` on error.
+template <typename K>
+inline int resident_per_sm(K kernel, int threads, size_t smem, int fallback) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return fallback;
+    }
+    return n;
+}
+
 // status plumbing (api.cu)
 int kvt_set_cuda_error(cudaError_t e);
 int kvt_check_launch();

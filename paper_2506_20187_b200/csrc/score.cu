@@ -362,7 +362,9 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = 200 * 1024;
     }
-    const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
+    static int per_sm = 0;  // one per template instance
+    if (!per_sm) per_sm = resident_per_sm(score_tma_kernel<QT, T, G, IMPL, AccT>, TS_THREADS, smem,
+                                          smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1));
     const int grid = sm_count() * per_sm;
     score_tma_kernel<QT, T, G, IMPL, AccT><<<grid, TS_THREADS, smem, st>>>(
         (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, (int)n_lanes, items, item_stride, n_items, n_impl,

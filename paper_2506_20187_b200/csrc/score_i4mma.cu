@@ -9,23 +9,24 @@
 // groups) x 16 tokens sums c_j qi_{p,j} exactly in int32, the record's nibbles become MMA
 // operands with one mask (lo) or shift+mask (hi) per 4 codes -- the K order is permuted to the
 // nibble order and the query digits are laid out to match (kvt_i4_qprep).  The epilogue is a
-// few f64 fmas per (token, group): inner_g is exact in f64 (<= 37 significant bits), and so
-// are s_g * inner_g and m_g * Qt_g, so est(t) carries only a handful of f64 roundings before
-// the final rounding to f32.  A rigorous per-token bound
-//     |est32(t) - canonical f64 dot(t)| <= e(t) = 1.001 [u |est32(t)| + sum_g (15|s_g| + |m_g|) w_g(t)]
-// (u = 2^-24) covers the final f32 rounding, the f64 roundings, the digit residual q - qt, the
-// canonical dot's own f64 rounding and -- only for groups where fmaf(c, s, m) is not exact in
-// f32 for some code c (a test on the fp16 exponents of s and m) -- the fp32 rounding of the
-// dequantised element the canonical dot sees; w_g per lane and group comes from
-// kvt_i4_qprep.  The per-lane max of e(t) is atomically max-ed into err[4 lane + 3], where
+// few f32 fmas per (token, group): the MMA partials D_p (|D_p| < 2^16) and the power-of-two
+// digit scales make every product exact, so est(t) carries <= 10 f32 roundings per group
+// (3 in inner_g, the m_g Qt_g product and its fma, the r-accumulation, the group tree).  A
+// rigorous per-token bound
+//     |est32(t) - canonical f64 dot(t)| <= e(t) = 1.001 [u |est32(t)| + sum_g (15|s_g| + |m_g|) W_g]
+// (u = 2^-24) covers the final rounding, the epilogue roundings (11 u qd_g, qd_g = sum over the
+// group of sum_p s_p |qi_p|, which bounds |inner_g| / 15 and |Qt_g|, incl. Qt_g's own f32
+// rounding), the digit residual q - qt, the canonical dot's own f64 rounding and the fp32
+// rounding of the dequantised element the canonical dot sees; W_g per lane and group comes
+// from kvt_i4_qprep.  The per-lane max of e(t) is atomically max-ed into err[4 lane + 3], where
 // the band select (select2/select3) takes it as E: the band is then a few ulps wide and the
 // selected set stays the exact canonical top-k.
 //
 // Dataflow: the persistent TMA ring of score.cu (one producer thread issuing cp.async.bulk
-// of 64-token items, plus the lane's 560 B digit block on a lane change), 4 consumer warps,
-// warp w owning tokens 16w..16w+15 of the item.  Per 16 tokens and 128 dims a warp issues
-// 2 LDS.128 of codes, 8 MMAs and ~40 f32 ops -- a few instructions per token instead of the
-// ~4 per dim of CUDA-core dequantisation, so the kernel streams at HBM rate.
+// of 64-token items, plus the lane's digit block on a lane change), 4 consumer warps, warp w
+// owning tokens 16w..16w+15 of the item.  Per 16 tokens and 128 dims a warp issues 2 LDS.128
+// of codes, 8 MMAs and ~40 f32 ops -- a few instructions per token instead of the ~4 per dim
+// of CUDA-core dequantisation.
 #include <cfloat>
 #include <algorithm>
 #include <cmath>
@@ -36,12 +37,13 @@ namespace kvt {
 
 constexpr int QM_CONSUMERS = 4;
 constexpr int QM_THREADS = (QM_CONSUMERS + 1) * 32;
-constexpr int QM_STAGES = 8;
+constexpr int QM_STAGES = 3;
+constexpr int QM_ROWS = 128;  // rows per stage: up to two contiguous 64-token plan items
 
 __host__ __device__ __forceinline__ int qprep_bytes(int d) { return (d / 32) * 144 + 16; }
 
 // ---- query digits: one warp per lane ---------------------------------------------------------
-// Block layout per lane: [G][4 parts][4 i][b0, b1] (G*128 B) | [G](Qt_g f64, w0_g, w1_g f32) |
+// Block layout per lane: [G][4 parts][4 i][b0, b1] (G*128 B) | [G](Qt_g f32, W_g f32, 0, 0) |
 // s_0..s_3 f32.
 // b0 byte j = qi_p[32g + 8i + 2j], b1 byte j = qi_p[32g + 8i + 2j + 1] (the nibble order).
 template <typename QT>
@@ -90,32 +92,21 @@ __global__ void qprep_kernel(const QT* __restrict__ q, int64_t n_lanes, int d, u
             qts += __shfl_xor_sync(KVT_FULL, qts, o);  // exact: multiples of s_3, < 2^40 s_3
         }
         if (lane == 0) {
-            // w0_g (always): canonical f64 ((2n+4) 2^-53) on sum|q|, the digit residual, and
-            // (G + 3) 2^-53 on sum_p s_p|qi| for the f64 epilogue.  w1_g (groups whose
-            // dequantisation rounds): u on sum|q|.  1% slack for the f64 evaluation here.
-            const double w0 = 1.01 * (qabs * (2.0 * n_can + 4.0) * 0x1p-53 + r1 * (1.0 + 0x1p-40) +
-                                      (G + 3.0) * 0x1p-53 * qd) + DBL_MIN;
-            const double w1 = 1.01 * u * qabs;
-            float f0 = (float)w0, f1 = (float)w1;
-            if ((double)f0 < w0) f0 = nextafterf(f0, INFINITY);
-            if ((double)f1 < w1) f1 = nextafterf(f1, INFINITY);
-            *reinterpret_cast<double*>(cst + 16 * g) = qts;
-            reinterpret_cast<float*>(cst + 16 * g)[2] = f0;
-            reinterpret_cast<float*>(cst + 16 * g)[3] = f1;
+            // W_g: canonical f64 ((2n+4) 2^-53) and the dequantised element's f32 rounding (u)
+            // on sum|q|, the digit residual, and 11 u on qd for the f32 epilogue (module
+            // header).  1% slack for the f64 evaluation here; rounded up to f32.
+            const double w = 1.01 * (qabs * ((2.0 * n_can + 4.0) * 0x1p-53 + u) + r1 * (1.0 + 0x1p-40) +
+                                     11.0 * u * (1.0 + 0x1p-10) * qd) + DBL_MIN;
+            float fw = (float)w;
+            if ((double)fw < w) fw = nextafterf(fw, INFINITY);
+            float* c4 = reinterpret_cast<float*>(cst + 16 * g);
+            c4[0] = (float)qts;
+            c4[1] = fw;
+            c4[2] = 0.f;
+            c4[3] = 0.f;
         }
     }
     if (lane < 4) reinterpret_cast<float*>(blk + G * 144)[lane] = (float)ldexp(s0, -7 * lane);
-}
-
-// fmaf(c, s, m) is exact in f32 for every code c in 0..15 when s and m (fp16) are multiples
-// of 2^L and 15|s| + |m| < 2^(L + 24); L from the fp16 exponent fields (lsb of the format).
-__device__ __forceinline__ bool i4_group_exact(uint32_t hm2, float sc, float mn) {
-    const uint32_t hs = hm2 & 0xffffu, hmn = hm2 >> 16;
-    const int es = (int)((hs >> 10) & 31u), em = (int)((hmn >> 10) & 31u);
-    const int ls = (es ? es : 1) - 25, lm = (em ? em : 1) - 25;
-    const bool zs = (hs & 0x7fffu) == 0u, zm = (hmn & 0x7fffu) == 0u;
-    const int L = zs ? lm : (zm ? ls : min(ls, lm));
-    return __fmaf_rn(15.f, fabsf(sc), fabsf(mn)) < __int_as_float((L + 24 + 127) << 23);
 }
 
 __device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -129,14 +120,14 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, ui
 
 // ---- the scoring kernel --------------------------------------------------------------------
 template <int R>  // R = d / 128 rounds of 4 groups
-__global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
+__global__ void __launch_bounds__(QM_THREADS, 8) score_i4mma_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
     int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
     float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err) {
     constexpr int d = 128 * R;
     constexpr int G = 4 * R;
     constexpr int row_b = d / 2 + G * 4;
-    constexpr int tile_b = 64 * row_b;
+    constexpr int tile_b = QM_ROWS * row_b;
     constexpr int qb = G * 144 + 16;
     constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -175,13 +166,16 @@ __global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
     if (warp == QM_CONSUMERS) {  // ---- producer warp: lane 0 drives the bulk-copy engine ----
         // Item metadata is fetched 32 items at a time (one coalesced load per lane, handed to
         // lane 0 by shuffles), so the issue loop pays one memory latency per batch, not per item.
+        // Consecutive items of a lane that continue each other (tokens and output positions)
+        // are merged into one stage of up to QM_ROWS rows: one bulk copy, two MMA tiles per warp.
+        // A final stage with cnt = -1 tells the consumers to stop.
+        int ps = 0, pr = 0;
         if (n_my > 0) {
             int cur = (int)start_info[0];
             long long it = start_info[1];
             long long cnt_cur = n_items[cur];
             long long cnt_next = cur + 1 < n_lanes ? n_items[cur + 1] : 0;
             int prev = -1;
-            int ps = 0, pr = 0;
             long long g = 0;
             while (g < n_my) {
                 while (it >= cnt_cur) {
@@ -197,8 +191,15 @@ __global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
                     m0 = m[0]; m1 = m[1]; m2 = m[2];
                 }
                 for (int j = 0; j < nb; ++j) {
-                    const int t0 = __shfl_sync(KVT_FULL, m0, j), cnt = __shfl_sync(KVT_FULL, m1, j);
+                    const int t0 = __shfl_sync(KVT_FULL, m0, j);
+                    int cnt = __shfl_sync(KVT_FULL, m1, j);
                     const int pos0 = __shfl_sync(KVT_FULL, m2, j);
+                    const int t1 = __shfl_sync(KVT_FULL, m0, (j + 1) & 31), c1 = __shfl_sync(KVT_FULL, m1, (j + 1) & 31);
+                    const int p1 = __shfl_sync(KVT_FULL, m2, (j + 1) & 31);
+                    if (j + 1 < nb && t1 == t0 + cnt && p1 == pos0 + cnt && cnt + c1 <= QM_ROWS) {
+                        cnt += c1;
+                        ++j;
+                    }
                     const int s = ps;
                     const bool newq = cur != prev;
                     if (lane == 0) {
@@ -218,22 +219,27 @@ __global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
                 g += nb;
             }
         }
+        if (lane == 0) {
+            if (pr > 0) mbar_wait(&empty[ps], (uint32_t)((pr - 1) & 1));
+            meta[ps] = make_int4(-1, 0, -1, 0);
+            mbar_arrive_expect_tx(&full[ps], 0u);
+        }
         return;
     }
 
     // ---- consumers ----
     const int gid = lane >> 2, tig = lane & 3;
     uint32_t B[R][2][4][2];
-    double qt[R], sp[4];
-    float w0[R], w1[R];
+    float qt[R], W[R], sp[4];
     int cur = -1;
     float emax = 0.f;
     int cs = 0, cr = 0;
-    for (long long g = 0; g < n_my; ++g) {
+    for (;;) {
         const int s = cs;
         mbar_wait(&full[s], (uint32_t)(cr & 1));
         if (++cs == QM_STAGES) { cs = 0; ++cr; }
         const int4 mt = meta[s];
+        if (mt.z < 0) break;
         const unsigned char* st = smem + (size_t)s * stage_b;
         if (mt.x != cur) {
             // flush the finished lane's error max, then load the new lane's digits
@@ -263,18 +269,19 @@ __global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
                         for (int i = 0; i < 4; ++i) B[r][S][i][0] = B[r][S][i][1] = 0u;
                     }
                 }
-                qt[r] = *reinterpret_cast<const double*>(qs + G * 128 + 16 * gq);
-                const float2 c2 = *reinterpret_cast<const float2*>(qs + G * 128 + 16 * gq + 8);
-                w0[r] = c2.x;
-                w1[r] = c2.y;
+                const float2 c2 = *reinterpret_cast<const float2*>(qs + G * 128 + 16 * gq);
+                qt[r] = c2.x;
+                W[r] = c2.y;
             }
             const float4 s4 = *reinterpret_cast<const float4*>(qs + G * 144);
             sp[0] = s4.x; sp[1] = s4.y; sp[2] = s4.z; sp[3] = s4.w;
         }
         const int cnt = mt.z, pos0 = mt.w, t0 = mt.y;
-        if (16 * warp < cnt) {
-            const int row0 = 16 * warp + gid, row1 = row0 + 8;
-            double est0 = 0.0, est1 = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < QM_ROWS / 64; ++tt) {
+          if (64 * tt + 16 * warp < cnt) {
+            const int row0 = 64 * tt + 16 * warp + gid, row1 = row0 + 8;
+            float est0 = 0.f, est1 = 0.f;
             float er0 = 0.f, er1 = 0.f;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -291,20 +298,18 @@ __global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
                     mma_s8(c1, a0, a1, a2, a3, B[r][1][i][0], B[r][1][i][1]);
                 }
                 // c0: parts 0,1 / c1: parts 2,3 of group gq; [0],[1] row0, [2],[3] row1.
-                // inner = sum_p s_p D_p exactly (multiples of s_3 below 2^40 s_3)
-                const double in0 =
-                    fma(sp[3], (double)c1[1], fma(sp[2], (double)c1[0], fma(sp[1], (double)c0[1], sp[0] * (double)c0[0])));
-                const double in1 =
-                    fma(sp[3], (double)c1[3], fma(sp[2], (double)c1[2], fma(sp[1], (double)c0[3], sp[0] * (double)c0[2])));
+                // inner = sum_p s_p D_p: exact products, 3 roundings (module header)
+                const float in0 = fmaf(sp[3], (float)c1[1], fmaf(sp[2], (float)c1[0], fmaf(sp[1], (float)c0[1], sp[0] * (float)c0[0])));
+                const float in1 = fmaf(sp[3], (float)c1[3], fmaf(sp[2], (float)c1[2], fmaf(sp[1], (float)c0[3], sp[0] * (float)c0[2])));
                 const uint32_t h0 = *reinterpret_cast<const uint32_t*>(st + row0 * row_b + d / 2 + 4 * gq);
                 const uint32_t h1 = *reinterpret_cast<const uint32_t*>(st + row1 * row_b + d / 2 + 4 * gq);
                 const __half2 p0 = *reinterpret_cast<const __half2*>(&h0), p1 = *reinterpret_cast<const __half2*>(&h1);
                 const float sc0 = __low2float(p0), mn0 = __high2float(p0);
                 const float sc1 = __low2float(p1), mn1 = __high2float(p1);
-                est0 += fma((double)sc0, in0, (double)mn0 * qt[r]);  // products exact, one rounding
-                est1 += fma((double)sc1, in1, (double)mn1 * qt[r]);
-                er0 += __fmaf_rn(15.f, fabsf(sc0), fabsf(mn0)) * (i4_group_exact(h0, sc0, mn0) ? w0[r] : w0[r] + w1[r]);
-                er1 += __fmaf_rn(15.f, fabsf(sc1), fabsf(mn1)) * (i4_group_exact(h1, sc1, mn1) ? w0[r] : w0[r] + w1[r]);
+                est0 += fmaf(sc0, in0, mn0 * qt[r]);
+                est1 += fmaf(sc1, in1, mn1 * qt[r]);
+                er0 = fmaf(fmaf(15.f, fabsf(sc0), fabsf(mn0)), W[r], er0);
+                er1 = fmaf(fmaf(15.f, fabsf(sc1), fabsf(mn1)), W[r], er1);
             }
 #pragma unroll
             for (int o = 1; o <= 2; o <<= 1) {
@@ -314,13 +319,14 @@ __global__ void __launch_bounds__(QM_THREADS) score_i4mma_kernel(
                 er1 += __shfl_xor_sync(KVT_FULL, er1, o);
             }
             const int row = tig == 0 ? row0 : row1;
-            const float est = (float)(tig == 0 ? est0 : est1);
+            const float est = tig == 0 ? est0 : est1;
             const float er = 1.001f * __fmaf_rn(0x1p-24f, fabsf(est), tig == 0 ? er0 : er1);
             if (tig < 2 && row < cnt) {
                 out32[(int64_t)cur * out_stride + pos0 + row] = est;
                 if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + row] = t0 + row;
                 emax = fmaxf(emax, er);
             }
+        }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -359,7 +365,7 @@ template <int R>
 static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const int32_t* items, int64_t item_stride,
                         const int32_t* n_items, const void* qprep, float* os, int32_t* ot, int64_t ostr, double* err,
                         cudaStream_t st) {
-    constexpr int d = 128 * R, G = 4 * R, row_b = d / 2 + G * 4, tile_b = 64 * row_b, qb = G * 144 + 16;
+    constexpr int d = 128 * R, G = 4 * R, row_b = d / 2 + G * 4, tile_b = QM_ROWS * row_b, qb = G * 144 + 16;
     constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
     const size_t smem = (size_t)QM_STAGES * stage_b;
     static bool configured = false;
@@ -371,8 +377,9 @@ static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const i
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_sm = (int)std::min<size_t>(4, (200 * 1024) / (smem + 2048));
-    score_i4mma_kernel<R><<<sms * std::max(per_sm, 1), QM_THREADS, smem, st>>>(
+    static int per_sm = 0;
+    if (!per_sm) per_sm = resident_per_sm(score_i4mma_kernel<R>, QM_THREADS, smem, 4);
+    score_i4mma_kernel<R><<<sms * per_sm, QM_THREADS, smem, st>>>(
         (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
         ostr, err);
     return kvt_check_launch();

@@ -6,6 +6,8 @@ Layout in HBM:
   K, V       [L][B*H][N_cap][d]   key/value rows, lanes contiguous (bf16 by default)
   amax/amin  per layer [B*H][ceil(N_cap/C_l)][d] bf16 chunk abstracts rounded outward
              (importance.py:56-87 summaries; exact f32 on request)
+  absmag     per layer [B*H][d] f32 max |key| over the lane's chunks (bf16 abstracts only):
+             enables the directed-rounding f32 bounds (bounds_fast.cu) in select_attend
   C_l        ChunkPlanConfig: early layers use early_chunk_size, the rest default_chunk_size
              (chunk_tree.py:111-123, steady state after the early steps)
   k_l        ceil(rate_l * n), rate 0.5 for layers < early_layers else 0.1 (engine.py:83-86,312)
@@ -49,6 +51,8 @@ class SparseDecoder:
         self.amax = [torch.empty((self.lanes, ops.n_grid_leaves(n_cap, C), head_dim), dtype=adt, device=self.device)
                      for C in self.C]
         self.amin = [torch.empty_like(a) for a in self.amax]
+        self.absmag = ([torch.zeros((self.lanes, head_dim), dtype=torch.float32, device=self.device)
+                        for _ in range(n_layers)] if adt == torch.bfloat16 else None)
         self.n = 0
         self._ws = None
         self._bufs = None
@@ -62,6 +66,8 @@ class SparseDecoder:
         self.n = n
         for l in range(self.L):
             ops.abstract_build(self.K[l], n, self.C[l], self.amax[l], self.amin[l])
+            if self.absmag is not None:
+                ops.lane_abs_mag(self.amax[l], self.amin[l], ops.n_grid_leaves(n, self.C[l]), out=self.absmag[l])
         self._bufs = None
 
     def load_layer(self, layer: int, k: torch.Tensor, v: torch.Tensor, t0: int = 0) -> None:
@@ -84,6 +90,9 @@ class SparseDecoder:
         for l in range(self.L):
             c = (self.n - 1) // self.C[l]
             ops.abstract_build(self.K[l], self.n, self.C[l], self.amax[l], self.amin[l], c, c + 1)
+            if self.absmag is not None:  # the refreshed tail chunk can only raise the maxima
+                tail = torch.maximum(self.amax[l][:, c].float().abs(), self.amin[l][:, c].float().abs())
+                torch.maximum(self.absmag[l], tail, out=self.absmag[l])
         self._bufs = None
 
     def k_for(self, layer: int) -> int:
@@ -118,7 +127,7 @@ class SparseDecoder:
         """Select + attend for layer l; q: [lanes, d] (f32 or f64).  Returns the layer buffers."""
         bufs = self._buffers()
         ops.select_attend(q, self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l), self.C[l],
-                          self._ws, bufs[l])
+                          self._ws, bufs[l], abs_mag=None if self.absmag is None else self.absmag[l])
         return bufs[l]
 
     def step(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -396,9 +396,11 @@ class LayerWorkspace:
 
 def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch.Tensor,
                   n: int, k: int, C: int, ws: LayerWorkspace, out: dict, attn_splits: int = 0,
-                  score_blocks: int = 0, exact_scores: bool = False) -> None:
+                  score_blocks: int = 0, exact_scores: bool = False, abs_mag: torch.Tensor | None = None) -> None:
     """One layer, all lanes: K3 -> plan -> K4 -> K5 -> K6 -> K7 into the caller's `out` buffers
-    (sel_tok, sel_score, n_sel, run_start, run_len, n_runs, out, evals)."""
+    (sel_tok, sel_score, n_sel, run_start, run_len, n_runs, out, evals).
+    abs_mag ([n_lanes, d] f32 max |key| per lane, see lane_abs_mag): directed-rounding f32
+    bounds for bf16 abstracts instead of the canonical f64 ones (same selected set)."""
     ls, d = _lanes(keys)
     a = L.KvtLayerArgs()
     a.n_lanes, a.n, a.k, a.d, a.C = keys.shape[0], n, k, d, C
@@ -415,7 +417,33 @@ def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch
     a.out = _p(out.get("out"))
     a.evals = _p(out.get("evals"))
     a.attn_splits, a.score_blocks, a.exact_scores = attn_splits, score_blocks, int(exact_scores)
+    a.abs_mag = _p(abs_mag)
     L.check(L.kvt_select_attend(a, ws.buf.data_ptr(), ws.bytes, _stream()), "select_attend")
+
+
+def lane_abs_mag(amax: torch.Tensor, amin: torch.Tensor, m: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-lane max |key| over chunks [0, m) from the (outward-rounded) abstracts -> f32 [n_lanes, d]
+    (the abs_mag operand of select_attend / kvt_chunk_bounds_fast)."""
+    mag = torch.maximum(amax[:, :m].float().abs().amax(dim=1), amin[:, :m].float().abs().amax(dim=1))
+    if out is None:
+        return mag.contiguous()
+    out.copy_(mag)
+    return out
+
+
+def chunk_bounds_fast(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int, C: int,
+                      abs_mag: torch.Tensor):
+    """Sound f32 directed-rounding (U, L, A_lane) over bf16 abstracts (kvt_chunk_bounds_fast)."""
+    require_cuda(q, amax, amin, abs_mag)
+    nl, d = q.shape
+    m = n_grid_leaves(n, C)
+    U = torch.empty((nl, max(m, 1)), dtype=torch.float64, device=q.device)
+    Lo = torch.empty_like(U)
+    A = torch.empty_like(U)
+    L.check(L.kvt_chunk_bounds_fast(q.contiguous().data_ptr(), nl, d, n, C, amax.data_ptr(), amin.data_ptr(),
+                                    amax.stride(0), abs_mag.data_ptr(), U.data_ptr(), Lo.data_ptr(), A.data_ptr(),
+                                    U.stride(0), _stream()), "chunk_bounds_fast")
+    return U, Lo, A
 
 
 def sqrt_d(d: int) -> float:

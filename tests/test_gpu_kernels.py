@@ -275,3 +275,36 @@ def test_select_plan_items_merge_candidate_runs(ops, C, n):
         for a, b in zip(it[:-1], it[1:]):
             if a[0] + a[1] == b[0]:
                 assert b[0] % 64 == 0
+
+
+@pytest.mark.parametrize("kind", ["random", "planted"])
+@pytest.mark.parametrize("d,C,n", [(128, 64, 4096), (128, 8, 1003), (256, 64, 2049)])
+def test_chunk_bounds_fast_sound_and_tight(ops, kind, d, C, n):
+    """Directed-rounding f32 bounds enclose the canonical f64 bounds of the same bf16 abstracts
+    (hence every dot of the chunk) and stay within ~1e-6 relative of them; A_lane bounds A."""
+    lanes = 3
+    K, V, Q = _lane_data(kind, lanes, n, d, seed=d + C)
+    kt = torch.from_numpy(K).to(torch.bfloat16).cuda()
+    qt = torch.from_numpy(Q).cuda()
+    amax, amin = ops.abstract_build(kt, n, C, abs_dtype=torch.bfloat16)
+    m = ops.n_grid_leaves(n, C)
+    mag = ops.lane_abs_mag(amax, amin, m)
+    Uf, Lf, Af = ops.chunk_bounds_fast(qt, amax, amin, n, C, mag)
+    Uc, Lc, Ac = ops.chunk_bounds(qt, amax, amin, n, C, want_A=True)
+    Uf, Lf, Af, Uc, Lc, Ac = (x[:, :m].cpu().numpy() for x in (Uf, Lf, Af, Uc, Lc, Ac))
+    # canonical bounds carry their own widening slack; compare against the exact abstract sums
+    mx = amax[:, :m].double().cpu().numpy()
+    mn = amin[:, :m].double().cpu().numpy()
+    q = Q.astype(np.float64)[:, None, :]
+    Ux = np.where(q >= 0, q * mx, q * mn).sum(-1)
+    Lx = np.where(q >= 0, q * mn, q * mx).sum(-1)
+    Ax = (np.abs(q) * np.maximum(np.abs(mx), np.abs(mn))).sum(-1)
+    assert np.all(Uf >= Ux) and np.all(Lf <= Lx)
+    assert np.all(Uf - Ux <= 1e-5 * Ax + 1e-30) and np.all(Lx - Lf <= 1e-5 * Ax + 1e-30)
+    assert np.all(Af >= Ax.max(1, keepdims=True) * (1 - 1e-12))
+    # every canonical dot of the chunk (bf16 keys) lies inside
+    dots = np.einsum("lnd,ld->ln", kt.double().cpu().numpy(), Q.astype(np.float64))
+    for i in range(lanes):
+        for c in range(m):
+            seg = dots[i, c * C:min(n, (c + 1) * C)]
+            assert seg.max() <= Uf[i, c] and seg.min() >= Lf[i, c]
