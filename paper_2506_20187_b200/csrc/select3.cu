@@ -25,6 +25,8 @@ constexpr int S3_WARPS = S3_THREADS / 32;
 constexpr int S3_BINS = 4096;
 constexpr int S3_LIST_CAP = 8192;
 constexpr int S3_BAND_CAP = 1024;
+constexpr int S3_UB = 8;  // float4 loads in flight per thread (block-strided passes)
+constexpr int S3_UW = 4;  // 128-element windows in flight per warp (warp-range passes)
 
 struct S3Shared {
     unsigned int hist[S3_BINS];
@@ -40,10 +42,12 @@ struct S3Shared {
     long long above;
 };
 
-__device__ __forceinline__ int s3_bucket(double s, double lo, double inv) {
-    if (s < lo) return -1;
-    const double x = (s - lo) * inv;
-    return x >= (double)(S3_BINS - 1) ? S3_BINS - 1 : (int)x;
+// Bucket of an estimate: any deterministic non-decreasing map works (the exact k-th value
+// comes from the bucket's own list), so f32 arithmetic is enough.
+__device__ __forceinline__ int s3_bucket(float s, float lo, float inv) {
+    if (!(s >= lo)) return -1;
+    const float x = (s - lo) * inv;
+    return x >= (float)(S3_BINS - 1) ? S3_BINS - 1 : (int)x;
 }
 
 // Block-wide: find the digit bin of `hist` (nb bins, descending order) where the running
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const unsigned char* kl = keys + li * lane_stride_b;
     int32_t* otok = sel_tok + li * sel_stride;
     double* osc = sel_score + li * sel_stride;
-    const bool vec = ((uintptr_t)sc % 16) == 0;
+    const bool vec = ((uintptr_t)sc % 16) == 0 && ((uintptr_t)tk % 16) == 0;
     if (kk <= 0) {
         if (tid == 0) { n_sel[li] = 0; if (run_start) n_runs[li] = 0; }
         return;
@@ -207,19 +211,25 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const double lo = rec[li * 4 + 1] - 2.0 * E;
     const double hi = rec[li * 4 + 2] + 2.0 * E;
     const double inv = hi > lo ? (double)S3_BINS / (hi - lo) : 0.0;
+    const float lo_f = (float)lo, inv_f = (float)inv;
 
     // ---- 1. bucket histogram of the estimates (4 per thread per iteration) ----
     for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
     if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; S.remaining = 0; }
     __syncthreads();
-    for (int64_t base = 0; base < n; base += 4 * S3_THREADS) {
-        const int64_t i = base + 4 * tid;
-        float v[4];
-        load4s(sc, i, n, vec, v);
+    // passes over the estimates batch S3_UB float4 loads per thread (memory-level parallelism)
+    for (int64_t base = 0; base < n; base += (int64_t)S3_UB * 4 * S3_THREADS) {
+        float v[S3_UB][4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int bkt = i + e < n ? s3_bucket((double)v[e], lo, inv) : -1;
-            if (bkt >= 0) atomicAdd(&S.hist[bkt], 1u);
+        for (int u = 0; u < S3_UB; ++u) load4s(sc, base + (int64_t)(u * S3_THREADS + tid) * 4, n, vec, v[u]);
+#pragma unroll
+        for (int u = 0; u < S3_UB; ++u) {
+            const int64_t i = base + (int64_t)(u * S3_THREADS + tid) * 4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int bkt = i + e < n ? s3_bucket(v[u][e], lo_f, inv_f) : -1;
+                if (bkt >= 0) atomicAdd(&S.hist[bkt], 1u);
+            }
         }
     }
     __syncthreads();
@@ -227,13 +237,17 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const int bstar = S.bstar;
     const long long need_in_bucket = kk - S.above;
     // ---- 2. gather the k-th bucket (unordered) ----
-    for (int64_t base = 0; base < n; base += 4 * S3_THREADS) {
-        const int64_t i = base + 4 * tid;
-        float v[4];
-        load4s(sc, i, n, vec, v);
+    for (int64_t base0 = 0; base0 < n; base0 += (int64_t)S3_UB * 4 * S3_THREADS) {
+      float vv[S3_UB][4];
+#pragma unroll
+      for (int u = 0; u < S3_UB; ++u) load4s(sc, base0 + (int64_t)(u * S3_THREADS + tid) * 4, n, vec, vv[u]);
+#pragma unroll
+      for (int u = 0; u < S3_UB; ++u) {
+        const int64_t i = base0 + (int64_t)(u * S3_THREADS + tid) * 4;
+        const float* v = vv[u];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const bool m = i + e < n && s3_bucket((double)v[e], lo, inv) == bstar;
+            const bool m = i + e < n && s3_bucket(v[e], lo_f, inv_f) == bstar;
             const unsigned ballot = __ballot_sync(KVT_FULL, m);
             unsigned wb = 0;
             if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
@@ -243,6 +257,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
                 if (slot < S3_LIST_CAP) lkey[slot] = ord_key32(v[e]);
             }
         }
+      }
     }
     __syncthreads();
     bool fallback = bstar < 0 || S.list_n > S3_LIST_CAP;
@@ -258,10 +273,14 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         // ---- 3. per-warp sure counts + band members (appended, unordered) ----
         if (tid == 0) S.list_n = 0;  // reused as the band counter
         __syncthreads();
-        for (int64_t base = wr.a; base < wr.b; base += 128) {
-            const int64_t i = base + 4 * lane;
-            float v[4];
-            load4s(sc, i, wr.b, vec, v);
+        for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
+          float vv[S3_UW][4];
+#pragma unroll
+          for (int u = 0; u < S3_UW; ++u) load4s(sc, base0 + 128 * u + 4 * lane, wr.b, vec, vv[u]);
+#pragma unroll
+          for (int u = 0; u < S3_UW; ++u) {
+            const int64_t i = base0 + 128 * u + 4 * lane;
+            const float* v = vv[u];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const double sv = (double)v[e];
@@ -277,6 +296,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
                     if (slot < S3_BAND_CAP) { S.band_t[slot] = tk[i + e]; band_pos[slot] = (int)(i + e); }
                 }
             }
+          }
         }
         if (lane == 0) w_sel[warp] = nsure;
         __syncthreads();
@@ -318,10 +338,25 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         __syncthreads();
         long long pos = 0;
         for (int w = 0; w < warp; ++w) pos += w_sel[w];
-        for (int64_t base = wr.a; base < wr.b; base += 128) {
-            const int64_t i = base + 4 * lane;
-            float v[4];
-            load4s(sc, i, wr.b, vec, v);
+        for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
+          float vv[S3_UW][4];
+          int tt[S3_UW][4];
+#pragma unroll
+          for (int u = 0; u < S3_UW; ++u) {
+              const int64_t i = base0 + 128 * u + 4 * lane;
+              load4s(sc, i, wr.b, vec, vv[u]);
+              if (vec && i + 4 <= wr.b) {
+                  const int4 x = *reinterpret_cast<const int4*>(tk + i);
+                  tt[u][0] = x.x; tt[u][1] = x.y; tt[u][2] = x.z; tt[u][3] = x.w;
+              } else {
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) tt[u][e] = i + e < wr.b ? tk[i + e] : 0;
+              }
+          }
+#pragma unroll
+          for (int u = 0; u < S3_UW; ++u) {
+            const int64_t i = base0 + 128 * u + 4 * lane;
+            const float* v = vv[u];
             bool m[4];
             double scr[4];
             int cnt = 0;
@@ -343,8 +378,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             long long p = pos + inc - cnt;
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-                if (m[e]) { otok[p] = tk[i + e]; osc[p] = scr[e]; ++p; }
+                if (m[e]) { otok[p] = tt[u][e]; osc[p] = scr[e]; ++p; }
             pos += __shfl_sync(KVT_FULL, inc, 31);
+          }
         }
         w_sel[warp] = w_sel[warp];  // (no-op: keeps the per-warp totals for the run scan below)
     } else {
@@ -453,31 +489,64 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     if (tid == 0) n_sel[li] = (int32_t)kk;
     if (!run_start) return;
 
-    // ---- 5. fused run scan (engine.py:176-183) over the k outputs ----
+    // ---- 5. fused run scan (engine.py:176-183) over the k outputs, warp-cooperative ----
+    // Warp w owns output positions [wa, wb); per 32-wide window a lane tests head (previous
+    // token not adjacent) and tail (next token not adjacent) with coalesced loads, run
+    // indices come from ballots + one block scan of the per-warp head counts.  Run starts
+    // and, temporarily, head positions are written first; lengths after a barrier.
     __syncthreads();
-    const long long per_t = (kk + S3_THREADS - 1) / S3_THREADS;
-    const long long p_lo = kvt::imin(kk, tid * per_t), p_hi = kvt::imin(kk, p_lo + per_t);
-    long long heads = 0;
-    for (long long p = p_lo; p < p_hi; ++p) heads += (p == 0 || otok[p] != otok[p - 1] + 1);
-    long long tot_h;
-    const long long ex_h = block_excl_scan<long long>(heads, S.scan_sh, tot_h);
-    int32_t* rs = run_start + li * run_stride;
-    int32_t* rl = run_len + li * run_stride;
-    long long ridx = ex_h - 1;
-    for (long long p = p_lo; p < p_hi; ++p) {
-        if (p == 0 || otok[p] != otok[p - 1] + 1) {
-            ++ridx;
-            rs[ridx] = otok[p];
-            rl[ridx] = (int32_t)p;
+    {
+        constexpr int RU = 4;
+        const long long per_w = ((kk + S3_WARPS - 1) / S3_WARPS + 31) / 32 * 32;
+        const long long wa = kvt::imin(kk, warp * per_w), wb = kvt::imin(kk, wa + per_w);
+        int32_t* rs = run_start + li * run_stride;
+        int32_t* rl = run_len + li * run_stride;
+        const unsigned le_mask = (2u << lane) - 1u;
+        long long nh = 0;
+        for (long long p0 = wa; p0 < wb; p0 += 32 * RU) {
+            bool hd[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const long long p = p0 + 32 * u + lane;
+                hd[u] = p < wb && (p == 0 || otok[p] != otok[p - 1] + 1);
+            }
+#pragma unroll
+            for (int u = 0; u < RU; ++u) nh += __popc(__ballot_sync(KVT_FULL, hd[u]));
         }
+        __syncthreads();  // w_sel is reused for the per-warp head counts
+        if (lane == 0) w_sel[warp] = nh;
+        __syncthreads();
+        long long base_r = 0, tot_h = 0;
+        for (int w = 0; w < S3_WARPS; ++w) {
+            if (w < warp) base_r += w_sel[w];
+            tot_h += w_sel[w];
+        }
+        for (int pass = 0; pass < 2; ++pass) {
+            long long r0 = base_r;
+            for (long long p0 = wa; p0 < wb; p0 += 32 * RU) {
+                int t[RU];
+                bool hd[RU], tl[RU];
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const long long p = p0 + 32 * u + lane;
+                    t[u] = p < wb ? otok[p] : 0;
+                    hd[u] = p < wb && (p == 0 || t[u] != otok[p - 1] + 1);
+                    tl[u] = p < wb && (p == kk - 1 || otok[p + 1] != t[u] + 1);
+                }
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const long long p = p0 + 32 * u + lane;
+                    const unsigned hm = __ballot_sync(KVT_FULL, hd[u]);
+                    const long long r = r0 + __popc(hm & le_mask) - 1;  // run of position p
+                    if (pass == 0 && hd[u]) { rs[r] = t[u]; rl[r] = (int32_t)p; }
+                    if (pass == 1 && tl[u]) rl[r] = (int32_t)(p + 1 - rl[r]);
+                    r0 += __popc(hm);
+                }
+            }
+            __syncthreads();
+        }
+        if (tid == 0) n_runs[li] = (int32_t)tot_h;
     }
-    __syncthreads();
-    ridx = ex_h - 1;
-    for (long long p = p_lo; p < p_hi; ++p) {
-        if (p == 0 || otok[p] != otok[p - 1] + 1) ++ridx;
-        if (p == kk - 1 || otok[p + 1] != otok[p] + 1) rl[ridx] = (int32_t)(p + 1 - rl[ridx]);
-    }
-    if (tid == 0) n_runs[li] = (int32_t)tot_h;
 }
 
 }  // namespace kvt
