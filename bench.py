@@ -489,6 +489,16 @@ def run_ours(args):
     launches_per_layer = 6 if is_i4 else 5
     sel_gather_bytes = algo["bounds"] + algo["score"] + algo["select"] + algo["attn"]
     frac_of = "measured" if "hbm_gbs" in peaks else "fallback"
+    # DRAM traffic of the dominant kernel: one ncu --set full capture (layer-2 launch), committed
+    # under profiles/ (tools/gpu_prof.sh); compared with the same launch's algorithmic bytes
+    traffic = traffic_algo = None
+    tj = ROOT / "profiles" / "traffic.json"
+    wl = workload_config(args, world)["workload"]
+    if tj.exists():
+        rec = json.loads(tj.read_text()).get("workloads", {}).get(wl, {}).get(dom)
+        if rec:
+            traffic = rec["dram_bytes"]
+            traffic_algo = dec.algorithmic_bytes(n_cand, layers=[rec["layer"]])[dom]
     line = {
         "metric": "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -499,7 +509,9 @@ def run_ours(args):
         "config": workload_config(args, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": per_kernel[dom]["gbs"], "peak": hbm_peak,
                      "unit": "GB/s", "frac": (per_kernel[dom]["gbs"] or 0) / hbm_peak,
-                     "traffic": None, "peak_source": frac_of,
+                     "traffic": traffic, "traffic_algo_bytes_same_launch": traffic_algo,
+                     "traffic_source": "profiles/traffic.json (ncu --set full, layer-2 launch)" if traffic else None,
+                     "peak_source": frac_of,
                      "algo_bytes_per_step": algo[dom], "kernel_ms_per_step": st_ms[dom],
                      "kernel_share_of_staged_step": st_ms[dom] / staged_total if staged_total else None},
         "selection_gather_gbs": sel_gather_bytes / (ms_max / 1e3) / 1e9,

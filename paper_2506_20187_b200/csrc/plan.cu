@@ -73,14 +73,10 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
                     w = (unsigned long long)leaf_rows(ls, nl, c, n, C);
                 }
             }
+            // warp-aggregated weighted histogram: leaves are disjoint, so 32 row counts sum to <= n
             const unsigned peers = __match_any_sync(KVT_FULL, digit);
-            unsigned long long sum = 0;
-#pragma unroll 4
-            for (int src = 0; src < 32; ++src) {
-                const unsigned long long ws = __shfl_sync(KVT_FULL, w, src);
-                if (peers & (1u << src)) sum += ws;
-            }
-            if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], sum);
+            const unsigned sum = __reduce_add_sync(peers, (unsigned)w);
+            if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned long long)sum);
         }
         __syncthreads();
         if (tid < 32) {
@@ -141,9 +137,11 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
             if (cand) umax_c = fmax(umax_c, Ul[c]);
             if (cand_leaf) cand_leaf[li * leaf_stride + c] = cand ? 1 : 0;
         }
-        long long tot_it, tot_tk;
-        const long long ex_it = block_excl_scan<long long>(it, scan_sh, tot_it);
-        const long long ex_tk = block_excl_scan<long long>(tk, scan_sh, tot_tk);
+        // one scan of (items << 40 | tokens): items < 2^23 and tokens < 2^40 per lane
+        long long tot_pk;
+        const long long ex_pk = block_excl_scan<long long>((it << 40) | tk, scan_sh, tot_pk);
+        const long long ex_it = ex_pk >> 40, ex_tk = ex_pk & ((1LL << 40) - 1);
+        const long long tot_it = tot_pk >> 40, tot_tk = tot_pk & ((1LL << 40) - 1);
         if (it > 0) {
             const int64_t e = s + rows;
             int32_t* out = items + li * item_stride * 3;
@@ -223,6 +221,7 @@ extern "C" int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t
     if (!U || !L || !items || !n_items || !n_cand || n_lanes < 0 || n < 0) return KVT_ERR_ARG;
     if (!leaf_start && C < 1) return KVT_ERR_ARG;
     if (k < 0 || k > n) return KVT_ERR_K;
+    if (n > (1LL << 22)) return KVT_ERR_SHAPE;  // packed (items, tokens) scan: <= 4M tokens per lane
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
     static bool configured = false;

@@ -134,21 +134,23 @@ class SparseDecoder:
         """All layers for one decode step; q: [L, lanes, d] -> attention outputs [L, lanes, d] f32."""
         if out is None:
             out = torch.empty((self.L, self.lanes, self.d), dtype=torch.float32, device=self.device)
-        for l in range(self.L):
-            b = self.layer(l, q[l])
-            out[l].copy_(b["out"])
+        bufs = self._buffers()
+        for l in range(self.L):  # attention outputs land directly in out[l]
+            ops.select_attend(q[l], self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l),
+                              self.C[l], self._ws, {**bufs[l], "out": out[l]},
+                              abs_mag=None if self.absmag is None else self.absmag[l])
         return out
 
     # -- accounting ---------------------------------------------------------------------------------
 
-    def algorithmic_bytes(self, n_cand: list[list[int]]) -> dict:
-        """Per-kernel algorithmic HBM bytes for one step (SURVEY.md sec. 8(d) formulas).
-        n_cand[l][lane] = candidate tokens of that lane at layer l."""
+    def algorithmic_bytes(self, n_cand: list[list[int]], layers: list[int] | None = None) -> dict:
+        """Per-kernel algorithmic HBM bytes for one step (SURVEY.md sec. 8(d) formulas), or for the
+        given layers only.  n_cand[l][lane] = candidate tokens of that lane at layer l."""
         sK = self.K.element_size()
         sA = self.amax[0].element_size()
         d = self.d
         out = {"bounds": 0, "score": 0, "select": 0, "attn": 0, "plan": 0, "runs": 0}
-        for l in range(self.L):
+        for l in (range(self.L) if layers is None else layers):
             m = ops.n_grid_leaves(self.n, self.C[l])
             k = self.k_for(l)
             nc = sum(n_cand[l])
