@@ -120,7 +120,7 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, ui
 
 // ---- the scoring kernel --------------------------------------------------------------------
 template <int R>  // R = d / 128 rounds of 4 groups
-__global__ void __launch_bounds__(QM_THREADS, 8) score_i4mma_kernel(
+__global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
     int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
     float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err) {
