@@ -219,9 +219,11 @@ KVT_API int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t 
  * sel_score are the scores from K5 (keys are not re-read); the softmax logit of token i is
  * (sel_score_i - max) * logit_scale, i.e. logit_scale = 1/sqrt(d) for raw dots and 1 for
  * logits.  Split over
- * `splits` blocks per lane with an online-softmax (m, l, o) merge.  out: float32
+ * `splits` blocks per lane with an online-softmax (m, l, o) merge; splits <= 0 picks the count
+ * (<= 64) that fills whole waves of the kernel at its residency.  out: float32
  * [n_lanes][d] (out64: optional float64 copy).  ws: workspace of
- * kvt_attn_workspace_bytes(n_lanes, d, splits) bytes, zero-filled once by the caller (the
+ * kvt_attn_workspace_bytes(n_lanes, d, splits) bytes (splits = 64 when auto), zero-filled
+ * once by the caller (the
  * per-lane merge tickets are left at zero by every call).  The last split CTA of each lane
  * performs the log-sum-exp merge, so this is a single kernel launch. */
 KVT_API size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits);

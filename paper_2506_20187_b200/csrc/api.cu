@@ -159,15 +159,7 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
 
     }
     if (a->out && a->values) {
-        int splits = a->attn_splits;
-        if (splits <= 0) {
-            // ~1024-row units (many small CTAs: no wave tail), >= 2 waves of 3 CTAs per SM when
-            // there are few lanes, >= 32 rows per unit
-            const int64_t by_rows = (a->k + 1023) / 1024;
-            const int64_t by_sms = ((int64_t)num_sms() * 6 + a->n_lanes - 1) / a->n_lanes;
-            const int64_t cap = kvt::imin(MAX_SPLITS, kvt::imax(1, (a->k + 31) / 32));
-            splits = (int)kvt::imax(1, kvt::imin(kvt::imax(by_rows, by_sms), cap));
-        }
+        int splits = a->attn_splits;  // 0 = auto: wave-aware choice in kvt_sparse_decode_attn
         if (splits > MAX_SPLITS) splits = MAX_SPLITS;
         rc = kvt_sparse_decode_attn(a->values, a->v_dtype, a->n_lanes, a->lane_stride, a->d, a->sel_tok, a->sel_score,
                                     a->n_sel, a->k, 1.0 / sqrt((double)a->d), splits, w.attn_part, a->out, nullptr,

@@ -502,6 +502,16 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
     return r;
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // INT4 records: lane = one 32-dim group (16 B of codes + its (scale, min)).
 // x^ = code * s + m, so sum_i w_i x^_ij = sum_i (w_i s_i) code_ij + sum_i w_i m_i: one packed
 // fma per two codes; code -> float by byte permute into 2^23 + code and a packed subtract.
@@ -517,6 +527,17 @@ struct FmtI4 {
         return r;
     }
     __device__ static Raw zero() { Raw r; r.c = make_uint4(0, 0, 0, 0); r.sm = 0; return r; }
+    // ring path: this lane's pieces of a row -> shared memory, and back
+    __device__ static void issue(uint32_t srow, const unsigned char* grow, int grp) {
+        cp_async16(srow + 16 * grp, grow + 16 * grp);
+        cp_async4(srow + D / 2 + 4 * grp, grow + D / 2 + 4 * grp);
+    }
+    __device__ static Raw lds(const unsigned char* srow, int grp) {
+        Raw r;
+        r.c = *reinterpret_cast<const uint4*>(srow + 16 * grp);
+        r.sm = *reinterpret_cast<const uint32_t*>(srow + D / 2 + 4 * grp);
+        return r;
+    }
     __device__ static void acc(uint64_t (&o2)[NE / 2], const Raw& r, float w, float& om) {
         const __half2 p = *reinterpret_cast<const __half2*>(&r.sm);
         const float ws = w * __low2float(p);
@@ -548,6 +569,12 @@ struct Fmt16 {
         return __ldg(reinterpret_cast<const uint4*>(row + 16 * grp));
     }
     __device__ static Raw zero() { return make_uint4(0, 0, 0, 0); }
+    __device__ static void issue(uint32_t srow, const unsigned char* grow, int grp) {
+        cp_async16(srow + 16 * grp, grow + 16 * grp);
+    }
+    __device__ static Raw lds(const unsigned char* srow, int grp) {
+        return *reinterpret_cast<const uint4*>(srow + 16 * grp);
+    }
     __device__ static void acc(uint64_t (&o2)[NE / 2], const Raw& r, float w, float&) {
         const uint64_t w2 = f2_pack(w, w);
         const uint32_t words[4] = {r.x, r.y, r.z, r.w};
@@ -683,6 +710,137 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_gather_kernel(
     attn_finish(part, splits, d, li, tickets, out, out64, scale);
 }
 
+// Ring variant (the decode-path default): bytes in flight are not bounded by registers.
+// Warp w owns a contiguous sub-range of the unit; it stages the sub-range's token ids and
+// scores in shared memory (one coalesced pass, warp max taken there: no rescaling later),
+// then streams its rows through a private S-slot ring with cp.async (each lane copies and
+// later reads only its own 16 B pieces, so no intra-warp synchronisation is needed).
+template <class F, int S>
+__global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
+    const unsigned char* __restrict__ values, int64_t lane_stride_b, int d, const int32_t* __restrict__ sel_tok,
+    const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
+    double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
+    double* __restrict__ out64, double scale) {
+    constexpr int LPR = F::LPR, NE = F::NE, RPW = 32 / LPR, RB = F::row_bytes(), SLOT = RPW * RB;
+    extern __shared__ __align__(16) unsigned char ring_smem[];
+    __shared__ double red_m[ATTN_WARPS];
+    __shared__ float red_o[ATTN_WARPS][LPR * NE];
+    __shared__ float red_l[ATTN_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t li = blockIdx.y;
+    const int s = blockIdx.x;
+    const int64_t k = n_sel[li];
+    const int64_t a = kvt::imin(k, (int64_t)s * R), b = kvt::imin(k, a + R);
+    const int nr = (int)(b - a);
+    const int per_w = (nr + ATTN_WARPS - 1) / ATTN_WARPS;
+    const int wa = min(nr, warp * per_w), wb = min(nr, wa + per_w);
+    unsigned char* ring = ring_smem + (size_t)warp * S * SLOT;
+    int32_t* tok_s = reinterpret_cast<int32_t*>(ring_smem + (size_t)ATTN_WARPS * S * SLOT);
+    float* w_s = reinterpret_cast<float*>(tok_s + R);
+    const int32_t* tok = sel_tok + li * sel_stride + a;
+    const double* sc = sel_score + li * sel_stride + a;
+    double m = -INFINITY;
+    for (int i = wa + lane; i < wb; i += 32) {
+        tok_s[i] = tok[i];
+        m = fmax(m, sc[i]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(KVT_FULL, m, off));
+    const double sl2 = scale * 1.4426950408889634;
+    __syncwarp();
+    for (int i = wa + lane; i < wb; i += 32) w_s[i] = exp2f((float)((sc[i] - m) * sl2));  // once per row (L2 hit)
+    __syncwarp();
+    const int sub = lane / LPR, grp = lane % LPR;
+    const unsigned char* base = values + li * lane_stride_b;
+    const uint32_t ring_a = (uint32_t)__cvta_generic_to_shared(ring);
+    const int nslots = (wb - wa + RPW - 1) / RPW;
+    uint64_t o2[NE / 2];
+#pragma unroll
+    for (int e = 0; e < NE / 2; ++e) o2[e] = 0ull;
+    float l = 0.f, om = 0.f;
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+        const int i = wa + j * RPW + sub;
+        if (j < nslots && i < wb) F::issue(ring_a + j * SLOT + sub * RB, base + (int64_t)tok_s[i] * RB, grp);
+        cp_async_commit();
+    }
+    for (int j = 0; j < nslots; ++j) {
+        const int jn = j + S - 1;
+        const int in = wa + jn * RPW + sub;
+        if (jn < nslots && in < wb)
+            F::issue(ring_a + (jn % S) * SLOT + sub * RB, base + (int64_t)tok_s[in] * RB, grp);
+        cp_async_commit();
+        cp_async_wait<S - 1>();
+        const int i = wa + j * RPW + sub;
+        if (i < wb) {
+            const float w = w_s[i];
+            F::acc(o2, F::lds(ring + (j % S) * SLOT + sub * RB, grp), w, om);
+            l += w;
+        }
+    }
+    cp_async_wait<0>();
+    float o[NE];
+#pragma unroll
+    for (int e = 0; e < NE / 2; ++e) f2_unpack(o2[e], o[2 * e], o[2 * e + 1]);
+    const float bias = F::bias(om);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) o[e] += bias;
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+        l += __shfl_xor_sync(KVT_FULL, l, off);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) o[e] += __shfl_xor_sync(KVT_FULL, o[e], off);
+    }
+    if (lane < LPR) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) red_o[warp][NE * grp + e] = o[e];
+    }
+    if (lane == 0) { red_l[warp] = l; red_m[warp] = m; }
+    __syncthreads();
+    double M = red_m[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_WARPS; ++w) M = fmax(M, red_m[w]);
+    float wsc[ATTN_WARPS];
+#pragma unroll
+    for (int w = 0; w < ATTN_WARPS; ++w) wsc[w] = red_m[w] == -INFINITY ? 0.f : exp2f((float)((red_m[w] - M) * sl2));
+    double* P = part + ((int64_t)li * splits + s) * (d + 2);
+    for (int j = tid; j < d; j += ATTN_THREADS) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) acc = fmaf(wsc[w], red_o[w][j], acc);
+        P[2 + j] = (double)acc;
+    }
+    if (tid == 0) {
+        float ls = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATTN_WARPS; ++w) ls = fmaf(wsc[w], red_l[w], ls);
+        P[0] = M;
+        P[1] = (double)ls;
+    }
+    attn_finish(part, splits, d, li, tickets, out, out64, scale);
+}
+
+template <class F, int S>
+static int launch_ring(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, const int32_t* sel_tok,
+                       const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, int R,
+                       double* part, unsigned int* tickets, float* out, double* out64, double scale,
+                       cudaStream_t st) {
+    constexpr int SLOT = (32 / F::LPR) * F::row_bytes();
+    const size_t smem = (size_t)ATTN_WARPS * S * SLOT + (size_t)R * 8;
+    static size_t configured = 0;
+    if (smem > configured && smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(attn_ring_kernel<F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return kvt_set_cuda_error(e);
+        configured = smem;
+    }
+    dim3 grid(splits, (unsigned)n_lanes);
+    attn_ring_kernel<F, S><<<grid, ATTN_THREADS, smem, st>>>((const unsigned char*)values, lane_stride_b, d, sel_tok,
+                                                            sel_score, n_sel, sel_stride, splits, R, part, tickets,
+                                                            out, out64, scale);
+    return kvt_check_launch();
+}
+
 template <class F, int U>
 static int launch_gather(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, const int32_t* sel_tok,
                          const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, int R,
@@ -767,6 +925,17 @@ static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_strid
     return kvt_check_launch();
 }
 
+// Auto split count for the ring kernel: units of <= ATTN_RMAX rows.  A sweep over splits on the
+// planted decode workload (tools/microbench.py attn; B200) shows per-unit fixed cost (staging,
+// pipeline fill, partial merge) dominating any wave-tail effect: the fewest units that keep the
+// staging bounded are best at k = 0.1 n and within ~8% at k = 0.5 n.
+// INT4 units are capped at half the rows of 2-byte ones (measured on the decode step).
+static int ring_auto_splits(int64_t kmax, int v_dtype) {
+    const int64_t rmax = v_dtype == KVT_I4 ? 1664 : 3328;
+    const int64_t cap = kvt::imax(1, kvt::imin(64, (kmax + 31) / 32));
+    return (int)kvt::imax(1, kvt::imin(cap, (kmax + rmax - 1) / rmax));
+}
+
 extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride, int d,
                                       const int32_t* sel_tok, const double* sel_score, const int32_t* n_sel,
                                       int64_t sel_stride, double logit_scale, int splits, void* ws, float* out,
@@ -775,31 +944,41 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
         return KVT_ERR_ARG;
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 65535) return KVT_ERR_ARG;
-    if (splits < 1) splits = 1;
-    if (splits > 64) splits = 64;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned int* tickets = (unsigned int*)ws;
     double* part = (double*)((char*)ws + ticket_bytes(n_lanes));
     int rc;
-    // rows per work unit: the whole selection in <= splits units
     const int64_t kmax = sel_stride;
+    if (splits <= 0) splits = ring_auto_splits(kmax, v_dtype);  // auto (the workspace must hold 64 splits)
+    if (splits > 64) splits = 64;
+    // rows per work unit: the whole selection in <= splits units
     const int R = (int)kvt::imax(32, ((kmax + splits - 1) / splits + 31) / 32 * 32);
     const bool aligned = ((uintptr_t)values % 16) == 0;
     switch (v_dtype) {
         case KVT_I4: {
             if ((d != 128 && d != 256) || !aligned || (lane_stride % 16)) return KVT_ERR_SHAPE;
-            rc = d == 128 ? launch_gather<FmtI4<128>, 4>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
-                                                         sel_stride, splits, R, part, tickets, out, out64, logit_scale, st)
-                          : launch_gather<FmtI4<256>, 2>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
-                                                         sel_stride, splits, R, part, tickets, out, out64, logit_scale, st);
+            if (R <= 8192)  // cp.async ring (the unit's ids + weights staged: 8 B per row)
+                rc = d == 128 ? launch_ring<FmtI4<128>, 8>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                                                           sel_stride, splits, R, part, tickets, out, out64, logit_scale, st)
+                              : launch_ring<FmtI4<256>, 6>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                                                           sel_stride, splits, R, part, tickets, out, out64, logit_scale, st);
+            else
+                rc = d == 128 ? launch_gather<FmtI4<128>, 4>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                                                             sel_stride, splits, R, part, tickets, out, out64, logit_scale, st)
+                              : launch_gather<FmtI4<256>, 2>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                                                             sel_stride, splits, R, part, tickets, out, out64, logit_scale, st);
             break;
         }
         case KVT_BF16:
         case KVT_F16:
             if ((d == 128 || d == 256) && aligned && (lane_stride * 2) % 16 == 0) {
                 const int64_t lsb = lane_stride * 2;
-#define KVT_G(TT, DD) launch_gather<Fmt16<TT, DD>, 4>(values, n_lanes, lsb, d, sel_tok, sel_score, n_sel, sel_stride, \
-                                                      splits, R, part, tickets, out, out64, logit_scale, st)
+#define KVT_G(TT, DD) (R <= 8192 ? launch_ring<Fmt16<TT, DD>, 12>(values, n_lanes, lsb, d, sel_tok, sel_score, n_sel, \
+                                                                  sel_stride, splits, R, part, tickets, out, out64, \
+                                                                  logit_scale, st)                                      \
+                                 : launch_gather<Fmt16<TT, DD>, 4>(values, n_lanes, lsb, d, sel_tok, sel_score, n_sel,  \
+                                                                   sel_stride, splits, R, part, tickets, out, out64,    \
+                                                                   logit_scale, st))
                 if (v_dtype == KVT_BF16) rc = d == 128 ? KVT_G(__nv_bfloat16, 128) : KVT_G(__nv_bfloat16, 256);
                 else rc = d == 128 ? KVT_G(__half, 128) : KVT_G(__half, 256);
 #undef KVT_G

@@ -351,13 +351,6 @@ def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition
     return {"run_start": rs, "run_len": rl, "n_runs": nr, "part_start": ps, "part_state": pst, "n_part": npart}
 
 
-def auto_splits(n_lanes: int, k: int) -> int:
-    """Same rule as kvt_select_attend (api.cu): ~1024-row units, >= 6 CTAs per SM overall."""
-    by_rows = (k + 1023) // 1024
-    by_sms = (148 * 6 + n_lanes - 1) // max(n_lanes, 1)
-    return max(1, min(max(by_rows, by_sms), 64, max(1, (k + 31) // 32)))
-
-
 def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor,
                        splits: int = 0, want_f64: bool = False, logit_scale: float | None = None):
     """softmax(sel_score * logit_scale) @ V[sel] (engine.py:145-154) -> out f32 [n_lanes, d] (and f64).
@@ -366,9 +359,9 @@ def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: t
     ls, d = _lanes(values)
     nl = values.shape[0]
     k = sel_tok.shape[1]
-    if splits <= 0:
-        splits = auto_splits(nl, k)
-    ws = torch.zeros(max(1, L.kvt_attn_workspace_bytes(nl, d, splits)), dtype=torch.uint8, device=values.device)
+    # splits <= 0: chosen by kvt_sparse_decode_attn (wave-aware); the workspace holds 64
+    ws = torch.zeros(max(1, L.kvt_attn_workspace_bytes(nl, d, 64 if splits <= 0 else splits)), dtype=torch.uint8,
+                     device=values.device)
     out = torch.empty((nl, d), dtype=torch.float32, device=values.device)
     out64 = torch.empty((nl, d), dtype=torch.float64, device=values.device) if want_f64 else None
     st = _nz(sel_tok)

@@ -85,5 +85,43 @@ def main():
         globals()[w](a)
 
 
+
+def _planted_sel(lanes, n, k, dev, seed=0):
+    """Sorted selected sets like the planted workload: k tokens inside 3 hot regions (30% of n)."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    hot = torch.cat([torch.arange(int(n * a), int(n * a) + n // 10) for a in (0.1, 0.45, 0.8)])
+    sel = torch.stack([torch.sort(hot[torch.randperm(hot.numel(), generator=g)[:k]]).values for _ in range(lanes)])
+    return sel.to(torch.int32).to(dev)
+
+
+def attn(a):
+    from paper_2506_20187_b200 import _lib as Lb
+    d = 128
+    for fmt in ("int4", "bf16"):
+        lanes = a.lanes if fmt == "int4" else a.lanes // 2
+        if fmt == "int4":
+            V = ops.I4KV.empty(lanes, a.n, d, "cuda")
+            V.data.random_(0, 255)
+            V.data.view(torch.float16)[..., d // 4:] = 0.01
+            rb = ops.row_bytes_i4(d)
+        else:
+            V = torch.randn((lanes, a.n, d), device="cuda", dtype=torch.bfloat16)
+            rb = 2 * d
+        for k in (a.n // 10, a.n // 2):
+            st = _planted_sel(lanes, a.n, k, "cuda") if k < a.n // 2 else \
+                torch.sort(torch.randperm(a.n, device="cuda")[:k]).values.to(torch.int32).expand(lanes, k).contiguous()
+            ss = torch.randn((lanes, k), dtype=torch.float64, device="cuda")
+            ns = torch.full((lanes,), k, dtype=torch.int32, device="cuda")
+            res = {}
+            for sp in [0, 2, 3, 4, 6, 7, 8, 10, 12, 16, 24, 32, 48, 64]:
+                if sp and (k + sp - 1) // sp > 4096:
+                    continue
+                ms = timeit(lambda: ops.sparse_decode_attn(V, st, ss, ns, splits=sp), reps=20)
+                res[sp] = round(ms * 1e3, 1)
+            best = min((v, s) for s, v in res.items() if s)
+            report(f"attn[{fmt}] k={k} best splits={best[1]}", best[0] / 1e3, lanes * k * (rb + 12), lanes=lanes,
+                   us_by_splits=res)
+
+
 if __name__ == "__main__":
     main()
