@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     __shared__ long long w_sel[S3_WARPS];
     __shared__ int band_pos[S3_BAND_CAP];
     uint32_t* lkey = reinterpret_cast<uint32_t*>(dyn_smem);
+    int32_t* lpos = reinterpret_cast<int32_t*>(dyn_smem + (size_t)S3_LIST_CAP * 4);  // merged path only
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t li = blockIdx.x;
     const int64_t n = n_cand[li];
@@ -236,6 +237,87 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     s3_find_bin(S, S.hist, S3_BINS, kk);
     const int bstar = S.bstar;
     const long long need_in_bucket = kk - S.above;
+    bool fallback = bstar < 0;
+    double hb = 0.0, lb = 0.0;
+    const WarpRange4 wr(n, warp);
+    long long nsure = 0;
+    unsigned int nband_total = 0;
+    // Merged path: when the band [T - 2E, T + 2E] is narrower than half a bucket it lies in
+    // buckets bstar-1..bstar+1, so ONE pass (in warp ranges) gathers those buckets' members
+    // with their positions and counts the certainly-selected elements above them; T, the
+    // band and the remaining sure counts then come from the short list.
+    const bool merged = !fallback && 2.0 * E * inv <= 0.5;
+    if (merged) {
+        __shared__ long long w_list_sure[S3_WARPS];
+        if (lane == 0) w_list_sure[warp] = 0;
+        for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
+          float vv[S3_UW][4];
+#pragma unroll
+          for (int u = 0; u < S3_UW; ++u) load4s(sc, base0 + 128 * u + 4 * lane, wr.b, vec, vv[u]);
+#pragma unroll
+          for (int u = 0; u < S3_UW; ++u) {
+            const int64_t i = base0 + 128 * u + 4 * lane;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const bool in = i + e < wr.b;
+                const int b = in ? s3_bucket(vv[u][e], lo_f, inv_f) : -1;
+                nsure += __popc(__ballot_sync(KVT_FULL, b > bstar + 1));
+                const bool m = in && b >= bstar - 1 && b <= bstar + 1;
+                const unsigned ballot = __ballot_sync(KVT_FULL, m);
+                unsigned wb = 0;
+                if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
+                wb = __shfl_sync(KVT_FULL, wb, 0);
+                if (m) {
+                    const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
+                    if (slot < S3_LIST_CAP) {
+                        lkey[slot] = ord_key32(vv[u][e]);
+                        lpos[slot] = (int32_t)((i + e) | (b == bstar ? 0x40000000 : 0));
+                    }
+                }
+            }
+          }
+        }
+        __syncthreads();
+        const int ln = (int)S.list_n;
+        if (ln > S3_LIST_CAP) {
+            fallback = true;
+        } else {
+            // T = the need_in_bucket-th largest key among the bucket-bstar members
+            for (int j = tid; j < ln; j += S3_THREADS) {
+                if (!(lpos[j] & 0x40000000)) continue;
+                const uint32_t kj = lkey[j];
+                int gt = 0, eq = 0;
+                for (int f = 0; f < ln; ++f) {
+                    if (!(lpos[f] & 0x40000000)) continue;
+                    gt += lkey[f] > kj;
+                    eq += lkey[f] == kj;
+                }
+                if (gt < need_in_bucket && need_in_bucket <= gt + eq) S.prefix = kj;
+            }
+            if (tid == 0) S.list_n = 0;  // reused as the band counter
+            __syncthreads();
+            const double Tk = (double)key32_to_float((uint32_t)S.prefix);
+            hb = Tk + 2.0 * E;
+            lb = Tk - 2.0 * E;
+            // sure list members counted into their owner warp's range (WarpRange4 spans of
+            // `per` elements); band members appended
+            const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128;
+            for (int j = tid; j < ln; j += S3_THREADS) {
+                const double sv = (double)key32_to_float(lkey[j]);
+                const int pj = lpos[j] & 0x3fffffff;
+                if (sv > hb) {
+                    const int ow = (int)kvt::imin(S3_WARPS - 1, pj / per);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&w_list_sure[ow]), 1ull);
+                } else if (sv >= lb) {
+                    const unsigned slot = atomicAdd(&S.list_n, 1u);
+                    if (slot < S3_BAND_CAP) { S.band_t[slot] = tk[pj]; band_pos[slot] = pj; }
+                }
+            }
+            __syncthreads();
+            nsure += w_list_sure[warp];
+        }
+    }
+    if (!merged && !fallback) {
     // ---- 2. gather the k-th bucket (unordered) ----
     for (int64_t base0 = 0; base0 < n; base0 += (int64_t)S3_UB * 4 * S3_THREADS) {
       float vv[S3_UB][4];
@@ -260,11 +342,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
       }
     }
     __syncthreads();
-    bool fallback = bstar < 0 || S.list_n > S3_LIST_CAP;
-    double hb = 0.0, lb = 0.0;
-    const WarpRange4 wr(n, warp);
-    long long nsure = 0;
-    unsigned int nband_total = 0;
+    fallback = S.list_n > S3_LIST_CAP;
     if (!fallback) {
         const uint32_t T32 = s3_list_select(S, lkey, (int)S.list_n, need_in_bucket);
         const double Tk = (double)key32_to_float(T32);
@@ -298,6 +376,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             }
           }
         }
+    }
+    }
+    if (!fallback) {
         if (lane == 0) w_sel[warp] = nsure;
         __syncthreads();
         nband_total = S.list_n;
@@ -567,7 +648,7 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
                           int64_t run_stride, int32_t* n_runs, cudaStream_t st) {
     const int row_b = RowLd<T>::row_bytes(d);
     const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
-    const size_t smem = (size_t)S3_LIST_CAP * 4;
+    const size_t smem = (size_t)S3_LIST_CAP * 8;  // list keys + positions
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(topk_select3_kernel<QT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
