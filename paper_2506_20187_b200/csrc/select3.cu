@@ -419,6 +419,21 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         __syncthreads();
         long long pos = 0;
         for (int w = 0; w < warp; ++w) pos += w_sel[w];
+        // run heads from the candidate stream (tokens ascending): a selected element is a head
+        // unless its stream predecessor is selected and holds the previous token.  Flags go to
+        // shared memory by output position (the list area is free now).
+        unsigned char* hflag = dyn_smem;
+        const bool runs_fused = run_start != nullptr && kk <= (int64_t)S3_LIST_CAP * 8;
+        bool carry_m = false;
+        int carry_t = 0;
+        if (wr.a > 0 && wr.a < wr.b) {
+            const double sv = (double)sc[wr.a - 1];
+            carry_t = tk[wr.a - 1];
+            if (sv > hb) carry_m = true;
+            else if (sv >= lb)
+                for (int j = 0; j < (int)nband_total; ++j)
+                    if (band_pos[j] == (int)(wr.a - 1)) { carry_m = S.band_sel[j] != 0; break; }
+        }
         for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
           float vv[S3_UW][4];
           int tt[S3_UW][4];
@@ -457,9 +472,23 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             }
             const int inc = warp_incl_scan(cnt, lane);
             long long p = pos + inc - cnt;
+            // predecessor of element e = 0: lane - 1's last element, or the carry
+            bool pm = __shfl_up_sync(KVT_FULL, m[3], 1);
+            int pt = __shfl_up_sync(KVT_FULL, tt[u][3], 1);
+            if (lane == 0) { pm = carry_m; pt = carry_t; }
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (m[e]) { otok[p] = tt[u][e]; osc[p] = scr[e]; ++p; }
+            for (int e = 0; e < 4; ++e) {
+                if (m[e]) {
+                    otok[p] = tt[u][e];
+                    osc[p] = scr[e];
+                    if (runs_fused) hflag[p] = !(pm && pt == tt[u][e] - 1);
+                    ++p;
+                }
+                pm = m[e];
+                pt = tt[u][e];
+            }
+            carry_m = __shfl_sync(KVT_FULL, m[3], 31);
+            carry_t = __shfl_sync(KVT_FULL, tt[u][3], 31);
             pos += __shfl_sync(KVT_FULL, inc, 31);
           }
         }
@@ -569,6 +598,49 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     }
     if (tid == 0) n_sel[li] = (int32_t)kk;
     if (!run_start) return;
+    if (!fallback && kk <= (int64_t)S3_LIST_CAP * 8) {
+        // ---- 5. runs from the head flags (shared memory): count, block prefix, write ----
+        __syncthreads();
+        const unsigned char* hflag = dyn_smem;
+        const long long per_w = ((kk + S3_WARPS - 1) / S3_WARPS + 31) / 32 * 32;
+        const long long pa = kvt::imin(kk, warp * per_w), pb = kvt::imin(kk, pa + per_w);
+        long long nh = 0;
+        for (long long p = pa + lane; p - lane < pb; p += 32)
+            nh += __popc(__ballot_sync(KVT_FULL, p < pb && hflag[p]));
+        __syncthreads();
+        if (lane == 0) w_sel[warp] = nh;
+        __syncthreads();
+        long long r0 = 0, tot_h = 0;
+        for (int w = 0; w < S3_WARPS; ++w) {
+            if (w < warp) r0 += w_sel[w];
+            tot_h += w_sel[w];
+        }
+        int32_t* rs = run_start + li * run_stride;
+        int32_t* rl = run_len + li * run_stride;
+        const unsigned le_mask = (2u << lane) - 1u;
+        for (long long p = pa + lane; p - lane < pb; p += 32) {
+            const bool h = p < pb && hflag[p];
+            const unsigned hm = __ballot_sync(KVT_FULL, h);
+            if (h) {
+                const long long r = r0 + __popc(hm & le_mask) - 1;
+                rs[r] = otok[p];
+                rl[r] = (int32_t)p;  // start position; turned into a length below
+            }
+            r0 += __popc(hm);
+        }
+        __syncthreads();
+        const long long per_r = (tot_h + S3_THREADS - 1) / S3_THREADS;
+        const long long ra = kvt::imin(tot_h, tid * per_r), rb = kvt::imin(tot_h, ra + per_r);
+        int32_t nxt = rb < tot_h ? rl[rb] : (int32_t)kk;  // read before any length is written
+        __syncthreads();
+        for (long long r = rb - 1; r >= ra; --r) {
+            const int32_t st = rl[r];
+            rl[r] = nxt - st;
+            nxt = st;
+        }
+        if (tid == 0) n_runs[li] = (int32_t)tot_h;
+        return;
+    }
 
     // ---- 5. fused run scan (engine.py:176-183) over the k outputs, warp-cooperative ----
     // Warp w owns output positions [wa, wb); per 32-wide window a lane tests head (previous
