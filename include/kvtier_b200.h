@@ -227,6 +227,14 @@ KVT_API int kvt_runs_scan(const int32_t* sel_tok, const int32_t* n_sel, int64_t 
  * per-lane merge tickets are left at zero by every call).  The last split CTA of each lane
  * performs the log-sum-exp merge, so this is a single kernel launch. */
 KVT_API size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits);
+/* Each lane's merged softmax state after kvt_sparse_decode_attn: lse_out[2 i] = m (max selected
+ * score), lse_out[2 i + 1] = l = sum exp((s - m) logit_scale).  Device buffer, stream-ordered. */
+KVT_API int kvt_attn_lse(const void* ws, int64_t n_lanes, double* lse_out, void* stream);
+/* Config 5 (sequence sharding): merge all-gathered shard partials
+ * parts[p][lane] = (m, l, o[d]) (o normalised, f64) into out (f32 and/or f64) with the
+ * log-sum-exp weights w_p = l_p exp((m_p - max m) logit_scale); n_parts <= 64. */
+KVT_API int kvt_lse_merge(const double* parts, int n_parts, int64_t n_lanes, int d, double logit_scale, float* out,
+                          double* out64, void* stream);
 KVT_API int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride,
                            int d, const int32_t* sel_tok, const double* sel_score,
                            const int32_t* n_sel, int64_t sel_stride, double logit_scale, int splits,

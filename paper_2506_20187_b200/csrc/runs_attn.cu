@@ -123,7 +123,7 @@ __device__ __forceinline__ void attn_finish(double* __restrict__ part, int split
                                             double* __restrict__ out64, double scale) {
     __shared__ int s_last;
     __shared__ double s_scale[64];
-    __shared__ double s_den;
+    __shared__ double s_den, s_M;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -149,10 +149,15 @@ __device__ __forceinline__ void attn_finish(double* __restrict__ part, int split
         }
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(KVT_FULL, den, off);
-        if (threadIdx.x == 0) s_den = den;
+        if (threadIdx.x == 0) { s_den = den; s_M = M; }
     }
     __syncthreads();
     const double den = s_den;
+    if (threadIdx.x == 0) {  // per-lane (m, l) of the merged softmax, for cross-shard merges
+        double* lse = part - 2 * (int64_t)gridDim.y;
+        lse[2 * li] = s_M;
+        lse[2 * li + 1] = den;
+    }
     for (int j = threadIdx.x; j < d; j += blockDim.x) {
         double acc = 0.0;
         for (int s = 0; s < splits; ++s) acc += s_scale[s] * __ldcg(P + s * (d + 2) + 2 + j);
@@ -877,7 +882,66 @@ static inline size_t ticket_bytes(int64_t n_lanes) { return ((size_t)n_lanes * 4
 extern "C" size_t kvt_attn_workspace_bytes(int64_t n_lanes, int d, int splits) {
     if (splits < 1) splits = 1;
     if (splits > 64) splits = 64;
-    return ticket_bytes(n_lanes) + (size_t)n_lanes * (size_t)splits * (size_t)(d + 2) * sizeof(double);
+    return ticket_bytes(n_lanes) + (size_t)n_lanes * 2 * sizeof(double) +
+           (size_t)n_lanes * (size_t)splits * (size_t)(d + 2) * sizeof(double);
+}
+
+// After kvt_sparse_decode_attn, the workspace holds each lane's merged softmax state
+// (m = max selected score, l = sum_i exp((s_i - m) logit_scale)): the partial a
+// sequence shard contributes to the cross-rank log-sum-exp merge (kvt_lse_merge).
+extern "C" int kvt_attn_lse(const void* ws, int64_t n_lanes, double* lse_out, void* stream) {
+    if (!ws || !lse_out || n_lanes < 0) return KVT_ERR_ARG;
+    if (n_lanes == 0) return KVT_OK;
+    const cudaError_t e = cudaMemcpyAsync(lse_out, (const char*)ws + ticket_bytes(n_lanes),
+                                          (size_t)n_lanes * 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                          (cudaStream_t)stream);
+    return e == cudaSuccess ? KVT_OK : kvt_set_cuda_error(e);
+}
+
+// Cross-shard merge (config 5, after an all-gather): parts [P][n_lanes][d + 2] f64, each
+// (m, l, o[d]) with o the shard's normalised output; out = sum_p w_p l_p o_p / sum_p w_p l_p,
+// w_p = exp((m_p - max m) logit_scale); parts with l = 0 (no selected token) are skipped.
+__global__ void lse_merge_kernel(const double* __restrict__ parts, int P, int64_t n_lanes, int d, double scale,
+                                 float* __restrict__ out, double* __restrict__ out64) {
+    const int64_t li = blockIdx.x;
+    __shared__ double s_w[64];
+    __shared__ double s_den;
+    if (threadIdx.x < 32) {
+        double M = -INFINITY;
+        for (int p = threadIdx.x; p < P; p += 32) {
+            const double* r = parts + ((int64_t)p * n_lanes + li) * (d + 2);
+            if (r[1] > 0) M = fmax(M, r[0]);
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) M = fmax(M, __shfl_xor_sync(KVT_FULL, M, off));
+        double den = 0.0;
+        for (int p = threadIdx.x; p < P; p += 32) {
+            const double* r = parts + ((int64_t)p * n_lanes + li) * (d + 2);
+            const double w = r[1] > 0 ? exp((r[0] - M) * scale) * r[1] : 0.0;
+            s_w[p] = w;
+            den += w;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(KVT_FULL, den, off);
+        if (threadIdx.x == 0) s_den = den;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double acc = 0.0;
+        for (int p = 0; p < P; ++p) acc += s_w[p] * parts[((int64_t)p * n_lanes + li) * (d + 2) + 2 + j];
+        const double r = s_den > 0 ? acc / s_den : 0.0;
+        if (out) out[li * d + j] = (float)r;
+        if (out64) out64[li * d + j] = r;
+    }
+}
+
+extern "C" int kvt_lse_merge(const double* parts, int n_parts, int64_t n_lanes, int d, double logit_scale, float* out,
+                             double* out64, void* stream) {
+    if (!parts || (!out && !out64) || n_parts < 1 || n_parts > 64 || n_lanes < 0 || d < 1) return KVT_ERR_ARG;
+    if (n_lanes == 0) return KVT_OK;
+    lse_merge_kernel<<<(unsigned)n_lanes, 128, 0, (cudaStream_t)stream>>>(parts, n_parts, n_lanes, d, logit_scale, out,
+                                                                           out64);
+    return kvt_check_launch();
 }
 
 static inline int agroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <= 512 ? 4 : 0; }
@@ -946,7 +1010,7 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
     if (n_lanes > 65535) return KVT_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned int* tickets = (unsigned int*)ws;
-    double* part = (double*)((char*)ws + ticket_bytes(n_lanes));
+    double* part = (double*)((char*)ws + ticket_bytes(n_lanes)) + 2 * n_lanes;  // after the lse slots
     int rc;
     const int64_t kmax = sel_stride;
     if (splits <= 0) splits = ring_auto_splits(kmax, v_dtype);  // auto (the workspace must hold 64 splits)

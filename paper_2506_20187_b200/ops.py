@@ -352,9 +352,11 @@ def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition
 
 
 def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor,
-                       splits: int = 0, want_f64: bool = False, logit_scale: float | None = None):
+                       splits: int = 0, want_f64: bool = False, logit_scale: float | None = None,
+                       want_lse: bool = False):
     """softmax(sel_score * logit_scale) @ V[sel] (engine.py:145-154) -> out f32 [n_lanes, d] (and f64).
-    logit_scale defaults to 1/sqrt(d) (sel_score = raw dots from K4/K5); pass 1.0 for logits."""
+    logit_scale defaults to 1/sqrt(d) (sel_score = raw dots from K4/K5); pass 1.0 for logits.
+    want_lse: also return the lanes' merged softmax state (m, l) f64 [n_lanes, 2] (kvt_attn_lse)."""
     require_cuda(values)
     ls, d = _lanes(values)
     nl = values.shape[0]
@@ -372,6 +374,23 @@ def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: t
     L.check(L.kvt_sparse_decode_attn(values.data_ptr(), dtype_code(values), nl, ls, d, st.data_ptr(), ss.data_ptr(),
                                      n_sel.data_ptr(), sstride, float(logit_scale), splits, ws.data_ptr(),
                                      out.data_ptr(), _p(out64), _stream()), "sparse_decode_attn")
+    res = (out, out64) if want_f64 else (out,)
+    if want_lse:
+        lse = torch.empty((nl, 2), dtype=torch.float64, device=values.device)
+        L.check(L.kvt_attn_lse(ws.data_ptr(), nl, lse.data_ptr(), _stream()), "attn_lse")
+        res = res + (lse,)
+    return res if len(res) > 1 else res[0]
+
+
+def lse_merge(parts: torch.Tensor, logit_scale: float, want_f64: bool = False):
+    """Merge shard partials parts [P, n_lanes, d + 2] f64 = (m, l, o normalised) (kvt_lse_merge)."""
+    require_cuda(parts)
+    P, nl, d2 = parts.shape
+    parts = parts.contiguous().double()
+    out = torch.empty((nl, d2 - 2), dtype=torch.float32, device=parts.device)
+    out64 = torch.empty((nl, d2 - 2), dtype=torch.float64, device=parts.device) if want_f64 else None
+    L.check(L.kvt_lse_merge(parts.data_ptr(), P, nl, d2 - 2, float(logit_scale), out.data_ptr(), _p(out64),
+                            _stream()), "lse_merge")
     return (out, out64) if want_f64 else out
 
 

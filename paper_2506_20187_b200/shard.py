@@ -112,6 +112,83 @@ def global_topk_mask(scores: torch.Tensor, k: int, group=None) -> torch.Tensor:
     return gt | (eq & (eq_rank < take))
 
 
+# ---- config 5 on the GPU: exact sequence-sharded select + attend ------------------------------
+
+
+def radix_threshold(keys: torch.Tensor, valid: torch.Tensor, k: torch.Tensor, allreduce) -> tuple:
+    """Per-lane exact k-th largest of the orderable int64 keys [lanes, m] (valid mask) across
+    shards: 8 rounds, each one all-reduce of a [lanes, 256] digit histogram (the "global
+    threshold exchange").  Returns (T keys [lanes], remaining ties to take at T [lanes])."""
+    lanes = keys.shape[0]
+    dev = keys.device
+    prefix = torch.zeros(lanes, dtype=torch.int64, device=dev)
+    mask = torch.zeros(lanes, dtype=torch.int64, device=dev)
+    remaining = k.to(torch.int64).clone()
+    ar = torch.arange(256, device=dev)
+    for shift in range(56, -8, -8):
+        sel = valid & ((keys & mask[:, None]) == prefix[:, None])
+        digits = (keys >> shift) & 0xFF
+        hist = torch.zeros((lanes, 256), dtype=torch.int64, device=dev)
+        hist.scatter_add_(1, digits, sel.to(torch.int64))
+        hist = allreduce(hist)
+        h = hist.flip(1).cumsum(1)  # counts from the top digit down
+        idx = torch.searchsorted(h, remaining[:, None]).squeeze(1).clamp_max(255)
+        b = 255 - idx
+        above = torch.where(idx > 0, h.gather(1, (idx - 1).clamp_min(0)[:, None]).squeeze(1), torch.zeros_like(idx))
+        prefix = prefix | (b << shift)
+        mask = mask | (torch.full_like(mask, 0xFF) << shift)
+        remaining = remaining - above
+    del ar
+    return prefix, remaining
+
+
+def seq_shard_select_attend(q: torch.Tensor, keys, values, n_local: int, C: int, k: int, shard_rank: int,
+                            allreduce, allgather, decoder_bufs=None):
+    """One layer of config 5 on this rank's token shard (GPU kernels + two small collectives).
+
+    1. exact local top-min(k, n_local) of every lane with the fused kernels (canonical scores):
+       every token of the global top-k is in its own shard's top-k, so this loses nothing;
+    2. the global k-th score by `radix_threshold` over those candidates (ties at T go to the
+       lowest tokens, i.e. to lower shard ranks first: one all-gather of per-rank tie counts);
+    3. K7 over this rank's globally selected subset -> (m, l, o) per lane;
+    4. all-gather of (m, l, o) and the log-sum-exp merge kernel (kvt_lse_merge).
+    Returns (attention output f32 [lanes, d], this rank's selected local token ids as a list
+    of int32 tensors).  `allreduce(t)` sums over ranks, `allgather(t)` stacks rank tensors in
+    rank order (torch.distributed wrappers on real ranks; emulated in single-GPU tests)."""
+    from . import ops
+    lanes, d = q.shape
+    kk = min(k, n_local)
+    amax, amin = ops.abstract_build(keys, n_local, C, abs_dtype=torch.bfloat16)
+    ws = ops.LayerWorkspace(lanes, n_local, ops.n_grid_leaves(n_local, C), d, q.device)
+    out = {"sel_tok": torch.empty((lanes, max(kk, 1)), dtype=torch.int32, device=q.device),
+           "sel_score": torch.empty((lanes, max(kk, 1)), dtype=torch.float64, device=q.device),
+           "n_sel": torch.empty(lanes, dtype=torch.int32, device=q.device),
+           "out": torch.empty((lanes, d), dtype=torch.float32, device=q.device)}
+    ops.select_attend(q, keys, values, amax, amin, n_local, kk, C, ws, out, exact_scores=True)
+    sc = out["sel_score"][:, :kk]
+    keys64 = _ord_keys(sc)
+    valid = torch.ones_like(keys64, dtype=torch.bool)
+    T, take = radix_threshold(keys64, valid, torch.full((lanes,), k, device=q.device), allreduce)
+    flip = torch.tensor(_MIN64, dtype=torch.int64, device=q.device)
+    gt = (keys64 ^ flip) > (T ^ flip)[:, None]
+    eq = keys64 == T[:, None]
+    eq_all = allgather(eq.sum(1))  # [world, lanes]
+    before = eq_all[:shard_rank].sum(0) if shard_rank > 0 else torch.zeros(lanes, dtype=torch.int64, device=q.device)
+    my_take = (take - before).clamp(min=0)
+    eq_rank = torch.cumsum(eq.to(torch.int64), 1) - 1
+    mine = gt | (eq & (eq_rank < my_take[:, None]))
+    # compact this rank's subset (token order is preserved: sel_tok is ascending)
+    n_mine = mine.sum(1).to(torch.int32)
+    order = torch.argsort((~mine).to(torch.int8), dim=1, stable=True)
+    st = torch.gather(out["sel_tok"][:, :kk], 1, order).contiguous()
+    ss = torch.gather(sc, 1, order).contiguous()
+    o, lse = ops.sparse_decode_attn(values, st, ss, n_mine, want_lse=True)
+    part = torch.cat([lse, o.double()], dim=1)  # [lanes, d + 2]
+    parts = allgather(part)  # [world, lanes, d + 2]
+    res = ops.lse_merge(parts, 1.0 / (d ** 0.5))
+    return res, [st[i, :int(n_mine[i])] for i in range(lanes)]
+
+
 def max_over_ranks(x: float, device=None, group=None) -> float:
     """Max of a per-rank scalar (multi-GPU timing is the slowest rank)."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:

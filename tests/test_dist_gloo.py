@@ -78,6 +78,24 @@ def _worker(rank, world, port, ret):
             allsel = sorted(x for g in gathered for x in g)
             ref = O.topk(full_scores, kk).tolist()
             ok_topk &= allsel == ref
+    # --- the batched per-lane threshold exchange used by the GPU config-5 path ---
+    from paper_2506_20187_b200.shard import _ord_keys, radix_threshold
+    rng3 = np.random.default_rng(7)
+    scores = np.round(rng3.normal(size=(5, 600)), 2)  # ties
+    t0, t1 = token_block(600, world, rank, align=1)
+    keys = _ord_keys(torch.tensor(scores[:, t0:t1]))
+    kv = torch.tensor([1, 60, 300, 599, 600])
+
+    def allreduce(x):
+        dist.all_reduce(x)
+        return x
+
+    T, take = radix_threshold(keys, torch.ones_like(keys, dtype=torch.bool), kv, allreduce)
+    for i in range(5):
+        kth_score = scores[i, O.topk(scores[i], int(kv[i]))].min()  # O.topk: the set, token order
+        ok_topk &= int(T[i]) == int(_ord_keys(torch.tensor([kth_score]))[0])
+        n_gt = int((scores[i] > kth_score).sum())
+        ok_topk &= int(take[i]) == int(kv[i]) - n_gt
     if rank == 0:
         ret.put((err_seq, err_lane, t, ok_topk))
     dist.destroy_process_group()
