@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
     const float* __restrict__ q, int64_t n, int C, int n_lanes, const __nv_bfloat16* __restrict__ amax,
     const __nv_bfloat16* __restrict__ amin, int64_t abs_lane_stride, const float* __restrict__ mag,
     double* __restrict__ U, double* __restrict__ L, double* __restrict__ A, int64_t bnd_stride, int stages) {
+    pdl_entry();
     constexpr int d = 128 * G;
     constexpr int tile = 2 * 64 * d * 2;  // 64 max rows then 64 min rows (bf16)
     extern __shared__ __align__(128) unsigned char smem[];
@@ -224,9 +225,9 @@ extern "C" int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int
             cudaFuncSetAttribute(bounds_fast_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
             per_sm[GG] = resident_per_sm(bounds_fast_kernel<GG>, BF_THREADS, smem, 1);                                \
         }                                                                                                             \
-        bounds_fast_kernel<GG><<<sms * per_sm[GG], BF_THREADS, smem, st>>>(                                            \
-            q, n, C, (int)n_lanes, (const __nv_bfloat16*)amax, (const __nv_bfloat16*)amin, abs_lane_stride, mag, U, L, \
-            A, bnd_stride, stages);                                                                                   \
+        launch_pdl(bounds_fast_kernel<GG>, dim3(sms * per_sm[GG]), dim3(BF_THREADS), smem, st, q, n, C,             \
+                   (int)n_lanes, (const __nv_bfloat16*)amax, (const __nv_bfloat16*)amin, abs_lane_stride, mag, U, L, \
+                   A, bnd_stride, stages);                                                                        \
     } while (0)
     if (G == 1) KVT_BF(1);
     else KVT_BF(2);

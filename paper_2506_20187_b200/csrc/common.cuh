@@ -359,6 +359,30 @@ int kvt_abstract_build_i4(const void* keys, int64_t n_lanes, int64_t lane_stride
                           int64_t c_begin, int64_t c_end, void* amax, void* amin, int64_t abs_lane_stride, bool bf,
                           cudaStream_t st);
 
+// Programmatic dependent launch (decode-path kernels): a kernel launched with
+// launch_pdl may start while its predecessor drains; pdl_entry() -- the first statement of
+// every such kernel -- waits for the predecessor grid (and its memory) before anything is
+// read, then lets the successor launch.  Launch latency overlaps the predecessor's tail.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Resident CTAs per SM of `kernel` at this block size / dynamic smem (occupancy API), so
 // persistent grids are exactly one wave.  Falls back to `fallback` on error.
 template <typename K>

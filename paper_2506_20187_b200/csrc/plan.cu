@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
     int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
     int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals, int stage_cap,
     const double* __restrict__ A, double* __restrict__ err, double err_factor) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char plan_smem[];
     uint64_t* kst = reinterpret_cast<uint64_t*>(plan_smem);  // staged keys (if they fit)
     __shared__ unsigned long long hist[256];
@@ -232,8 +233,8 @@ extern "C" int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t
     }
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
     const int cap = (int)kvt::imin(max_leaves, 16384);
-    plan_kernel<<<(unsigned)n_lanes, PLAN_THREADS, (size_t)cap * 8, (cudaStream_t)stream>>>(
-        n, C, leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand,
-        cand_leaf, evals, cap, A, err, f32_err_factor(d));
+    launch_pdl(plan_kernel, dim3((unsigned)n_lanes), dim3(PLAN_THREADS), (size_t)cap * 8, (cudaStream_t)stream, n, C,
+               leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand, cand_leaf,
+               evals, cap, A, err, f32_err_factor(d));
     return kvt_check_launch();
 }

@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_gather_kernel(
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
     double* __restrict__ out64, double scale) {
+    pdl_entry();
     // Each warp runs its own online softmax over rows warp*RPW + sub + u*STEP + it*U*STEP
     // (no block barrier before the first row load); the next iteration's token ids and
     // scores are fetched while the current rows are in flight.  Warps are combined in
@@ -726,6 +727,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
     double* __restrict__ out64, double scale) {
+    pdl_entry();
     constexpr int LPR = F::LPR, NE = F::NE, RPW = 32 / LPR, RB = F::row_bytes(), SLOT = RPW * RB;
     extern __shared__ __align__(16) unsigned char ring_smem[];
     __shared__ double red_m[ATTN_WARPS];
@@ -840,7 +842,7 @@ static int launch_ring(const void* values, int64_t n_lanes, int64_t lane_stride_
         configured = smem;
     }
     dim3 grid(splits, (unsigned)n_lanes);
-    attn_ring_kernel<F, S><<<grid, ATTN_THREADS, smem, st>>>((const unsigned char*)values, lane_stride_b, d, sel_tok,
+    launch_pdl(attn_ring_kernel<F, S>, grid, dim3(ATTN_THREADS), smem, st, (const unsigned char*)values, lane_stride_b, d, sel_tok,
                                                             sel_score, n_sel, sel_stride, splits, R, part, tickets,
                                                             out, out64, scale);
     return kvt_check_launch();
@@ -852,7 +854,7 @@ static int launch_gather(const void* values, int64_t n_lanes, int64_t lane_strid
                          double* part, unsigned int* tickets, float* out, double* out64, double scale,
                          cudaStream_t st) {
     dim3 grid(splits, (unsigned)n_lanes);
-    attn_gather_kernel<F, U><<<grid, ATTN_THREADS, 0, st>>>((const unsigned char*)values, lane_stride_b, d, sel_tok,
+    launch_pdl(attn_gather_kernel<F, U>, grid, dim3(ATTN_THREADS), 0, st, (const unsigned char*)values, lane_stride_b, d, sel_tok,
                                                                sel_score, n_sel, sel_stride, splits, R, part, tickets,
                                                                out, out64, scale);
     return kvt_check_launch();

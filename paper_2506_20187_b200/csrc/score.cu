@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     int n_lanes, const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items,
     int64_t n_implicit, double* __restrict__ out_score, float* __restrict__ out32, int32_t* __restrict__ out_tok,
     int64_t out_stride, int stages, int tile_bytes, int scaled) {
+    pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ long long scan_sh[33];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * tile_bytes);
@@ -366,8 +367,7 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
     if (!per_sm) per_sm = resident_per_sm(score_tma_kernel<QT, T, G, IMPL, AccT>, TS_THREADS, smem,
                                           smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1));
     const int grid = sm_count() * per_sm;
-    score_tma_kernel<QT, T, G, IMPL, AccT><<<grid, TS_THREADS, smem, st>>>(
-        (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, (int)n_lanes, items, item_stride, n_items, n_impl,
+    launch_pdl(score_tma_kernel<QT, T, G, IMPL, AccT>, dim3(grid), dim3(TS_THREADS), smem, st, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, (int)n_lanes, items, item_stride, n_items, n_impl,
         os, os32, ot, ostr, stages, tile, scaled);
     return kvt_check_launch();
 }

@@ -48,6 +48,7 @@ __host__ __device__ __forceinline__ int qprep_bytes(int d) { return (d / 32) * 1
 // b0 byte j = qi_p[32g + 8i + 2j], b1 byte j = qi_p[32g + 8i + 2j + 1] (the nibble order).
 template <typename QT>
 __global__ void qprep_kernel(const QT* __restrict__ q, int64_t n_lanes, int d, unsigned char* __restrict__ out) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const int64_t li = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (li >= n_lanes) return;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
     int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
     float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err) {
+    pdl_entry();
     constexpr int d = 128 * R;
     constexpr int G = 4 * R;
     constexpr int row_b = d / 2 + G * 4;
@@ -355,8 +357,11 @@ extern "C" int kvt_i4_qprep(const void* q, int q_dtype, int64_t n_lanes, int d, 
     cudaStream_t st = (cudaStream_t)stream;
     const int wpb = 8;
     const unsigned grid = (unsigned)((n_lanes + wpb - 1) / wpb);
-    if (q_dtype == KVT_F32) qprep_kernel<float><<<grid, 32 * wpb, 0, st>>>((const float*)q, n_lanes, d, (unsigned char*)out);
-    else if (q_dtype == KVT_F64) qprep_kernel<double><<<grid, 32 * wpb, 0, st>>>((const double*)q, n_lanes, d, (unsigned char*)out);
+    if (q_dtype == KVT_F32)
+        launch_pdl(qprep_kernel<float>, dim3(grid), dim3(32 * wpb), 0, st, (const float*)q, n_lanes, d, (unsigned char*)out);
+    else if (q_dtype == KVT_F64)
+        launch_pdl(qprep_kernel<double>, dim3(grid), dim3(32 * wpb), 0, st, (const double*)q, n_lanes, d,
+                   (unsigned char*)out);
     else return KVT_ERR_DTYPE;
     return kvt_check_launch();
 }
@@ -379,8 +384,7 @@ static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const i
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static int per_sm = 0;
     if (!per_sm) per_sm = resident_per_sm(score_i4mma_kernel<R>, QM_THREADS, smem, 4);
-    score_i4mma_kernel<R><<<sms * per_sm, QM_THREADS, smem, st>>>(
-        (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
+    launch_pdl(score_i4mma_kernel<R>, dim3(sms * per_sm), dim3(QM_THREADS), smem, st, (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
         ostr, err);
     return kvt_check_launch();
 }

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, double* __restrict__ scratch,
     int32_t* __restrict__ sel_tok, double* __restrict__ sel_score, int64_t sel_stride, int32_t* __restrict__ n_sel,
     int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ S3Shared S;
     __shared__ long long w_sel[S3_WARPS];
@@ -728,8 +729,7 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = true;
     }
-    topk_select3_kernel<QT, T><<<(unsigned)n_lanes, S3_THREADS, smem, st>>>(
-        cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
+    launch_pdl(topk_select3_kernel<QT, T>, dim3((unsigned)n_lanes), dim3(S3_THREADS), smem, st, cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
         sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs);
     return kvt_check_launch();
 }
