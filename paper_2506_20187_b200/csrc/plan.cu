@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
             unsigned long long inc = warp_incl_scan(loc, lane);
             const unsigned long long exc = inc - loc;
             const unsigned long long rem = (unsigned long long)s_remaining;
+            __syncwarp();  // all lanes have read s_remaining before one lane rewrites it
             const bool mine = exc < rem && rem <= inc;
             if (mine) {
                 unsigned long long run = exc;

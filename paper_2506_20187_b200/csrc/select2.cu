@@ -90,6 +90,7 @@ __device__ __forceinline__ void radix_pass(cg::cluster_group& cluster, S2Shared&
         const unsigned int inc = warp_incl_scan(lsum, lane);
         const unsigned int exc = inc - lsum;
         const unsigned int rem = S.remaining;
+        __syncwarp();  // every lane has read S.remaining before it is rewritten
         if (exc < rem && rem <= inc) {
             unsigned int run = exc;
             for (int i = 0; i < 8; ++i) {

@@ -116,6 +116,7 @@ __device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* 
 #pragma unroll
             for (int i = 0; i < 8; ++i) { loc[i] = S.rh[255 - 8 * lane - i]; ls += loc[i]; }
             const unsigned inc = warp_incl_scan(ls, lane), exc = inc - ls, rem = S.remaining;
+            __syncwarp();  // every lane has read S.remaining before it is rewritten
             if (exc < rem && rem <= inc) {
                 unsigned run = exc;
                 for (int i = 0; i < 8; ++i) {
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
                 }
                 if (gt < need_in_bucket && need_in_bucket <= gt + eq) S.prefix = kj;
             }
+            __syncthreads();  // every thread has read list_n before it is reset
             if (tid == 0) S.list_n = 0;  // reused as the band counter
             __syncthreads();
             const double Tk = (double)key32_to_float((uint32_t)S.prefix);
@@ -541,6 +543,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
 #pragma unroll
                 for (int i = 0; i < 8; ++i) { loc[i] = S.rh[255 - 8 * lane - i]; ls += loc[i]; }
                 const unsigned inc = warp_incl_scan(ls, lane), exc = inc - ls, rem = S.remaining;
+            __syncwarp();  // every lane has read S.remaining before it is rewritten
                 if (exc < rem && rem <= inc) {
                     unsigned run = exc;
                     for (int i = 0; i < 8; ++i) {

@@ -1,0 +1,49 @@
+"""Small end-to-end runs of every decode-path kernel, for compute-sanitizer (memcheck,
+racecheck, synccheck):  compute-sanitizer --tool racecheck python tools/sanitize.py"""
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2506_20187_b200 import ops, tier  # noqa: E402
+from paper_2506_20187_b200.decode import SparseDecoder  # noqa: E402
+
+torch.manual_seed(0)
+for dt in (ops.I4, torch.bfloat16):
+    dec = SparseDecoder(3, 1, 4, 128, 2048, dtype=dt, device="cuda")
+    k = torch.randn((dec.lanes, 2048, 128), device="cuda", dtype=torch.bfloat16)
+    v = torch.randn_like(k)
+    for l in range(3):
+        dec.load_layer(l, k, v)
+    dec.set_length(2048)
+    q = torch.randn((3, dec.lanes, 128), device="cuda")
+    out = dec.step(q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+# few lanes, long context: the cluster select path (select2.cu)
+kt = torch.randn((2, 16384, 128), device="cuda", dtype=torch.bfloat16)
+amax, amin = ops.abstract_build(kt, 16384, 64)
+ws = ops.LayerWorkspace(2, 16384, ops.n_grid_leaves(16384, 64), 128, kt.device)
+kk = math.ceil(0.1 * 16384)
+o = {"sel_tok": torch.empty((2, kk), dtype=torch.int32, device="cuda"),
+     "sel_score": torch.empty((2, kk), dtype=torch.float64, device="cuda"),
+     "n_sel": torch.empty(2, dtype=torch.int32, device="cuda"),
+     "run_start": torch.empty((2, kk), dtype=torch.int32, device="cuda"),
+     "run_len": torch.empty((2, kk), dtype=torch.int32, device="cuda"),
+     "n_runs": torch.empty(2, dtype=torch.int32, device="cuda"),
+     "out": torch.empty((2, 128), dtype=torch.float32, device="cuda")}
+ops.select_attend(torch.randn((2, 128), device="cuda"), kt, kt, amax, amin, 16384, kk, 64, ws, o)
+torch.cuda.synchronize()
+# codec round trip + attention helpers
+x = torch.randn((4, 777, 128), device="cuda", dtype=torch.bfloat16)
+rec = ops.I4KV.empty(4, 777, 128, "cuda")
+ops.kv_quant(x, rec)
+y = torch.empty_like(x)
+tier.kv_dequant(rec, y)
+parts = torch.randn((3, 4, 130), device="cuda", dtype=torch.float64)
+parts[:, :, 1] = parts[:, :, 1].abs()
+ops.lse_merge(parts, 0.1)
+torch.cuda.synchronize()
+print("sanitize run ok")
