@@ -273,6 +273,10 @@ typedef struct {
     const float* abs_mag;       /* [n_lanes][d] per-lane max |key| over all chunks, or NULL.  With bf16
                                    abstracts, f32 q, a uniform grid and d = 128/256 it selects the
                                    directed-rounding f32 bounds (kvt_chunk_bounds_fast) */
+    int kv_group;               /* GQA: query lanes per KV lane (0/1 = none).  Query lane i reads keys,
+                                   values, abstracts and abs_mag of KV lane i / kv_group; keys/values/
+                                   amax/amin/abs_mag then hold n_lanes / kv_group lanes.  Decode path
+                                   (abs_mag, bf16 abstracts, f32 q) only */
 } kvt_layer_args;
 
 /* K3 for the decode path (bounds_fast.cu): sound f32 bounds of raw dots over bf16 abstracts on a
@@ -284,6 +288,10 @@ KVT_API int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int64_
                                   const void* amin, int64_t abs_lane_stride, const float* mag, double* U,
                                   double* L, double* A, int64_t bnd_stride, void* stream);
 
+/* Workspace of kvt_select_attend: zero-filled once by the caller and then reusable by every
+ * layer with the same n_lanes and d, whatever its chunk size (size it for the largest
+ * max_leaves).  Its first region holds the attention merge tickets, which every call leaves
+ * at zero. */
 KVT_API size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d);
 KVT_API int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream);
 

@@ -71,6 +71,9 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     Carve c(base);
     LayerWs w;
     const int64_t item_cap = (n + ITEM_TOKENS - 1) / ITEM_TOKENS + max_leaves;
+    // the attention region goes first: its merge tickets must stay zero between calls, and
+    // its offset must not depend on max_leaves, which changes with the layer's chunk size
+    w.attn_part = c.take<char>(kvt_attn_workspace_bytes(n_lanes, d, MAX_SPLITS));  // tickets + lse + partials
     w.U = c.take<double>((size_t)(n_lanes * max_leaves));
     w.L = c.take<double>((size_t)(n_lanes * max_leaves));
     w.A = c.take<double>((size_t)(n_lanes * max_leaves));
@@ -81,7 +84,6 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     w.cand_score = c.take<double>((size_t)(n_lanes * n));
     w.cand_tok = c.take<int32_t>((size_t)(n_lanes * n));
     w.cs32 = c.take<float>((size_t)(n_lanes * n));
-    w.attn_part = c.take<char>(kvt_attn_workspace_bytes(n_lanes, d, MAX_SPLITS));  // tickets + partials
     w.qprep = c.take<unsigned char>(kvt_i4_qprep_bytes(n_lanes, d));              // INT4 query digits
     w.bytes = c.used;
     return w;
@@ -103,8 +105,18 @@ extern "C" size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t 
     return carve(nullptr, n_lanes, n, max_leaves, d).bytes;
 }
 
+int& kv_group_tls() {
+    static thread_local int g = 1;
+    return g;
+}
+
 extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream) {
     if (!a || !ws) return KVT_ERR_ARG;
+    const int kvg = a->kv_group > 1 ? a->kv_group : 1;
+    if (kvg > 1 && (a->n_lanes % kvg || !a->abs_mag || a->abs_dtype != KVT_BF16 || a->q_dtype != KVT_F32 ||
+                    a->leaf_start || a->exact_scores || !kvt_fast_ok(a->key_dtype, a->d)))
+        return KVT_ERR_ARG;  // GQA sharing runs on the decode path's kernels only
+    KvGroupScope group_scope(kvg);
     if (a->k < 0 || a->k > a->n) return KVT_ERR_K;
     if (a->n_lanes <= 0 || a->n <= 0) return a->n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
     if (!a->leaf_start && a->C < 1) return KVT_ERR_ARG;

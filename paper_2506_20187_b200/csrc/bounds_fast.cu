@@ -76,7 +76,7 @@ template <int G>  // G = d / 128
 __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
     const float* __restrict__ q, int64_t n, int C, int n_lanes, const __nv_bfloat16* __restrict__ amax,
     const __nv_bfloat16* __restrict__ amin, int64_t abs_lane_stride, const float* __restrict__ mag,
-    double* __restrict__ U, double* __restrict__ L, double* __restrict__ A, int64_t bnd_stride, int stages) {
+    double* __restrict__ U, double* __restrict__ L, double* __restrict__ A, int64_t bnd_stride, int stages, int kvg) {
     pdl_entry();
     constexpr int d = 128 * G;
     constexpr int tile = 2 * 64 * d * 2;  // 64 max rows then 64 min rows (bf16)
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
                 const uint32_t half = (uint32_t)(cnt * d * 2);
                 mbar_arrive_expect_tx(&full[s], 2 * half);
                 unsigned char* dst = smem + (size_t)s * tile;
-                bulk_g2s(dst, amax + li * abs_lane_stride + c0 * d, half, &full[s]);
-                bulk_g2s(dst + tile / 2, amin + li * abs_lane_stride + c0 * d, half, &full[s]);
+                bulk_g2s(dst, amax + (li / kvg) * abs_lane_stride + c0 * d, half, &full[s]);
+                bulk_g2s(dst + tile / 2, amin + (li / kvg) * abs_lane_stride + c0 * d, half, &full[s]);
                 c0 += 64;
                 if (c0 >= per_lane * 64) { c0 = 0; ++li; }
             }
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
 #pragma unroll
             for (int r = 0; r < G; ++r) {
                 const float4 qv = *reinterpret_cast<const float4*>(q + li * d + 4 * (lane + 32 * r));
-                const float4 mv = *reinterpret_cast<const float4*>(mag + li * d + 4 * (lane + 32 * r));
+                const float4 mv = *reinterpret_cast<const float4*>(mag + (li / kvg) * d + 4 * (lane + 32 * r));
                 qp[r][0] = pk2(fmaxf(qv.x, 0.f), fmaxf(qv.y, 0.f));
                 qp[r][1] = pk2(fmaxf(qv.z, 0.f), fmaxf(qv.w, 0.f));
                 qn[r][0] = pk2(fminf(qv.x, 0.f), fminf(qv.y, 0.f));
@@ -227,7 +227,7 @@ extern "C" int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int
         }                                                                                                             \
         launch_pdl(bounds_fast_kernel<GG>, dim3(sms * per_sm[GG]), dim3(BF_THREADS), smem, st, q, n, C,             \
                    (int)n_lanes, (const __nv_bfloat16*)amax, (const __nv_bfloat16*)amin, abs_lane_stride, mag, U, L, \
-                   A, bnd_stride, stages);                                                                        \
+                   A, bnd_stride, stages, kv_group_current());                                                                        \
     } while (0)
     if (G == 1) KVT_BF(1);
     else KVT_BF(2);

@@ -359,6 +359,17 @@ int kvt_abstract_build_i4(const void* keys, int64_t n_lanes, int64_t lane_stride
                           int64_t c_begin, int64_t c_end, void* amax, void* amin, int64_t abs_lane_stride, bool bf,
                           cudaStream_t st);
 
+// GQA: query lane i reads the K/V/abstracts of lane i / kv_group (LLaMA-3 layout: the query
+// heads of one KV head are adjacent).  kvt_select_attend sets the group for the launches it
+// makes through this host thread-local scope; the standalone entry points run with 1.
+int& kv_group_tls();
+struct KvGroupScope {
+    int saved;
+    explicit KvGroupScope(int g) : saved(kv_group_tls()) { kv_group_tls() = g > 1 ? g : 1; }
+    ~KvGroupScope() { kv_group_tls() = saved; }
+};
+inline int kv_group_current() { return kv_group_tls(); }
+
 // Programmatic dependent launch (decode-path kernels): a kernel launched with
 // launch_pdl may start while its predecessor drains; pdl_entry() -- the first statement of
 // every such kernel -- waits for the predecessor grid (and its memory) before anything is

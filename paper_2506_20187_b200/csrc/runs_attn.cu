@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_gather_kernel(
     const unsigned char* __restrict__ values, int64_t lane_stride_b, int d, const int32_t* __restrict__ sel_tok,
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
-    double* __restrict__ out64, double scale) {
+    double* __restrict__ out64, double scale, int kvg) {
     pdl_entry();
     // Each warp runs its own online softmax over rows warp*RPW + sub + u*STEP + it*U*STEP
     // (no block barrier before the first row load); the next iteration's token ids and
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_gather_kernel(
     const int32_t* tok = sel_tok + li * sel_stride + a;
     const double* sc = sel_score + li * sel_stride + a;
     const int sub = lane / LPR, grp = lane % LPR;
-    const unsigned char* base = values + li * lane_stride_b;
+    const unsigned char* base = values + (li / kvg) * lane_stride_b;
     const double sl2 = scale * 1.4426950408889634;
 
     uint64_t o2[NE / 2];
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     const unsigned char* __restrict__ values, int64_t lane_stride_b, int d, const int32_t* __restrict__ sel_tok,
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
-    double* __restrict__ out64, double scale) {
+    double* __restrict__ out64, double scale, int kvg) {
     pdl_entry();
     constexpr int LPR = F::LPR, NE = F::NE, RPW = 32 / LPR, RB = F::row_bytes(), SLOT = RPW * RB;
     extern __shared__ __align__(16) unsigned char ring_smem[];
@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     for (int i = wa + lane; i < wb; i += 32) w_s[i] = exp2f((float)((sc[i] - m) * sl2));  // once per row (L2 hit)
     __syncwarp();
     const int sub = lane / LPR, grp = lane % LPR;
-    const unsigned char* base = values + li * lane_stride_b;
+    const unsigned char* base = values + (li / kvg) * lane_stride_b;
     const uint32_t ring_a = (uint32_t)__cvta_generic_to_shared(ring);
     const int nslots = (wb - wa + RPW - 1) / RPW;
     uint64_t o2[NE / 2];
@@ -844,7 +844,7 @@ static int launch_ring(const void* values, int64_t n_lanes, int64_t lane_stride_
     dim3 grid(splits, (unsigned)n_lanes);
     launch_pdl(attn_ring_kernel<F, S>, grid, dim3(ATTN_THREADS), smem, st, (const unsigned char*)values, lane_stride_b, d, sel_tok,
                                                             sel_score, n_sel, sel_stride, splits, R, part, tickets,
-                                                            out, out64, scale);
+                                                            out, out64, scale, kv_group_current());
     return kvt_check_launch();
 }
 
@@ -856,7 +856,7 @@ static int launch_gather(const void* values, int64_t n_lanes, int64_t lane_strid
     dim3 grid(splits, (unsigned)n_lanes);
     launch_pdl(attn_gather_kernel<F, U>, grid, dim3(ATTN_THREADS), 0, st, (const unsigned char*)values, lane_stride_b, d, sel_tok,
                                                                sel_score, n_sel, sel_stride, splits, R, part, tickets,
-                                                               out, out64, scale);
+                                                               out, out64, scale, kv_group_current());
     return kvt_check_launch();
 }
 

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
     const QT* __restrict__ q, const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d,
     int n_lanes, const int32_t* __restrict__ items, int64_t item_stride, const int32_t* __restrict__ n_items,
     int64_t n_implicit, double* __restrict__ out_score, float* __restrict__ out32, int32_t* __restrict__ out_tok,
-    int64_t out_stride, int stages, int tile_bytes, int scaled) {
+    int64_t out_stride, int stages, int tile_bytes, int scaled, int kvg) {
     pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ long long scan_sh[33];
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
                     const uint32_t bytes = (uint32_t)(cnt * row_b);
                     meta[s] = make_int4(cur, (int)t0, (int)cnt, pos0);
                     mbar_arrive_expect_tx(&full[s], bytes);
-                    bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)cur * lane_stride_b + t0 * row_b, bytes,
+                    bulk_g2s(smem + (size_t)s * tile_bytes, keys + (int64_t)(cur / kvg) * lane_stride_b + t0 * row_b, bytes,
                              &full[s]);
                 }
                 if (++ps == stages) { ps = 0; ++pr; }
@@ -368,7 +368,7 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
                                           smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1));
     const int grid = sm_count() * per_sm;
     launch_pdl(score_tma_kernel<QT, T, G, IMPL, AccT>, dim3(grid), dim3(TS_THREADS), smem, st, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, (int)n_lanes, items, item_stride, n_items, n_impl,
-        os, os32, ot, ostr, stages, tile, scaled);
+        os, os32, ot, ostr, stages, tile, scaled, kv_group_current());
     return kvt_check_launch();
 }
 

@@ -124,7 +124,7 @@ template <int R>  // R = d / 128 rounds of 4 groups
 __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
     int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
-    float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err) {
+    float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err, int kvg) {
     pdl_entry();
     constexpr int d = 128 * R;
     constexpr int G = 4 * R;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                         meta[s] = make_int4(cur, t0, cnt, pos0);
                         mbar_arrive_expect_tx(&full[s], bytes);
                         unsigned char* st = smem + (size_t)s * stage_b;
-                        bulk_g2s(st, keys + (int64_t)cur * lane_stride_b + (int64_t)t0 * row_b,
+                        bulk_g2s(st, keys + (int64_t)(cur / kvg) * lane_stride_b + (int64_t)t0 * row_b,
                                  (uint32_t)(cnt * row_b), &full[s]);
                         if (newq) bulk_g2s(st + tile_b, qprep + (int64_t)cur * qb, (uint32_t)qb, &full[s]);
                     }
@@ -385,7 +385,7 @@ static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const i
     static int per_sm = 0;
     if (!per_sm) per_sm = resident_per_sm(score_i4mma_kernel<R>, QM_THREADS, smem, 4);
     launch_pdl(score_i4mma_kernel<R>, dim3(sms * per_sm), dim3(QM_THREADS), smem, st, (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
-        ostr, err);
+        ostr, err, kv_group_current());
     return kvt_check_launch();
 }
 

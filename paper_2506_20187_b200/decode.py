@@ -27,11 +27,16 @@ class SparseDecoder:
     def __init__(self, n_layers: int, batch: int, n_heads: int, head_dim: int, n_cap: int,
                  dtype: torch.dtype = torch.bfloat16, plan: ChunkPlanConfig | None = None,
                  importance_rate: float = 0.10, early_layer_rate: float = 0.50, device=None,
-                 abstract_dtype: torch.dtype = torch.bfloat16):
+                 abstract_dtype: torch.dtype = torch.bfloat16, n_kv_heads: int | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("SparseDecoder needs a CUDA device (B200, sm_100a)")
         self.L, self.B, self.H, self.d = n_layers, batch, n_heads, head_dim
-        self.lanes = batch * n_heads
+        self.lanes = batch * n_heads  # query lanes
+        self.Hkv = n_kv_heads or n_heads
+        if n_heads % self.Hkv:
+            raise ValueError("n_heads must be a multiple of n_kv_heads")
+        self.kv_group = n_heads // self.Hkv  # GQA: query heads per KV head (adjacent)
+        self.kv_lanes = batch * self.Hkv
         self.n_cap = n_cap
         self.dtype = dtype
         self.plan = plan or ChunkPlanConfig()
@@ -40,19 +45,21 @@ class SparseDecoder:
                   for l in range(n_layers)]
         self.device = torch.device(device or "cuda")
         if dtype == ops.I4:  # INT4 records (K8), 0.3125x of bf16 at d = 128
-            self.K = ops.I4KV(torch.empty((n_layers, self.lanes, n_cap, ops.row_bytes_i4(head_dim)),
+            self.K = ops.I4KV(torch.empty((n_layers, self.kv_lanes, n_cap, ops.row_bytes_i4(head_dim)),
                                           dtype=torch.uint8, device=self.device), head_dim)
             self.V = ops.I4KV(torch.empty_like(self.K.data), head_dim)
         else:
-            self.K = torch.empty((n_layers, self.lanes, n_cap, head_dim), dtype=dtype, device=self.device)
+            self.K = torch.empty((n_layers, self.kv_lanes, n_cap, head_dim), dtype=dtype, device=self.device)
             self.V = torch.empty_like(self.K)
         # bf16 abstracts rounded outward (max up, min down): half the bound-pass bytes, still sound
         adt = abstract_dtype if abstract_dtype is not None else ops.abs_dtype_for(dtype)
-        self.amax = [torch.empty((self.lanes, ops.n_grid_leaves(n_cap, C), head_dim), dtype=adt, device=self.device)
-                     for C in self.C]
+        self.amax = [torch.empty((self.kv_lanes, ops.n_grid_leaves(n_cap, C), head_dim), dtype=adt,
+                                 device=self.device) for C in self.C]
         self.amin = [torch.empty_like(a) for a in self.amax]
-        self.absmag = ([torch.zeros((self.lanes, head_dim), dtype=torch.float32, device=self.device)
+        self.absmag = ([torch.zeros((self.kv_lanes, head_dim), dtype=torch.float32, device=self.device)
                         for _ in range(n_layers)] if adt == torch.bfloat16 else None)
+        if self.kv_group > 1 and self.absmag is None:
+            raise ValueError("GQA sharing needs bf16 abstracts (the decode-path bounds)")
         self.n = 0
         self._ws = None
         self._bufs = None
@@ -71,7 +78,7 @@ class SparseDecoder:
         self._bufs = None
 
     def load_layer(self, layer: int, k: torch.Tensor, v: torch.Tensor, t0: int = 0) -> None:
-        """Write rows [t0, t0 + T) of one layer from [lanes, T, d] tensors (quantising for INT4)."""
+        """Write rows [t0, t0 + T) of one layer from [kv_lanes, T, d] tensors (quantising for INT4)."""
         T = k.shape[1]
         if self.dtype == ops.I4:
             ops.kv_quant(k, ops.I4KV(self.K.data[layer, :, t0:t0 + T], self.d))
@@ -81,7 +88,7 @@ class SparseDecoder:
             self.V[layer, :, t0:t0 + T] = v.to(self.dtype)
 
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
-        """Append one token per lane ([L, lanes, d]) and refresh the tail chunk abstracts."""
+        """Append one token per KV lane ([L, kv_lanes, d]) and refresh the tail chunk abstracts."""
         if self.n >= self.n_cap:
             raise ValueError("cache full")
         for l in range(self.L):
@@ -127,7 +134,8 @@ class SparseDecoder:
         """Select + attend for layer l; q: [lanes, d] (f32 or f64).  Returns the layer buffers."""
         bufs = self._buffers()
         ops.select_attend(q, self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l), self.C[l],
-                          self._ws, bufs[l], abs_mag=None if self.absmag is None else self.absmag[l])
+                          self._ws, bufs[l], abs_mag=None if self.absmag is None else self.absmag[l],
+                          kv_group=self.kv_group)
         return bufs[l]
 
     def step(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -138,7 +146,7 @@ class SparseDecoder:
         for l in range(self.L):  # attention outputs land directly in out[l]
             ops.select_attend(q[l], self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l),
                               self.C[l], self._ws, {**bufs[l], "out": out[l]},
-                              abs_mag=None if self.absmag is None else self.absmag[l])
+                              abs_mag=None if self.absmag is None else self.absmag[l], kv_group=self.kv_group)
         return out
 
     # -- accounting ---------------------------------------------------------------------------------

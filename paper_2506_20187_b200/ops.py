@@ -408,14 +408,18 @@ class LayerWorkspace:
 
 def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch.Tensor,
                   n: int, k: int, C: int, ws: LayerWorkspace, out: dict, attn_splits: int = 0,
-                  score_blocks: int = 0, exact_scores: bool = False, abs_mag: torch.Tensor | None = None) -> None:
+                  score_blocks: int = 0, exact_scores: bool = False, abs_mag: torch.Tensor | None = None,
+                  kv_group: int = 1) -> None:
     """One layer, all lanes: K3 -> plan -> K4 -> K5 -> K6 -> K7 into the caller's `out` buffers
     (sel_tok, sel_score, n_sel, run_start, run_len, n_runs, out, evals).
     abs_mag ([n_lanes, d] f32 max |key| per lane, see lane_abs_mag): directed-rounding f32
-    bounds for bf16 abstracts instead of the canonical f64 ones (same selected set)."""
+    bounds for bf16 abstracts instead of the canonical f64 ones (same selected set).
+    kv_group (GQA): q has kv_group lanes per lane of keys/values/abstracts/abs_mag."""
     ls, d = _lanes(keys)
+    if q.shape[0] != keys.shape[0] * max(kv_group, 1):
+        raise ValueError("q must have kv_group lanes per key lane")
     a = L.KvtLayerArgs()
-    a.n_lanes, a.n, a.k, a.d, a.C = keys.shape[0], n, k, d, C
+    a.n_lanes, a.n, a.k, a.d, a.C = q.shape[0], n, k, d, C
     a.key_dtype, a.v_dtype, a.q_dtype, a.abs_dtype = dtype_code(keys), dtype_code(values), dtype_code(q), dtype_code(amax)
     a.q, a.keys, a.values, a.lane_stride = q.data_ptr(), keys.data_ptr(), values.data_ptr(), ls
     if values.stride(0) != ls:
@@ -430,6 +434,7 @@ def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch
     a.evals = _p(out.get("evals"))
     a.attn_splits, a.score_blocks, a.exact_scores = attn_splits, score_blocks, int(exact_scores)
     a.abs_mag = _p(abs_mag)
+    a.kv_group = max(kv_group, 1)
     L.check(L.kvt_select_attend(a, ws.buf.data_ptr(), ws.bytes, _stream()), "select_attend")
 
 

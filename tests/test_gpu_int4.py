@@ -188,3 +188,56 @@ def test_codec_reciprocal_exhaustive(ops):
     bad = torch.zeros(1, dtype=torch.int32, device="cuda")
     L.check(L.kvt_i4_recip_check(bad.data_ptr(), torch.cuda.current_stream().cuda_stream), "recip_check")
     assert int(bad.item()) == 0
+
+
+@pytest.mark.parametrize("dt", ["int4", "bf16"])
+@pytest.mark.parametrize("kind", ["random", "planted"])
+@pytest.mark.parametrize("Hkv", [2, 8])
+def test_gqa_kv_sharing_matches_oracle(ops, dt, kind, Hkv):
+    """Config 4 layout (GQA): query lanes b*H + h read KV lane b*Hkv + h // g.  Each query lane's
+    selection is the oracle top-k of ITS query against the shared keys (the reference
+    replicates the KV head per query head, adapters.py:121-136 -- identical results).
+    Hkv = H is the plain multi-layer decoder (one workspace shared by layers of different C)."""
+    from paper_2506_20187_b200.decode import SparseDecoder
+    B, H, d, n, L = 2, 8, 128, 4096, 3
+    g = H // Hkv
+    rng = np.random.default_rng(11)
+    if kind == "random":
+        K = rng.normal(size=(B * Hkv, n, d)).astype(np.float32)
+        V = rng.normal(size=(B * Hkv, n, d)).astype(np.float32)
+        Q = rng.normal(size=(B * H, d)).astype(np.float32)
+    else:
+        K = np.empty((B * Hkv, n, d), np.float32)
+        V = np.empty_like(K)
+        Q = np.empty((B * H, d), np.float32)
+        for j in range(B * Hkv):
+            k, q, v, _ = synth.lane(synth.Profile(0.7, 3, 1.0, 5), 0, j, n, d, 1)
+            K[j], V[j] = k, v
+            for h in range(g):  # query heads of a group: same planted direction, own noise
+                Q[j * g + h] = q[0] * (1.0 + 0.1 * h) + rng.normal(size=d).astype(np.float32) * 0.05
+    dec = SparseDecoder(L, B, H, d, n, dtype=ops.I4 if dt == "int4" else torch.bfloat16, device="cuda",
+                        n_kv_heads=Hkv)
+    kt = torch.from_numpy(K).to(torch.bfloat16).cuda()
+    vt = torch.from_numpy(V).to(torch.bfloat16).cuda()
+    for l in range(L):
+        dec.load_layer(l, kt, vt)
+    dec.set_length(n)
+    q = torch.from_numpy(Q).cuda()[None].expand(L, -1, -1).contiguous()
+    out = dec.step(q)
+    torch.cuda.synchronize()
+    if dt == "int4":
+        Kd = np.stack([O.i4_dequant(dec.K.data[0, j].cpu().numpy(), d) for j in range(B * Hkv)]).astype(np.float64)
+        Vd = np.stack([O.i4_dequant(dec.V.data[0, j].cpu().numpy(), d) for j in range(B * Hkv)]).astype(np.float64)
+    else:
+        Kd, Vd = kt.double().cpu().numpy(), vt.double().cpu().numpy()
+    for l in (0, 2):
+        bufs = dec._buffers()[l]
+        k = dec.k_for(l)
+        for i in range(B * H):
+            j = i // g
+            ref = O.topk(O.dots(Q[i], Kd[j]), k)
+            got = bufs["sel_tok"][i, :k].cpu().numpy().astype(np.int64)
+            assert np.array_equal(got, ref), (dt, kind, l, i)
+            att = O.attention(Q[i], Kd[j], Vd[j], ref)
+            err = np.linalg.norm(out[l, i].cpu().numpy() - att) / np.linalg.norm(att)
+            assert err <= 1e-2, (dt, kind, l, i, err)
