@@ -412,6 +412,20 @@ def run_ours(args):
         e2e = {"value": args.batch * world / (float(ems.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": float(ems.item())}
 
+    # ---- self-check: the fused step's attention equals the standalone K7 on its selections ----
+    # (a GPU-vs-GPU consistency probe of the decoder's shared workspace across layers; the
+    # oracle parity itself lives in tests/)
+    with torch.cuda.stream(stream):
+        q_static.copy_(Q[args.warmup])
+        ref_out = dec.step(q_static)
+        bufs = dec._buffers()
+        chk = 0.0
+        for l in range(L):
+            b = bufs[l]
+            o = ops.sparse_decode_attn(dec.V[l], b["sel_tok"], b["sel_score"], b["n_sel"])
+            chk = max(chk, float((o - ref_out[l]).abs().max() / ref_out[l].abs().max().clamp_min(1e-30)))
+        stream.synchronize()
+
     # ---- per-kernel attribution ----
     # The staged pipeline (same kernels as the fused call) is run once to materialise every
     # layer's intermediates; then each stage's 32 per-layer launches are captured in their
@@ -523,6 +537,7 @@ def run_ours(args):
             "prefill_quant_ms": quant_ms,
             "prefill_quant_gbs": (2 * L * dec.lanes * args.ctx * (HEAD_DIM * 2 + 80)) / (quant_ms / 1e3) / 1e9},
         "gpu_launches": launches_per_layer * L * args.steps,
+        "self_check_max_rel_diff": chk,
         "clocks": clocks,
         "e2e": e2e,
     }
