@@ -15,6 +15,9 @@ barrier + synchronize, CUDA events on the launching stream, max over ranks.  KV 
 measurement through the same public API with the step's queries copied from pinned host
 memory and the attention outputs copied back every step.
 
+--kv-heads 8 --ctx 131072 --batch 16: config 4 (LLaMA-3-8B GQA shape, 4 query heads per KV
+head sharing its K/V and abstracts).
+
 Multi-GPU (torchrun): every rank owns a disjoint batch of lanes (batch x head sharding,
 no collective on the data path); value = all ranks' tokens / max-over-ranks time.
 
@@ -56,6 +59,8 @@ def parse():
     p.add_argument("--dtype", choices=["bf16", "f32", "int4"], default="int4",
                    help="KV storage: bf16/f32 rows or INT4 records (K8 compression, config 3)")
     p.add_argument("--layers", type=int, default=N_LAYERS)
+    p.add_argument("--kv-heads", type=int, default=N_HEADS,
+                   help="KV heads (GQA; config 4 = LLaMA-3-8B: 8 KV heads for 32 query heads)")
     p.add_argument("--cpu-lanes", type=int, default=16, help="lanes in the CPU baseline sample")
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -271,7 +276,9 @@ def run_reference(args):
 
 
 def workload_config(args, world):
-    return {"workload": f"llama7b-attn-{args.ctx // 1024}k-b{args.batch * world}-{args.dtype}-{args.data}",
+    model = "llama7b" if args.kv_heads == N_HEADS else f"llama3-8b-gqa{N_HEADS // args.kv_heads}"
+    return {"workload": f"{model}-attn-{args.ctx // 1024}k-b{args.batch * world}-{args.dtype}-{args.data}",
+            "kv_heads": args.kv_heads,
             "layers": args.layers, "heads": N_HEADS, "head_dim": HEAD_DIM, "context": args.ctx,
             "global_batch": args.batch * world, "batch_per_gpu": args.batch, "importance_rate": 0.10,
             "early_layer_rate": 0.50, "chunk": {"early_layers": 8, "other": 64},
@@ -300,15 +307,16 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     dt = {"bf16": torch.bfloat16, "f32": torch.float32, "int4": ops.I4}[args.dtype]
     L = args.layers
-    dec = SparseDecoder(L, args.batch, N_HEADS, HEAD_DIM, args.ctx, dtype=dt, device=dev)
+    dec = SparseDecoder(L, args.batch, N_HEADS, HEAD_DIM, args.ctx, dtype=dt, device=dev, n_kv_heads=args.kv_heads)
+    gqa = ops.kv_group(dec.kv_group)  # standalone stage calls (attribution, self-check) read KV lane i // g
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * args.seed + rank)
     rng = np.random.default_rng([args.seed, rank])
-    u = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
+    u = torch.empty((L, dec.kv_lanes, HEAD_DIM), device=dev, dtype=torch.float32)  # per KV lane
     quant_ms = None
     if args.dtype == "int4":
         # generate each layer in bf16, then compress it with K8 (timed: prefill compression)
-        kb = torch.empty((dec.lanes, args.ctx, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+        kb = torch.empty((dec.kv_lanes, args.ctx, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         vb = torch.empty_like(kb)
         qt = 0.0
         for l in range(L):
@@ -327,7 +335,8 @@ def run_ours(args):
             fill_layer(torch, dec.K[l], dec.V[l], args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
     dec.set_length(args.ctx)
     steps_total = args.warmup + args.steps
-    Q = make_queries(torch, u, steps_total, args.data, gen)
+    # query lanes of a GQA group share their KV head's planted direction (own gains)
+    Q = make_queries(torch, u.repeat_interleave(dec.kv_group, dim=1), steps_total, args.data, gen)
     q_static = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
     out_static = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
     torch.cuda.synchronize()
@@ -422,7 +431,8 @@ def run_ours(args):
         chk = 0.0
         for l in range(L):
             b = bufs[l]
-            o = ops.sparse_decode_attn(dec.V[l], b["sel_tok"], b["sel_score"], b["n_sel"])
+            with gqa:
+                o = ops.sparse_decode_attn(dec.V[l], b["sel_tok"], b["sel_score"], b["n_sel"])
             chk = max(chk, float((o - ref_out[l]).abs().max() / ref_out[l].abs().max().clamp_min(1e-30)))
         stream.synchronize()
 
@@ -443,7 +453,7 @@ def run_ours(args):
             return ops.chunk_bounds_fast(q_static[l], dec.amax[l], dec.amin[l], n, C, dec.absmag[l])
         return ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
 
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream), gqa:
         q_static.copy_(Q[args.warmup])
         for l in range(L):
             C, n, k = dec.C[l], dec.n, dec.k_for(l)
@@ -476,7 +486,7 @@ def run_ours(args):
     reps = 3
     for name in stages:
         fn = stage_fn(name)
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(stream), gqa:
             fn()  # warm (allocator, attributes)
             stream.synchronize()
             g = torch.cuda.CUDAGraph()

@@ -294,6 +294,11 @@ KVT_API int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int64_
  * at zero. */
 KVT_API size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d);
 KVT_API int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream);
+/* GQA for the standalone decode-path entry points (kvt_chunk_bounds_fast, kvt_cand_score_f32 /
+ * _i4mma, kvt_topk_select_band, kvt_sparse_decode_attn) called from this host thread: query
+ * lane i reads key/value/abstract lane i / kv_group.  Returns the previous value (1 = none).
+ * kvt_select_attend uses its own kv_group field. */
+KVT_API int kvt_set_kv_group(int kv_group);
 
 #ifdef __cplusplus
 }

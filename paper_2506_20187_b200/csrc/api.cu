@@ -110,6 +110,12 @@ int& kv_group_tls() {
     return g;
 }
 
+extern "C" int kvt_set_kv_group(int kv_group) {
+    const int old = kv_group_tls();
+    kv_group_tls() = kv_group > 1 ? kv_group : 1;
+    return old;
+}
+
 extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes, void* stream) {
     if (!a || !ws) return KVT_ERR_ARG;
     const int kvg = a->kv_group > 1 ? a->kv_group : 1;

@@ -162,7 +162,8 @@ class SparseDecoder:
             m = ops.n_grid_leaves(self.n, self.C[l])
             k = self.k_for(l)
             nc = sum(n_cand[l])
-            out["bounds"] += self.lanes * (m * 2 * d * sA + d * 8 + m * 24)       # + U, L, A out
+            # abstracts once per KV lane (GQA query lanes of a group share them), q + U, L, A per lane
+            out["bounds"] += self.kv_lanes * m * 2 * d * sA + self.lanes * (d * 8 + m * 24)
             out["plan"] += self.lanes * m * 24 + nc // 64 * 12
             out["score"] += nc * (d * sK + 8)                                      # f32 estimate + token
             out["select"] += nc * 8 + self.lanes * k * 12

@@ -75,6 +75,21 @@ def abs_dtype_for(key_dtype) -> torch.dtype:
     return torch.float64 if key_dtype == torch.float64 else torch.float32
 
 
+class kv_group:
+    """GQA scope for the standalone decode-path wrappers (kvt_set_kv_group): inside
+    `with ops.kv_group(g):` query lane i reads key/value/abstract lane i // g."""
+
+    def __init__(self, g: int):
+        self.g = max(int(g), 1)
+
+    def __enter__(self):
+        self.old = L.kvt_set_kv_group(self.g)
+        return self
+
+    def __exit__(self, *exc):
+        L.kvt_set_kv_group(self.old)
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -255,7 +270,7 @@ def cand_score_f32(q: torch.Tensor, keys, plan: dict, n: int):
     """Fast f32 estimates of the candidate dots (|err| <= plan["err"]) -> (cs32 f32, cand_tok i32)."""
     require_cuda(q, keys)
     ls, d = _lanes(keys)
-    nl = keys.shape[0]
+    nl = q.shape[0]
     cs = torch.empty((nl, max(n, 1)), dtype=torch.float32, device=q.device)
     ct = torch.empty((nl, max(n, 1)), dtype=torch.int32, device=q.device)
     L.check(L.kvt_cand_score_f32(q.data_ptr(), dtype_code(q), keys.data_ptr(), dtype_code(keys), nl, ls, d,
@@ -270,7 +285,7 @@ def cand_score_i4mma(q: torch.Tensor, keys: "I4KV", plan: dict, n: int):
     topk_select_band) -> (cs32 f32, cand_tok i32)."""
     require_cuda(q, keys)
     ls, d = _lanes(keys)
-    nl = keys.shape[0]
+    nl = q.shape[0]
     cs = torch.empty((nl, max(n, 1)), dtype=torch.float32, device=q.device)
     ct = torch.empty((nl, max(n, 1)), dtype=torch.int32, device=q.device)
     ws = torch.empty(max(int(L.kvt_i4_qprep_bytes(nl, d)), 16), dtype=torch.uint8, device=q.device)
@@ -359,7 +374,7 @@ def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: t
     want_lse: also return the lanes' merged softmax state (m, l) f64 [n_lanes, 2] (kvt_attn_lse)."""
     require_cuda(values)
     ls, d = _lanes(values)
-    nl = values.shape[0]
+    nl = n_sel.shape[0]
     k = sel_tok.shape[1]
     # splits <= 0: chosen by kvt_sparse_decode_attn (wave-aware); the workspace holds 64
     ws = torch.zeros(max(1, L.kvt_attn_workspace_bytes(nl, d, 64 if splits <= 0 else splits)), dtype=torch.uint8,
