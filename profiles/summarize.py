@@ -90,5 +90,31 @@ def launches(path: str) -> None:
         print(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {v / cnt[k] / 1e3:.2f} | {100 * v / allk:.1f}% |")
 
 
+def traffic(spec: str) -> None:
+    """traffic <workload>=<raw.csv>[,<workload>=<raw.csv>...] -> JSON on stdout: per bench stage, the
+    DRAM bytes (read + write) of the first captured launch of its kernel (a layer >= 2 launch)."""
+    import json
+    out = {}
+    for item in spec.split(","):
+        wl, path = item.split("=")
+        txt = open(path).read()
+        rows = list(csv.reader(io.StringIO(txt[txt.index('"ID"'):])))
+        hdr, units = rows[0], rows[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        stages = {}
+        for r in rows[2:]:
+            name = short(r[hdr.index("Kernel Name")])
+            stage = next((st for key, st in (("score", "score"), ("attn", "attn"), ("bounds", "bounds"),
+                                              ("select", "select"), ("plan", "plan")) if key in name), None)
+            if stage is None or stage in stages:
+                continue
+            b = sum(float(r[hdr.index(m)].replace(",", "")) * scale[units[hdr.index(m)]]
+                    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            stages[stage] = {"kernel": name, "dram_bytes": b, "layer": 2}
+        out[wl] = stages
+    print(json.dumps({"source": "ncu --set full, one layer-2 launch per kernel (tools/gpu_prof.sh)", "workloads": out},
+                     indent=1))
+
+
 if __name__ == "__main__":
-    {"raw": raw, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"raw": raw, "launches": launches, "traffic": traffic}[sys.argv[1]](sys.argv[2])
