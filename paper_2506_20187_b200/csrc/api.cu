@@ -89,6 +89,24 @@ LayerWs carve(void* base, int64_t n_lanes, int64_t n, int64_t max_leaves, int d)
     return w;
 }
 
+// A per-thread side stream + fork/join events: the INT4 query-digit prep (depends on q only)
+// runs concurrently with bounds and plan; inside CUDA-graph capture it becomes a parallel branch.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool ok = false;
+    SideStream() {
+        ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+    }
+};
+SideStream& side_stream() {
+    static thread_local SideStream ss;
+    return ss;
+}
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -135,6 +153,17 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     const bool fast = kvt_fast_ok(a->key_dtype, a->d) && !a->exact_scores;
     const bool fast_bounds = fast && a->abs_mag && a->abs_dtype == KVT_BF16 && a->q_dtype == KVT_F32 &&
                              !a->leaf_start && (a->d == 128 || a->d == 256);
+    // INT4 fast path: query digits on the side stream, joined before the scoring launch
+    const bool i4_fast = fast && a->key_dtype == KVT_I4;
+    SideStream& ss = side_stream();
+    const bool forked = i4_fast && ss.ok;
+    if (forked) {
+        cudaEventRecord(ss.fork, (cudaStream_t)stream);
+        cudaStreamWaitEvent(ss.s, ss.fork, 0);
+        rc = kvt_i4_qprep(a->q, a->q_dtype, a->n_lanes, a->d, w.qprep, ss.s);
+        if (rc) return rc;
+        cudaEventRecord(ss.join, ss.s);
+    }
     if (fast_bounds)  // sound f32 directed-rounding bounds (bounds_fast.cu)
         rc = kvt_chunk_bounds_fast((const float*)a->q, a->n_lanes, a->d, a->n, a->C, a->amax, a->amin,
                                    a->abs_lane_stride, a->abs_mag, w.U, w.L, w.A, max_leaves, stream);
@@ -149,9 +178,12 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
     if (rc) return rc;
     if (fast) {
         if (a->key_dtype == KVT_I4)  // exact int32 inner products on the tensor cores + per-lane bound
-            rc = kvt_cand_score_i4mma(a->q, a->q_dtype, a->keys, a->n_lanes, a->lane_stride, a->d, w.items, item_cap,
+        {
+            if (forked) cudaStreamWaitEvent((cudaStream_t)stream, ss.join, 0);
+            rc = kvt_cand_score_i4mma(forked ? nullptr : a->q, a->q_dtype, a->keys, a->n_lanes, a->lane_stride, a->d,
+                                      w.items, item_cap,
                                       w.n_items, w.cs32, w.cand_tok, a->n, w.err, w.qprep, stream);
-        else
+        } else
             rc = kvt_cand_score_f32(a->q, a->q_dtype, a->keys, a->key_dtype, a->n_lanes, a->lane_stride, a->d, w.items,
                                     item_cap, w.n_items, w.cs32, w.cand_tok, a->n, stream);
         if (rc) return rc;

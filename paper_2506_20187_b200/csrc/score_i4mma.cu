@@ -397,8 +397,10 @@ extern "C" int kvt_cand_score_i4mma(const void* q, int q_dtype, const void* keys
     if (n_lanes <= 0) return n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
     if (!keys || !items || !n_items || !cand_score32 || !err || !qprep_ws) return KVT_ERR_ARG;
     if (((uintptr_t)keys % 16) || (lane_stride % 16) || n_lanes > INT32_MAX) return KVT_ERR_SHAPE;
-    int rc = kvt_i4_qprep(q, q_dtype, n_lanes, d, qprep_ws, stream);
-    if (rc) return rc;
+    if (q) {  // q == nullptr: qprep_ws already holds the digits (kvt_select_attend runs kvt_i4_qprep on a side stream)
+        int rc = kvt_i4_qprep(q, q_dtype, n_lanes, d, qprep_ws, stream);
+        if (rc) return rc;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     return d == 128 ? launch_i4mma<1>(keys, n_lanes, lane_stride, items, item_stride, n_items, qprep_ws, cand_score32,
                                       cand_tok, cand_stride, err, st)
