@@ -348,6 +348,8 @@ def run_ours(args):
             q_static.copy_(Q[s])
             dec.step(q_static, out_static)
         stream.synchronize()
+        # layers whose fine bounds pruned nothing during warm-up prune on C = 64 abstracts
+        bound_grid = dec.adapt_bound_granularity()
         if not args.no_graph:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
@@ -449,14 +451,15 @@ def run_ours(args):
     n_cand = []
 
     def bounds_fn(l, n, C):  # the K3 variant select_attend runs (fast f32 when absmag is kept)
+        _, amax, amin = dec.grid(l)
         if dec.absmag is not None:
-            return ops.chunk_bounds_fast(q_static[l], dec.amax[l], dec.amin[l], n, C, dec.absmag[l])
-        return ops.chunk_bounds(q_static[l], dec.amax[l], dec.amin[l], n, C, want_A=True)
+            return ops.chunk_bounds_fast(q_static[l], amax, amin, n, C, dec.absmag[l])
+        return ops.chunk_bounds(q_static[l], amax, amin, n, C, want_A=True)
 
     with torch.cuda.stream(stream), gqa:
         q_static.copy_(Q[args.warmup])
         for l in range(L):
-            C, n, k = dec.C[l], dec.n, dec.k_for(l)
+            C, n, k = dec.grid(l)[0], dec.n, dec.k_for(l)
             U, Lo, A = bounds_fn(l, n, C)
             plan = ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
             cs, ct = score_fn(q_static[l], dec.K[l], plan, n)
@@ -468,7 +471,7 @@ def run_ours(args):
     def stage_fn(name):
         def run():
             for l in range(L):
-                C, n, k = dec.C[l], dec.n, dec.k_for(l)
+                C, n, k = dec.grid(l)[0], dec.n, dec.k_for(l)
                 U, Lo, A, plan, cs, ct, st_, ss_, ns_ = inter[l]
                 if name == "bounds":
                     bounds_fn(l, n, C)
@@ -547,6 +550,8 @@ def run_ours(args):
             "prefill_quant_ms": quant_ms,
             "prefill_quant_gbs": (2 * L * dec.lanes * args.ctx * (HEAD_DIM * 2 + 80)) / (quant_ms / 1e3) / 1e9},
         "gpu_launches": launches_per_layer * L * args.steps,
+        "bound_grid": {"fine_C": sorted(set(dec.C)), "coarse_layers": [l for l in range(L) if bound_grid[l]],
+                       "rule": "candidate fraction >= 0.9 in warm-up -> prune on C=64 abstracts"},
         "self_check_max_rel_diff": chk,
         "clocks": clocks,
         "e2e": e2e,

@@ -8,6 +8,10 @@ Layout in HBM:
              (importance.py:56-87 summaries; exact f32 on request)
   absmag     per layer [B*H][d] f32 max |key| over the lane's chunks (bf16 abstracts only):
              enables the directed-rounding f32 bounds (bounds_fast.cu) in select_attend
+  coarse     layers whose plan chunk C_l is finer than default_chunk_size also keep C = 64
+             abstracts; adapt_bound_granularity() switches a layer's pruning to them when its
+             observed candidate fraction shows the fine bounds prune nothing (layers 0-1 at
+             rate 0.5).  The selected set is exact either way; only bound bytes change.
   C_l        ChunkPlanConfig: early layers use early_chunk_size, the rest default_chunk_size
              (chunk_tree.py:111-123, steady state after the early steps)
   k_l        ceil(rate_l * n), rate 0.5 for layers < early_layers else 0.1 (engine.py:83-86,312)
@@ -60,6 +64,12 @@ class SparseDecoder:
                         for _ in range(n_layers)] if adt == torch.bfloat16 else None)
         if self.kv_group > 1 and self.absmag is None:
             raise ValueError("GQA sharing needs bf16 abstracts (the decode-path bounds)")
+        self.coarse_C = self.plan.default_chunk_size
+        self.amax_c = [torch.empty((self.kv_lanes, ops.n_grid_leaves(n_cap, self.coarse_C), head_dim), dtype=adt,
+                                   device=self.device) if C < self.coarse_C and self.absmag is not None else None
+                       for C in self.C]
+        self.amin_c = [None if a is None else torch.empty_like(a) for a in self.amax_c]
+        self.use_coarse = [False] * n_layers
         self.n = 0
         self._ws = None
         self._bufs = None
@@ -75,6 +85,8 @@ class SparseDecoder:
             ops.abstract_build(self.K[l], n, self.C[l], self.amax[l], self.amin[l])
             if self.absmag is not None:
                 ops.lane_abs_mag(self.amax[l], self.amin[l], ops.n_grid_leaves(n, self.C[l]), out=self.absmag[l])
+            if self.amax_c[l] is not None:
+                ops.abstract_build(self.K[l], n, self.coarse_C, self.amax_c[l], self.amin_c[l])
         self._bufs = None
 
     def load_layer(self, layer: int, k: torch.Tensor, v: torch.Tensor, t0: int = 0) -> None:
@@ -100,7 +112,35 @@ class SparseDecoder:
             if self.absmag is not None:  # the refreshed tail chunk can only raise the maxima
                 tail = torch.maximum(self.amax[l][:, c].float().abs(), self.amin[l][:, c].float().abs())
                 torch.maximum(self.absmag[l], tail, out=self.absmag[l])
+            if self.amax_c[l] is not None:
+                cc = (self.n - 1) // self.coarse_C
+                ops.abstract_build(self.K[l], self.n, self.coarse_C, self.amax_c[l], self.amin_c[l], cc, cc + 1)
         self._bufs = None
+
+    def grid(self, l: int):
+        """(C, amax, amin) the layer's pruning runs on (fine plan chunk, or coarse -- see
+        adapt_bound_granularity)."""
+        if self.use_coarse[l]:
+            return self.coarse_C, self.amax_c[l], self.amin_c[l]
+        return self.C[l], self.amax[l], self.amin[l]
+
+    def adapt_bound_granularity(self, threshold: float = 0.9) -> list[bool]:
+        """After a step: layers whose candidate fraction (tokens left after pruning / n) was
+        >= threshold prune on the coarse abstracts from now on (their fine bounds cost bytes and
+        removed nothing); a coarse layer returns to the fine grid when pruning becomes useful
+        (< threshold - 0.2).  Outside graph capture only: it reads the step's counters."""
+        bufs = self._buffers()
+        for l in range(self.L):
+            if self.amax_c[l] is None:
+                continue
+            C = self.coarse_C if self.use_coarse[l] else self.C[l]
+            evals = bufs[l]["evals"].double().mean().item()
+            frac = (evals - ops.n_grid_leaves(self.n, C)) / max(self.n, 1)
+            if not self.use_coarse[l] and frac >= threshold:
+                self.use_coarse[l] = True
+            elif self.use_coarse[l] and frac < threshold - 0.2:
+                self.use_coarse[l] = False
+        return list(self.use_coarse)
 
     def k_for(self, layer: int) -> int:
         return math.ceil(self.rates[layer] * self.n)
@@ -133,7 +173,8 @@ class SparseDecoder:
     def layer(self, l: int, q: torch.Tensor) -> dict:
         """Select + attend for layer l; q: [lanes, d] (f32 or f64).  Returns the layer buffers."""
         bufs = self._buffers()
-        ops.select_attend(q, self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l), self.C[l],
+        C, amax, amin = self.grid(l)
+        ops.select_attend(q, self.K[l], self.V[l], amax, amin, self.n, self.k_for(l), C,
                           self._ws, bufs[l], abs_mag=None if self.absmag is None else self.absmag[l],
                           kv_group=self.kv_group)
         return bufs[l]
@@ -144,8 +185,9 @@ class SparseDecoder:
             out = torch.empty((self.L, self.lanes, self.d), dtype=torch.float32, device=self.device)
         bufs = self._buffers()
         for l in range(self.L):  # attention outputs land directly in out[l]
-            ops.select_attend(q[l], self.K[l], self.V[l], self.amax[l], self.amin[l], self.n, self.k_for(l),
-                              self.C[l], self._ws, {**bufs[l], "out": out[l]},
+            C, amax, amin = self.grid(l)
+            ops.select_attend(q[l], self.K[l], self.V[l], amax, amin, self.n, self.k_for(l),
+                              C, self._ws, {**bufs[l], "out": out[l]},
                               abs_mag=None if self.absmag is None else self.absmag[l], kv_group=self.kv_group)
         return out
 
@@ -159,7 +201,7 @@ class SparseDecoder:
         d = self.d
         out = {"bounds": 0, "score": 0, "select": 0, "attn": 0, "plan": 0, "runs": 0}
         for l in (range(self.L) if layers is None else layers):
-            m = ops.n_grid_leaves(self.n, self.C[l])
+            m = ops.n_grid_leaves(self.n, self.grid(l)[0])
             k = self.k_for(l)
             nc = sum(n_cand[l])
             # abstracts once per KV lane (GQA query lanes of a group share them), q + U, L, A per lane

@@ -241,3 +241,27 @@ def test_gqa_kv_sharing_matches_oracle(ops, dt, kind, Hkv):
             att = O.attention(Q[i], Kd[j], Vd[j], ref)
             err = np.linalg.norm(out[l, i].cpu().numpy() - att) / np.linalg.norm(att)
             assert err <= 1e-2, (dt, kind, l, i, err)
+
+
+@pytest.mark.parametrize("dt", ["int4", "bf16"])
+def test_adaptive_bound_granularity_keeps_the_selection(ops, dt):
+    """Switching a C = 8 layer's pruning to the C = 64 abstracts changes only how much is
+    pruned: the selected sets and the attention outputs are identical."""
+    from paper_2506_20187_b200.decode import SparseDecoder
+    B, H, d, n, L = 1, 4, 128, 4096, 3
+    rng = np.random.default_rng(3)
+    K = torch.from_numpy(rng.normal(size=(B * H, n, d)).astype(np.float32)).to(torch.bfloat16).cuda()
+    dec = SparseDecoder(L, B, H, d, n, dtype=ops.I4 if dt == "int4" else torch.bfloat16, device="cuda")
+    for l in range(L):
+        dec.load_layer(l, K, K)
+    dec.set_length(n)
+    q = torch.from_numpy(rng.normal(size=(L, B * H, d)).astype(np.float32)).cuda()
+    out0 = dec.step(q).clone()
+    sel0 = [dec._buffers()[l]["sel_tok"].clone() for l in range(L)]
+    flags = dec.adapt_bound_granularity(threshold=0.0)  # force the coarse grid where one exists
+    assert flags[:2] == [True, True] and not flags[2]
+    out1 = dec.step(q)
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert torch.equal(dec._buffers()[l]["sel_tok"], sel0[l]), l
+    assert torch.equal(out0, out1)
