@@ -83,7 +83,7 @@ __device__ __forceinline__ void s3_find_bin(S3Shared& S, const unsigned int* his
 // barrier instead of four radix rounds.
 __device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* keys, int n, long long want) {
     const int tid = threadIdx.x, lane = tid & 31;
-    if (n <= 1024) {
+    if (n <= 128) {
         for (int j = tid; j < n; j += S3_THREADS) {
             const uint32_t kj = keys[j];
             int gt = 0, eq = 0;
@@ -163,15 +163,15 @@ __device__ __forceinline__ double s3_canon(const QT* q, const unsigned char* row
 // Per-warp contiguous ranges in units of 128 elements (32 lanes x float4), so a warp's
 // iteration covers 128 consecutive candidates and lane l owns elements 4l..4l+3 of it.
 struct WarpRange4 {
-    int64_t a, b;
+    int a, b;  // candidate counts are < 2^31: 32-bit indices in the hot loops
     __device__ WarpRange4(int64_t n, int warp) {
-        const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128;
-        a = kvt::imin(n, warp * per);
-        b = kvt::imin(n, a + per);
+        const int per = (int)(((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128);
+        a = (int)kvt::imin(n, (int64_t)warp * per);
+        b = (int)kvt::imin(n, (int64_t)a + per);
     }
 };
 
-__device__ __forceinline__ void load4s(const float* sc, int64_t i, int64_t end, bool vec, float v[4]) {
+__device__ __forceinline__ void load4s(const float* sc, int i, int end, bool vec, float v[4]) {
     if (vec && i + 4 <= end) {
         const float4 x = *reinterpret_cast<const float4*>(sc + i);
         v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
@@ -215,22 +215,23 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const double hi = rec[li * 4 + 2] + 2.0 * E;
     const double inv = hi > lo ? (double)S3_BINS / (hi - lo) : 0.0;
     const float lo_f = (float)lo, inv_f = (float)inv;
+    const int n32 = (int)n;
 
     // ---- 1. bucket histogram of the estimates (4 per thread per iteration) ----
     for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
     if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; S.remaining = 0; }
     __syncthreads();
     // passes over the estimates batch S3_UB float4 loads per thread (memory-level parallelism)
-    for (int64_t base = 0; base < n; base += (int64_t)S3_UB * 4 * S3_THREADS) {
+    for (int base = 0; base < n32; base += S3_UB * 4 * S3_THREADS) {
         float v[S3_UB][4];
 #pragma unroll
-        for (int u = 0; u < S3_UB; ++u) load4s(sc, base + (int64_t)(u * S3_THREADS + tid) * 4, n, vec, v[u]);
+        for (int u = 0; u < S3_UB; ++u) load4s(sc, base + (u * S3_THREADS + tid) * 4, n32, vec, v[u]);
 #pragma unroll
         for (int u = 0; u < S3_UB; ++u) {
-            const int64_t i = base + (int64_t)(u * S3_THREADS + tid) * 4;
+            const int i = base + (u * S3_THREADS + tid) * 4;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int bkt = i + e < n ? s3_bucket(v[u][e], lo_f, inv_f) : -1;
+                const int bkt = i + e < n32 ? s3_bucket(v[u][e], lo_f, inv_f) : -1;
                 if (bkt >= 0) atomicAdd(&S.hist[bkt], 1u);
             }
         }
@@ -252,13 +253,13 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     if (merged) {
         __shared__ long long w_list_sure[S3_WARPS];
         if (lane == 0) w_list_sure[warp] = 0;
-        for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
+        for (int base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
           float vv[S3_UW][4];
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) load4s(sc, base0 + 128 * u + 4 * lane, wr.b, vec, vv[u]);
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) {
-            const int64_t i = base0 + 128 * u + 4 * lane;
+            const int i = base0 + 128 * u + 4 * lane;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const bool in = i + e < wr.b;
@@ -284,22 +285,29 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         if (ln > S3_LIST_CAP) {
             fallback = true;
         } else {
-            // T = the need_in_bucket-th largest key among the bucket-bstar members
-            for (int j = tid; j < ln; j += S3_THREADS) {
-                if (!(lpos[j] & 0x40000000)) continue;
-                const uint32_t kj = lkey[j];
-                int gt = 0, eq = 0;
-                for (int f = 0; f < ln; ++f) {
-                    if (!(lpos[f] & 0x40000000)) continue;
-                    gt += lkey[f] > kj;
-                    eq += lkey[f] == kj;
-                }
-                if (gt < need_in_bucket && need_in_bucket <= gt + eq) S.prefix = kj;
+            // T = the need_in_bucket-th largest key among the bucket-bstar members: compact
+            // their keys behind the list (ballot + one atomic per warp), then the bounded
+            // list select (rank count for tiny lists, 8-bit radix rounds otherwise)
+            uint32_t* bkey = S.hist;  // the bucket histogram is dead once bstar is known
+            __shared__ unsigned int s_nb;
+            if (tid == 0) s_nb = 0;
+            __syncthreads();
+            for (int j0 = 0; j0 < ln; j0 += S3_THREADS) {
+                const int j = j0 + tid;
+                const bool m = j < ln && (lpos[j] & 0x40000000);
+                const unsigned ballot = __ballot_sync(KVT_FULL, m);
+                unsigned wb = 0;
+                if (lane == 0 && ballot) wb = atomicAdd(&s_nb, (unsigned)__popc(ballot));
+                wb = __shfl_sync(KVT_FULL, wb, 0);
+                const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
+                if (m && slot < S3_BINS) bkey[slot] = lkey[j];
             }
             __syncthreads();  // every thread has read list_n before it is reset
+            if (s_nb > (unsigned)S3_BINS) fallback = true;  // (block-uniform)
+            const uint32_t T32m = fallback ? 0u : s3_list_select(S, bkey, (int)s_nb, need_in_bucket);
             if (tid == 0) S.list_n = 0;  // reused as the band counter
             __syncthreads();
-            const double Tk = (double)key32_to_float((uint32_t)S.prefix);
+            const double Tk = (double)key32_to_float(T32m);
             hb = Tk + 2.0 * E;
             lb = Tk - 2.0 * E;
             // sure list members counted into their owner warp's range (WarpRange4 spans of
@@ -322,17 +330,17 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     }
     if (!merged && !fallback) {
     // ---- 2. gather the k-th bucket (unordered) ----
-    for (int64_t base0 = 0; base0 < n; base0 += (int64_t)S3_UB * 4 * S3_THREADS) {
+    for (int base0 = 0; base0 < n32; base0 += S3_UB * 4 * S3_THREADS) {
       float vv[S3_UB][4];
 #pragma unroll
-      for (int u = 0; u < S3_UB; ++u) load4s(sc, base0 + (int64_t)(u * S3_THREADS + tid) * 4, n, vec, vv[u]);
+      for (int u = 0; u < S3_UB; ++u) load4s(sc, base0 + (u * S3_THREADS + tid) * 4, n32, vec, vv[u]);
 #pragma unroll
       for (int u = 0; u < S3_UB; ++u) {
-        const int64_t i = base0 + (int64_t)(u * S3_THREADS + tid) * 4;
+        const int i = base0 + (u * S3_THREADS + tid) * 4;
         const float* v = vv[u];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const bool m = i + e < n && s3_bucket(v[e], lo_f, inv_f) == bstar;
+            const bool m = i + e < n32 && s3_bucket(v[e], lo_f, inv_f) == bstar;
             const unsigned ballot = __ballot_sync(KVT_FULL, m);
             unsigned wb = 0;
             if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
@@ -354,13 +362,13 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         // ---- 3. per-warp sure counts + band members (appended, unordered) ----
         if (tid == 0) S.list_n = 0;  // reused as the band counter
         __syncthreads();
-        for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
+        for (int base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
           float vv[S3_UW][4];
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) load4s(sc, base0 + 128 * u + 4 * lane, wr.b, vec, vv[u]);
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) {
-            const int64_t i = base0 + 128 * u + 4 * lane;
+            const int i = base0 + 128 * u + 4 * lane;
             const float* v = vv[u];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -437,12 +445,12 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
                 for (int j = 0; j < (int)nband_total; ++j)
                     if (band_pos[j] == (int)(wr.a - 1)) { carry_m = S.band_sel[j] != 0; break; }
         }
-        for (int64_t base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
+        for (int base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
           float vv[S3_UW][4];
           int tt[S3_UW][4];
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) {
-              const int64_t i = base0 + 128 * u + 4 * lane;
+              const int i = base0 + 128 * u + 4 * lane;
               load4s(sc, i, wr.b, vec, vv[u]);
               if (vec && i + 4 <= wr.b) {
                   const int4 x = *reinterpret_cast<const int4*>(tk + i);
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
           }
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) {
-            const int64_t i = base0 + 128 * u + 4 * lane;
+            const int i = base0 + 128 * u + 4 * lane;
             const float* v = vv[u];
             bool m[4];
             double scr[4];
