@@ -257,6 +257,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
           float vv[S3_UW][4];
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) load4s(sc, base0 + 128 * u + 4 * lane, wr.b, vec, vv[u]);
+          // flags of this lane's 4 x S3_UW elements as a bitmask; one warp scan + one atomic
+          // per iteration place the list members (sure counts stay per lane until the end)
+          unsigned mbits = 0, cbits = 0;
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) {
             const int i = base0 + 128 * u + 4 * lane;
@@ -264,22 +267,37 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             for (int e = 0; e < 4; ++e) {
                 const bool in = i + e < wr.b;
                 const int b = in ? s3_bucket(vv[u][e], lo_f, inv_f) : -1;
-                nsure += __popc(__ballot_sync(KVT_FULL, b > bstar + 1));
-                const bool m = in && b >= bstar - 1 && b <= bstar + 1;
-                const unsigned ballot = __ballot_sync(KVT_FULL, m);
-                unsigned wb = 0;
-                if (lane == 0 && ballot) wb = atomicAdd(&S.list_n, (unsigned)__popc(ballot));
-                wb = __shfl_sync(KVT_FULL, wb, 0);
-                if (m) {
-                    const unsigned slot = wb + __popc(ballot & ((1u << lane) - 1));
-                    if (slot < S3_LIST_CAP) {
-                        lkey[slot] = ord_key32(vv[u][e]);
-                        lpos[slot] = (int32_t)((i + e) | (b == bstar ? 0x40000000 : 0));
-                    }
-                }
+                nsure += b > bstar + 1;
+                mbits |= (unsigned)(in && b >= bstar - 1 && b <= bstar + 1) << (4 * u + e);
+                cbits |= (unsigned)(b == bstar) << (4 * u + e);
             }
           }
+          const int cnt = __popc(mbits);
+          const int inc = warp_incl_scan(cnt, lane);
+          unsigned wb = 0;
+          if (lane == 31 && inc) wb = atomicAdd(&S.list_n, (unsigned)inc);
+          wb = __shfl_sync(KVT_FULL, wb, 31);
+          unsigned slot = wb + (unsigned)(inc - cnt);
+          while (mbits) {
+            const int f = __ffs(mbits) - 1;
+            mbits &= mbits - 1;
+            if (slot < S3_LIST_CAP) {
+                const int u = f >> 2, e = f & 3;
+                const int i = base0 + 128 * u + 4 * lane + e;
+                float v = vv[0][0];
+#pragma unroll
+                for (int uu = 0; uu < S3_UW; ++uu)
+#pragma unroll
+                    for (int ee = 0; ee < 4; ++ee)
+                        if (uu == u && ee == e) v = vv[uu][ee];
+                lkey[slot] = ord_key32(v);
+                lpos[slot] = (int32_t)(i | ((cbits >> f) & 1 ? 0x40000000 : 0));
+            }
+            ++slot;
+          }
         }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) nsure += __shfl_xor_sync(KVT_FULL, nsure, off);
         __syncthreads();
         const int ln = (int)S.list_n;
         if (ln > S3_LIST_CAP) {
