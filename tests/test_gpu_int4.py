@@ -265,3 +265,36 @@ def test_adaptive_bound_granularity_keeps_the_selection(ops, dt):
     for l in range(L):
         assert torch.equal(dec._buffers()[l]["sel_tok"], sel0[l]), l
     assert torch.equal(out0, out1)
+
+
+@pytest.mark.parametrize("dt", ["int4", "bf16"])
+def test_decoder_head_dim_256(ops, dt):
+    """d = 256 through the decode path (fast bounds G = 2, INT4 MMA scoring R = 2, 256-wide
+    attention formats): every layer's selection equals the oracle and attention is within 1e-2."""
+    from paper_2506_20187_b200.decode import SparseDecoder
+    B, H, d, n, L = 1, 4, 256, 2048, 3
+    rng = np.random.default_rng(9)
+    K = rng.normal(size=(B * H, n, d)).astype(np.float32)
+    V = rng.normal(size=(B * H, n, d)).astype(np.float32)
+    Q = rng.normal(size=(L, B * H, d)).astype(np.float32)
+    dec = SparseDecoder(L, B, H, d, n, dtype=ops.I4 if dt == "int4" else torch.bfloat16, device="cuda")
+    kt = torch.from_numpy(K).to(torch.bfloat16).cuda()
+    vt = torch.from_numpy(V).to(torch.bfloat16).cuda()
+    for l in range(L):
+        dec.load_layer(l, kt, vt)
+    dec.set_length(n)
+    out = dec.step(torch.from_numpy(Q).cuda())
+    torch.cuda.synchronize()
+    for l in range(L):
+        if dt == "int4":
+            Kd = np.stack([O.i4_dequant(dec.K.data[l, j].cpu().numpy(), d) for j in range(B * H)]).astype(np.float64)
+            Vd = np.stack([O.i4_dequant(dec.V.data[l, j].cpu().numpy(), d) for j in range(B * H)]).astype(np.float64)
+        else:
+            Kd, Vd = kt.double().cpu().numpy(), vt.double().cpu().numpy()
+        k = dec.k_for(l)
+        for i in range(B * H):
+            ref = O.topk(O.dots(Q[l, i], Kd[i]), k)
+            got = dec._buffers()[l]["sel_tok"][i, :k].cpu().numpy().astype(np.int64)
+            assert np.array_equal(got, ref), (dt, l, i)
+            att = O.attention(Q[l, i], Kd[i], Vd[i], ref)
+            assert np.linalg.norm(out[l, i].cpu().numpy() - att) / np.linalg.norm(att) <= 1e-2
