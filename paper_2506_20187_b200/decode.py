@@ -212,3 +212,34 @@ class SparseDecoder:
             out["runs"] += self.lanes * k * 4 * 3
             out["attn"] += self.lanes * k * (d * sK + 4 + 8) + self.lanes * d * 4
         return out
+
+
+def run_trace(trace, dtype=torch.float32, importance_rate: float = 0.10, early_layer_rate: float = 0.50,
+              plan: ChunkPlanConfig | None = None, device=None) -> dict:
+    """Decode every step of a `.kvtr` trace on the GPU (the selection + attention of
+    engine.run's lane loop, engine.py:307-357; every (layer, head) is one lane, B = 1).
+    f32 keys keep the canonical scores identical to the reference's f64 arithmetic on the
+    trace's f32 inputs.  Returns {"selected": [step][layer][head] sorted token arrays,
+    "out": f32 [steps, layers, heads, d] attention outputs (zeros when the trace has no values)}."""
+    import numpy as np
+    h = trace.header
+    dev = torch.device(device or "cuda")
+    dec = SparseDecoder(h.n_layers, 1, h.n_heads, h.head_dim, h.n_context, dtype=dtype, plan=plan,
+                        importance_rate=importance_rate, early_layer_rate=early_layer_rate, device=dev)
+    for l in range(h.n_layers):
+        k = torch.from_numpy(np.array(trace.keys[l], dtype=np.float32)).to(dev)  # copy: mmap is read-only
+        v = torch.from_numpy(np.array(trace.values[l], dtype=np.float32)).to(dev) if trace.values is not None \
+            else torch.zeros_like(k)
+        dec.load_layer(l, k, v)
+    dec.set_length(h.n_context)
+    selected, outs = [], []
+    for s in range(h.n_steps):
+        q = torch.from_numpy(np.array(trace.queries[s], dtype=np.float32)).to(dev)
+        outs.append(dec.step(q).clone())
+        bufs = dec._buffers()
+        selected.append([[bufs[l]["sel_tok"][i, :dec.k_for(l)].cpu().numpy().astype(np.int64)
+                          for i in range(h.n_heads)] for l in range(h.n_layers)])
+    out = torch.stack(outs)
+    if trace.values is None:
+        out.zero_()
+    return {"selected": selected, "out": out}
