@@ -298,3 +298,49 @@ def test_decoder_head_dim_256(ops, dt):
             assert np.array_equal(got, ref), (dt, l, i)
             att = O.attention(Q[l, i], Kd[i], Vd[i], ref)
             assert np.linalg.norm(out[l, i].cpu().numpy() - att) / np.linalg.norm(att) <= 1e-2
+
+
+@pytest.mark.parametrize("dt", ["int4", "bf16"])
+def test_decoder_append_odd_context_matches_oracle(ops, dt):
+    """Decode while appending: an odd context (not a multiple of 8 or 64), one appended token per
+    step (tail-chunk abstracts, |key| maxima and coarse abstracts refreshed), the adaptive
+    coarse grid switched on midway.  Every step's selection equals the oracle top-k over the
+    current context and attention is within 1e-2."""
+    from paper_2506_20187_b200.decode import SparseDecoder
+    B, H, d, n0, L, steps = 1, 2, 128, 1001, 3, 4
+    rng = np.random.default_rng(21)
+    cap = n0 + steps
+    K = rng.normal(size=(B * H, cap, d)).astype(np.float32)
+    V = rng.normal(size=(B * H, cap, d)).astype(np.float32)
+    K[:, -2:] *= 3.0  # appended tokens with large keys: they must enter the selection
+    dec = SparseDecoder(L, B, H, d, cap, dtype=ops.I4 if dt == "int4" else torch.bfloat16, device="cuda")
+    kt = torch.from_numpy(K).to(torch.bfloat16).cuda()
+    vt = torch.from_numpy(V).to(torch.bfloat16).cuda()
+    for l in range(L):
+        dec.load_layer(l, kt[:, :n0], vt[:, :n0])
+    dec.set_length(n0)
+    for s in range(steps):
+        q = torch.from_numpy(rng.normal(size=(L, B * H, d)).astype(np.float32)).cuda()
+        out = dec.step(q)
+        torch.cuda.synchronize()
+        n = dec.n
+        for l in range(L):
+            if dt == "int4":
+                Kd = np.stack([O.i4_dequant(dec.K.data[l, j, :n].cpu().numpy(), d) for j in range(B * H)]).astype(np.float64)
+                Vd = np.stack([O.i4_dequant(dec.V.data[l, j, :n].cpu().numpy(), d) for j in range(B * H)]).astype(np.float64)
+            else:
+                Kd, Vd = kt[:, :n].double().cpu().numpy(), vt[:, :n].double().cpu().numpy()
+            k = dec.k_for(l)
+            for i in range(B * H):
+                qi = q[l, i].cpu().numpy()
+                ref = O.topk(O.dots(qi, Kd[i]), k)
+                got = dec._buffers()[l]["sel_tok"][i, :k].cpu().numpy().astype(np.int64)
+                assert np.array_equal(got, ref), (dt, s, l, i)
+                att = O.attention(qi, Kd[i], Vd[i], ref)
+                assert np.linalg.norm(out[l, i].cpu().numpy() - att) / np.linalg.norm(att) <= 1e-2
+        if s == 1:
+            dec.adapt_bound_granularity(threshold=0.0)
+        if s < steps - 1:
+            kn = kt[:, n:n + 1].permute(1, 0, 2).expand(L, -1, -1).contiguous()
+            vn = vt[:, n:n + 1].permute(1, 0, 2).expand(L, -1, -1).contiguous()
+            dec.append(kn, vn)
