@@ -28,6 +28,11 @@ from dataclasses import dataclass
 from pathlib import Path
 from typing import Callable, Iterable, Sequence
 
+import numpy as np
+
+from . import cold_files as CF
+from .cold_files import ColdStoreError  # (tiered_store.py:71-72)  noqa: F401
+
 HOT, WARM, COLD = "hot", "warm", "cold"
 LEDGER_COLUMNS = ("step", "layer", "abstract_bytes", "cold_to_warm", "warm_to_hot", "hot_to_warm", "r")
 
@@ -50,8 +55,6 @@ class ResidencyError(RuntimeError):
     """An operation's tier precondition does not hold (tiered_store.py:67-68)."""
 
 
-class ColdStoreError(RuntimeError):
-    """The cold tier is missing data (tiered_store.py:71-72)."""
 
 
 @dataclass(frozen=True)
@@ -90,6 +93,7 @@ class ChunkRecord:
     tier: str
     pinned: bool
     access_count: int = 0
+    offset: int = 0  # payload offset in the lane's KVCF file (file-backed stores)
     last_touch: int = -1
 
     @property
@@ -138,6 +142,8 @@ class TieredStore:
         self.row: LedgerRow | None = None
         self.touch_log: dict[tuple[int, int], dict[int, deque]] = {}
         self.ledger_rows: list[LedgerRow] = []
+        # file-backed cold tier (place_initial(trace, ...) with a cold_dir): KVCF/KVAB files
+        self.cold_dir: Path | None = None
 
     # -- views ------------------------------------------------------------------------------
     @property
@@ -252,7 +258,10 @@ class TieredStore:
         if bad:
             raise ResidencyError(f"lane ({layer}, {head}): fetch needs cold records, "
                                  f"got {[(r.start, r.tier) for r in bad]}")
+        payload = []
         for rec in sorted(hit, key=lambda r: r.start):
+            if self.cold_dir is not None:
+                payload.append(CF.read_record(self.data_path(layer, head), rec.offset, rec.n_tokens, self.head_dim))
             self._move(rec, WARM)
             rec.last_touch = self.step
             rec.access_count += 1
@@ -260,7 +269,11 @@ class TieredStore:
             if self.row is not None:
                 self.row.fetch_ops += 1
         self._evict_warm({id(r) for r in hit})
-        return hit
+        if self.cold_dir is None:
+            return hit
+        # file-backed: the reference's return value, widened f32 (keys, values)
+        return (np.concatenate([k for k, _ in payload]).astype(np.float32),
+                np.concatenate([v for _, v in payload]).astype(np.float32))
 
     def promote_hot(self, layer: int, head: int, spans: Iterable[tuple[int, int]]) -> int:
         moved = 0
@@ -315,12 +328,32 @@ class TieredStore:
                 raise CapacityError(f"warm budget {self.config.warm_capacity} B below this step's working set")
             self._move(min(cand, key=ChunkRecord.order_key), COLD)  # replica exists: no write
 
-    def load_abstracts(self, layer: int, head: int) -> list[tuple[int, int]]:
-        """Bill one summary per currently-cold record of the lane (the decoder keeps every
-        lane's abstracts resident in HBM, so nothing moves); returns the cold spans."""
+    def load_abstracts(self, layer: int, head: int):
+        """Bill one summary per currently-cold record of the lane.  In-memory store: the
+        decoder keeps every lane's abstracts resident in HBM, nothing moves, the cold spans
+        are returned.  File-backed store: the lane's KVAB file is read and validated and the
+        cold records' summaries are returned as ChunkAbstracts (tiered_store.py:390-408),
+        ColdStoreError if one is missing."""
         spans = self.cold_spans(layer, head)
+        if self.cold_dir is None:
+            self._count("abstract_bytes", len(spans) * abstract_nbytes(self.head_dim))
+            return spans
+        if not spans:
+            return []
+        lane = CF.read_abstract_file(self.abstract_path(layer, head), self.head_dim)
+        every = {(a.start, a.end): a for a in lane.as_chunk_abstracts()}  # validates each record
+        missing = [sp for sp in spans if sp not in every]
+        if missing:
+            raise ColdStoreError(f"no summary record for cold chunk [{missing[0][0]}, {missing[0][1]}) in "
+                                 f"{self.abstract_path(layer, head)}")
         self._count("abstract_bytes", len(spans) * abstract_nbytes(self.head_dim))
-        return spans
+        return [every[sp] for sp in spans]
+
+    def data_path(self, layer: int, head: int) -> Path:
+        return CF.data_path(self.cold_dir, layer, head)
+
+    def abstract_path(self, layer: int, head: int) -> Path:
+        return CF.abstract_path(self.cold_dir, layer, head)
 
     # -- integrity (tiered_store.py:412-435) -------------------------------------------------
     def check_invariants(self) -> None:
@@ -343,21 +376,48 @@ class TieredStore:
             raise AssertionError("; ".join(problems))
 
 
-def place_initial(n_layers: int, n_heads: int, head_dim: int, n_context: int, config: TierConfig,
-                  chunk_size: int = 64, spans_by_lane: dict | None = None,
-                  on_move: Callable[[ChunkRecord, str, str], None] | None = None) -> TieredStore:
+def place_initial(*args, chunk_size: int = 64, spans_by_lane: dict | None = None,
+                  on_move: Callable[[ChunkRecord, str, str], None] | None = None, **kw) -> TieredStore:
     """Initial residency (tiered_store.py:510-592): pinned early layers first, then the most
     recent tokens of every lane claim hot, then warm; the rest starts cold.  Pinned layers
-    must fit in hot + warm."""
+    must fit in hot + warm.
+
+    Two call forms:
+      place_initial(trace, config, chunk_size=64, *, spans_by_lane=None)   -- the reference's;
+          with config.cold_dir set, every non-pinned lane is written through to its KVCF/KVAB
+          pair (byte-identical to the reference's files) and fetch_chunk / load_abstracts
+          read them back;
+      place_initial(n_layers, n_heads, head_dim, n_context, config, chunk_size=64, ...)
+          -- bookkeeping only (the decoder holds the bytes in HBM / pinned host memory)."""
+    trace = None
+    if args and hasattr(args[0], "header"):
+        trace, config = args[0], (args[1] if len(args) > 1 else kw.pop("config"))
+        if len(args) > 2:
+            chunk_size = args[2]
+        h = trace.header
+        n_layers, n_heads, head_dim, n_context = h.n_layers, h.n_heads, h.head_dim, h.n_context
+    else:
+        n_layers, n_heads, head_dim, n_context, config = args[:5]
+        if len(args) > 5:
+            chunk_size = args[5]
     store = TieredStore(config, n_layers, n_heads, head_dim, on_move)
+    files = trace is not None and config.cold_dir is not None
+    if files:
+        store.cold_dir = Path(config.cold_dir)
+        store.cold_dir.mkdir(parents=True, exist_ok=True)
     every: list[ChunkRecord] = []
     for layer in range(n_layers):
         pinned = layer < config.early_layers_pinned
         for head in range(n_heads):
             spans = (spans_by_lane[(layer, head)] if spans_by_lane is not None else
                      [(s, min(s + chunk_size, n_context)) for s in range(0, n_context, chunk_size)])
-            recs = sorted((ChunkRecord(layer, head, s, e, kv_nbytes(e - s, head_dim), COLD, pinned)
-                           for s, e in spans), key=lambda r: r.start)
+            offs = [0] * len(spans)
+            if files and not pinned:
+                offs = CF.write_lane_files(store.data_path(layer, head), store.abstract_path(layer, head), spans,
+                                           trace.keys[layer, head],
+                                           None if trace.values is None else trace.values[layer, head], head_dim)
+            recs = sorted((ChunkRecord(layer, head, s, e, kv_nbytes(e - s, head_dim), COLD, pinned, offset=o)
+                           for (s, e), o in zip(spans, offs)), key=lambda r: r.start)
             store.lanes[(layer, head)] = recs
             every.extend(recs)
     if sum(r.nbytes for r in every if r.pinned) > config.hot_capacity + config.warm_capacity:
