@@ -5,8 +5,8 @@ output over a selected set, its quality metrics and the selected-token runs, on 
 canonical logits from K4 (keys are scored once).  This drop-in widens V to f64 and
 accumulates in f64 like the reference (engine.py:149-154); the batched decode path keeps
 bf16/f32 values with f32 accumulation (tolerance 1e-2 / 2e-3, BASELINE.json north_star).
-Report writing, ablations and the tier ledger (engine.py:222-532) are out of scope
-(SURVEY.md sec. 2.1).
+The decode loop, its reports and the ablation ladder (engine.py:48-532) are in `runner.py`
+on the batched GPU selection path and re-exported here.
 """
 
 from __future__ import annotations
@@ -82,3 +82,10 @@ def token_runs(tokens) -> list[tuple[int, int]]:
 
 
 _token_runs = token_runs
+
+
+from .runner import (ABLATE_COLUMNS, ABLATION_ROWS, STEP_COLUMNS, RunConfig, RunReport, StepRow,  # noqa: E402
+                     ablate, ablation_table, default_tier, run, run_and_report, write_ablation, write_report)
+
+__all__ += ["ABLATE_COLUMNS", "ABLATION_ROWS", "STEP_COLUMNS", "RunConfig", "RunReport", "StepRow", "ablate",
+            "ablation_table", "default_tier", "run", "run_and_report", "write_ablation", "write_report"]

@@ -111,6 +111,12 @@ class LayerTiming:
     def gpu_end(self) -> float:
         return self.compute[1]
 
+    eval_ms = property(lambda self: self.eval[1] - self.eval[0])
+    cold_ms = property(lambda self: self.cold[1] - self.cold[0])
+    warm_ms = property(lambda self: self.warm[1] - self.warm[0])
+    decompress_ms = property(lambda self: self.decompress[1] - self.decompress[0])
+    compute_ms = property(lambda self: self.compute[1] - self.compute[0])
+
 
 @dataclass(frozen=True)
 class StepSchedule:
@@ -173,6 +179,17 @@ def build_schedule(loads: Sequence[LayerLoad], params: PipelineParams, mode: str
                                gpu_start - gpu_free))
         lane_free, gpu_free = lane_end, gpu_end
     return StepSchedule(mode=mode, layers=tuple(out), total_ms=gpu_free)
+
+
+SCHEDULE_COLUMNS = ("step", "layer", "mode", "eval_ms", "cold_ms", "warm_ms", "compute_ms", "decompress_ms",
+                    "theta", "idle_ms")
+
+
+def schedule_rows(step: int, schedule: StepSchedule) -> list[list]:
+    """schedule.csv rows (pipeline.py:244-276)."""
+    return [[step, t.layer, schedule.mode] + [str(v) for v in (t.eval_ms, t.cold_ms, t.warm_ms, t.compute_ms,
+                                                                 t.decompress_ms, t.theta, t.idle_ms)]
+            for t in schedule.layers]
 
 
 def compare_modes(loads: Sequence[LayerLoad], params: PipelineParams) -> dict[str, float]:
