@@ -344,3 +344,26 @@ def test_decoder_append_odd_context_matches_oracle(ops, dt):
             kn = kt[:, n:n + 1].permute(1, 0, 2).expand(L, -1, -1).contiguous()
             vn = vt[:, n:n + 1].permute(1, 0, 2).expand(L, -1, -1).contiguous()
             dec.append(kn, vn)
+
+
+def test_int4_select3_many_lanes(ops):
+    """INT4 keys (many exact score ties from the 4-bit codes) through the many-lane selector at
+    64K: sets bit-exact against the canonical scores of the dequantised keys."""
+    lanes, n, d, C = 38, 65536, 128, 64
+    k = math.ceil(0.1 * n)
+    kt, vt, Kd, Vd, Q = _i4_lanes(ops, "random", lanes, n, d, seed=9)
+    del Vd
+    qt = torch.from_numpy(Q).cuda()
+    amax, amin = ops.abstract_build(kt, n, C)
+    ws = ops.LayerWorkspace(lanes, n, ops.n_grid_leaves(n, C), d, qt.device)
+    out = {"sel_tok": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "sel_score": torch.empty((lanes, k), dtype=torch.float64, device="cuda"),
+           "n_sel": torch.empty(lanes, dtype=torch.int32, device="cuda"),
+           "out": torch.empty((lanes, d), dtype=torch.float32, device="cuda")}
+    ops.select_attend(qt, kt, vt, amax, amin, n, k, C, ws, out)
+    s = ops.token_scores(qt.double(), torch.from_numpy(Kd).cuda(), n)
+    ref = torch.sort(torch.sort(-s, dim=1, stable=True).indices[:, :k], dim=1).values
+    bad = (out["sel_tok"].long() != ref).any(1).nonzero().flatten().tolist()
+    assert not bad, bad[:5]
+    for i in (0, lanes - 1):
+        assert np.array_equal(out["sel_tok"][i].cpu().numpy().astype(np.int64), O.topk(O.dots(Q[i], Kd[i]), k))

@@ -308,3 +308,34 @@ def test_chunk_bounds_fast_sound_and_tight(ops, kind, d, C, n):
         for c in range(m):
             seg = dots[i, c * C:min(n, (c + 1) * C)]
             assert seg.max() <= Uf[i, c] and seg.min() >= Lf[i, c]
+
+
+@pytest.mark.parametrize("kind", ["ties", "neartie", "planted"])
+def test_select3_many_lanes_matches_oracle(ops, kind):
+    """The many-lane selector (CTA per lane, used from 37 lanes up; the decode step runs it at
+    256 lanes) at 64K with exact and near ties: sets bit-exact, ties to the lowest index.
+    Reference: the canonical K4 scores (bit-exact vs the oracle, test_token_scores_bitexact)
+    ordered by (score desc, index asc); three lanes re-checked against the C oracle itself."""
+    lanes, n, d, C = 38, 65536, 128, 64
+    k = math.ceil(0.1 * n)
+    K, V, Q = _lane_data(kind, lanes, n, d, seed=77)
+    kt = torch.from_numpy(K).bfloat16().cuda()
+    del K
+    vt = torch.from_numpy(V).bfloat16().cuda()
+    del V
+    qt = torch.from_numpy(Q).cuda()
+    amax, amin = ops.abstract_build(kt, n, C)
+    ws = ops.LayerWorkspace(lanes, n, ops.n_grid_leaves(n, C), d, kt.device)
+    out = {"sel_tok": torch.empty((lanes, k), dtype=torch.int32, device="cuda"),
+           "sel_score": torch.empty((lanes, k), dtype=torch.float64, device="cuda"),
+           "n_sel": torch.empty(lanes, dtype=torch.int32, device="cuda"),
+           "out": torch.empty((lanes, d), dtype=torch.float32, device="cuda")}
+    ops.select_attend(qt, kt, vt, amax, amin, n, k, C, ws, out)
+    s = ops.token_scores(qt.double(), kt, n)
+    ref = torch.sort(torch.sort(-s, dim=1, stable=True).indices[:, :k], dim=1).values
+    got = out["sel_tok"].long()
+    bad = (got != ref).any(1).nonzero().flatten().tolist()
+    assert not bad, (kind, bad[:5])
+    Kh = kt.double().cpu().numpy()
+    for i in (0, lanes // 2, lanes - 1):
+        assert np.array_equal(got[i].cpu().numpy(), O.topk(O.dots(Q[i], Kh[i]), k)), i
