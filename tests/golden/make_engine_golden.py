@@ -50,7 +50,29 @@ def main():
                            "summary": (od / "summary.json-lines").read_text()}
         E.write_ablation(results, Path(td) / "abl")
         ablate_csv = (Path(td) / "abl" / "ablate.csv").read_text()
-    OUT.write_text(json.dumps({"spec": SPEC, "rows": rows, "ablate": ablate_csv}))
+    # second case: no values (quality columns nan), explicit tier budget, placement chunk 16
+    spec2 = dict(SPEC, has_values=False, seed=12, n_context=300, placement_chunk=16, n_steps=2)
+    hdr2 = TraceHeader(n_layers=spec2["n_layers"], n_heads=spec2["n_heads"], head_dim=spec2["head_dim"],
+                       n_context=spec2["n_context"], n_steps=spec2["n_steps"], has_values=False)
+    tr2 = generate_synthetic(DesertProfile(seed=spec2["seed"]), hdr2)
+    rec = 2 * 16 * spec2["head_dim"] * 2
+    tier2 = {"hot_capacity": 2 * spec2["n_heads"] * 2 * spec2["n_context"] * spec2["head_dim"] * 2 + 6 * rec,
+             "warm_capacity": 5 * rec, "early_layers_pinned": 2}
+    rows2 = {}
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "t2.kvtr"
+        write_trace(tr2, p)
+        from kvtier.tiered_store import TierConfig
+        cfg = E.RunConfig(trace_path=str(p), placement_chunk=16, tier=TierConfig(cold_dir=td, **tier2))
+        for label, rep in E.ablate(cfg, Path(td) / "work"):
+            od = Path(td) / ("out-" + label.replace("+", "plus-").lower())
+            E.write_report(rep, od)
+            with open(od / "steps.csv") as fh:
+                rows2[label] = {"steps": list(csv.reader(fh)), "ledger": (od / "ledger.csv").read_text(),
+                                "schedule": (od / "schedule.csv").read_text(),
+                                "summary": (od / "summary.json-lines").read_text()}
+    OUT.write_text(json.dumps({"spec": SPEC, "rows": rows, "ablate": ablate_csv,
+                               "case2": {"spec": spec2, "tier": tier2, "rows": rows2}}))
     print(f"wrote {OUT}")
 
 

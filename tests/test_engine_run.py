@@ -22,9 +22,9 @@ CASE = json.loads((Path(__file__).parent / "golden" / "engine_cases.json").read_
 FLOAT_TOL = ("output_similarity", "dropped_mass")
 
 
-def _write_trace(path):
+def _write_trace(path, sp=None):
     from paper_2506_20187_b200 import trace as T
-    sp = CASE["spec"]
+    sp = sp or CASE["spec"]
     prof = synth.Profile(desert_rate=sp["desert_rate"], n_hot_regions=sp["n_hot_regions"],
                          score_gap=sp["score_gap"], seed=sp["seed"])
     K, Q, V = synth.trace(prof, sp["n_layers"], sp["n_heads"], sp["n_context"], sp["head_dim"], sp["n_steps"],
@@ -88,3 +88,38 @@ def test_ablation_reports_match_reference(tmp_path):
         assert g.split(",")[:4] == w.split(",")[:4] and g.split(",")[5] == w.split(",")[5]
     means = {lab: np.mean([r.eval_count for r in rep.rows]) for lab, rep in results}
     assert means["+IAKM"] < means["+LKA"]  # adaptive evaluation scores fewer than every token
+
+
+@pytest.mark.gpu
+def test_no_values_trace_with_explicit_tier(tmp_path):
+    """Second reference run: a trace without values (output_similarity / dropped_mass are nan
+    in both), an explicit TierConfig and 16-token records."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_20187_b200 import engine as E
+    from paper_2506_20187_b200.tiered_store import TierConfig
+    c2 = CASE["case2"]
+    tp = tmp_path / "t2.kvtr"
+    _write_trace(tp, c2["spec"])
+    cfg = E.RunConfig(trace_path=str(tp), placement_chunk=c2["spec"]["placement_chunk"],
+                      tier=TierConfig(cold_dir=tmp_path / "unused", **c2["tier"]))
+    for label, rep in E.ablate(cfg, tmp_path / "work"):
+        ref = c2["rows"][label]
+        od = tmp_path / ("out-" + label.replace("+", "plus-").lower())
+        E.write_report(rep, od)
+        with open(od / "steps.csv") as fh:
+            got = list(csv.reader(fh))
+        cols = ref["steps"][0]
+        iakm = "iakm" in dict(E.ABLATION_ROWS)[label]
+        check = ["step", "layer", "recall", "desert_rate", "output_similarity", "dropped_mass"] if iakm else cols
+        assert len(got) == len(ref["steps"])
+        for g, w in zip(got[1:], ref["steps"][1:]):
+            gr, wr = dict(zip(cols, g)), dict(zip(cols, w))
+            for col in check:
+                assert gr[col] == wr[col], (label, gr["step"], gr["layer"], col, gr[col], wr[col])
+        assert json.loads((od / "summary.json-lines").read_text().splitlines()[0]) == \
+            json.loads(ref["summary"].splitlines()[0])
+        if not iakm:
+            assert (od / "ledger.csv").read_text() == ref["ledger"], label
+            assert (od / "schedule.csv").read_text() == ref["schedule"], label
