@@ -391,15 +391,21 @@ def place_initial(*args, chunk_size: int = 64, spans_by_lane: dict | None = None
           -- bookkeeping only (the decoder holds the bytes in HBM / pinned host memory)."""
     trace = None
     if args and hasattr(args[0], "header"):
-        trace, config = args[0], (args[1] if len(args) > 1 else kw.pop("config"))
+        if len(args) > 3:
+            raise TypeError("place_initial(trace, config, chunk_size=64, *, spans_by_lane=None)")
+        trace, config = args[0], (args[1] if len(args) > 1 else kw.pop("config", None))
         if len(args) > 2:
             chunk_size = args[2]
         h = trace.header
         n_layers, n_heads, head_dim, n_context = h.n_layers, h.n_heads, h.head_dim, h.n_context
     else:
+        if len(args) not in (5, 6):
+            raise TypeError("place_initial(n_layers, n_heads, head_dim, n_context, config, chunk_size=64, ...)")
         n_layers, n_heads, head_dim, n_context, config = args[:5]
         if len(args) > 5:
             chunk_size = args[5]
+    if kw or config is None:
+        raise TypeError(f"place_initial: unexpected arguments {sorted(kw)}" if kw else "place_initial: missing config")
     store = TieredStore(config, n_layers, n_heads, head_dim, on_move)
     files = trace is not None and config.cold_dir is not None
     if files:

@@ -89,3 +89,15 @@ def test_ledger_csv_and_move_hook(tmp_path):
     store.write_ledger(tmp_path / "ledger.csv")
     lines = (tmp_path / "ledger.csv").read_text().splitlines()
     assert lines[0].split(",") == list(ts.LEDGER_COLUMNS) and len(lines) == 2
+
+
+def test_place_initial_call_forms():
+    from paper_2506_20187_b200 import tiered_store as ts
+    cfg = ts.TierConfig(hot_capacity=4096, warm_capacity=4096, early_layers_pinned=0)
+    a = ts.place_initial(1, 1, 8, 64, cfg, 16)
+    b = ts.place_initial(1, 1, 8, 64, cfg, chunk_size=16)
+    assert [r.start for r in a.lane_records(0, 0)] == [r.start for r in b.lane_records(0, 0)] == [0, 16, 32, 48]
+    with pytest.raises(TypeError):
+        ts.place_initial(1, 1, 8, 64, cfg, chunk=16)
+    with pytest.raises(TypeError):
+        ts.place_initial(1, 1, 8)
