@@ -36,6 +36,21 @@ o = {"sel_tok": torch.empty((2, kk), dtype=torch.int32, device="cuda"),
      "out": torch.empty((2, 128), dtype=torch.float32, device="cuda")}
 ops.select_attend(torch.randn((2, 128), device="cuda"), kt, kt, amax, amin, 16384, kk, 64, ws, o)
 torch.cuda.synchronize()
+# many lanes (>= 37: the CTA-per-lane select3 path the decode step uses), random keys (every
+# token a candidate) and all-equal keys (one tie bucket larger than the list: the fallback)
+for dt in (ops.I4, torch.bfloat16):
+    for kind in ("random", "ties"):
+        dec = SparseDecoder(3, 10, 4, 128, 8192, dtype=dt, device="cuda")
+        k = torch.randn((dec.lanes, 8192, 128), device="cuda", dtype=torch.bfloat16)
+        if kind == "ties":
+            k = torch.ones_like(k)
+        v = torch.randn_like(k)
+        for l in range(3):
+            dec.load_layer(l, k, v)
+        dec.set_length(8192)
+        out = dec.step(torch.randn((3, dec.lanes, 128), device="cuda"))
+        torch.cuda.synchronize()
+        assert torch.isfinite(out).all()
 # codec round trip + attention helpers
 x = torch.randn((4, 777, 128), device="cuda", dtype=torch.bfloat16)
 rec = ops.I4KV.empty(4, 777, 128, "cuda")
