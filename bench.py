@@ -1,30 +1,42 @@
 """bench.py -- decode tokens/s of the LeoAM selection + sparse-decode hot path on B200.
 
-Workload (BASELINE.json metric "decode tokens/s @ LLaMA-7B shape, 64K ctx"): one decode
-step = for every one of the 32 layers, for every (batch row, head) lane: chunk bounds (K3),
-lower-bound pruning (plan), canonical f64 scoring of candidate keys (K4), exact top-k
+Workload (BASELINE.json metric "decode tokens/s @ LLaMA-7B shape, 64K ctx"; configs[2] =
+config 3): one decode step = for every one of the 32 layers, for every (batch row, head)
+lane: chunk bounds (K3), lower-bound pruning (plan), candidate scoring (K4), exact top-k
 (K5, rate 0.5 in layers 0-1 and 0.1 after, engine.py:83-86), runs (K6) and sparse
 attention over the selected set (K7).  LLaMA-7B attention shape: 32 layers x 32 heads x
-d=128, 64K tokens of resident bf16 KV per lane, synthetic planted-desert KV
-(trace.py:270-315 model, generated on device) or N(0,1) KV.  The dense model body (QKV/O/MLP
-GEMMs) is not part of the hot path and is not run.
+d = 128, 64K resident tokens per lane, global batch 8, KV stored as INT4 records (K8
+compression: config 3 is 256 GiB in bf16 and does not fit one B200).  The KV is the
+planted-desert model of the reference generator (trace.py:270-315) drawn by the counter-hash
+generator in workload.py / csrc/synth.cu, so any lane can be regenerated on the host.  The
+dense model body (QKV/O/MLP GEMMs) is not part of the hot path and is not run.
 
-Timing: W warm-up steps, then K steps replayed from one CUDA graph, bracketed by
-barrier + synchronize, CUDA events on the launching stream, max over ranks.  KV is
->= 32 GiB per GPU, far beyond the 126 MB L2, so no flush is needed.  `e2e` repeats the
-measurement through the same public API with the step's queries copied from pinned host
-memory and the attention outputs copied back every step.
+Timing: W warm-up steps, then K steps replayed from one CUDA graph, bracketed by barrier +
+synchronize, CUDA events on the launching stream, max over ranks.  KV >= 10 GiB per GPU,
+far beyond the 126 MB L2, so no flush is needed.  `e2e` repeats the measurement through the
+same public API with the step's queries copied from pinned host memory and the attention
+outputs copied back every step.
 
---kv-heads 8 --ctx 131072 --batch 16: config 4 (LLaMA-3-8B GQA shape, 4 query heads per KV
-head sharing its K/V and abstracts).
+After timing, `parity` checks a sample of lanes of the measured workload against the C
+oracle (checker only): the device-resident INT4 codes against the oracle codec applied to
+the host-regenerated lane, the selected set against the oracle's canonical exact top-k over
+the dequantised keys, and the attention output against the oracle's f64 attention.
 
-Multi-GPU (torchrun): every rank owns a disjoint batch of lanes (batch x head sharding,
-no collective on the data path); value = all ranks' tokens / max-over-ranks time.
+Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run; the driver's own
+torchrun launch is used as is).  Strong scaling (default): config 3's global batch stays 8
+and its (batch row, KV head) lanes are split over the ranks -- batch x head sharding, no
+collective on the data path; value = global batch / max-over-ranks step time.
+`--scaling weak`: --batch rows per GPU.
+
+--kv-heads 8 --ctx 131072 --batch 16: config 4 (LLaMA-3-8B GQA shape).
 
 --impl reference: the reference algorithm (kvtier's branch-and-bound select_top_k +
-attention_output, restated in C in oracle/, the reference itself is pure Python and
-cannot travel to the GPU box) on a bounded sample of the same workload's lanes, all host
-threads, extrapolated to the whole step.
+attention_output, restated in C in oracle/; the reference itself is pure Python and cannot
+travel to the GPU box) over a bounded sample of the SAME lanes (regenerated on the host,
+INT4 round trip through the oracle codec = the values the GPU decodes), all host threads,
+extrapolated to the whole step.
+
+--dry-run: the launcher / sharding / max-over-ranks plumbing on CPU (gloo), no kernels.
 """
 
 from __future__ import annotations
@@ -36,6 +48,7 @@ import os
 import subprocess
 import sys
 import time
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 import numpy as np
@@ -44,88 +57,110 @@ ROOT = Path(__file__).resolve().parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
+import workload as W  # noqa: E402
+
 N_LAYERS, N_HEADS, HEAD_DIM = 32, 32, 128  # LLaMA-7B attention shape
+METRIC = "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline"
+SPEC_HBM_GBS = 8000.0
+EARLY_LAYERS, EARLY_RATE, RATE, EARLY_C, C_DEFAULT = 2, 0.5, 0.1, 8, 64
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--batch", type=int, default=8, help="batch rows per GPU (config 3: 8)")
+    p.add_argument("--batch", type=int, default=8, help="global batch (strong scaling; config 3: 8)")
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="strong: --batch is the global batch split over the GPUs; weak: --batch rows per GPU")
     p.add_argument("--ctx", type=int, default=65536)
     p.add_argument("--data", choices=["planted", "random"], default="planted")
-    p.add_argument("--dtype", choices=["bf16", "f32", "int4"], default="int4",
-                   help="KV storage: bf16/f32 rows or INT4 records (K8 compression, config 3)")
+    p.add_argument("--dtype", choices=["bf16", "int4"], default="int4",
+                   help="KV storage: bf16 rows or INT4 records (K8 compression, config 3)")
     p.add_argument("--layers", type=int, default=N_LAYERS)
     p.add_argument("--kv-heads", type=int, default=N_HEADS,
                    help="KV heads (GQA; config 4 = LLaMA-3-8B: 8 KV heads for 32 query heads)")
-    p.add_argument("--cpu-lanes", type=int, default=16, help="lanes in the CPU baseline sample")
-    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--cpu-lanes", type=int, default=64,
+                   help="CPU sample: half from layer 0 (rate 0.5, C=8), half from layer 16 (rate 0.1, C=64)")
+    p.add_argument("--cpu-steps", type=int, default=2, help="decode steps per CPU sample lane (first = cold)")
+    p.add_argument("--parity-lanes", type=int, default=6, help="KV lanes per checked layer")
+    p.add_argument("--no-parity", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--sub", type=str, default="random,config2",
+                   help="extra sub-records in the same run: 'random' (config 3 with N(0,1) KV), "
+                        "'config2' (32K, B=1, bf16); '' for none")
+    p.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no kernels")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--json-out", type=str, default="")
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 # ------------------------------------------------------------------------------------------------
-# synthetic workload
+# sharding (batch x KV-head lanes)
 # ------------------------------------------------------------------------------------------------
 
 
-def planted_regions(rng, n, desert_rate=0.7, n_regions=3):
-    """Hot-region placement of trace.py:220-267 (multinomial gaps between 3 runs)."""
-    n_hot = math.ceil((1.0 - desert_rate) * n)
-    r = min(n_regions, n_hot, n - n_hot + 1)
-    base, extra = divmod(n_hot, r)
-    sizes = [base + (1 if i < extra else 0) for i in range(r)]
-    slack = n - n_hot - (r - 1)
-    gaps = rng.multinomial(slack, [1.0 / (r + 1)] * (r + 1)) if slack > 0 else [0] * (r + 1)
-    out, pos = [], int(gaps[0])
-    for i, s in enumerate(sizes):
-        out.append((pos, pos + s))
-        pos += s + (1 + int(gaps[i + 1]) if i < r - 1 else 0)
-    return out
+def shard_plan(batch: int, heads: int, kv_heads: int, world: int, rank: int, scaling: str = "strong") -> dict:
+    """Lanes owned by `rank`.  A unit is one (batch row, KV head) lane with its g query heads;
+    strong scaling splits the global batch's units into contiguous equal blocks (batch rows
+    when world divides the batch, else heads within rows); weak gives every rank `batch` rows."""
+    if heads % kv_heads:
+        raise ValueError("heads must be a multiple of kv_heads")
+    g = heads // kv_heads
+    if scaling == "weak":
+        units = batch * kv_heads
+        kv0 = rank * units
+        global_batch = batch * world
+    else:
+        total = batch * kv_heads
+        if total % world:
+            raise ValueError(f"{world} GPUs do not divide {batch} x {kv_heads} (batch x KV head) lanes")
+        units = total // world
+        kv0 = rank * units
+        global_batch = batch
+    return {"kv0": kv0, "kv_lanes": units, "q0": kv0 * g, "q_lanes": units * g, "group": g,
+            "global_batch": global_batch, "world": world, "rank": rank}
 
 
-def fill_layer(torch, K, V, n, d, data, rng, gen, u_out):
-    """Fill one layer's K/V [lanes, n_cap, d] on device; returns per-lane unit directions."""
-    lanes = K.shape[0]
-    dev = K.device
-    if data == "random":
-        for i in range(lanes):
-            K[i, :n].normal_(generator=gen)
-            V[i, :n].normal_(generator=gen)
-        u = torch.randn((lanes, d), device=dev, generator=gen)
-        u_out.copy_(u)
-        return
-    u = torch.randn((lanes, d), device=dev, generator=gen, dtype=torch.float64)
-    u /= u.norm(dim=1, keepdim=True)
-    u_out.copy_(u)
-    scale = 0.05 / math.sqrt(d)
-    for i in range(lanes):
-        amps = rng.uniform(-0.25, 0.25, size=n)
-        hot_base = 0.25 + 1.0 + 0.02
-        for s, e in planted_regions(rng, n):
-            amps[s:e] = hot_base + rng.uniform(0.0, 0.5, size=e - s)
-        a = torch.from_numpy(amps).to(dev)
-        noise = torch.randn((n, d), device=dev, generator=gen, dtype=torch.float32) * scale
-        ui = u[i].float()
-        noise -= (noise @ ui)[:, None] * ui[None, :]
-        K[i, :n] = (a.float()[:, None] * ui[None, :] + noise).to(K.dtype)
-        V[i, :n].normal_(generator=gen)
+def rate_of(layer: int) -> float:
+    return EARLY_RATE if layer < EARLY_LAYERS else RATE
 
 
-def make_queries(torch, u, steps, data, gen):
-    """[steps, L, lanes, d] f32: gain*u for planted lanes (trace.py:309-310), N(0,1) otherwise."""
-    L, lanes, d = u.shape
-    if data == "random":
-        return torch.randn((steps, L, lanes, d), device=u.device, generator=gen)
-    gains = torch.rand((steps, L, lanes, 1), device=u.device, generator=gen, dtype=torch.float64) + 1.0
-    return (gains * u[None].double()).float()
+def chunk_of(layer: int) -> int:
+    return EARLY_C if layer < EARLY_LAYERS else C_DEFAULT
+
+
+def workload_config(args, world: int, global_batch: int) -> dict:
+    model = "llama7b" if args.kv_heads == N_HEADS else f"llama3-8b-gqa{N_HEADS // args.kv_heads}"
+    return {"workload": f"{model}-attn-{args.ctx // 1024}k-b{global_batch}-{args.dtype}-{args.data}",
+            "kv_heads": args.kv_heads, "layers": args.layers, "heads": N_HEADS, "head_dim": HEAD_DIM,
+            "context": args.ctx, "global_batch": global_batch,
+            "batch_per_gpu": global_batch / world, "importance_rate": RATE, "early_layer_rate": EARLY_RATE,
+            "chunk": {"early_layers": EARLY_C, "other": C_DEFAULT},
+            "parallelism": f"batch x KV-head lane sharding over {world} GPU(s) ({args.scaling} scaling), "
+                           "no collective on the data path",
+            "generator": "workload.py counter-hash planted-desert model (trace.py:270-315), seed "
+                         f"{args.seed}",
+            "l2": "inputs (KV >= 10 GiB/GPU) >> 126 MB L2; no flush"}
+
+
+# ------------------------------------------------------------------------------------------------
+# launcher
+# ------------------------------------------------------------------------------------------------
+
+
+def relaunch(argv: list[str], n: int) -> int:
+    """Re-exec this script under torch.distributed.run with n ranks on 127.0.0.1."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + argv
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 # ------------------------------------------------------------------------------------------------
@@ -196,56 +231,65 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-# reference arm / cpu baseline
+# CPU reference sample (checker library; cpu_baseline leg and --impl reference only)
 # ------------------------------------------------------------------------------------------------
 
 
-def cpu_sample_lanes(args):
-    """Bounded sample of the workload's lanes: heads 0..h-1 of layer 0 (rate 0.5, C=8) and
-    layer 16 (rate 0.1, C=64) -- BASELINE.md sec. 3 -- generated on the host."""
-    from oracle import synth
-    h = max(1, args.cpu_lanes // 2)
+def host_lane(O, n, d, p, i, gen, dtype, keys=True, values=True):
+    """Host regeneration of KV lane i of a layer's params -> (K, V) f32, as the GPU decodes them
+    (bf16 values; INT4: round trip through the oracle codec, bit-identical to K8)."""
+    K, V = O.synth_lane(n, d, p["seed"][i], p["u"][i], p["regions"][i], gen, keys, values)
+    if dtype == "int4":
+        K = None if K is None else O.i4_dequant(O.i4_quant(K), d)
+        V = None if V is None else O.i4_dequant(O.i4_quant(V), d)
+    return K, V
+
+
+def cpu_sample(args, O, threads: int) -> list[dict]:
+    """BASELINE.md sec. 3 sample: query lanes 0..h-1 (batch row 0) of layer 0 (rate 0.5, C=8)
+    and layer 16 (rate 0.1, C=64), --cpu-steps decode steps each, regenerated on the host."""
     n, d = args.ctx, HEAD_DIM
-    groups = []
-    for layer, rate, C in ((0, 0.5, 8), (16, 0.1, 64)):
-        K = np.empty((h, n, d), np.float32)
-        V = np.empty((h, n, d), np.float32)
-        Q = np.empty((args.cpu_steps, h, d), np.float32)
-        for i in range(h):
-            if args.data == "planted":
-                k, q, v, _ = synth.lane(synth.Profile(0.7, 3, 1.0, args.seed), layer, i, n, d, args.cpu_steps)
-            else:
-                rng = np.random.default_rng([args.seed, layer, i])
-                k = rng.normal(size=(n, d)).astype(np.float32)
-                v = rng.normal(size=(n, d)).astype(np.float32)
-                q = rng.normal(size=(args.cpu_steps, d)).astype(np.float32)
-            K[i], V[i], Q[:, i] = k, v, q
-        groups.append((layer, rate, C, K, V, Q))
-    return groups
+    g = N_HEADS // args.kv_heads
+    h = max(1, args.cpu_lanes // 2)
+    gen = W.gen_args(None, d, args.data)
+    out = []
+    for layer in (0, min(16, args.layers - 1)):
+        q_lanes = np.arange(h)
+        kv = np.unique(q_lanes // g)
+        p = W.lane_params(args.seed, layer, kv, n, d, args.data)
+        with ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL
+            kvs = list(ex.map(lambda i: host_lane(O, n, d, p, i, gen, args.dtype), range(len(kv))))
+        K = np.stack([kvs[int(j) // g][0] for j in q_lanes])
+        V = np.stack([kvs[int(j) // g][1] for j in q_lanes])
+        Q = W.queries(args.seed, args.cpu_steps, layer, q_lanes, g, p["u"], 0, d, args.data)
+        out.append({"layer": layer, "rate": rate_of(layer), "C": chunk_of(layer), "K": K, "V": V, "Q": Q})
+    return out
 
 
-def cpu_baseline(args, lanes_per_layer):
-    """Time the reference algorithm on the sample with all host threads; extrapolate."""
-    from oracle import oracle as O
-    threads = O.host_threads()
-    groups = cpu_sample_lanes(args)
-    per_lane = {}
-    total_lane_steps = 0
-    wall = 0.0
-    for layer, rate, C, K, V, Q in groups:
-        n = K.shape[1]
-        r = O.bench_lanes(K, V, Q, math.ceil(rate * n), O.next_pow2(n) // C, threads)
-        lane_steps = K.shape[0] * Q.shape[0]
-        per_lane[layer] = r["lane_step_s"]  # thread-seconds per lane-step (select + attention)
-        total_lane_steps += lane_steps
-        wall += r["wall_s"]
-    early = 2
-    cpu_s = (early * lanes_per_layer * per_lane[0] + (args.layers - early) * lanes_per_layer * per_lane[16])
-    step_s = cpu_s / threads
-    return {"step_s": step_s, "threads": threads, "per_lane_s": per_lane, "sample_wall_s": wall,
-            "sample": (f"{total_lane_steps} lane-steps: heads 0-{K.shape[0]-1} of layers 0 (rate 0.5, C=8) and 16 "
-                       f"(rate 0.1, C=64), {args.ctx} tokens, {args.data} KV; extrapolated linearly to "
-                       f"{args.layers}x{lanes_per_layer} lanes per step, ideal scaling over {threads} threads")}
+def cpu_run(args, O, sample: list[dict], threads: int, lanes_per_layer: int) -> dict:
+    """One pass of the reference algorithm over the sample; extrapolated step time from the
+    warm decode step (the last of --cpu-steps; the first builds the partition's refinement)."""
+    n = args.ctx
+    step_s = 0.0
+    per = {}
+    for s in sample:
+        r = O.bench_lanes(s["K"], s["V"], s["Q"], math.ceil(s["rate"] * n), O.next_pow2(n) // s["C"], threads)
+        wall = float(r["step_wall_s"][-1])  # warm step, critical path over the threads
+        n_layers = EARLY_LAYERS if s["layer"] < EARLY_LAYERS else max(0, args.layers - EARLY_LAYERS)
+        step_s += wall * n_layers * lanes_per_layer / s["K"].shape[0]
+        per[s["layer"]] = {"warm_wall_s": wall, "lanes": int(s["K"].shape[0]),
+                           "lane_step_s_warm": float(r["lane_step_times"][-1].mean()),
+                           "lane_step_s_cold": float(r["lane_step_times"][0].mean()),
+                           "evals_warm_mean": float(r["evals"][-1].mean())}
+    return {"step_s": step_s, "per_layer": per}
+
+
+def cpu_sample_text(args, sample, threads, lanes_per_layer):
+    return (f"{sum(s['K'].shape[0] for s in sample)} lanes x {args.cpu_steps} steps: query lanes 0-"
+            f"{sample[0]['K'].shape[0] - 1} of layers 0 (rate 0.5, C=8) and {sample[-1]['layer']} (rate 0.1, C=64), "
+            f"{args.ctx} tokens, the bench's own {args.data} lanes regenerated on the host "
+            f"({args.dtype} values as decoded by the GPU); warm step timed, critical path over {threads} threads, "
+            f"extrapolated linearly to {args.layers} x {lanes_per_layer} lanes per step")
 
 
 def run_reference(args):
@@ -253,37 +297,64 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    lanes = args.batch * N_HEADS * max(1, world)
-    samples = []
+    from oracle import oracle as O
+    n_gpus = max(args.gpus, world)
+    sp = shard_plan(args.batch, N_HEADS, args.kv_heads, n_gpus if args.scaling == "weak" else 1, 0, args.scaling)
+    gb = sp["global_batch"] if args.scaling == "strong" else args.batch * n_gpus
+    lanes = gb * N_HEADS
+    threads = O.host_threads()
+    sample = cpu_sample(args, O, threads)
+    steps = []
     for s in range(args.warmup + args.steps):
-        r = cpu_baseline(args, lanes)
+        r = cpu_run(args, O, sample, threads, lanes)
         if s >= args.warmup:
-            samples.append(r)
-    step_s = float(np.mean([r["step_s"] for r in samples]))
-    value = args.batch * max(1, world) / step_s
+            steps.append(r["step_s"])
+    step_s = float(np.mean(steps))
+    value = gb / step_s
     line = {
-        "metric": "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline",
-        "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": f"synthetic {args.data} KV (host, oracle.synth)",
-        "config": workload_config(args, max(1, world)),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": samples[0]["threads"], "kind": "port",
-                         "sample": samples[0]["sample"]},
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic {args.data} KV (workload.py generator, regenerated on the host)",
+        "config": workload_config(args, n_gpus, gb),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": cpu_sample_text(args, sample, threads, lanes)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(args, world):
-    model = "llama7b" if args.kv_heads == N_HEADS else f"llama3-8b-gqa{N_HEADS // args.kv_heads}"
-    return {"workload": f"{model}-attn-{args.ctx // 1024}k-b{args.batch * world}-{args.dtype}-{args.data}",
-            "kv_heads": args.kv_heads,
-            "layers": args.layers, "heads": N_HEADS, "head_dim": HEAD_DIM, "context": args.ctx,
-            "global_batch": args.batch * world, "batch_per_gpu": args.batch, "importance_rate": 0.10,
-            "early_layer_rate": 0.50, "chunk": {"early_layers": 8, "other": 64},
-            "parallelism": f"batch x head sharding over {world} GPU(s), no collective",
-            "l2": "inputs (KV >= 32 GiB/GPU) >> 126 MB L2; no flush"}
+# ------------------------------------------------------------------------------------------------
+# dry run (CPU plumbing)
+# ------------------------------------------------------------------------------------------------
+
+
+def run_dry(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    sp = shard_plan(args.batch, N_HEADS, args.kv_heads, world, rank, args.scaling)
+    p = W.lane_params(args.seed, 0, np.arange(sp["kv0"], sp["kv0"] + sp["kv_lanes"]), args.ctx, HEAD_DIM, args.data)
+    t0 = time.perf_counter()
+    _ = W.queries(args.seed, 1, 0, np.arange(sp["q0"], sp["q0"] + sp["q_lanes"]), sp["group"], p["u"], sp["kv0"],
+                  HEAD_DIM, args.data)
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / max(args.steps, 1)], dtype=torch.float64)
+    lanes = torch.tensor([sp["q_lanes"]], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lanes)
+        dist.destroy_process_group()
+    if rank == 0:
+        gb = sp["global_batch"]
+        print(json.dumps({"metric": METRIC, "dry_run": True, "value": gb / (float(ms) / 1e3), "unit": "tokens/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(ms),
+                          "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+                          "lanes_total": int(lanes), "config": workload_config(args, world, gb)}), flush=True)
+    return 0
 
 
 # ------------------------------------------------------------------------------------------------
@@ -291,52 +362,103 @@ def workload_config(args, world):
 # ------------------------------------------------------------------------------------------------
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    from paper_2506_20187_b200 import ops
-    from paper_2506_20187_b200.decode import SparseDecoder
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    dt = {"bf16": torch.bfloat16, "f32": torch.float32, "int4": ops.I4}[args.dtype]
-    L = args.layers
-    dec = SparseDecoder(L, args.batch, N_HEADS, HEAD_DIM, args.ctx, dtype=dt, device=dev, n_kv_heads=args.kv_heads)
-    gqa = ops.kv_group(dec.kv_group)  # standalone stage calls (attribution, self-check) read KV lane i // g
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000 * args.seed + rank)
-    rng = np.random.default_rng([args.seed, rank])
-    u = torch.empty((L, dec.kv_lanes, HEAD_DIM), device=dev, dtype=torch.float32)  # per KV lane
-    quant_ms = None
+def build_decoder(args, sp, dev, torch, ops, SparseDecoder):
+    """Decoder over the rank's lanes, KV generated on device and compressed with K8 (timed)."""
+    L, n, d = args.layers, args.ctx, HEAD_DIM
+    dt = {"bf16": torch.bfloat16, "int4": ops.I4}[args.dtype]
+    dec = SparseDecoder(L, 1, sp["q_lanes"], d, n, dtype=dt, device=dev, n_kv_heads=sp["kv_lanes"])
+    kv_ids = np.arange(sp["kv0"], sp["kv0"] + sp["kv_lanes"])
+    params = []
+    quant_ms = 0.0
+    gen = W.gen_args(None, d, args.data)
+    kb = vb = None
     if args.dtype == "int4":
-        # generate each layer in bf16, then compress it with K8 (timed: prefill compression)
-        kb = torch.empty((dec.kv_lanes, args.ctx, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+        kb = torch.empty((sp["kv_lanes"], n, d), dtype=torch.bfloat16, device=dev)
         vb = torch.empty_like(kb)
-        qt = 0.0
-        for l in range(L):
-            fill_layer(torch, kb, vb, args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
+    for l in range(L):
+        p = W.lane_params(args.seed, l, kv_ids, n, d, args.data)
+        params.append(p)
+        if args.dtype == "int4":
+            ops.synth_layer(kb, vb, p, n, gen)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             dec.load_layer(l, kb, vb)
             e1.record()
             e1.synchronize()
-            qt += e0.elapsed_time(e1)
-        quant_ms = qt
-        del kb, vb
-        torch.cuda.empty_cache()
-    else:
-        for l in range(L):
-            fill_layer(torch, dec.K[l], dec.V[l], args.ctx, HEAD_DIM, args.data, rng, gen, u[l])
-    dec.set_length(args.ctx)
+            quant_ms += e0.elapsed_time(e1)
+        else:
+            ops.synth_layer(dec.K[l], dec.V[l], p, n, gen)
+    del kb, vb
+    torch.cuda.empty_cache()
+    dec.set_length(n)
+    return dec, params, (quant_ms if args.dtype == "int4" else None)
+
+
+def make_queries(args, sp, params, steps: int) -> np.ndarray:
+    """[steps, L, q_lanes, d] f32 on the host."""
+    q_ids = np.arange(sp["q0"], sp["q0"] + sp["q_lanes"])
+    return np.stack([W.queries(args.seed, steps, l, q_ids, sp["group"], params[l]["u"], sp["kv0"], HEAD_DIM,
+                               args.data) for l in range(args.layers)], axis=1)
+
+
+def parity_check(args, dec, params, q_host: np.ndarray, sp, torch) -> dict:
+    """Checker (oracle) on a sample of the measured workload's lanes; see the module docstring."""
+    from oracle import oracle as O
+    n, d, g = dec.n, HEAD_DIM, sp["group"]
+    gen = W.gen_args(None, d, args.data)
+    layers = sorted({l for l in (0, 2, 16, args.layers - 1) if 0 <= l < args.layers})
+    nkv = sp["kv_lanes"]
+    step = max(1, nkv // max(1, args.parity_lanes))
+    kv_sample = list(range(0, nkv, step))[:max(1, args.parity_lanes)]
+    qd = torch.from_numpy(q_host).to(dec.device)
+    out = dec.step(qd)
+    torch.cuda.synchronize()
+    bufs = dec._buffers()
+    set_mis = code_mis = checked = 0
+    max_err = 0.0
+    cos_min = 1.0
+    for l in layers:
+        k = dec.k_for(l)
+        sel = bufs[l]["sel_tok"][:, :k].cpu().numpy()
+        o = out[l].cpu().numpy()
+        for i in kv_sample:
+            Kh, Vh = O.synth_lane(n, d, params[l]["seed"][i], params[l]["u"][i], params[l]["regions"][i], gen)
+            if args.dtype == "int4":
+                rk, rv = dec.K.data[l, i, :n].cpu().numpy(), dec.V.data[l, i, :n].cpu().numpy()
+                code_mis += int(np.any(rk != O.i4_quant(Kh), axis=1).sum() + np.any(rv != O.i4_quant(Vh), axis=1).sum())
+                Kd, Vd = O.i4_dequant(rk, d), O.i4_dequant(rv, d)
+            else:
+                Kd = dec.K[l, i, :n].float().cpu().numpy()
+                Vd = dec.V[l, i, :n].float().cpu().numpy()
+                code_mis += int(np.any(Kd != Kh, axis=1).sum() + np.any(Vd != Vh, axis=1).sum())
+            for j in ([i * g + x for x in range(g)] if i == 0 else [i * g]):
+                ref = O.select(q_host[l, j], Kd, k)
+                got = np.sort(sel[j].astype(np.int64))
+                set_mis += int(not np.array_equal(got, ref))
+                att = O.attention(q_host[l, j], Kd, Vd, ref)
+                err = float(np.linalg.norm(o[j] - att) / max(np.linalg.norm(att), 1e-300))
+                max_err = max(max_err, err)
+                cos_min = min(cos_min, float(np.dot(o[j], att) / max(np.linalg.norm(o[j]) * np.linalg.norm(att), 1e-300)))
+                checked += 1
+    return {"lanes_checked": checked, "layers": layers, "kv_lanes": [sp["kv0"] + i for i in kv_sample],
+            "set_mismatches": set_mis, "code_mismatches": code_mis, "max_rel_err": max_err,
+            "min_cosine": cos_min, "attn_tolerance": 2e-3,
+            "oracle": "oracle/kvt_oracle.c: canonical exact top-k (score desc, index asc) + f64 attention "
+                      "over the device-resident KV (dequantised by the oracle codec); codes vs the oracle "
+                      "codec on the host-regenerated lane"}
+
+
+def measure(args, torch, dist, world, rank, local, dev, tag="main", want_cpu=True, want_attrib=True):
+    """Build the workload, time it, check parity.  Returns a dict (JSON-ready pieces)."""
+    from paper_2506_20187_b200 import ops
+    from paper_2506_20187_b200.decode import SparseDecoder
+
+    sp = shard_plan(args.batch, N_HEADS, args.kv_heads, world, rank, args.scaling)
+    L = args.layers
+    dec, params, quant_ms = build_decoder(args, sp, dev, torch, ops, SparseDecoder)
     steps_total = args.warmup + args.steps
-    # query lanes of a GQA group share their KV head's planted direction (own gains)
-    Q = make_queries(torch, u.repeat_interleave(dec.kv_group, dim=1), steps_total, args.data, gen)
+    Qh = make_queries(args, sp, params, steps_total + 1)  # + 1: the parity step
+    Q = torch.from_numpy(Qh).to(dev)
     q_static = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
     out_static = torch.empty((L, dec.lanes, HEAD_DIM), device=dev, dtype=torch.float32)
     torch.cuda.synchronize()
@@ -370,7 +492,7 @@ def run_ours(args):
     # ---- timed region (device-resident inputs) ----
     # KVT_PROFILE_RANGE=1: cudaProfilerStart/Stop around it, for `ncu --profile-from-start off`
     # (launch lists and captures of the decode step only; never a bench number).
-    prof = os.environ.get("KVT_PROFILE_RANGE") == "1"
+    prof = os.environ.get("KVT_PROFILE_RANGE") == "1" and tag == "main"
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -396,13 +518,12 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(ms_all, op=dist.ReduceOp.MAX)
     ms_max = float(ms_all.item())
-    value = args.batch * world / (ms_max / 1e3)
+    value = sp["global_batch"] / (ms_max / 1e3)
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        hq = torch.empty((args.steps, L, dec.lanes, HEAD_DIM), dtype=torch.float32, pin_memory=True)
-        hq.copy_(Q[args.warmup:].cpu())
+        hq = torch.from_numpy(Qh[args.warmup:args.warmup + args.steps]).pin_memory()
         ho = torch.empty((args.steps, L, dec.lanes, HEAD_DIM), dtype=torch.float32, pin_memory=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
@@ -420,35 +541,34 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         nb = L * dec.lanes * HEAD_DIM * 4
-        e2e = {"value": args.batch * world / (float(ems.item()) / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": float(ems.item())}
+        e2e = {"value": sp["global_batch"] / (float(ems.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": float(ems.item()),
+               "per_rank_bytes": True}
+    del graph
+    res = {"sp": sp, "value": value, "ms_max": ms_max, "clocks": clocks, "e2e": e2e, "quant_ms": quant_ms,
+           "bound_grid": bound_grid, "dec": dec}
 
-    # ---- self-check: the fused step's attention equals the standalone K7 on its selections ----
-    # (a GPU-vs-GPU consistency probe of the decoder's shared workspace across layers; the
-    # oracle parity itself lives in tests/)
-    with torch.cuda.stream(stream):
-        q_static.copy_(Q[args.warmup])
-        ref_out = dec.step(q_static)
-        bufs = dec._buffers()
-        chk = 0.0
-        for l in range(L):
-            b = bufs[l]
-            with gqa:
-                o = ops.sparse_decode_attn(dec.V[l], b["sel_tok"], b["sel_score"], b["n_sel"])
-            chk = max(chk, float((o - ref_out[l]).abs().max() / ref_out[l].abs().max().clamp_min(1e-30)))
+    # ---- parity on the measured workload (checker) ----
+    if not args.no_parity:
+        with torch.cuda.stream(stream):
+            res["parity"] = parity_check(args, dec, params, Qh[steps_total], sp, torch)
         stream.synchronize()
 
     # ---- per-kernel attribution ----
-    # The staged pipeline (same kernels as the fused call) is run once to materialise every
-    # layer's intermediates; then each stage's 32 per-layer launches are captured in their
-    # own CUDA graph and replayed between CUDA events on the launching stream, so each
-    # number is the device time of that kernel alone (no host gaps), averaged over reps.
-    stages = ["bounds", "plan", "score", "select", "attn"]
+    if want_attrib:
+        res.update(attribute(args, dec, Q[args.warmup], stream, torch, ops))
+    return res
+
+
+def attribute(args, dec, q_step, stream, torch, ops) -> dict:
+    """Each stage's 32 per-layer launches captured in their own CUDA graph and replayed between
+    CUDA events on the launching stream: the device time of that kernel alone."""
+    L = args.layers
+    gqa = ops.kv_group(dec.kv_group)
     is_i4 = isinstance(dec.K, ops.I4KV)
-    # INT4 keys: estimates from exact int32 inner products on the tensor cores (+ qprep launch)
     score_fn = ops.cand_score_i4mma if is_i4 else ops.cand_score_f32
+    q_static = q_step.clone()
     inter = []
-    n_cand = []
 
     def bounds_fn(l, n, C):  # the K3 variant select_attend runs (fast f32 when absmag is kept)
         _, amax, amin = dec.grid(l)
@@ -457,7 +577,6 @@ def run_ours(args):
         return ops.chunk_bounds(q_static[l], amax, amin, n, C, want_A=True)
 
     with torch.cuda.stream(stream), gqa:
-        q_static.copy_(Q[args.warmup])
         for l in range(L):
             C, n, k = dec.grid(l)[0], dec.n, dec.k_for(l)
             U, Lo, A = bounds_fn(l, n, C)
@@ -482,15 +601,16 @@ def run_ours(args):
                 elif name == "select":
                     ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
                 elif name == "attn":
-                    ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)  # logit_scale 1/sqrt(d): raw dots
+                    ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)
         return run
 
+    stages = ["bounds", "plan", "score", "select", "attn"]
     st_ms = {}
     reps = 3
     for name in stages:
         fn = stage_fn(name)
         with torch.cuda.stream(stream), gqa:
-            fn()  # warm (allocator, attributes)
+            fn()
             stream.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
@@ -505,61 +625,141 @@ def run_ours(args):
             e1.synchronize()
         st_ms[name] = e0.elapsed_time(e1) / reps
         del g
-    algo = dec.algorithmic_bytes(n_cand)
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    return {"stage_ms": st_ms, "n_cand": n_cand, "algo": dec.algorithmic_bytes(n_cand)}
+
+
+def roofline_of(args, res, peaks, world, wl) -> dict:
+    dec = res["dec"]
+    st_ms, algo = res["stage_ms"], res["algo"]
+    stages = list(st_ms)
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    dom = max(stages, key=lambda s: st_ms[s])
     per_kernel = {s: {"ms_per_step": st_ms[s], "algo_bytes": algo[s],
-                      "gbs": algo[s] / (st_ms[s] / 1e3) / 1e9 if st_ms[s] > 0 else None} for s in stages}
+                      "gbs": algo[s] / (st_ms[s] / 1e3) / 1e9 if st_ms[s] > 0 else None,
+                      "frac_measured_peak": (algo[s] / (st_ms[s] / 1e3) / 1e9 / hbm_peak) if st_ms[s] > 0 else None}
+                  for s in stages}
+    dom = max(stages, key=lambda s: st_ms[s])
     staged_total = sum(st_ms.values())
-    # bounds, plan, [INT4: qprep,] score (TMA), select+runs, attn (split + ticket merge)
-    launches_per_layer = 6 if is_i4 else 5
-    sel_gather_bytes = algo["bounds"] + algo["score"] + algo["select"] + algo["attn"]
-    frac_of = "measured" if "hbm_gbs" in peaks else "fallback"
-    # DRAM traffic of the dominant kernel: one ncu --set full capture (layer-2 launch), committed
-    # under profiles/ (tools/gpu_prof.sh); compared with the same launch's algorithmic bytes
     traffic = traffic_algo = None
     tj = ROOT / "profiles" / "traffic.json"
-    wl = workload_config(args, world)["workload"]
     if tj.exists():
         rec = json.loads(tj.read_text()).get("workloads", {}).get(wl, {}).get(dom)
         if rec:
             traffic = rec["dram_bytes"]
-            traffic_algo = dec.algorithmic_bytes(n_cand, layers=[rec["layer"]])[dom]
+            traffic_algo = dec.algorithmic_bytes(res["n_cand"], layers=[rec["layer"]])[dom]
+    ach = per_kernel[dom]["gbs"] or 0.0
+    roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ach / hbm_peak, "spec_peak": SPEC_HBM_GBS, "frac_of_spec": ach / SPEC_HBM_GBS,
+            "traffic": traffic, "traffic_algo_bytes_same_launch": traffic_algo,
+            "traffic_source": "profiles/traffic.json (ncu --set full, one launch)" if traffic else None,
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback",
+            "algo_bytes_per_step": algo[dom], "kernel_ms_per_step": st_ms[dom],
+            "kernel_share_of_staged_step": st_ms[dom] / staged_total if staged_total else None}
+    sel_gather = algo["bounds"] + algo["score"] + algo["select"] + algo["attn"]
+    return {"roofline": roof, "per_kernel": per_kernel,
+            "selection_gather_gbs": sel_gather / (res["ms_max"] / 1e3) / 1e9,
+            "selection_gather_frac": sel_gather / (res["ms_max"] / 1e3) / 1e9 / hbm_peak,
+            "candidate_fraction": float(np.sum(res["n_cand"]) / (args.layers * dec.lanes * dec.n))}
+
+
+def sub_args(args, which: str):
+    a = argparse.Namespace(**vars(args))
+    a.steps = min(args.steps, 20)
+    a.no_e2e = False
+    a.parity_lanes = 3
+    if which == "random":
+        a.data = "random"
+    elif which == "config2":
+        a.ctx, a.batch, a.dtype = 32768, 1, "bf16"
+    else:
+        raise ValueError(f"unknown sub-record {which!r}")
+    return a
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+
+    res = measure(args, torch, dist, world, rank, local, dev)
+    sp, dec = res["sp"], res["dec"]
+    L = args.layers
+    wl = workload_config(args, world, sp["global_batch"])["workload"]
+    rl = roofline_of(args, res, peaks, world, wl)
+    is_i4 = args.dtype == "int4"
     line = {
-        "metric": "decode tokens/s @ LLaMA-7B shape, 64K ctx; selection+gather HBM GB/s vs roofline",
-        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64",
-        "kv_dtype": args.dtype,
-        "data": f"synthetic {args.data} KV generated on device (trace.py:270-315 model); no model weights",
-        "config": workload_config(args, world),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": per_kernel[dom]["gbs"], "peak": hbm_peak,
-                     "unit": "GB/s", "frac": (per_kernel[dom]["gbs"] or 0) / hbm_peak,
-                     "traffic": traffic, "traffic_algo_bytes_same_launch": traffic_algo,
-                     "traffic_source": "profiles/traffic.json (ncu --set full, layer-2 launch)" if traffic else None,
-                     "peak_source": frac_of,
-                     "algo_bytes_per_step": algo[dom], "kernel_ms_per_step": st_ms[dom],
-                     "kernel_share_of_staged_step": st_ms[dom] / staged_total if staged_total else None},
-        "selection_gather_gbs": sel_gather_bytes / (ms_max / 1e3) / 1e9,
-        "selection_gather_frac": sel_gather_bytes / (ms_max / 1e3) / 1e9 / hbm_peak,
-        "per_kernel": per_kernel,
-        "candidate_fraction": float(np.sum(n_cand) / (L * dec.lanes * dec.n)),
-        "kv_compression": None if quant_ms is None else {
+        "metric": METRIC, "value": res["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["ms_max"], "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32",
+        "dtype_detail": {"kv": args.dtype, "selection": "canonical f64 dot order: f32 estimates (INT4: exact int32 "
+                         "tensor-core partials) + f64 re-score of the boundary band", "attention": "f32 accumulate",
+                         "abstracts": "bf16 rounded outward"},
+        "data": f"synthetic {args.data} KV generated on device (workload.py / csrc/synth.cu, trace.py:270-315 model); "
+                "no model weights",
+        "config": workload_config(args, world, sp["global_batch"]),
+        **rl,
+        "kv_compression": None if res["quant_ms"] is None else {
             "codec": "INT4 group-32, fp16 (scale, min), 80 B/token/head vs 256 B bf16",
-            "prefill_quant_ms": quant_ms,
-            "prefill_quant_gbs": (2 * L * dec.lanes * args.ctx * (HEAD_DIM * 2 + 80)) / (quant_ms / 1e3) / 1e9},
-        "gpu_launches": launches_per_layer * L * args.steps,
-        "bound_grid": {"fine_C": sorted(set(dec.C)), "coarse_layers": [l for l in range(L) if bound_grid[l]],
+            "prefill_quant_ms": res["quant_ms"],
+            "prefill_quant_gbs": (2 * L * dec.kv_lanes * args.ctx * (HEAD_DIM * 2 + 80)) / (res["quant_ms"] / 1e3) / 1e9,
+            "note": "in situ: kv_quant over each layer's bf16 staging, CUDA events around the K and V launches"},
+        "gpu_launches": (6 if is_i4 else 5) * L * args.steps,
+        "bound_grid": {"fine_C": sorted(set(dec.C)), "coarse_layers": [l for l in range(L) if res["bound_grid"][l]],
                        "rule": "candidate fraction >= 0.9 in warm-up -> prune on C=64 abstracts"},
-        "self_check_max_rel_diff": chk,
-        "clocks": clocks,
-        "e2e": e2e,
+        "shard": {k: sp[k] for k in ("kv0", "kv_lanes", "q_lanes", "global_batch")},
+        "clocks": res["clocks"],
+        "e2e": res["e2e"],
     }
+    if "parity" in res:
+        par = res["parity"]
+        if world > 1:  # every rank checked its own lanes
+            t = torch.tensor([par["lanes_checked"], par["set_mismatches"], par["code_mismatches"]], device=dev,
+                             dtype=torch.int64)
+            dist.all_reduce(t)
+            e = torch.tensor([par["max_rel_err"]], device=dev, dtype=torch.float64)
+            dist.all_reduce(e, op=dist.ReduceOp.MAX)
+            par.update(lanes_checked=int(t[0]), set_mismatches=int(t[1]), code_mismatches=int(t[2]),
+                       max_rel_err=float(e), ranks=world)
+        line["parity"] = par
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(args, dec.lanes)
-        line["cpu_baseline"] = {"value": args.batch / cb["step_s"], "unit": "tokens/s", "cores": cb["threads"],
-                                "kind": "port", "sample": cb["sample"], "ms_per_step": cb["step_s"] * 1e3}
+        from oracle import oracle as O
+        threads = O.host_threads()
+        sample = cpu_sample(args, O, threads)
+        cb = cpu_run(args, O, sample, threads, sp["global_batch"] * N_HEADS)
+        line["cpu_baseline"] = {"value": sp["global_batch"] / cb["step_s"], "unit": "tokens/s", "cores": threads,
+                                "kind": "port", "sample": cpu_sample_text(args, sample, threads,
+                                                                          sp["global_batch"] * N_HEADS),
+                                "ms_per_step": cb["step_s"] * 1e3, "per_layer": cb["per_layer"]}
+        del sample
+    del res, dec
+    torch.cuda.empty_cache()
+    subs = []
+    for which in [s for s in args.sub.split(",") if s.strip()]:
+        a = sub_args(args, which.strip())
+        try:
+            r = measure(a, torch, dist, world, rank, local, dev, tag=which)
+        except Exception as exc:  # a sub-record must not sink the headline line
+            subs.append({"sub": which, "error": f"{type(exc).__name__}: {exc}"})
+            torch.cuda.empty_cache()
+            continue
+        sw = workload_config(a, world, r["sp"]["global_batch"])["workload"]
+        rr = roofline_of(a, r, peaks, world, sw)
+        subs.append({"sub": which, "workload": sw, "value": r["value"], "ms_per_step": r["ms_max"],
+                     "e2e": r["e2e"], "steps": a.steps, "kernel": rr["roofline"]["kernel"],
+                     "frac": rr["roofline"]["frac"], "candidate_fraction": rr["candidate_fraction"],
+                     "per_kernel_ms": {k: v["ms_per_step"] for k, v in rr["per_kernel"].items()},
+                     "parity": r.get("parity"), "clocks": r["clocks"]})
+        del r
+        torch.cuda.empty_cache()
+    if subs:
+        line["sub_records"] = subs
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
@@ -570,10 +770,18 @@ def run_ours(args):
     return 0
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if not args.dry_run:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show the rank count
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        return relaunch(argv, args.gpus)
+    if args.dry_run:
+        return run_dry(args)
     return run_ours(args)
 
 

@@ -300,6 +300,17 @@ KVT_API int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes
  * kvt_select_attend uses its own kv_group field. */
 KVT_API int kvt_set_kv_group(int kv_group);
 
+/* ---- synthetic workload (bench / test input generator; not on the decode path) ----------
+ * The planted-desert model of trace.py:270-315 (generate_synthetic) as a counter hash, so
+ * any lane can be regenerated bit-identically on the host (oracle ora_synth_lane): fills
+ * bf16 keys and/or values [n_lanes] x lane_stride elements, tokens [0, n).  u: [n_lanes, d]
+ * f32 unit directions; regions: [n_lanes, n_regions, 2] hot token ranges; planted = 0 gives
+ * N(0,1)-like keys.  Recipe in paper_2506_20187_b200/csrc/synth.cu. */
+KVT_API int kvt_synth_layer(void* keys, void* values, int64_t n_lanes, int64_t lane_stride, int64_t n, int d,
+                            const uint32_t* lane_seed, const float* u, const int32_t* regions, int n_regions,
+                            float desert_base, float desert_span, float hot_base, float hot_span,
+                            float noise_scale, int planted, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

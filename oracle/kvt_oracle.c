@@ -17,6 +17,8 @@
  *                             chunk_tree.py:344-379 merge_desert
  *   ora_runs                  engine.py:176-183     _token_runs
  *   ora_attention             engine.py:145-154     attention_output (+ importance.py:36-43 softmax)
+ *   ora_synth_lane            trace.py:270-315      generate_synthetic's planted model, as the
+ *                             counter-hash generator of csrc/synth.cu (bench/test inputs)
  *
  * Canonical arithmetic (shared *definition* with the CUDA kernels, written independently):
  *   A dot product over d dims is accumulated in 32 partial sums.  Dim j goes to partial
@@ -32,7 +34,8 @@
  * Bounds are made *sound with respect to the canonical scores* by widening the computed
  * upper/lower sums by 2*gamma_n*A, A = sum_j |q_j| max(|max_j|, |min_j|), n = chain length
  * + tree depth (see ora_bound_slack).  Single-row abstracts are exact (no widening), as in
- * the reference (importance.py:114 "Exact ... on singletons").
+ * the reference (importance.py:114 "Exact ... on singletons"), and so are abstracts whose
+ * unwidened U == L (all rows equal; see ora_bounds2).
  *
  * Compile: see oracle/Makefile (-O2 -ffp-contract=off; fma() is the explicit fused op).
  */
@@ -117,7 +120,10 @@ ORA_API void ora_bounds2(const double* q, const double* mx, const double* mn, in
             pa[l] = fma(fabs(qj), fmax(fabs(M[j]), fabs(N[j])), pa[l]);
         }
         double u = tree32(pu), lo = tree32(pl), a = tree32(pa);
-        if (rows == NULL || rows[c] > 1) {
+        /* U == L before widening: RN fma/add are monotone, so the unwidened chains enclose
+         * every canonical dot of the chunk, and equal ends pin them all -- exact, no widening
+         * (a chunk of identical rows; the walkthrough's flat chunks, test_chunk_tree.py:214) */
+        if ((rows == NULL || rows[c] > 1) && u != lo) {
             double slack = a * fac;
             u = u + slack;
             lo = lo - slack;
@@ -273,6 +279,63 @@ ORA_API void ora_i4_dequant(const uint8_t* rec, int64_t n, int d, float* x) {
                 int c = (r[dim >> 1] >> ((dim & 1) * 4)) & 15;
                 x[t * d + dim] = fmaf((float)c, sc, mn);
             }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Synthetic lanes (bench / test inputs).  Host restatement of the counter-hash generator
+ * defined in paper_2506_20187_b200/csrc/synth.cu (the planted-desert model of
+ * trace.py:270-315 generate_synthetic): same hash, same sequence of round-to-nearest f32
+ * operations (this file builds with -ffp-contract=off), bf16 round-to-nearest-even.  K and
+ * V receive the bf16 values widened to f32, [n, d] each (either may be NULL). */
+
+static uint32_t syn_mix(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+static uint32_t syn_hash(uint32_t s, uint32_t x) { return syn_mix(syn_mix(x) ^ s); }
+static float syn_normal(uint32_t s, uint32_t x) {
+    uint32_t h0 = syn_hash(s, 2u * x), h1 = syn_hash(s, 2u * x + 1u);
+    uint32_t isum = (h0 & 0xffffu) + (h0 >> 16) + (h1 & 0xffffu) + (h1 >> 16);
+    volatile float z = (float)isum * 0x1p-16f;
+    z = z - 2.0f;
+    return z * 1.7320508075688772f;
+}
+static float bf16_rne(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;  /* finite inputs only */
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+ORA_API void ora_synth_lane(float* K, float* V, int64_t n, int d, uint32_t lane_seed, const float* u,
+                            const int32_t* regions, int R, float desert_base, float desert_span,
+                            float hot_base, float hot_span, float noise_scale, int planted) {
+    uint32_t s_k = syn_mix(lane_seed ^ 0x9e3779b9u), s_v = syn_mix(lane_seed ^ 0x85ebca6bu);
+    uint32_t s_a = syn_mix(lane_seed ^ 0xc2b2ae35u);
+    for (int64_t t = 0; t < n; ++t) {
+        float a = 0.0f;
+        if (planted) {
+            int hot = 0;
+            for (int r = 0; r < R; ++r) hot |= (t >= regions[2 * r] && t < regions[2 * r + 1]);
+            float r24 = (float)(syn_hash(s_a, (uint32_t)t) >> 8) * 0x1p-24f;
+            volatile float prod = r24 * (hot ? hot_span : desert_span);
+            a = prod + (hot ? hot_base : desert_base);
+        }
+        for (int j = 0; j < d; ++j) {
+            uint32_t x = (uint32_t)(t * d + j);
+            if (K) {
+                float k = syn_normal(s_k, x);
+                if (planted) {
+                    volatile float au = a * u[j];
+                    volatile float nz = k * noise_scale;
+                    k = au + nz;
+                }
+                K[t * d + j] = bf16_rne(k);
+            }
+            if (V) V[t * d + j] = bf16_rne(syn_normal(s_v, x));
         }
     }
 }
@@ -593,6 +656,7 @@ typedef struct {
     double* out;          /* [steps][lanes][d] attention outputs (may be NULL) */
     int64_t* evals;       /* [steps][lanes] */
     double timed_s;       /* per-thread time inside select+attention */
+    double* lane_step_s;  /* [steps][lanes] time of each lane-step (NULL: not recorded) */
 } bench_arg_t;
 
 static double now_s(void) {
@@ -624,7 +688,9 @@ static void* bench_worker(void* p) {
             qsort(tok, (size_t)a->k, sizeof(int64_t), cmp_i64);   /* engine.py:353 sorted */
             ora_attention(q64, k64, v64, tok, a->k, d, o);        /* engine.py:354 */
             if (a->merge) ora_part_merge(P);
-            a->timed_s += now_s() - t0;
+            double dt = now_s() - t0;
+            a->timed_s += dt;
+            if (a->lane_step_s) a->lane_step_s[(int64_t)s * a->lanes + lane] = dt;
             if (a->evals) a->evals[(int64_t)s * a->lanes + lane] = ev;
             if (a->out) memcpy(a->out + ((int64_t)s * a->lanes + lane) * d, o, sizeof(double) * (size_t)d);
         }
@@ -641,7 +707,7 @@ static void* bench_worker(void* p) {
 ORA_API double ora_bench_lanes(int64_t lanes, int64_t n, int d, int64_t m, int64_t k, int steps,
                                int merge, const float* keys, const float* vals, const float* q,
                                int nthreads, double* out, int64_t* evals, double* max_thread_s,
-                               double* sum_thread_s) {
+                               double* sum_thread_s, double* lane_step_s) {
     if (nthreads < 1) nthreads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
     bench_arg_t* args = (bench_arg_t*)calloc((size_t)nthreads, sizeof(bench_arg_t));
@@ -650,7 +716,7 @@ ORA_API double ora_bench_lanes(int64_t lanes, int64_t n, int d, int64_t m, int64
         bench_arg_t* a = &args[t];
         a->n = n; a->d = d; a->m = m; a->k = k; a->steps = steps; a->merge = merge;
         a->keys = keys; a->vals = vals; a->q = q; a->lanes = lanes;
-        a->tid = t; a->nthreads = nthreads; a->out = out; a->evals = evals;
+        a->tid = t; a->nthreads = nthreads; a->out = out; a->evals = evals; a->lane_step_s = lane_step_s;
         pthread_create(&th[t], NULL, bench_worker, a);
     }
     double mx = 0.0, sum = 0.0;

@@ -63,6 +63,9 @@ def lib():
         L.ora_i4_record_bytes.argtypes = [ctypes.c_int]
         L.ora_i4_quant.argtypes = [_fp, _i64, ctypes.c_int, ctypes.c_void_p]
         L.ora_i4_dequant.argtypes = [ctypes.c_void_p, _i64, ctypes.c_int, _fp]
+        L.ora_synth_lane.argtypes = [_fp, _fp, _i64, ctypes.c_int, ctypes.c_uint32, _fp, _i32p, ctypes.c_int,
+                                     ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                     ctypes.c_int]
         L.ora_topk.restype = _i64
         L.ora_topk.argtypes = [_dp, _i64, _i64, _ip]
         L.ora_runs.restype = _i64
@@ -82,7 +85,7 @@ def lib():
         L.ora_bench_lanes.restype = ctypes.c_double
         L.ora_bench_lanes.argtypes = [_i64, _i64, ctypes.c_int, _i64, _i64, ctypes.c_int,
                                       ctypes.c_int, _fp, _fp, _fp, ctypes.c_int, _dp, _ip,
-                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _dp]
         _lib = L
     return _lib
 
@@ -184,6 +187,21 @@ def i4_dequant(rec, d: int) -> np.ndarray:
     x = np.empty((n, d), dtype=np.float32)
     lib().ora_i4_dequant(R.ctypes.data_as(ctypes.c_void_p), n, d, _p(x, _fp))
     return x
+
+
+def synth_lane(n: int, d: int, seed: int, u, regions, g: dict, keys: bool = True, values: bool = True):
+    """Host regeneration of one synthetic lane (csrc/synth.cu recipe) -> (K, V) f32 [n, d]
+    holding the bf16 values the GPU generator writes (None where not requested).
+    g: workload.gen_args(...)."""
+    K = np.empty((n, d), np.float32) if keys else None
+    V = np.empty((n, d), np.float32) if values else None
+    uu = np.ascontiguousarray(np.asarray(u, dtype=np.float32).reshape(d))
+    rr = np.ascontiguousarray(np.asarray(regions, dtype=np.int32).reshape(-1, 2))
+    lib().ora_synth_lane(None if K is None else _p(K, _fp), None if V is None else _p(V, _fp), n, d,
+                         int(seed) & 0xFFFFFFFF, _p(uu, _fp), rr.ctypes.data_as(_i32p), rr.shape[0],
+                         g["desert_base"], g["desert_span"], g["hot_base"], g["hot_span"], g["noise_scale"],
+                         g["planted"])
+    return K, V
 
 
 def topk(score_vec, k: int) -> np.ndarray:
@@ -293,12 +311,17 @@ def bench_lanes(keys: np.ndarray, values: np.ndarray, queries: np.ndarray, k: in
     out = np.zeros((steps, lanes, d)) if want_out else None
     mx = ctypes.c_double(0.0)
     sm = ctypes.c_double(0.0)
+    ls = np.zeros((steps, lanes))
     wall = lib().ora_bench_lanes(lanes, n, d, m, k, steps, int(merge), _p(K, _fp), _p(V, _fp),
                                  _p(Q, _fp), nthreads, None if out is None else _p(out),
-                                 _p(evals, _ip), ctypes.byref(mx), ctypes.byref(sm))
+                                 _p(evals, _ip), ctypes.byref(mx), ctypes.byref(sm), _p(ls))
+    # step-synchronous wall estimate: lanes run round-robin on threads, so a step's critical
+    # path is the busiest thread's sum of its lane-step times
+    t = min(nthreads, lanes) if lanes else 1
+    step_wall = np.array([max(ls[s, i::t].sum() for i in range(t)) for s in range(steps)]) if lanes else np.zeros(steps)
     return {"wall_s": wall, "max_thread_s": mx.value, "sum_thread_s": sm.value,
-            "lane_step_s": sm.value / max(1, lanes * steps), "evals": evals, "out": out,
-            "lanes": lanes, "steps": steps, "threads": nthreads}
+            "lane_step_s": sm.value / max(1, lanes * steps), "lane_step_times": ls, "step_wall_s": step_wall,
+            "evals": evals, "out": out, "lanes": lanes, "steps": steps, "threads": nthreads}
 
 
 def host_threads() -> int:

@@ -102,6 +102,9 @@ kvt_i4_recip_check = _sig("kvt_i4_recip_check", ctypes.c_int, _vp, _vp)
 kvt_kv_dequant = _sig("kvt_kv_dequant", ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _i32, _i64, _vp)
 kvt_layer_workspace_bytes = _sig("kvt_layer_workspace_bytes", _sz, _i64, _i64, _i64, _i32)
 kvt_select_attend = _sig("kvt_select_attend", ctypes.c_int, ctypes.POINTER(KvtLayerArgs), _vp, _sz, _vp)
+_f32 = ctypes.c_float
+kvt_synth_layer = _sig("kvt_synth_layer", ctypes.c_int, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _f32,
+                       _f32, _f32, _f32, _f32, _i32, _vp)
 
 EXPORTED = [
     "kvt_version", "kvt_status_string", "kvt_last_error", "kvt_abstract_build", "kvt_abstract_spans",
@@ -110,6 +113,7 @@ EXPORTED = [
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
     "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_i4_recip_check", "kvt_select_plan2", "kvt_cand_score_f32",
     "kvt_topk_select_band", "kvt_kv_dequant", "kvt_chunk_bounds_fast", "kvt_attn_lse", "kvt_lse_merge", "kvt_set_kv_group", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
+    "kvt_synth_layer",
 ]
 
 

@@ -8,7 +8,8 @@ they can hold a selected token, `RuntimeError` for a cold chunk without a store 
 evaluates it the GPU way instead of a serial heap:
 
   level A  K3 bounds of every live leaf; plan: tau = k-th largest lower bound (row
-           weighted); leaves with U < tau are pruned;
+           weighted); leaves with U < tau are pruned, and so are leaves that >= k tokens
+           rank before under the tie-break (L_i == U_j, i before j; _dominance_prune);
   level B  surviving leaves wider than the base grid are re-bounded per base chunk
            (abstracts built once at build_partition) and pruned again;
   cold     candidate regions inside abstract-only leaves are fetched via ChunkSource;
@@ -18,8 +19,9 @@ evaluates it the GPU way instead of a serial heap:
 After selection the partition is the canonical one the reference reaches after
 select_top_k + merge_desert: maximal runs of selected tokens (IMPORTANT) and their
 complement (DESERT, exact merged abstracts), plus the original PAD tail.  `important_tokens`
-is returned in ascending order (the reference returns confirmation order; its tests
-compare sets).  eval_count = bounds evaluated + tokens exactly scored.
+is returned in rank order (score desc, index asc) -- the order the reference's heap confirms
+singletons in; a chunk it confirms whole is appended in index order there, so the two orders
+can differ inside such a chunk (its tests compare sets).  eval_count = bounds evaluated + tokens exactly scored.
 """
 
 from __future__ import annotations
@@ -236,12 +238,41 @@ class SelectionResult:
         return set(self.important_tokens)
 
 
+def _dominance_prune(U: torch.Tensor, L: torch.Tensor, starts: np.ndarray, n: int, k: int) -> torch.Tensor:
+    """Tie-aware pruning under the reference's order (score desc, index asc; chunk_tree.py:233-338).
+
+    The tokens of leaf i rank strictly before every token of leaf j when L_i > U_j, or when
+    L_i == U_j and leaf i lies before leaf j (equal scores go to the lower index).  Leaf j can
+    hold no selected token once such leaves cover >= k tokens.  This is the rule the heap
+    applies implicitly -- it never pops j before the budget fills -- and it subsumes the plan's
+    tau rule (U_j < k-th largest L).  It matters where bounds tie exactly: chunks of identical
+    rows have U == L (exact, no widening), e.g. the flat chunks of the walkthrough
+    (test_chunk_tree.py:214-228).  Returns U with -inf at the pruned leaves; on device."""
+    m = len(starts)
+    if k <= 0 or m < 2:
+        return U
+    dev = U.device
+    u, lo = U[0, :m], L[0, :m]
+    st = torch.from_numpy(np.asarray(starts, dtype=np.int64)).to(dev)
+    size = torch.diff(st, append=torch.tensor([n], dtype=torch.int64, device=dev)).to(torch.float64)
+    cnt = torch.empty(m, dtype=torch.float64, device=dev)
+    blk = max(1, (1 << 24) // m)
+    for j0 in range(0, m, blk):
+        j1 = min(m, j0 + blk)
+        uj, sj = u[j0:j1, None], st[j0:j1, None]
+        before = (lo[None, :] > uj) | ((lo[None, :] == uj) & (st[None, :] < sj))
+        cnt[j0:j1] = (before.to(torch.float64) * size[None, :]).sum(dim=1)
+    out = U.clone()
+    out[0, :m] = torch.where(cnt >= k, torch.full_like(u, -math.inf), u)
+    return out
+
+
 def _bounds_plan(q, amax, amin, starts: np.ndarray, n: int, k: int):
     dev = q.device
     ls = torch.from_numpy(np.ascontiguousarray(starts, dtype=np.int32))[None].to(dev)
     nl = torch.tensor([len(starts)], dtype=torch.int32, device=dev)
     U, L = ops.chunk_bounds(q[None], amax[None], amin[None], n, 0, ls, nl)
-    plan = ops.select_plan(U, L, n, k, 0, ls, nl, want_cand_leaf=True)
+    plan = ops.select_plan(_dominance_prune(U, L, starts, n, k), L, n, k, 0, ls, nl, want_cand_leaf=True)
     return U, L, plan
 
 
@@ -338,8 +369,10 @@ def select_top_k(partition: Partition, query: np.ndarray, k: int, store: ChunkSo
     n_cand = int(plan["n_cand"][0].item())
     result.eval_count += n_cand
     sel_tok, sel_score, n_sel = ops.topk_select(cs, ct, plan["n_cand"], k)
-    sel = sel_tok[0].cpu().numpy().astype(np.int64)
-    result.important_tokens = [int(t) for t in sel]
+    sel = sel_tok[0, :k].cpu().numpy().astype(np.int64)
+    sc = sel_score[0, :k].cpu().numpy()
+    # rank order (score desc, index asc): the order the reference's heap confirms singletons in
+    result.important_tokens = [int(t) for t in sel[np.lexsort((sel, -sc))]]
 
     # ---- canonical partition: selected runs + complement runs (K6) ----
     _rebuild(partition, sel_tok, sel_score, n_sel, k)

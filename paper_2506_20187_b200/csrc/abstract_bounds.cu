@@ -8,7 +8,9 @@
 // K3 replaces importance.py:108-137 bound_chunk / bound_chunks_batch: per dimension the
 // query sign picks the max or min key, U = sum q*hi, L = sum q*lo, in the canonical f64
 // order, widened by 2*gamma*A (A = sum |q| max(|hi|,|lo|)) so U >= every canonical token
-// score in the chunk >= L.  Exact for single-row chunks.  One warp per chunk, reads the
+// score in the chunk >= L.  Exact for single-row chunks and for chunks whose unwidened U == L
+// (round-to-nearest fma/add are monotone, so the unwidened chains already enclose every
+// canonical dot; U == L pins them all to that value).  One warp per chunk, reads the
 // 2*d abstract floats once.  HBM-bound on abstract bytes (m*2*d*4 per lane).
 #include "common.cuh"
 
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(256, 3) bounds_kernel(
             int64_t rows;
             if (ls) rows = ((c + 1 < nl) ? (int64_t)ls[c + 1] : n) - ls[c];
             else rows = kvt::imin((int64_t)C, n - c * C);
-            if (rows > 1) {
+            if (rows > 1 && u_ != l_) {  // u_ == l_: every canonical dot equals u_ (exact)
                 const double slack = a_ * fac;
                 u_ = u_ + slack;
                 l_ = l_ - slack;
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2) bounds_tma_kernel(
             const int64_t c = c0 + base + t;
             if ((lane & 3) == 0 && base + t < cnt) {
                 const int64_t rows = kvt::imin((int64_t)C, n - c * C);
-                if (rows > 1) {
+                if (rows > 1 && u_ != l_) {  // degenerate chunk (max == min): exact
                     const double slack = a_ * fac;
                     u_ = u_ + slack;
                     l_ = l_ - slack;
@@ -448,8 +450,6 @@ extern "C" int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_
     }
 }
 
-static int g_bt_sms = 0;
-
 template <typename QT, typename AT, int G>
 static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int C, const int32_t* ls,
                           const int32_t* nl, int64_t lstr, const void* amax, const void* amin, int64_t als,
@@ -461,18 +461,12 @@ static void launch_bounds(const void* q, int64_t n_lanes, int d, int64_t n, int 
         const int tile = (int)(2 * 64 * row);
         const int stages = (int)kvt::imax(2, kvt::imin(4, (100 * 1024) / tile));
         const size_t smem = (size_t)stages * tile + 16 * (size_t)stages + 16;
-        static bool configured = false;
+        KVT_PER_DEVICE(bool, configured);
         if (!configured) {
             cudaFuncSetAttribute(bounds_tma_kernel<QT, AT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             configured = true;
         }
-        if (!g_bt_sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&g_bt_sms, cudaDevAttrMultiProcessorCount, dev);
-            if (g_bt_sms <= 0) g_bt_sms = 148;
-        }
-        bounds_tma_kernel<QT, AT, G><<<g_bt_sms * (smem <= 110 * 1024 ? 2 : 1), BT_THREADS, smem, st>>>(
+        bounds_tma_kernel<QT, AT, G><<<kvt::sm_count() * (smem <= 110 * 1024 ? 2 : 1), BT_THREADS, smem, st>>>(
             (const QT*)q, d, n, C, (int)n_lanes, (const AT*)amax, (const AT*)amin, als, U, L, A, bs, scaled, stages);
         return;
     }

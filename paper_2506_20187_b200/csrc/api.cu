@@ -102,20 +102,14 @@ struct SideStream {
         if (!ok) cudaGetLastError();
     }
 };
-SideStream& side_stream() {
-    static thread_local SideStream ss;
-    return ss;
+SideStream& side_stream() {  // one per thread and device (streams belong to a device)
+    static thread_local SideStream* ss[kvt::kMaxDevices] = {};
+    const int dev = kvt::current_device();
+    if (!ss[dev]) ss[dev] = new SideStream();  // lives as long as the thread's CUDA context use
+    return *ss[dev];
 }
 
-int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    }
-    return sms;
-}
+int num_sms() { return kvt::sm_count(); }
 
 }  // namespace
 

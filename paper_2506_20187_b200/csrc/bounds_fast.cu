@@ -210,14 +210,9 @@ extern "C" int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int
     const int tile = 2 * 64 * d * 2;
     const int stages = (int)kvt::imax(2, kvt::imin(4, (100 * 1024) / tile));
     const size_t smem = (size_t)stages * tile + 16 * (size_t)stages + 16;
-    static int per_sm[3] = {0, 0, 0};
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    static int per_sm_slots[kvt::kMaxDevices][3] = {};
+    int (&per_sm)[3] = per_sm_slots[kvt::current_device()];
+    const int sms = kvt::sm_count();
     const int G = d / 128;
 #define KVT_BF(GG)                                                                                                    \
     do {                                                                                                              \

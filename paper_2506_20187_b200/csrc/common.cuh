@@ -19,6 +19,30 @@
 
 namespace kvt {
 
+// Per-device host state.  Function attributes (the dynamic shared-memory opt-in), SM counts
+// and occupancy are per device, and one process may drive several GPUs, so every one-time
+// launch setup lives in a slot of the current device (cudaGetDevice).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    return dev;
+}
+inline int sm_count() {
+    static int sms[kMaxDevices] = {0};
+    const int dev = current_device();
+    if (sms[dev] <= 0) {
+        if (cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms[dev] <= 0)
+            sms[dev] = 148;
+    }
+    return sms[dev];
+}
+// `static T name = 0;` made per device: KVT_PER_DEVICE(bool, configured) binds `configured`
+// to the current device's slot.
+#define KVT_PER_DEVICE(T, name) \
+    static T name##_slots_[::kvt::kMaxDevices] = {}; \
+    T& name = name##_slots_[::kvt::current_device()]
+
 template <typename A, typename B>
 __host__ __device__ __forceinline__ int64_t imin(A a, B b) { return (int64_t)a < (int64_t)b ? (int64_t)a : (int64_t)b; }
 template <typename A, typename B>

@@ -226,7 +226,7 @@ extern "C" int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t
     if (n > (1LL << 22)) return KVT_ERR_SHAPE;  // packed (items, tokens) scan: <= 4M tokens per lane
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
-    static bool configured = false;
+    KVT_PER_DEVICE(bool, configured);
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);

@@ -834,7 +834,7 @@ static int launch_ring(const void* values, int64_t n_lanes, int64_t lane_stride_
                        cudaStream_t st) {
     constexpr int SLOT = (32 / F::LPR) * F::row_bytes();
     const size_t smem = (size_t)ATTN_WARPS * S * SLOT + (size_t)R * 8;
-    static size_t configured = 0;
+    KVT_PER_DEVICE(size_t, configured);
     if (smem > configured) {  // opt in for any size: static smem counts against the 48 KB default too
         cudaError_t e = cudaFuncSetAttribute(attn_ring_kernel<F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);

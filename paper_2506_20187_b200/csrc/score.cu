@@ -325,16 +325,7 @@ using namespace kvt;
 
 static inline int sgroups_for(int d) { return d <= 128 ? 1 : d <= 256 ? 2 : d <= 512 ? 4 : d <= 1024 ? 8 : 0; }
 
-static int g_sms = 0;
-static int sm_count() {
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_sms <= 0)
-            g_sms = 148;
-    }
-    return g_sms;
-}
+using kvt::sm_count;
 
 // TMA path eligibility: whole-row bulk copies need 16 B aligned rows and lane bases.
 // lane_stride is in elements (bytes for I4).
@@ -356,14 +347,14 @@ static int launch_score_tma(const void* q, const void* keys, int64_t n_lanes, in
     int stages = (int)kvt::imin(std::is_same<T, I4>::value ? 6 : 3, (150 * 1024) / tile);
     if (stages < 2) stages = 2;
     const size_t smem = (size_t)stages * tile + 32 * (size_t)stages + 4 * (size_t)(n_lanes + 1) + 16;
-    static size_t configured = 0;
+    KVT_PER_DEVICE(size_t, configured);
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(score_tma_kernel<QT, T, G, IMPL, AccT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = 200 * 1024;
     }
-    static int per_sm = 0;  // one per template instance
+    KVT_PER_DEVICE(int, per_sm);  // one per template instance and device
     if (!per_sm) per_sm = resident_per_sm(score_tma_kernel<QT, T, G, IMPL, AccT>, TS_THREADS, smem,
                                           smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1));
     const int grid = sm_count() * per_sm;

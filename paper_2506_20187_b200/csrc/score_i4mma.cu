@@ -373,16 +373,14 @@ static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const i
     constexpr int d = 128 * R, G = 4 * R, row_b = d / 2 + G * 4, tile_b = QM_ROWS * row_b, qb = G * 144 + 16;
     constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
     const size_t smem = (size_t)QM_STAGES * stage_b;
-    static bool configured = false;
+    KVT_PER_DEVICE(bool, configured);
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(score_i4mma_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = true;
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static int per_sm = 0;
+    const int sms = kvt::sm_count();
+    KVT_PER_DEVICE(int, per_sm);
     if (!per_sm) per_sm = resident_per_sm(score_i4mma_kernel<R>, QM_THREADS, smem, 4);
     launch_pdl(score_i4mma_kernel<R>, dim3(sms * per_sm), dim3(QM_THREADS), smem, st, (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
         ostr, err, kv_group_current());

@@ -237,7 +237,6 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_select_kernel(
 
 using namespace kvt;
 
-static int g_sel_smem_cap_set = 0;
 constexpr int SEL_SLICE_CAP = 20480;  // 160 KB of staged keys per CTA
 
 extern "C" int kvt_topk_select_runs(const double* cand_score, const int32_t* cand_tok, const int32_t* n_cand,
@@ -253,6 +252,7 @@ extern "C" int kvt_topk_select_runs(const double* cand_score, const int32_t* can
     const int64_t slice = (cand_stride + CL - 1) / CL;
     const int cap = (int)kvt::imin(slice, SEL_SLICE_CAP);
     const size_t smem = (size_t)cap * sizeof(uint64_t);
+    KVT_PER_DEVICE(int, g_sel_smem_cap_set);
     if (!g_sel_smem_cap_set) {
         cudaError_t e = cudaFuncSetAttribute(topk_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              SEL_SLICE_CAP * (int)sizeof(uint64_t));

@@ -431,7 +431,7 @@ static int launch_select2(const float* cs32, const int32_t* ctok, const int32_t*
     const int64_t slice = (cand_stride + CL - 1) / CL;
     if (slice > S2_SLICE_CAP) return KVT_ERR_SHAPE;
     const size_t smem = (size_t)slice * sizeof(uint64_t);
-    static bool configured = false;
+    KVT_PER_DEVICE(bool, configured);
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(topk_select2_kernel<QT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              S2_SLICE_CAP * (int)sizeof(uint64_t));

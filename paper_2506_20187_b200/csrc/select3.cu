@@ -751,7 +751,7 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
     const int row_b = RowLd<T>::row_bytes(d);
     const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
     const size_t smem = (size_t)S3_LIST_CAP * 8;  // list keys + positions
-    static bool configured = false;
+    KVT_PER_DEVICE(bool, configured);
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(topk_select3_kernel<QT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -776,9 +776,7 @@ extern "C" int kvt_topk_select_band(const float* cs32, const int32_t* ctok, cons
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
     // very few lanes: one CTA per lane would leave most SMs idle -> cluster of CTAs per lane
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = kvt::sm_count();
     if (n_lanes * 4 < sms && cand_stride >= 8192 && cand_stride <= 8 * 20480 && n_lanes <= 65535)
         return kvt_topk_select_band_cluster(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, q_dtype, keys,
                                             key_dtype, lane_stride, d, sel_tok, sel_score, sel_stride, n_sel,

@@ -34,8 +34,8 @@ def attention_output(query: np.ndarray, keys: np.ndarray, values: np.ndarray) ->
     if K.ndim != 2 or q.ndim != 1 or K.shape[1] != q.shape[0]:
         raise ValueError(f"shape mismatch: keys {K.shape} vs query {q.shape}")
     n, d = K.shape
-    if n == 0:
-        return np.full(d, np.nan)
+    if n == 0:  # softmax([]) @ V[0, d] is zeros(d) in the reference (engine.py:149-154)
+        return np.zeros(d)
     qd = to_device(q, torch.float64)[None]
     kd = to_device(K)[None]
     vd = to_device(V, torch.float64)[None]  # f64 accumulation, as the reference (engine.py:150)

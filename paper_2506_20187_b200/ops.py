@@ -7,6 +7,7 @@ contiguous rows (lane stride = tensor.stride(0)), queries are [n_lanes, d].
 
 from __future__ import annotations
 
+import functools
 import math
 
 import torch
@@ -94,6 +95,24 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def _on_device(fn):
+    """Device guard: run the wrapper with its first CUDA operand's device current, so the ABI
+    launches on that device and on torch's current stream *of that device* (the library
+    launches on cudaGetDevice's device)."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        dev = None
+        for a in list(args) + list(kw.values()):
+            if isinstance(a, (torch.Tensor, I4KV)) and a.is_cuda:
+                dev = a.device
+                break
+        if dev is None or dev.index is None or dev.index == torch.cuda.current_device():
+            return fn(*args, **kw)
+        with torch.cuda.device(dev):
+            return fn(*args, **kw)
+    return wrapper
+
+
 def _p(t: torch.Tensor | None):
     return None if t is None else t.data_ptr()
 
@@ -129,6 +148,7 @@ def n_grid_leaves(n: int, C: int) -> int:
 # -- K8 ----------------------------------------------------------------------------------------
 
 
+@_on_device
 def kv_quant(src: torch.Tensor, dst: I4KV, t_begin: int = 0, t_end: int | None = None) -> I4KV:
     """INT4-compress rows [t_begin, t_end) of every lane of src [n_lanes, N, d] into dst (K8)."""
     require_cuda(src)
@@ -144,6 +164,7 @@ def kv_quant(src: torch.Tensor, dst: I4KV, t_begin: int = 0, t_end: int | None =
 # -- K1 ----------------------------------------------------------------------------------------
 
 
+@_on_device
 def abstract_build(keys, n: int, C: int, amax: torch.Tensor | None = None,
                    amin: torch.Tensor | None = None, c_begin: int = 0, c_end: int | None = None,
                    abs_dtype: torch.dtype | None = None):
@@ -168,6 +189,7 @@ def abstract_build(keys, n: int, C: int, amax: torch.Tensor | None = None,
     return amax, amin
 
 
+@_on_device
 def abstract_spans(keys: torch.Tensor, lane_of: torch.Tensor, starts: torch.Tensor, ends: torch.Tensor):
     """Exact abstracts of arbitrary spans -> (amax, amin) [S, d]."""
     require_cuda(keys)
@@ -189,6 +211,7 @@ def abstract_spans(keys: torch.Tensor, lane_of: torch.Tensor, starts: torch.Tens
 # -- K3 ----------------------------------------------------------------------------------------
 
 
+@_on_device
 def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int, C: int = 0,
                  leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
                  scaled: bool = False, want_A: bool = False):
@@ -214,6 +237,7 @@ def chunk_bounds(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int
 # -- K4 ----------------------------------------------------------------------------------------
 
 
+@_on_device
 def token_scores(q: torch.Tensor, keys: torch.Tensor, n: int | None = None) -> torch.Tensor:
     """Canonical f64 logits of all tokens (importance.py:27-33) -> [n_lanes, n]."""
     require_cuda(q, keys)
@@ -228,6 +252,7 @@ def token_scores(q: torch.Tensor, keys: torch.Tensor, n: int | None = None) -> t
     return out[:, :n]
 
 
+@_on_device
 def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
                 leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
                 want_cand_leaf: bool = False, A: torch.Tensor | None = None, d: int = 0):
@@ -251,6 +276,7 @@ def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
             "item_cap": item_cap, "err": err}
 
 
+@_on_device
 def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_per_lane: int = 0):
     """Raw canonical dots of candidate tokens -> (cand_score f64 [n_lanes, n], cand_tok i32)."""
     require_cuda(q, keys)
@@ -266,6 +292,7 @@ def cand_score(q: torch.Tensor, keys: torch.Tensor, plan: dict, n: int, blocks_p
     return cs, ct
 
 
+@_on_device
 def cand_score_f32(q: torch.Tensor, keys, plan: dict, n: int):
     """Fast f32 estimates of the candidate dots (|err| <= plan["err"]) -> (cs32 f32, cand_tok i32)."""
     require_cuda(q, keys)
@@ -279,6 +306,7 @@ def cand_score_f32(q: torch.Tensor, keys, plan: dict, n: int):
     return cs, ct
 
 
+@_on_device
 def cand_score_i4mma(q: torch.Tensor, keys: "I4KV", plan: dict, n: int):
     """INT4 keys: estimates with exact int32 inner products on the tensor cores.  Also max-es
     the per-lane bound on |estimate - canonical dot| into plan["err"][:, 3] (used as E by
@@ -295,6 +323,7 @@ def cand_score_i4mma(q: torch.Tensor, keys: "I4KV", plan: dict, n: int):
     return cs, ct
 
 
+@_on_device
 def topk_select_band(cs32: torch.Tensor, ct: torch.Tensor, plan: dict, k: int, q: torch.Tensor, keys,
                      want_runs: bool = True):
     """Exact canonical top-k from f32 estimates (band re-scoring) -> (sel_tok, sel_score, n_sel[, runs])."""
@@ -323,6 +352,7 @@ def topk_select_band(cs32: torch.Tensor, ct: torch.Tensor, plan: dict, k: int, q
     return st[:, :k], ss[:, :k], ns
 
 
+@_on_device
 def topk_select(cs: torch.Tensor, ct: torch.Tensor, n_cand: torch.Tensor, k: int, want_runs: bool = False):
     """Exact top-k (score desc, token asc) -> (sel_tok i32 [n_lanes,k] ascending, sel_score f64, n_sel)
     [+ dict(run_start, run_len, n_runs) from the fused run scan]."""
@@ -345,6 +375,7 @@ def topk_select(cs: torch.Tensor, ct: torch.Tensor, n_cand: torch.Tensor, k: int
     return st[:, :k], ss[:, :k], ns
 
 
+@_on_device
 def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition: bool = True):
     """Selected runs (+ canonical partition) -> dict."""
     nl = sel_tok.shape[0]
@@ -366,6 +397,7 @@ def runs_scan(sel_tok: torch.Tensor, n_sel: torch.Tensor, n: int, want_partition
     return {"run_start": rs, "run_len": rl, "n_runs": nr, "part_start": ps, "part_state": pst, "n_part": npart}
 
 
+@_on_device
 def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor,
                        splits: int = 0, want_f64: bool = False, logit_scale: float | None = None,
                        want_lse: bool = False):
@@ -397,6 +429,7 @@ def sparse_decode_attn(values: torch.Tensor, sel_tok: torch.Tensor, sel_score: t
     return res if len(res) > 1 else res[0]
 
 
+@_on_device
 def lse_merge(parts: torch.Tensor, logit_scale: float, want_f64: bool = False):
     """Merge shard partials parts [P, n_lanes, d + 2] f64 = (m, l, o normalised) (kvt_lse_merge)."""
     require_cuda(parts)
@@ -421,6 +454,7 @@ class LayerWorkspace:
         self.key = (n_lanes, n_cap, max_leaves, d)
 
 
+@_on_device
 def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch.Tensor,
                   n: int, k: int, C: int, ws: LayerWorkspace, out: dict, attn_splits: int = 0,
                   score_blocks: int = 0, exact_scores: bool = False, abs_mag: torch.Tensor | None = None,
@@ -463,6 +497,7 @@ def lane_abs_mag(amax: torch.Tensor, amin: torch.Tensor, m: int, out: torch.Tens
     return out
 
 
+@_on_device
 def chunk_bounds_fast(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n: int, C: int,
                       abs_mag: torch.Tensor):
     """Sound f32 directed-rounding (U, L, A_lane) over bf16 abstracts (kvt_chunk_bounds_fast)."""
@@ -480,3 +515,31 @@ def chunk_bounds_fast(q: torch.Tensor, amax: torch.Tensor, amin: torch.Tensor, n
 
 def sqrt_d(d: int) -> float:
     return math.sqrt(d)
+
+
+# -- synthetic workload (bench / tests; not on the decode path) ------------------------------------
+
+
+@_on_device
+def synth_layer(keys: torch.Tensor | None, values: torch.Tensor | None, params: dict, n: int, gen: dict) -> None:
+    """Fill rows [0, n) of bf16 keys / values [n_lanes, N_cap, d] with the counter-hash synthetic
+    workload (kvt_synth_layer).  params: per-lane {"seed" u32, "u" f32 [lanes, d], "regions" i32
+    [lanes, R, 2]} (workload.lane_params); gen: workload.gen_args."""
+    t = keys if keys is not None else values
+    require_cuda(t)
+    if t.dtype != torch.bfloat16:
+        raise ValueError("synth_layer writes bf16 rows")
+    ls, d = _lanes(t)
+    nl = t.shape[0]
+    if keys is not None and values is not None and (values.shape != keys.shape or values.stride(0) != ls):
+        raise ValueError("keys and values must share shape and lane stride")
+    dev = t.device
+    seed = torch.from_numpy(params["seed"].astype("uint32").view("int32")).to(dev)
+    u = torch.from_numpy(params["u"]).to(device=dev, dtype=torch.float32).contiguous()
+    reg = torch.from_numpy(params["regions"]).to(device=dev, dtype=torch.int32).contiguous()
+    if seed.numel() != nl or u.shape != (nl, d):
+        raise ValueError("synth_layer: params do not match the lanes")
+    L.check(L.kvt_synth_layer(_p(keys), _p(values), nl, ls, n, d, seed.data_ptr(), u.data_ptr(), reg.data_ptr(),
+                              reg.shape[1], float(gen["desert_base"]), float(gen["desert_span"]),
+                              float(gen["hot_base"]), float(gen["hot_span"]), float(gen["noise_scale"]),
+                              int(gen["planted"]), _stream()), "synth_layer")
