@@ -566,6 +566,8 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
     L = args.layers
     gqa = ops.kv_group(dec.kv_group)
     is_i4 = isinstance(dec.K, ops.I4KV)
+    ugrp = dec.kv_group if is_i4 else 1  # select_attend's GQA union candidates (INT4 keys)
+    cgrp = ops.cand_group(ugrp)
     score_fn = ops.cand_score_i4mma if is_i4 else ops.cand_score_f32
     q_static = q_step.clone()
     inter = []
@@ -576,11 +578,11 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
             return ops.chunk_bounds_fast(q_static[l], amax, amin, n, C, dec.absmag[l])
         return ops.chunk_bounds(q_static[l], amax, amin, n, C, want_A=True)
 
-    with torch.cuda.stream(stream), gqa:
+    with torch.cuda.stream(stream), gqa, cgrp:
         for l in range(L):
             C, n, k = dec.grid(l)[0], dec.n, dec.k_for(l)
             U, Lo, A = bounds_fn(l, n, C)
-            plan = ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
+            plan = ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM, group=ugrp)
             cs, ct = score_fn(q_static[l], dec.K[l], plan, n)
             st_, ss_, ns_, _ = ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
             inter.append((U, Lo, A, plan, cs, ct, st_, ss_, ns_))
@@ -595,7 +597,7 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
                 if name == "bounds":
                     bounds_fn(l, n, C)
                 elif name == "plan":
-                    ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM)
+                    ops.select_plan(U, Lo, n, k, C, A=A, d=HEAD_DIM, group=ugrp)
                 elif name == "score":
                     score_fn(q_static[l], dec.K[l], plan, n)
                 elif name == "select":
@@ -609,7 +611,7 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
     reps = 3
     for name in stages:
         fn = stage_fn(name)
-        with torch.cuda.stream(stream), gqa:
+        with torch.cuda.stream(stream), gqa, cgrp:
             fn()
             stream.synchronize()
             g = torch.cuda.CUDAGraph()
@@ -741,7 +743,7 @@ def run_ours(args):
     del res, dec
     torch.cuda.empty_cache()
     subs = []
-    for which in [s for s in args.sub.split(",") if s.strip()]:
+    for which in [s for s in args.sub.split(",") if s.strip() and s.strip() != "none"]:
         a = sub_args(args, which.strip())
         try:
             r = measure(a, torch, dist, world, rank, local, dev, tag=which)

@@ -159,6 +159,15 @@ KVT_API int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t* l
                     int64_t bnd_stride, int64_t k, int32_t* items, int64_t item_stride,
                     int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf, int64_t* evals,
                     const double* A, double* err, int d, void* stream);
+/* kvt_select_plan_group = kvt_select_plan2 for GQA groups of `grp` adjacent query lanes sharing
+ * a KV lane (decode path: uniform grid, no leaf_start): tau per query lane, candidates = the
+ * union over the group (U_h >= tau_h for any h), items / n_items per KV lane (n_lanes / grp
+ * rows), n_cand / evals / err per query lane.  grp = 1 is kvt_select_plan2. */
+KVT_API int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start,
+                    const int32_t* n_leaves, int64_t leaf_stride, const double* U, const double* L,
+                    int64_t bnd_stride, int64_t k, int32_t* items, int64_t item_stride,
+                    int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf, int64_t* evals,
+                    const double* A, double* err, int d, int grp, void* stream);
 KVT_API int kvt_cand_score_f32(const void* q, int q_dtype, const void* keys, int key_dtype,
                     int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,
                     int64_t item_stride, const int32_t* n_items, float* cand_score32,
@@ -299,6 +308,11 @@ KVT_API int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_bytes
  * lane i reads key/value/abstract lane i / kv_group.  Returns the previous value (1 = none).
  * kvt_select_attend uses its own kv_group field. */
 KVT_API int kvt_set_kv_group(int kv_group);
+/* GQA union candidates for the standalone entry points (kvt_cand_score_i4mma,
+ * kvt_topk_select_band) on this host thread: items from kvt_select_plan_group(grp = g), token
+ * ids shared per group (row of the group's first query lane).  kvt_select_attend sets it
+ * itself for INT4 keys.  Returns the previous value (1 = one candidate list per lane). */
+KVT_API int kvt_set_cand_group(int g);
 
 /* ---- synthetic workload (bench / test input generator; not on the decode path) ----------
  * The planted-desert model of trace.py:270-315 (generate_synthetic) as a counter hash, so

@@ -122,6 +122,17 @@ int& kv_group_tls() {
     return g;
 }
 
+int& cand_group_tls() {
+    static thread_local int g = 1;
+    return g;
+}
+
+extern "C" int kvt_set_cand_group(int g) {
+    const int old = cand_group_tls();
+    cand_group_tls() = g > 1 ? g : 1;
+    return old;
+}
+
 extern "C" int kvt_set_kv_group(int kv_group) {
     const int old = kv_group_tls();
     kv_group_tls() = kv_group > 1 ? kv_group : 1;
@@ -166,9 +177,13 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
                               a->leaf_stride, a->amax, a->amin, a->abs_dtype, a->abs_lane_stride, w.U, w.L,
                               fast ? w.A : nullptr, max_leaves, 0, stream);
     if (rc) return rc;
-    rc = kvt_select_plan2(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L, max_leaves,
-                          a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals, fast ? w.A : nullptr,
-                          fast ? w.err : nullptr, a->d, stream);
+    // GQA with INT4 keys: one candidate list per KV lane (union over its query lanes), scored
+    // once for the whole group (score_i4mma QG > 1); selectors read the shared token-id row
+    const int ugrp = (kvg > 1 && i4_fast) ? kvg : 1;
+    CandGroupScope cand_scope(ugrp);
+    rc = kvt_select_plan_group(a->n_lanes, a->n, a->C, a->leaf_start, a->n_leaves, a->leaf_stride, w.U, w.L,
+                               max_leaves, a->k, w.items, item_cap, w.n_items, w.n_cand, nullptr, a->evals,
+                               fast ? w.A : nullptr, fast ? w.err : nullptr, a->d, ugrp, stream);
     if (rc) return rc;
     if (fast) {
         if (a->key_dtype == KVT_I4)  // exact int32 inner products on the tensor cores + per-lane bound

@@ -15,6 +15,11 @@
 // A (the scoring error bound's sum |q||k| over a chunk) is replaced by one per-lane value,
 // A_lane = RU(sum_j |q_j| M_j), with M the lane's max-|key| vector over all chunks (kept by
 // the decoder next to the abstracts): A_lane >= every chunk's A, written for every chunk.
+//
+// GQA (kv_group g > 1): the work is enumerated over KV lanes; a stage's abstracts (one bulk
+// copy per 64 chunks of a KV lane) serve all g query lanes of the group, so abstract bytes
+// are read once per KV lane instead of once per query head (the reference replicates the KV
+// head per query head, adapters.py:121-136 -- identical bounds, g x the bytes).
 #include "common.cuh"
 
 namespace kvt {
@@ -86,7 +91,8 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t m = (n + C - 1) / C;
     const int64_t per_lane = (m + 63) / 64;
-    const int64_t total = per_lane * n_lanes;
+    const int n_kv = n_lanes / kvg;  // stages are per KV lane; kvg query lanes share each
+    const int64_t total = per_lane * n_kv;
     if (tid == 0) {
         for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BF_CONSUMERS); }
         fence_mbar_init();
@@ -106,40 +112,52 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
                 const uint32_t half = (uint32_t)(cnt * d * 2);
                 mbar_arrive_expect_tx(&full[s], 2 * half);
                 unsigned char* dst = smem + (size_t)s * tile;
-                bulk_g2s(dst, amax + (li / kvg) * abs_lane_stride + c0 * d, half, &full[s]);
-                bulk_g2s(dst + tile / 2, amin + (li / kvg) * abs_lane_stride + c0 * d, half, &full[s]);
+                bulk_g2s(dst, amax + li * abs_lane_stride + c0 * d, half, &full[s]);
+                bulk_g2s(dst + tile / 2, amin + li * abs_lane_stride + c0 * d, half, &full[s]);
                 c0 += 64;
                 if (c0 >= per_lane * 64) { c0 = 0; ++li; }
             }
         }
         return;
     }
+    constexpr int KVG_MAX = 8;
     int64_t cur = -1;
     uint64_t qp[G][2], qn[G][2];
-    float a_lane = 0.f;
+    float a_lane[KVG_MAX];
     int cs = 0, cr = 0;
     int64_t li = g0 / per_lane, c0 = (g0 % per_lane) * 64;
-    for (int64_t g = g0; g < g1; ++g) {
-        const int64_t cnt = kvt::imin(64, m - c0);
-        if (li != cur) {
-            cur = li;
-            float aa = 0.f;
+    // q+ / q- of query lane ql (packed pairs) and, optionally, A_lane (RU sum |q| M)
+    auto load_q = [&](int64_t ql, bool with_a) -> float {
+        float aa = 0.f;
 #pragma unroll
-            for (int r = 0; r < G; ++r) {
-                const float4 qv = *reinterpret_cast<const float4*>(q + li * d + 4 * (lane + 32 * r));
-                const float4 mv = *reinterpret_cast<const float4*>(mag + (li / kvg) * d + 4 * (lane + 32 * r));
-                qp[r][0] = pk2(fmaxf(qv.x, 0.f), fmaxf(qv.y, 0.f));
-                qp[r][1] = pk2(fmaxf(qv.z, 0.f), fmaxf(qv.w, 0.f));
-                qn[r][0] = pk2(fminf(qv.x, 0.f), fminf(qv.y, 0.f));
-                qn[r][1] = pk2(fminf(qv.z, 0.f), fminf(qv.w, 0.f));
+        for (int r = 0; r < G; ++r) {
+            const float4 qv = *reinterpret_cast<const float4*>(q + ql * d + 4 * (lane + 32 * r));
+            qp[r][0] = pk2(fmaxf(qv.x, 0.f), fmaxf(qv.y, 0.f));
+            qp[r][1] = pk2(fmaxf(qv.z, 0.f), fmaxf(qv.w, 0.f));
+            qn[r][0] = pk2(fminf(qv.x, 0.f), fminf(qv.y, 0.f));
+            qn[r][1] = pk2(fminf(qv.z, 0.f), fminf(qv.w, 0.f));
+            if (with_a) {
+                const float4 mv = *reinterpret_cast<const float4*>(mag + (ql / kvg) * d + 4 * (lane + 32 * r));
                 aa = __fmaf_ru(fabsf(qv.x), mv.x, aa);
                 aa = __fmaf_ru(fabsf(qv.y), mv.y, aa);
                 aa = __fmaf_ru(fabsf(qv.z), mv.z, aa);
                 aa = __fmaf_ru(fabsf(qv.w), mv.w, aa);
             }
+        }
+        if (with_a) {
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) aa = __fadd_ru(aa, __shfl_xor_sync(KVT_FULL, aa, o));
-            a_lane = aa;
+        }
+        return aa;
+    };
+    for (int64_t g = g0; g < g1; ++g) {
+        const int64_t cnt = kvt::imin(64, m - c0);
+        if (li != cur) {
+            cur = li;
+#pragma unroll
+            for (int h = 0; h < KVG_MAX; ++h)
+                if (h < kvg) a_lane[h] = load_q(li * kvg + h, true);
+            if (kvg > 1) load_q(li * kvg, false);
         }
         const int s = cs;
         mbar_wait(&full[s], (uint32_t)(cr & 1));
@@ -148,42 +166,52 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
         const unsigned char* Mn = Mx + tile / 2;
         const int base = 8 * warp;
         if (base < cnt) {
-            float pu[8], pl[8];
+#pragma unroll 1
+            for (int h = 0; h < kvg; ++h) {
+                if (h > 0) load_q(li * kvg + h, false);  // L1-resident: 512 B per head
+                float pu[8], pl[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                uint64_t u2 = 0ull, l2 = 0ull;
-                if (base + u < cnt) {
+                for (int u = 0; u < 8; ++u) {
+                    uint64_t u2 = 0ull, l2 = 0ull;
+                    if (base + u < cnt) {
 #pragma unroll
-                    for (int r = 0; r < G; ++r) {
-                        const int off = ((base + u) * d + 4 * (lane + 32 * r)) * 2;
-                        uint64_t h01, h23, l01, l23;
-                        bf4_pairs(*reinterpret_cast<const uint2*>(Mx + off), h01, h23);
-                        bf4_pairs(*reinterpret_cast<const uint2*>(Mn + off), l01, l23);
-                        u2 = fma2_rp(qp[r][0], h01, u2);
-                        u2 = fma2_rp(qn[r][0], l01, u2);
-                        u2 = fma2_rp(qp[r][1], h23, u2);
-                        u2 = fma2_rp(qn[r][1], l23, u2);
-                        l2 = fma2_rm(qp[r][0], l01, l2);
-                        l2 = fma2_rm(qn[r][0], h01, l2);
-                        l2 = fma2_rm(qp[r][1], l23, l2);
-                        l2 = fma2_rm(qn[r][1], h23, l2);
+                        for (int r = 0; r < G; ++r) {
+                            const int off = ((base + u) * d + 4 * (lane + 32 * r)) * 2;
+                            uint64_t h01, h23, l01, l23;
+                            bf4_pairs(*reinterpret_cast<const uint2*>(Mx + off), h01, h23);
+                            bf4_pairs(*reinterpret_cast<const uint2*>(Mn + off), l01, l23);
+                            u2 = fma2_rp(qp[r][0], h01, u2);
+                            u2 = fma2_rp(qn[r][0], l01, u2);
+                            u2 = fma2_rp(qp[r][1], h23, u2);
+                            u2 = fma2_rp(qn[r][1], l23, u2);
+                            l2 = fma2_rm(qp[r][0], l01, l2);
+                            l2 = fma2_rm(qn[r][0], h01, l2);
+                            l2 = fma2_rm(qp[r][1], l23, l2);
+                            l2 = fma2_rm(qn[r][1], h23, l2);
+                        }
                     }
+                    float a, b;
+                    upk2(u2, a, b);
+                    pu[u] = __fadd_ru(a, b);
+                    upk2(l2, a, b);
+                    pl[u] = __fadd_rd(a, b);
                 }
-                float a, b;
-                upk2(u2, a, b);
-                pu[u] = __fadd_ru(a, b);
-                upk2(l2, a, b);
-                pl[u] = __fadd_rd(a, b);
+                const float uu = rs8<true>(pu, lane);
+                const float ll = rs8<false>(pl, lane);
+                const int t = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
+                float ah = a_lane[0];
+#pragma unroll
+                for (int x = 1; x < KVG_MAX; ++x)
+                    if (x == h) ah = a_lane[x];
+                if ((lane & 3) == 0 && base + t < cnt) {
+                    const int64_t c = c0 + base + t;
+                    const int64_t ql = li * kvg + h;
+                    U[ql * bnd_stride + c] = (double)uu;
+                    L[ql * bnd_stride + c] = (double)ll;
+                    if (A) A[ql * bnd_stride + c] = (double)ah;
+                }
             }
-            const float uu = rs8<true>(pu, lane);
-            const float ll = rs8<false>(pl, lane);
-            const int t = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
-            if ((lane & 3) == 0 && base + t < cnt) {
-                const int64_t c = c0 + base + t;
-                U[li * bnd_stride + c] = (double)uu;
-                L[li * bnd_stride + c] = (double)ll;
-                if (A) A[li * bnd_stride + c] = (double)a_lane;
-            }
+            if (kvg > 1) load_q(li * kvg, false);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -206,6 +234,7 @@ extern "C" int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int
         return KVT_ERR_SHAPE;
     if (n_lanes == 0 || n == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
+    if (kv_group_current() > 8 || n_lanes % kv_group_current()) return KVT_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const int tile = 2 * 64 * d * 2;
     const int stages = (int)kvt::imax(2, kvt::imin(4, (100 * 1024) / tile));

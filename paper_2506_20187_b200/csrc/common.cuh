@@ -393,6 +393,17 @@ struct KvGroupScope {
     ~KvGroupScope() { kv_group_tls() = saved; }
 };
 inline int kv_group_current() { return kv_group_tls(); }
+// GQA union candidates (kvt_select_attend, INT4 keys): the plan emits one candidate list per
+// KV lane (the union over its query lanes) and the scorer writes the candidates' token ids
+// once per group, in the row of the group's first query lane; the selectors read row
+// (i / g) * g.  1 = one list per query lane.
+int& cand_group_tls();
+struct CandGroupScope {
+    int saved;
+    explicit CandGroupScope(int g) : saved(cand_group_tls()) { cand_group_tls() = g > 1 ? g : 1; }
+    ~CandGroupScope() { cand_group_tls() = saved; }
+};
+inline int cand_group_current() { return cand_group_tls(); }
 
 // Programmatic dependent launch (decode-path kernels): a kernel launched with
 // launch_pdl may start while its predecessor drains; pdl_entry() -- the first statement of

@@ -13,6 +13,13 @@
 // Runs of adjacent candidate leaves are merged: items start at a run's first token and at
 // every multiple of 64 inside a run, and end at the next multiple of 64 or the run's end,
 // so small leaves (C = 8 in the early layers) still give full 64-token items.
+//
+// GQA union mode (grp = g > 1, decode path): one CTA per KV lane.  tau_h is found for each of
+// the g query lanes h of the group (their own bounds and k), and a leaf is a candidate when
+// U_h >= tau_h for ANY h.  The union's items are emitted once per KV lane, so the scorer
+// reads each candidate record once for all g heads; every query lane's candidate list is the
+// union (a superset of its own candidates -- its exact top-k is unchanged, only eval_count
+// grows).  The per-query-lane error record takes max U_h and max A over the union.
 #include "common.cuh"
 
 namespace kvt {
@@ -31,94 +38,117 @@ __device__ __forceinline__ int64_t leaf_begin(const int32_t* ls, int64_t c, int 
     return ls ? (int64_t)ls[c] : c * C;
 }
 
-__global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
+template <int GMAX>  // 1: one query lane per CTA; 8: GQA union over grp <= 8 query lanes
+__global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
     int64_t n, int C, const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ n_leaves,
     int64_t leaf_stride, const double* __restrict__ U, const double* __restrict__ L, int64_t bnd_stride,
     int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
     int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals, int stage_cap,
-    const double* __restrict__ A, double* __restrict__ err, double err_factor) {
+    const double* __restrict__ A, double* __restrict__ err, double err_factor, int grp) {
     pdl_entry();
+    if (GMAX == 1) grp = 1;
     extern __shared__ __align__(16) unsigned char plan_smem[];
     uint64_t* kst = reinterpret_cast<uint64_t*>(plan_smem);  // staged keys (if they fit)
+    int8_t* fl = reinterpret_cast<int8_t*>(plan_smem) + (size_t)stage_cap * 8;  // union flags (grp > 1)
     __shared__ unsigned long long hist[256];
     __shared__ long long scan_sh[33];
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ long long s_remaining;
     __shared__ int s_done;
+    __shared__ double s_tau[GMAX];
     const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t li = blockIdx.x;
+    const int64_t li = blockIdx.x;  // query lane, or KV lane when grp > 1
+    const int64_t q0 = li * grp;    // first query lane of the group
     const int32_t* ls = leaf_start ? leaf_start + li * leaf_stride : nullptr;
     const int64_t nl = leaf_start ? (int64_t)n_leaves[li] : (n + C - 1) / C;
-    const double* Ul = U + li * bnd_stride;
-    const double* Ll = L + li * bnd_stride;
-
     const bool staged = nl <= stage_cap;
-    if (staged)
-        for (int64_t c = tid; c < nl; c += PLAN_THREADS) kst[c] = ord_key(Ll[c]);
-    if (tid == 0) { s_prefix = 0; s_mask = 0; s_remaining = k; s_done = (k <= 0); }
-    __syncthreads();
 
-    // ---- weighted radix select on the top 24 key bits ----
-    for (int shift = 56; shift >= 40 && !s_done; shift -= 8) {
-        for (int i = tid; i < 256; i += PLAN_THREADS) hist[i] = 0;
+    for (int h = 0; h < grp; ++h) {
+        const double* Ll = L + (q0 + h) * bnd_stride;
+        if (staged)
+            for (int64_t c = tid; c < nl; c += PLAN_THREADS) kst[c] = ord_key(Ll[c]);
+        if (tid == 0) { s_prefix = 0; s_mask = 0; s_remaining = k; s_done = (k <= 0); }
         __syncthreads();
-        const unsigned long long prefix = s_prefix, mask = s_mask;
-        for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
-            const int64_t c = base + tid;
-            int digit = 256;
-            unsigned long long w = 0;
-            if (c < nl) {
-                const uint64_t key = staged ? kst[c] : ord_key(Ll[c]);
-                if ((key & mask) == prefix) {
-                    digit = (int)((key >> shift) & 0xff);
-                    w = (unsigned long long)leaf_rows(ls, nl, c, n, C);
+
+        // ---- weighted radix select on the top 24 key bits ----
+        for (int shift = 56; shift >= 40 && !s_done; shift -= 8) {
+            for (int i = tid; i < 256; i += PLAN_THREADS) hist[i] = 0;
+            __syncthreads();
+            const unsigned long long prefix = s_prefix, mask = s_mask;
+            for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
+                const int64_t c = base + tid;
+                int digit = 256;
+                unsigned long long w = 0;
+                if (c < nl) {
+                    const uint64_t key = staged ? kst[c] : ord_key(Ll[c]);
+                    if ((key & mask) == prefix) {
+                        digit = (int)((key >> shift) & 0xff);
+                        w = (unsigned long long)leaf_rows(ls, nl, c, n, C);
+                    }
+                }
+                // warp-aggregated weighted histogram: leaves are disjoint, so 32 row counts sum to <= n
+                const unsigned peers = __match_any_sync(KVT_FULL, digit);
+                const unsigned sum = __reduce_add_sync(peers, (unsigned)w);
+                if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned long long)sum);
+            }
+            __syncthreads();
+            if (tid < 32) {
+                // lane covers bins 255-8*lane .. 248-8*lane (descending)
+                unsigned long long loc = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) loc += hist[255 - 8 * lane - i];
+                unsigned long long inc = warp_incl_scan(loc, lane);
+                const unsigned long long exc = inc - loc;
+                const unsigned long long rem = (unsigned long long)s_remaining;
+                __syncwarp();  // all lanes have read s_remaining before one lane rewrites it
+                const bool mine = exc < rem && rem <= inc;
+                if (mine) {
+                    unsigned long long run = exc;
+                    for (int i = 0; i < 8; ++i) {
+                        const int b = 255 - 8 * lane - i;
+                        if (run + hist[b] >= rem) {
+                            s_prefix = prefix | ((unsigned long long)b << shift);
+                            s_mask = mask | (0xffull << shift);
+                            s_remaining = (long long)(rem - run);
+                            break;
+                        }
+                        run += hist[b];
+                    }
                 }
             }
-            // warp-aggregated weighted histogram: leaves are disjoint, so 32 row counts sum to <= n
-            const unsigned peers = __match_any_sync(KVT_FULL, digit);
-            const unsigned sum = __reduce_add_sync(peers, (unsigned)w);
-            if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned long long)sum);
+            __syncthreads();
         }
-        __syncthreads();
-        if (tid < 32) {
-            // lane covers bins 255-8*lane .. 248-8*lane (descending)
-            unsigned long long loc = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) loc += hist[255 - 8 * lane - i];
-            unsigned long long inc = warp_incl_scan(loc, lane);
-            const unsigned long long exc = inc - loc;
-            const unsigned long long rem = (unsigned long long)s_remaining;
-            __syncwarp();  // all lanes have read s_remaining before one lane rewrites it
-            const bool mine = exc < rem && rem <= inc;
-            if (mine) {
-                unsigned long long run = exc;
-                for (int i = 0; i < 8; ++i) {
-                    const int b = 255 - 8 * lane - i;
-                    if (run + hist[b] >= rem) {
-                        s_prefix = prefix | ((unsigned long long)b << shift);
-                        s_mask = mask | (0xffull << shift);
-                        s_remaining = (long long)(rem - run);
-                        break;
-                    }
-                    run += hist[b];
-                }
+        const double tau_h = (k <= 0) ? INFINITY : key_to_double(s_prefix);
+        if (tid == 0) s_tau[h] = tau_h;
+        if (grp > 1 && staged) {  // union flags: OR over the group's heads
+            const double* Uh = U + (q0 + h) * bnd_stride;
+            for (int64_t c = tid; c < nl; c += PLAN_THREADS) {
+                const int8_t f = Uh[c] >= tau_h ? 1 : 0;
+                fl[c] = h == 0 ? f : (int8_t)(fl[c] | f);
             }
         }
         __syncthreads();
     }
-    const double tau = (k <= 0) ? INFINITY : key_to_double(s_prefix);
+    const double tau = s_tau[0];
+    const double* Ul = U + q0 * bnd_stride;
 
-    // ---- candidate flags (staged over the keys, which are no longer needed) ----
-    int8_t* fl = reinterpret_cast<int8_t*>(plan_smem);
+    // ---- candidate flags (single head: staged over the keys, which are no longer needed) ----
+    int8_t* fl1 = reinterpret_cast<int8_t*>(plan_smem);
+    if (grp == 1 && staged)
+        for (int64_t c = tid; c < nl; c += PLAN_THREADS) fl1[c] = Ul[c] >= tau ? 1 : 0;
     __syncthreads();
-    if (staged)
-        for (int64_t c = tid; c < nl; c += PLAN_THREADS) fl[c] = Ul[c] >= tau ? 1 : 0;
-    __syncthreads();
-    auto is_cand = [&](int64_t c) -> bool { return staged ? fl[c] != 0 : Ul[c] >= tau; };
+    auto is_cand = [&](int64_t c) -> bool {
+        if (staged) return (grp == 1 ? fl1[c] : fl[c]) != 0;
+        for (int h = 0; h < grp; ++h)
+            if (U[(q0 + h) * bnd_stride + c] >= s_tau[h]) return true;
+        return false;
+    };
 
-    // ---- candidate compaction -> items (+ max A over candidates for the f32 error bound) ----
+    // ---- candidate compaction -> items (+ max A / max U over candidates, per query lane) ----
     long long carry_items = 0, carry_tok = 0;
-    double amax_c = 0.0, umax_c = -INFINITY;
+    double amax_c[GMAX], umax_c[GMAX];
+#pragma unroll
+    for (int h = 0; h < GMAX; ++h) { amax_c[h] = 0.0; umax_c[h] = -INFINITY; }
     for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
         const int64_t c = base + tid;
         long long it = 0, tk = 0;
@@ -134,9 +164,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
                 first = (run_start || s % ITEM_TOKENS == 0) ? s : (s / ITEM_TOKENS + 1) * ITEM_TOKENS;
                 const int64_t e = s + rows;
                 it = first < e ? 1 + ((e - 1) / ITEM_TOKENS - first / ITEM_TOKENS) : 0;
+#pragma unroll
+                for (int h = 0; h < GMAX; ++h) {
+                    if (h < grp) {
+                        if (A) amax_c[h] = fmax(amax_c[h], A[(q0 + h) * bnd_stride + c]);
+                        umax_c[h] = fmax(umax_c[h], U[(q0 + h) * bnd_stride + c]);
+                    }
+                }
             }
-            if (cand && A) amax_c = fmax(amax_c, A[li * bnd_stride + c]);
-            if (cand) umax_c = fmax(umax_c, Ul[c]);
             if (cand_leaf) cand_leaf[li * leaf_stride + c] = cand ? 1 : 0;
         }
         // one scan of (items << 40 | tokens): items < 2^23 and tokens < 2^40 per lane
@@ -167,29 +202,38 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(
         carry_tok += tot_tk;
     }
     if (err) {
-        // err record per lane: [bound on |f32 estimate - canonical dot|, tau, max U over candidates, 0]
+        // err record per query lane: [bound on |f32 estimate - canonical dot|, tau, max U over candidates, 0]
+        __syncthreads();
+        double* red = reinterpret_cast<double*>(hist);  // 256 x 8 B: [amax | umax] x 16 warps
+        for (int h = 0; h < grp; ++h) {
+            double am = 0.0, um = -INFINITY;
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-            amax_c = fmax(amax_c, __shfl_xor_sync(KVT_FULL, amax_c, off));
-            umax_c = fmax(umax_c, __shfl_xor_sync(KVT_FULL, umax_c, off));
-        }
-        __syncthreads();
-        double* red = reinterpret_cast<double*>(hist);
-        if (lane == 0) { red[tid >> 5] = amax_c; red[32 + (tid >> 5)] = umax_c; }
-        __syncthreads();
-        if (tid == 0) {
-            double m = 0.0, um = -INFINITY;
-            for (int w = 0; w < PLAN_THREADS / 32; ++w) { m = fmax(m, red[w]); um = fmax(um, red[32 + w]); }
-            err[li * 4 + 0] = m * err_factor;
-            err[li * 4 + 1] = tau;
-            err[li * 4 + 2] = um;
-            err[li * 4 + 3] = 0.0;
+            for (int x = 0; x < GMAX; ++x)
+                if (x == h) { am = amax_c[x]; um = umax_c[x]; }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                am = fmax(am, __shfl_xor_sync(KVT_FULL, am, off));
+                um = fmax(um, __shfl_xor_sync(KVT_FULL, um, off));
+            }
+            if (lane == 0) { red[tid >> 5] = am; red[32 + (tid >> 5)] = um; }
+            __syncthreads();
+            if (tid == 0) {
+                double m = 0.0, umx = -INFINITY;
+                for (int w = 0; w < PLAN_THREADS / 32; ++w) { m = fmax(m, red[w]); umx = fmax(umx, red[32 + w]); }
+                err[(q0 + h) * 4 + 0] = m * err_factor;
+                err[(q0 + h) * 4 + 1] = s_tau[h];
+                err[(q0 + h) * 4 + 2] = umx;
+                err[(q0 + h) * 4 + 3] = 0.0;
+            }
+            __syncthreads();
         }
     }
     if (tid == 0) {
         n_items[li] = (int32_t)carry_items;
-        n_cand[li] = (int32_t)carry_tok;
-        if (evals) evals[li] = (int64_t)nl + carry_tok;
+        for (int h = 0; h < grp; ++h) {
+            n_cand[q0 + h] = (int32_t)carry_tok;
+            if (evals) evals[q0 + h] = (int64_t)nl + carry_tok;
+        }
     }
 }
 
@@ -220,6 +264,16 @@ extern "C" int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t
                         int64_t leaf_stride, const double* U, const double* L, int64_t bnd_stride, int64_t k,
                         int32_t* items, int64_t item_stride, int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf,
                         int64_t* evals, const double* A, double* err, int d, void* stream) {
+    return kvt_select_plan_group(n_lanes, n, C, leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items,
+                                 item_stride, n_items, n_cand, cand_leaf, evals, A, err, d, 1, stream);
+}
+
+extern "C" int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const int32_t* leaf_start,
+                                     const int32_t* n_leaves, int64_t leaf_stride, const double* U, const double* L,
+                                     int64_t bnd_stride, int64_t k, int32_t* items, int64_t item_stride,
+                                     int32_t* n_items, int32_t* n_cand, int8_t* cand_leaf, int64_t* evals,
+                                     const double* A, double* err, int d, int grp, void* stream) {
+    if (grp < 1 || grp > 8 || n_lanes % grp || (grp > 1 && leaf_start)) return KVT_ERR_ARG;
     if (!U || !L || !items || !n_items || !n_cand || n_lanes < 0 || n < 0) return KVT_ERR_ARG;
     if (!leaf_start && C < 1) return KVT_ERR_ARG;
     if (k < 0 || k > n) return KVT_ERR_K;
@@ -228,14 +282,17 @@ extern "C" int kvt_select_plan2(int64_t n_lanes, int64_t n, int C, const int32_t
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
     KVT_PER_DEVICE(bool, configured);
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(plan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(plan_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 9);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = true;
     }
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
     const int cap = (int)kvt::imin(max_leaves, 16384);
-    launch_pdl(plan_kernel, dim3((unsigned)n_lanes), dim3(PLAN_THREADS), (size_t)cap * 8, (cudaStream_t)stream, n, C,
+    const size_t smem = (size_t)cap * (grp > 1 ? 9 : 8);
+    launch_pdl(grp > 1 ? plan_kernel<8> : plan_kernel<1>, dim3((unsigned)(n_lanes / grp)), dim3(PLAN_THREADS), smem, (cudaStream_t)stream, n, C,
                leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand, cand_leaf,
-               evals, cap, A, err, f32_err_factor(d));
+               evals, cap, A, err, f32_err_factor(d), grp);
     return kvt_check_launch();
 }

@@ -27,6 +27,16 @@
 // owning tokens 16w..16w+15 of the item.  Per 16 tokens and 128 dims a warp issues 2 LDS.128
 // of codes, 8 MMAs and ~40 f32 ops -- a few instructions per token instead of the ~4 per dim
 // of CUDA-core dequantisation.
+//
+// GQA union mode (QG = group size > 1, kvt_select_plan_group items): items are per KV lane,
+// so each candidate record is read from HBM once for all QG query lanes of the group, and
+// the heads fill the MMA's N dimension instead of zero padding.  The K order of one MMA is
+// then the 32 dims of ONE group (thread tig holds word tig of the group's 16 code bytes),
+// and column n = 2h + (p & 1) carries digit p of head h (parts 0,1 in the first MMA, 2,3 in
+// the second): per 16 tokens and 128 dims still 8 MMAs, now for 4 heads, and thread tig
+// owns head tig's partials of every group -- the epilogue needs no shuffles.  Heads 4..7
+// (QG = 8) take a second pass with their digits reloaded (L1).  Token ids are written once,
+// in the group's first query-lane row.
 #include <cfloat>
 #include <algorithm>
 #include <cmath>
@@ -120,7 +130,7 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, ui
 }
 
 // ---- the scoring kernel --------------------------------------------------------------------
-template <int R>  // R = d / 128 rounds of 4 groups
+template <int R, int QG>  // R = d / 128 rounds of 4 groups; QG = query lanes per item row (GQA union)
 __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
     int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
@@ -131,7 +141,7 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     constexpr int row_b = d / 2 + G * 4;
     constexpr int tile_b = QM_ROWS * row_b;
     constexpr int qb = G * 144 + 16;
-    constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
+    constexpr int stage_b = (tile_b + QG * qb + 15) / 16 * 16;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[QM_STAGES], empty[QM_STAGES];
     __shared__ int4 meta[QM_STAGES];
@@ -206,13 +216,14 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                     const bool newq = cur != prev;
                     if (lane == 0) {
                         if (pr > 0) mbar_wait(&empty[s], (uint32_t)((pr - 1) & 1));
-                        const uint32_t bytes = (uint32_t)(cnt * row_b) + (newq ? (uint32_t)qb : 0u);
+                        const uint32_t bytes = (uint32_t)(cnt * row_b) + (newq ? (uint32_t)(QG * qb) : 0u);
                         meta[s] = make_int4(cur, t0, cnt, pos0);
                         mbar_arrive_expect_tx(&full[s], bytes);
                         unsigned char* st = smem + (size_t)s * stage_b;
-                        bulk_g2s(st, keys + (int64_t)(cur / kvg) * lane_stride_b + (int64_t)t0 * row_b,
+                        const int64_t kv_row = QG > 1 ? (int64_t)cur : (int64_t)(cur / kvg);
+                        bulk_g2s(st, keys + kv_row * lane_stride_b + (int64_t)t0 * row_b,
                                  (uint32_t)(cnt * row_b), &full[s]);
-                        if (newq) bulk_g2s(st + tile_b, qprep + (int64_t)cur * qb, (uint32_t)qb, &full[s]);
+                        if (newq) bulk_g2s(st + tile_b, qprep + (int64_t)cur * QG * qb, (uint32_t)(QG * qb), &full[s]);
                     }
                     prev = cur;
                     if (++ps == QM_STAGES) { ps = 0; ++pr; }
@@ -231,6 +242,7 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
 
     // ---- consumers ----
     const int gid = lane >> 2, tig = lane & 3;
+    if constexpr (QG == 1) {
     uint32_t B[R][2][4][2];
     float qt[R], W[R], sp[4];
     int cur = -1;
@@ -328,7 +340,7 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                 if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + row] = t0 + row;
                 emax = fmaxf(emax, er);
             }
-        }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -339,6 +351,128 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     if (lane == 0 && cur >= 0 && e > 0.f)
         atomicMax(reinterpret_cast<unsigned long long*>(err + (int64_t)cur * 4 + 3),
                   (unsigned long long)__double_as_longlong((double)e));
+    } else {
+    // ---- GQA: heads on the MMA N dimension (module header) ----
+    constexpr int NQ = (QG + 3) / 4;  // passes of 4 heads
+    uint32_t B[G][2][2];
+    float qt[G], W[G], sp[4];
+    int cur = -1;
+    float emax = 0.f;  // this thread's head of the current pass... per pass below
+    float emaxq[NQ];
+#pragma unroll
+    for (int x = 0; x < NQ; ++x) emaxq[x] = 0.f;
+    int cs = 0, cr = 0;
+    // head (4 hq + gid / 2) digits for the B operand; head (4 hq + tig) epilogue constants
+    auto load_quad = [&](const unsigned char* qs, int hq) {
+        const int hb = 4 * hq + (gid >> 1);
+        const unsigned char* qb_ = qs + (size_t)(hb < QG ? hb : 0) * qb;
+#pragma unroll
+        for (int G_ = 0; G_ < G; ++G_) {
+#pragma unroll
+            for (int S = 0; S < 2; ++S) {
+                const int p = 2 * S + (gid & 1);
+                const uint2 x = *reinterpret_cast<const uint2*>(qb_ + G_ * 128 + p * 32 + tig * 8);
+                B[G_][S][0] = hb < QG ? x.x : 0u;
+                B[G_][S][1] = hb < QG ? x.y : 0u;
+            }
+        }
+        const int he = 4 * hq + tig;
+        const unsigned char* qe = qs + (size_t)(he < QG ? he : 0) * qb;
+#pragma unroll
+        for (int G_ = 0; G_ < G; ++G_) {
+            const float2 c2 = *reinterpret_cast<const float2*>(qe + G * 128 + 16 * G_);
+            qt[G_] = c2.x;
+            W[G_] = c2.y;
+        }
+        const float4 s4 = *reinterpret_cast<const float4*>(qe + G * 144);
+        sp[0] = s4.x; sp[1] = s4.y; sp[2] = s4.z; sp[3] = s4.w;
+    };
+    auto flush = [&]() {
+#pragma unroll
+        for (int x = 0; x < NQ; ++x) {
+            float e2 = emaxq[x];
+            // lanes of one tig share a head: reduce over gid (lane bits 2..4)
+#pragma unroll
+            for (int o = 16; o >= 4; o >>= 1) e2 = fmaxf(e2, __shfl_xor_sync(KVT_FULL, e2, o));
+            const int he = 4 * x + tig;
+            if (gid == 0 && cur >= 0 && he < QG && e2 > 0.f)
+                atomicMax(reinterpret_cast<unsigned long long*>(err + ((int64_t)cur * QG + he) * 4 + 3),
+                          (unsigned long long)__double_as_longlong((double)e2));
+            emaxq[x] = 0.f;
+        }
+    };
+    (void)emax;
+    const unsigned char* qglob = nullptr;
+    for (;;) {
+        const int s = cs;
+        mbar_wait(&full[s], (uint32_t)(cr & 1));
+        if (++cs == QM_STAGES) { cs = 0; ++cr; }
+        const int4 mt = meta[s];
+        if (mt.z < 0) break;
+        const unsigned char* st = smem + (size_t)s * stage_b;
+        if (mt.x != cur) {
+            flush();
+            cur = mt.x;
+            qglob = qprep + (int64_t)cur * QG * qb;
+            load_quad(st + tile_b, 0);
+        }
+        const int cnt = mt.z, pos0 = mt.w, t0 = mt.y;
+#pragma unroll
+        for (int tt = 0; tt < QM_ROWS / 64; ++tt) {
+          if (64 * tt + 16 * warp < cnt) {
+            const int row0 = 64 * tt + 16 * warp + gid, row1 = row0 + 8;
+#pragma unroll 1
+            for (int hq = 0; hq < NQ; ++hq) {
+                if (NQ > 1) load_quad(qglob, hq);  // heads 4 hq.. (L1-resident digit blocks)
+                float est0 = 0.f, est1 = 0.f, er0 = 0.f, er1 = 0.f;
+#pragma unroll
+                for (int G_ = 0; G_ < G; ++G_) {
+                    const uint32_t w0 = *reinterpret_cast<const uint32_t*>(st + row0 * row_b + 16 * G_ + 4 * tig);
+                    const uint32_t w1 = *reinterpret_cast<const uint32_t*>(st + row1 * row_b + 16 * G_ + 4 * tig);
+                    const uint32_t a0 = w0 & 0x0f0f0f0fu, a2 = (w0 >> 4) & 0x0f0f0f0fu;
+                    const uint32_t a1 = w1 & 0x0f0f0f0fu, a3 = (w1 >> 4) & 0x0f0f0f0fu;
+                    int c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+                    mma_s8(c0, a0, a1, a2, a3, B[G_][0][0], B[G_][0][1]);
+                    mma_s8(c1, a0, a1, a2, a3, B[G_][1][0], B[G_][1][1]);
+                    // thread tig: head 4 hq + tig, parts 0,1 (c0) and 2,3 (c1), rows gid / gid + 8
+                    const float in0 = fmaf(sp[3], (float)c1[1], fmaf(sp[2], (float)c1[0], fmaf(sp[1], (float)c0[1], sp[0] * (float)c0[0])));
+                    const float in1 = fmaf(sp[3], (float)c1[3], fmaf(sp[2], (float)c1[2], fmaf(sp[1], (float)c0[3], sp[0] * (float)c0[2])));
+                    const uint32_t h0 = *reinterpret_cast<const uint32_t*>(st + row0 * row_b + d / 2 + 4 * G_);
+                    const uint32_t h1 = *reinterpret_cast<const uint32_t*>(st + row1 * row_b + d / 2 + 4 * G_);
+                    const __half2 p0 = *reinterpret_cast<const __half2*>(&h0), p1 = *reinterpret_cast<const __half2*>(&h1);
+                    const float sc0 = __low2float(p0), mn0 = __high2float(p0);
+                    const float sc1 = __low2float(p1), mn1 = __high2float(p1);
+                    est0 += fmaf(sc0, in0, mn0 * qt[G_]);
+                    est1 += fmaf(sc1, in1, mn1 * qt[G_]);
+                    er0 = fmaf(fmaf(15.f, fabsf(sc0), fabsf(mn0)), W[G_], er0);
+                    er1 = fmaf(fmaf(15.f, fabsf(sc1), fabsf(mn1)), W[G_], er1);
+                }
+                const int he = 4 * hq + tig;
+                if (he < QG) {
+                    const int64_t orow = (int64_t)cur * QG + he;
+                    const float e0 = 1.001f * __fmaf_rn(0x1p-24f, fabsf(est0), er0);
+                    const float e1 = 1.001f * __fmaf_rn(0x1p-24f, fabsf(est1), er1);
+                    float em = 0.f;
+                    if (row0 < cnt) { out32[orow * out_stride + pos0 + row0] = est0; em = e0; }
+                    if (row1 < cnt) { out32[orow * out_stride + pos0 + row1] = est1; em = fmaxf(em, e1); }
+#pragma unroll
+                    for (int x = 0; x < NQ; ++x)
+                        if (x == hq) emaxq[x] = fmaxf(emaxq[x], em);
+                    if (out_tok && he == 0) {
+                        const int64_t trow = (int64_t)cur * QG * out_stride + pos0;
+                        if (row0 < cnt) out_tok[trow + row0] = t0 + row0;
+                        if (row1 < cnt) out_tok[trow + row1] = t0 + row1;
+                    }
+                }
+            }
+            if (NQ > 1) load_quad(qglob, 0);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    flush();
+    }
 }
 
 }  // namespace kvt
@@ -366,24 +500,25 @@ extern "C" int kvt_i4_qprep(const void* q, int q_dtype, int64_t n_lanes, int d, 
     return kvt_check_launch();
 }
 
-template <int R>
-static int launch_i4mma(const void* keys, int64_t n_lanes, int64_t ls_b, const int32_t* items, int64_t item_stride,
+template <int R, int QG>
+static int launch_i4mma(const void* keys, int64_t n_rows, int64_t ls_b, const int32_t* items, int64_t item_stride,
                         const int32_t* n_items, const void* qprep, float* os, int32_t* ot, int64_t ostr, double* err,
                         cudaStream_t st) {
     constexpr int d = 128 * R, G = 4 * R, row_b = d / 2 + G * 4, tile_b = QM_ROWS * row_b, qb = G * 144 + 16;
-    constexpr int stage_b = (tile_b + qb + 15) / 16 * 16;
+    constexpr int stage_b = (tile_b + QG * qb + 15) / 16 * 16;
     const size_t smem = (size_t)QM_STAGES * stage_b;
     KVT_PER_DEVICE(bool, configured);
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(score_i4mma_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(score_i4mma_kernel<R, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = true;
     }
     const int sms = kvt::sm_count();
     KVT_PER_DEVICE(int, per_sm);
-    if (!per_sm) per_sm = resident_per_sm(score_i4mma_kernel<R>, QM_THREADS, smem, 4);
-    launch_pdl(score_i4mma_kernel<R>, dim3(sms * per_sm), dim3(QM_THREADS), smem, st, (const unsigned char*)keys, ls_b, (int)n_lanes, items, item_stride, n_items, (const unsigned char*)qprep, os, ot,
-        ostr, err, kv_group_current());
+    if (!per_sm) per_sm = resident_per_sm(score_i4mma_kernel<R, QG>, QM_THREADS, smem, 4);
+    launch_pdl(score_i4mma_kernel<R, QG>, dim3(sms * per_sm), dim3(QM_THREADS), smem, st, (const unsigned char*)keys, ls_b,
+               (int)n_rows, items, item_stride, n_items, (const unsigned char*)qprep, os, ot, ostr, err,
+               kv_group_current());
     return kvt_check_launch();
 }
 
@@ -395,13 +530,20 @@ extern "C" int kvt_cand_score_i4mma(const void* q, int q_dtype, const void* keys
     if (n_lanes <= 0) return n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
     if (!keys || !items || !n_items || !cand_score32 || !err || !qprep_ws) return KVT_ERR_ARG;
     if (((uintptr_t)keys % 16) || (lane_stride % 16) || n_lanes > INT32_MAX) return KVT_ERR_SHAPE;
+    // GQA union mode (cand_group g > 1): items per KV lane; g must divide n_lanes (query lanes)
+    const int qg = cand_group_current();
+    if (qg > 1 && (qg > 8 || n_lanes % qg || qg != kv_group_current())) return KVT_ERR_ARG;
     if (q) {  // q == nullptr: qprep_ws already holds the digits (kvt_select_attend runs kvt_i4_qprep on a side stream)
         int rc = kvt_i4_qprep(q, q_dtype, n_lanes, d, qprep_ws, stream);
         if (rc) return rc;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    return d == 128 ? launch_i4mma<1>(keys, n_lanes, lane_stride, items, item_stride, n_items, qprep_ws, cand_score32,
-                                      cand_tok, cand_stride, err, st)
-                    : launch_i4mma<2>(keys, n_lanes, lane_stride, items, item_stride, n_items, qprep_ws, cand_score32,
-                                      cand_tok, cand_stride, err, st);
+    const int64_t rows = n_lanes / qg;
+#define KVT_QM(RR, QQ) launch_i4mma<RR, QQ>(keys, rows, lane_stride, items, item_stride, n_items, qprep_ws, \
+                                            cand_score32, cand_tok, cand_stride, err, st)
+    if (qg == 1) return d == 128 ? KVT_QM(1, 1) : KVT_QM(2, 1);
+    if (qg == 2) return d == 128 ? KVT_QM(1, 2) : KVT_QM(2, 2);
+    if (qg <= 4) return qg == 4 ? (d == 128 ? KVT_QM(1, 4) : KVT_QM(2, 4)) : KVT_ERR_ARG;
+    return qg == 8 ? (d == 128 ? KVT_QM(1, 8) : KVT_QM(2, 8)) : KVT_ERR_ARG;
+#undef KVT_QM
 }

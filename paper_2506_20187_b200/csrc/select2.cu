@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(S2_THREADS) topk_select2_kernel(
     int64_t cand_stride, const double* __restrict__ err, int64_t k, const QT* __restrict__ q,
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, int32_t* __restrict__ sel_tok,
     double* __restrict__ sel_score, int64_t sel_stride, int32_t* __restrict__ n_sel, int slice_cap,
-    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs, int kvg) {
+    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs, int kvg, int tkg) {
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ S2Shared S;
     cg::cluster_group cluster = cg::this_cluster();
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(S2_THREADS) topk_select2_kernel(
     const int64_t lo = kvt::imin(n, (int64_t)rank * slice);
     const int64_t cnt = kvt::imin(n, lo + slice) - lo;
     const float* sc = cs32 + li * cand_stride + lo;
-    const int32_t* tk = ctok + li * cand_stride + lo;
+    const int32_t* tk = ctok + (li / tkg) * tkg * cand_stride + lo;  // GQA union: one id row per group
     const QT* ql = q + li * d;
     const unsigned char* kl = keys + (li / kvg) * lane_stride_b;
     uint32_t* k32 = reinterpret_cast<uint32_t*>(dyn_smem);
@@ -453,7 +453,7 @@ static int launch_select2(const float* cs32, const int32_t* ctok, const int32_t*
     cudaError_t e = cudaLaunchKernelEx(&cfg, topk_select2_kernel<QT, T>, cs32, ctok, n_cand, cand_stride, err, k,
                                        (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, sel_tok, sel_score,
                                        sel_stride, n_sel, (int)slice, run_start, run_len, run_stride, n_runs,
-                                       kv_group_current());
+                                       kv_group_current(), cand_group_current());
     if (e != cudaSuccess) return kvt_set_cuda_error(e);
     return kvt_check_launch();
 }

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     int64_t cand_stride, const double* __restrict__ rec, int64_t k, const QT* __restrict__ q,
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, double* __restrict__ scratch,
     int32_t* __restrict__ sel_tok, double* __restrict__ sel_score, int64_t sel_stride, int32_t* __restrict__ n_sel,
-    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs, int kvg) {
+    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs, int kvg, int tkg) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ S3Shared S;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const int64_t n = n_cand[li];
     const int64_t kk = kvt::imin(k, n);
     const float* sc = cs32 + li * cand_stride;
-    const int32_t* tk = ctok + li * cand_stride;
+    const int32_t* tk = ctok + (li - (int64_t)(blockIdx.x % (unsigned)tkg)) * cand_stride;  // GQA union: one id row per group
     const QT* ql = q + li * d;
     const unsigned char* kl = keys + (li / kvg) * lane_stride_b;
     int32_t* otok = sel_tok + li * sel_stride;
@@ -759,7 +759,7 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
         configured = true;
     }
     launch_pdl(topk_select3_kernel<QT, T>, dim3((unsigned)n_lanes), dim3(S3_THREADS), smem, st, cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
-        sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current());
+        sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current(), cand_group_current());
     return kvt_check_launch();
 }
 

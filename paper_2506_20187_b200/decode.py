@@ -207,7 +207,12 @@ class SparseDecoder:
             # abstracts once per KV lane (GQA query lanes of a group share them), q + U, L, A per lane
             out["bounds"] += self.kv_lanes * m * 2 * d * sA + self.lanes * (d * 8 + m * 24)
             out["plan"] += self.lanes * m * 24 + nc // 64 * 12
-            out["score"] += nc * (d * sK + 8)                                      # f32 estimate + token
+            if self.kv_group > 1 and self.dtype == ops.I4:
+                # GQA union: each KV lane's candidate records are read once for its g heads
+                # (n_cand of every query lane is the union), one f32 estimate per head
+                out["score"] += nc // self.kv_group * (d * sK + 4) + nc * 4
+            else:
+                out["score"] += nc * (d * sK + 8)                                  # f32 estimate + token
             out["select"] += nc * 8 + self.lanes * k * 12
             out["runs"] += self.lanes * k * 4 * 3
             out["attn"] += self.lanes * k * (d * sK + 4 + 8) + self.lanes * d * 4

@@ -91,6 +91,23 @@ class kv_group:
         L.kvt_set_kv_group(self.old)
 
 
+class cand_group:
+    """GQA union candidates for the standalone wrappers (kvt_set_cand_group): inside
+    `with ops.cand_group(g):` cand_score_i4mma scores the per-KV-lane union items of
+    select_plan(..., group=g) for all g query lanes, and topk_select_band reads the shared
+    token-id row of each group."""
+
+    def __init__(self, g: int):
+        self.g = max(int(g), 1)
+
+    def __enter__(self):
+        self.old = L.kvt_set_cand_group(self.g)
+        return self
+
+    def __exit__(self, *exc):
+        L.kvt_set_cand_group(self.old)
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -255,9 +272,11 @@ def token_scores(q: torch.Tensor, keys: torch.Tensor, n: int | None = None) -> t
 @_on_device
 def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
                 leaf_start: torch.Tensor | None = None, n_leaves: torch.Tensor | None = None,
-                want_cand_leaf: bool = False, A: torch.Tensor | None = None, d: int = 0):
+                want_cand_leaf: bool = False, A: torch.Tensor | None = None, d: int = 0, group: int = 1):
     """tau + candidate items -> dict(items, n_items, n_cand, cand_leaf, evals[, err]).
-    With A (from chunk_bounds(want_A=True)) and d, also the f32 scoring error bound err."""
+    With A (from chunk_bounds(want_A=True)) and d, also the f32 scoring error bound err.
+    group = g > 1 (GQA union, kvt_select_plan_group): items / n_items per KV lane (the union of
+    its g query lanes' candidates); n_cand, evals, err per query lane."""
     nl = U.shape[0]
     maxl = leaf_start.shape[1] if leaf_start is not None else n_grid_leaves(n, C)
     item_cap = (n + ITEM_TOKENS - 1) // ITEM_TOKENS + maxl
@@ -269,9 +288,10 @@ def select_plan(U: torch.Tensor, Lo: torch.Tensor, n: int, k: int, C: int = 0,
     cand_leaf = torch.zeros((nl, max(maxl, 1)), dtype=torch.int8, device=dev) if want_cand_leaf else None
     lstride = leaf_start.shape[1] if leaf_start is not None else maxl
     err = torch.empty((nl, 4), dtype=torch.float64, device=dev) if A is not None else None
-    L.check(L.kvt_select_plan2(nl, n, C, _p(leaf_start), _p(n_leaves), lstride, U.data_ptr(), Lo.data_ptr(),
-                               U.stride(0), k, items.data_ptr(), item_cap, n_items.data_ptr(), n_cand.data_ptr(),
-                               _p(cand_leaf), evals.data_ptr(), _p(A), _p(err), d, _stream()), "select_plan")
+    L.check(L.kvt_select_plan_group(nl, n, C, _p(leaf_start), _p(n_leaves), lstride, U.data_ptr(), Lo.data_ptr(),
+                                    U.stride(0), k, items.data_ptr(), item_cap, n_items.data_ptr(),
+                                    n_cand.data_ptr(), _p(cand_leaf), evals.data_ptr(), _p(A), _p(err), d,
+                                    max(int(group), 1), _stream()), "select_plan")
     return {"items": items, "n_items": n_items, "n_cand": n_cand, "cand_leaf": cand_leaf, "evals": evals,
             "item_cap": item_cap, "err": err}
 

@@ -192,7 +192,7 @@ def test_codec_reciprocal_exhaustive(ops):
 
 @pytest.mark.parametrize("dt", ["int4", "bf16"])
 @pytest.mark.parametrize("kind", ["random", "planted"])
-@pytest.mark.parametrize("Hkv", [2, 8])
+@pytest.mark.parametrize("Hkv", [1, 2, 8])
 def test_gqa_kv_sharing_matches_oracle(ops, dt, kind, Hkv):
     """Config 4 layout (GQA): query lanes b*H + h read KV lane b*Hkv + h // g.  Each query lane's
     selection is the oracle top-k of ITS query against the shared keys (the reference
@@ -241,6 +241,25 @@ def test_gqa_kv_sharing_matches_oracle(ops, dt, kind, Hkv):
             att = O.attention(Q[i], Kd[j], Vd[j], ref)
             err = np.linalg.norm(out[l, i].cpu().numpy() - att) / np.linalg.norm(att)
             assert err <= 1e-2, (dt, kind, l, i, err)
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_gqa_shared_bounds_equal_replicated(ops, g):
+    """Group-shared K3 (one abstract read per KV lane for its g query lanes) gives bit-identical
+    U, L, A to the same kernel over replicated abstracts (the reference's per-head replication,
+    adapters.py:121-136)."""
+    n_kv, d, n, C = 5, 128, 3000, 64
+    rng = np.random.default_rng(g)
+    K = torch.from_numpy(rng.normal(size=(n_kv, n, d)).astype(np.float32)).to(torch.bfloat16).cuda()
+    q = torch.from_numpy(rng.normal(size=(n_kv * g, d)).astype(np.float32)).cuda()
+    amax, amin = ops.abstract_build(K, n, C, abs_dtype=torch.bfloat16)
+    mag = ops.lane_abs_mag(amax, amin, ops.n_grid_leaves(n, C))
+    with ops.kv_group(g):
+        U1, L1, A1 = ops.chunk_bounds_fast(q, amax, amin, n, C, mag)
+    rep = lambda t: t.repeat_interleave(g, dim=0).contiguous()
+    U0, L0, A0 = ops.chunk_bounds_fast(q, rep(amax), rep(amin), n, C, rep(mag))
+    torch.cuda.synchronize()
+    assert torch.equal(U1, U0) and torch.equal(L1, L0) and torch.equal(A1, A0)
 
 
 @pytest.mark.parametrize("dt", ["int4", "bf16"])
