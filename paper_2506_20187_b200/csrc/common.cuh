@@ -441,6 +441,11 @@ inline int resident_per_sm(K kernel, int threads, size_t smem, int fallback) {
     return n;
 }
 
+// GQA union attention over INT4 values (attn_gqa.cu); KVT_ERR_ARG = shape not covered
+int kvt_attn_gqa_i4(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, int kvg, int64_t n_ctx,
+                    const int32_t* sel_tok, const double* sel_score, const int32_t* n_sel, int64_t sel_stride,
+                    double logit_scale, void* ws, float* out, double* out64, cudaStream_t st);
+
 // status plumbing (api.cu)
 int kvt_set_cuda_error(cudaError_t e);
 int kvt_check_launch();

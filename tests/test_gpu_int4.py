@@ -243,6 +243,47 @@ def test_gqa_kv_sharing_matches_oracle(ops, dt, kind, Hkv):
             assert err <= 1e-2, (dt, kind, l, i, err)
 
 
+@pytest.mark.parametrize("g", [2, 4])
+@pytest.mark.parametrize("overlap", ["same", "mixed", "disjoint"])
+@pytest.mark.parametrize("k", [700, 2200])
+def test_gqa_union_attention_matches_oracle(ops, g, overlap, k, monkeypatch):
+    """The GQA union kernel (attn_gqa.cu: one pass over the group's union, P.V on the tensor
+    cores with the heads as MMA rows) against the f64 oracle over the same selections, with
+    identical, partly shared and disjoint per-head selections across several token windows."""
+    monkeypatch.setenv("KVT_GQA_UNION", "1")
+    n_kv, d, n = 3, 128, 9000
+    rng = np.random.default_rng(7 + g)
+    V = torch.from_numpy(rng.normal(size=(n_kv, n, d)).astype(np.float32)).cuda()
+    vi = ops.I4KV.empty(n_kv, n, d, "cuda")
+    ops.kv_quant(V, vi)
+    Vd = np.stack([O.i4_dequant(vi.data[j].cpu().numpy(), d) for j in range(n_kv)]).astype(np.float64)
+    sel = np.zeros((n_kv * g, k), np.int32)
+    for j in range(n_kv):
+        base = np.sort(rng.choice(n, size=k, replace=False))
+        for h in range(g):
+            if overlap == "same":
+                s_ = base
+            elif overlap == "disjoint":
+                s_ = np.sort(rng.choice(np.arange(h, n, g), size=k, replace=False))
+            else:
+                s_ = np.sort(np.unique(np.concatenate([base[: k // 2], rng.choice(n, size=k, replace=False)]))[:k])
+                if len(s_) < k:
+                    s_ = base
+            sel[j * g + h] = s_
+    score = (rng.normal(size=(n_kv * g, k)) * 30.0).astype(np.float64)
+    st = torch.from_numpy(sel).cuda()
+    ss = torch.from_numpy(score).cuda()
+    ns = torch.full((n_kv * g,), k, dtype=torch.int32, device="cuda")
+    with ops.kv_group(g):
+        out = ops.sparse_decode_attn(vi, st, ss, ns).cpu().numpy()
+    scale = 1.0 / np.sqrt(d)
+    for i in range(n_kv * g):
+        w = np.exp((score[i] - score[i].max()) * scale)
+        ref = (w[:, None] * Vd[i // g][sel[i]]).sum(0) / w.sum()
+        err = np.linalg.norm(out[i] - ref) / np.linalg.norm(ref)
+        assert err <= 2e-5, (g, overlap, i, err)
+
+
 @pytest.mark.parametrize("g", [2, 4, 8])
 def test_gqa_shared_bounds_equal_replicated(ops, g):
     """Group-shared K3 (one abstract read per KV lane for its g query lanes) gives bit-identical
