@@ -12,6 +12,8 @@
 // (round-to-nearest fma/add are monotone, so the unwidened chains already enclose every
 // canonical dot; U == L pins them all to that value).  One warp per chunk, reads the
 // 2*d abstract floats once.  HBM-bound on abstract bytes (m*2*d*4 per lane).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace kvt {
@@ -40,32 +42,40 @@ __global__ void __launch_bounds__(256) abstract_grid_kernel(
     const int64_t nchunks = c_end - c_begin;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const T* base = keys + lane_i * lane_stride;
+    // extrema in the key's own precision (f32 holds f32/bf16/f16 keys exactly); rows in
+    // flight per lane shrink with G so the d = 512/1024 instantiations stay in registers
+    using W = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+    constexpr int GW = G * (int)sizeof(W) / 4;  // register words per element group
+    constexpr int UR = GW <= 2 ? 8 : (GW <= 4 ? 4 : (GW <= 8 ? 2 : 1));
     for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks; w += warps) {
         const int64_t c = c_begin + w;
         const int64_t s = c * C, e = min(n, s + C);
-        double mx[G][4], mn[G][4];
+        W mx[G][4], mn[G][4];
 #pragma unroll
         for (int r = 0; r < G; ++r)
 #pragma unroll
             for (int i = 0; i < 4; ++i) { mx[r][i] = -INFINITY; mn[r][i] = INFINITY; }
         int64_t t = s;
-        for (; t + 8 <= e; t += 8) {
-            double v[8][G][4];
+        for (; t + UR <= e; t += UR) {
+            W v[UR][G][4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < UR; ++u)
 #pragma unroll
                 for (int r = 0; r < G; ++r) {
                     const int g = lane + 32 * r;
-                    if (4 * g < d) load_group<T, VEC>(base + (t + u) * d, g, d, v[u][r]);
+                    double x[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (4 * g < d) load_group<T, VEC>(base + (t + u) * d, g, d, x);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[u][r][i] = (W)x[i];
                 }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < UR; ++u)
 #pragma unroll
                 for (int r = 0; r < G; ++r)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        mx[r][i] = fmax(mx[r][i], v[u][r][i]);
-                        mn[r][i] = fmin(mn[r][i], v[u][r][i]);
+                        mx[r][i] = max(mx[r][i], v[u][r][i]);
+                        mn[r][i] = min(mn[r][i], v[u][r][i]);
                     }
         }
         for (; t < e; ++t) {
@@ -76,7 +86,7 @@ __global__ void __launch_bounds__(256) abstract_grid_kernel(
                     double v[4];
                     load_group<T, VEC>(base + t * d, g, d, v);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) { mx[r][i] = fmax(mx[r][i], v[i]); mn[r][i] = fmin(mn[r][i], v[i]); }
+                    for (int i = 0; i < 4; ++i) { mx[r][i] = max(mx[r][i], (W)v[i]); mn[r][i] = min(mn[r][i], (W)v[i]); }
                 }
             }
         }

@@ -446,8 +446,8 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_i4_kernel(
                 const uint32_t lo4 = words[q] & 0x0f0f0f0fu, hi4 = (words[q] >> 4) & 0x0f0f0f0fu;
 #pragma unroll
                 for (int bb = 0; bb < 4; ++bb) {
-                    const float c0 = __uint_as_float(__byte_perm(lo4, 0x4B000000u, 0x7440 + bb)) - 8388608.0f;
-                    const float c1 = __uint_as_float(__byte_perm(hi4, 0x4B000000u, 0x7440 + bb)) - 8388608.0f;
+                    const float c0 = __uint_as_float(__byte_perm(0x4B000000u, lo4, 0x3004 + bb)) - 8388608.0f;
+                    const float c1 = __uint_as_float(__byte_perm(0x4B000000u, hi4, 0x3004 + bb)) - 8388608.0f;
                     o[8 * q + 2 * bb] = fmaf(ws, c0, o[8 * q + 2 * bb]);
                     o[8 * q + 2 * bb + 1] = fmaf(ws, c1, o[8 * q + 2 * bb + 1]);
                 }
@@ -551,13 +551,17 @@ struct FmtI4 {
         om = fmaf(w, __high2float(p), om);
         const uint64_t ws2 = f2_pack(ws, ws), neg = f2_pack(-8388608.0f, -8388608.0f);
         const uint32_t words[4] = {r.c.x, r.c.y, r.c.z, r.c.w};
+        // 2^23 + code as an f32 bit pattern: byte 3 = 0x4B from the magic word (first PRMT
+        // source, a register), byte 0 = the code (second source); the selector stays an
+        // immediate, so no per-use selector moves are issued
+        const uint32_t magic = 0x4B000000u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const uint32_t lo4 = words[q] & 0x0f0f0f0fu, hi4 = (words[q] >> 4) & 0x0f0f0f0fu;
 #pragma unroll
             for (int bb = 0; bb < 4; ++bb) {
-                const uint64_t c2 = f2_add(f2_pack(__uint_as_float(__byte_perm(lo4, 0x4B000000u, 0x7440 + bb)),
-                                                   __uint_as_float(__byte_perm(hi4, 0x4B000000u, 0x7440 + bb))),
+                const uint64_t c2 = f2_add(f2_pack(__uint_as_float(__byte_perm(magic, lo4, 0x3004 + bb)),
+                                                   __uint_as_float(__byte_perm(magic, hi4, 0x3004 + bb))),
                                            neg);
                 o2[4 * q + bb] = f2_fma(ws2, c2, o2[4 * q + bb]);
             }
@@ -1006,10 +1010,17 @@ static bool gqa_union_enabled() {
     return e && e[0] == '1';
 }
 
-static int ring_auto_splits(int64_t kmax, int v_dtype) {
+// Few lanes (small batch): the fewest-units rule would leave most of the 148 SMs idle, so
+// the split count is raised until the grid covers about two CTAs per SM, with units kept at
+// >= 256 rows.
+static int ring_auto_splits(int64_t kmax, int v_dtype, int64_t n_lanes) {
     const int64_t rmax = v_dtype == KVT_I4 ? 1664 : 3328;
     const int64_t cap = kvt::imax(1, kvt::imin(64, (kmax + 31) / 32));
-    return (int)kvt::imax(1, kvt::imin(cap, (kmax + rmax - 1) / rmax));
+    int64_t s = kvt::imax(1, kvt::imin(cap, (kmax + rmax - 1) / rmax));
+    const int64_t fill = (2 * (int64_t)kvt::sm_count() + n_lanes - 1) / kvt::imax(1, n_lanes);
+    const int64_t by_rows = kvt::imax(1, kmax / 256);
+    s = kvt::imax(s, kvt::imin(kvt::imin(fill, by_rows), cap));
+    return (int)s;
 }
 
 extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n_lanes, int64_t lane_stride, int d,
@@ -1032,7 +1043,7 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
                              n_sel, sel_stride, logit_scale, ws, out, out64, st);
         if (rc != KVT_ERR_ARG) return rc;
     }
-    if (splits <= 0) splits = ring_auto_splits(kmax, v_dtype);  // auto (the workspace must hold 64 splits)
+    if (splits <= 0) splits = ring_auto_splits(kmax, v_dtype, n_lanes);  // auto (the workspace must hold 64 splits)
     if (splits > 64) splits = 64;
     // rows per work unit: the whole selection in <= splits units
     const int R = (int)kvt::imax(32, ((kmax + splits - 1) / splits + 31) / 32 * 32);

@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             // code -> float without I2F: one byte permute builds 0x4B0000cc = 2^23 + c
-                            const float c0 = __uint_as_float(__byte_perm(lo4, 0x4B000000u, 0x7440 + b)) - 8388608.0f;
-                            const float c1 = __uint_as_float(__byte_perm(hi4, 0x4B000000u, 0x7440 + b)) - 8388608.0f;
+                            const float c0 = __uint_as_float(__byte_perm(0x4B000000u, lo4, 0x3004 + b)) - 8388608.0f;
+                            const float c1 = __uint_as_float(__byte_perm(0x4B000000u, hi4, 0x3004 + b)) - 8388608.0f;
                             const int e = 8 * wi + 2 * b;
                             acc[wi] = fmaf(qg[e], __fmaf_rn(c0, sc_, mn), acc[wi]);
                             acc[wi] = fmaf(qg[e + 1], __fmaf_rn(c1, sc_, mn), acc[wi]);
