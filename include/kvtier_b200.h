@@ -313,6 +313,10 @@ KVT_API int kvt_set_kv_group(int kv_group);
  * ids shared per group (row of the group's first query lane).  kvt_select_attend sets it
  * itself for INT4 keys.  Returns the previous value (1 = one candidate list per lane). */
 KVT_API int kvt_set_cand_group(int g);
+/* Development aid: when buf (device, >= 8 x n_lanes u64) is non-null, every later
+ * kvt_topk_select_band CTA b writes %globaltimer at its phase boundaries p = 0..7 to
+ * buf[b * 8 + p] (tools/select_phases.py).  nullptr turns it off (the default). */
+KVT_API int kvt_debug_select_phases(unsigned long long* buf);
 
 /* ---- synthetic workload (bench / test input generator; not on the decode path) ----------
  * The planted-desert model of trace.py:270-315 (generate_synthetic) as a counter hash, so

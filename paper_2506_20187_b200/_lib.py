@@ -97,6 +97,7 @@ kvt_sparse_decode_attn = _sig("kvt_sparse_decode_attn", ctypes.c_int, _vp, _i32,
                               _i64, ctypes.c_double, _i32, _vp, _vp, _vp, _vp)
 kvt_set_kv_group = _sig("kvt_set_kv_group", ctypes.c_int, _i32)
 kvt_set_cand_group = _sig("kvt_set_cand_group", ctypes.c_int, _i32)
+kvt_debug_select_phases = _sig("kvt_debug_select_phases", ctypes.c_int, _vp)
 kvt_attn_lse = _sig("kvt_attn_lse", ctypes.c_int, _vp, _i64, _vp, _vp)
 kvt_lse_merge = _sig("kvt_lse_merge", ctypes.c_int, _vp, _i32, _i64, _i32, ctypes.c_double, _vp, _vp, _vp)
 kvt_kv_quant = _sig("kvt_kv_quant", ctypes.c_int, _vp, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _vp)
@@ -116,7 +117,7 @@ EXPORTED = [
     "kvt_runs_scan", "kvt_attn_workspace_bytes", "kvt_sparse_decode_attn", "kvt_layer_workspace_bytes",
     "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_i4_recip_check", "kvt_select_plan2", "kvt_cand_score_f32",
     "kvt_topk_select_band", "kvt_kv_dequant", "kvt_chunk_bounds_fast", "kvt_attn_lse", "kvt_lse_merge", "kvt_set_kv_group", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
-    "kvt_synth_layer", "kvt_select_plan_group", "kvt_set_cand_group",
+    "kvt_synth_layer", "kvt_select_plan_group", "kvt_set_cand_group", "kvt_debug_select_phases",
 ]
 
 

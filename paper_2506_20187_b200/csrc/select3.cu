@@ -28,6 +28,18 @@ constexpr int S3_BAND_CAP = 1024;
 constexpr int S3_UB = 8;  // float4 loads in flight per thread (block-strided passes)
 constexpr int S3_UW = 4;  // 128-element windows in flight per warp (warp-range passes)
 
+// Phase timestamps (development aid, off unless kvt_debug_select_phases set a buffer):
+// thread 0 of CTA b writes %globaltimer at phase p to buf[b * 8 + p].
+__device__ unsigned long long* g_s3_phase = nullptr;
+__device__ __forceinline__ void s3_mark(int p) {
+    unsigned long long* P = g_s3_phase;
+    if (P && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P[blockIdx.x * 8 + p] = t;
+    }
+}
+
 struct S3Shared {
     unsigned int hist[S3_BINS];
     double band_c[S3_BAND_CAP];
@@ -216,6 +228,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const double inv = hi > lo ? (double)S3_BINS / (hi - lo) : 0.0;
     const float lo_f = (float)lo, inv_f = (float)inv;
     const int n32 = (int)n;
+    s3_mark(0);
 
     // ---- 1. bucket histogram of the estimates (4 per thread per iteration) ----
     for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
@@ -237,7 +250,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         }
     }
     __syncthreads();
+    s3_mark(1);
     s3_find_bin(S, S.hist, S3_BINS, kk);
+    s3_mark(2);
     const int bstar = S.bstar;
     const long long need_in_bucket = kk - S.above;
     bool fallback = bstar < 0;
@@ -299,6 +314,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) nsure += __shfl_xor_sync(KVT_FULL, nsure, off);
         __syncthreads();
+        s3_mark(3);
         const int ln = (int)S.list_n;
         if (ln > S3_LIST_CAP) {
             fallback = true;
@@ -407,6 +423,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         }
     }
     }
+    s3_mark(4);
     if (!fallback) {
         if (lane == 0) w_sel[warp] = nsure;
         __syncthreads();
@@ -436,6 +453,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         }
     }
     __syncthreads();
+    s3_mark(5);
     if (!fallback) {
         // ---- 4. stable compaction: per-warp offsets, lane-level scan inside each window ----
         long long extra = 0;  // selected band members inside this warp's range
@@ -626,6 +644,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             eq_seen += __popc(eqb);
         }
     }
+    s3_mark(6);
     if (tid == 0) n_sel[li] = (int32_t)kk;
     if (!run_start) return;
     if (!fallback && kk <= (int64_t)S3_LIST_CAP * 8) {
@@ -669,6 +688,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             nxt = st;
         }
         if (tid == 0) n_runs[li] = (int32_t)tot_h;
+        s3_mark(7);
         return;
     }
 
@@ -761,6 +781,11 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
     launch_pdl(topk_select3_kernel<QT, T>, dim3((unsigned)n_lanes), dim3(S3_THREADS), smem, st, cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
         sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current(), cand_group_current());
     return kvt_check_launch();
+}
+
+extern "C" int kvt_debug_select_phases(unsigned long long* buf) {
+    const cudaError_t e = cudaMemcpyToSymbol(g_s3_phase, &buf, sizeof(buf));
+    return e == cudaSuccess ? KVT_OK : kvt_set_cuda_error(e);
 }
 
 extern "C" int kvt_topk_select_band(const float* cs32, const int32_t* ctok, const int32_t* n_cand,
