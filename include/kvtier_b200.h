@@ -329,6 +329,61 @@ KVT_API int kvt_synth_layer(void* keys, void* values, int64_t n_lanes, int64_t l
                             float desert_base, float desert_span, float hot_base, float hot_span,
                             float noise_scale, int planted, void* stream);
 
+/* ---- tiered KV: HBM hot tier over a pinned-host warm tier ----------
+ * Replaces the byte movement behind TieredStore.touch / ensure_hot / promote_hot / _evict_hot
+ * (tiered_store.py:224-372, driven per lane from engine.py:342-343) for V records of C_rec
+ * tokens.  Device state (caller-owned, see paper_2506_20187_b200/host_tier.py):
+ *   table [L][kv_lanes][n_rec] i32  slot of each record, -1 = warm only (-2 transient)
+ *   owner [n_slots] i64  record id (lk * n_rec + rec, lk = layer * kv_lanes + lane), -1 free
+ *   stamp [n_slots] i32  step of the last touch;  free_stack [n_slots] + free_top
+ *   pool  [n_slots][C_rec][row] INT4 records;  ctl: kvt_tier_ctl_bytes() zeroed once
+ *   host_i4 (+ optional host_raw bf16) = the layer's pinned host rows [kv_lanes][N][row]
+ * One kvt_tier_layer call per (step, layer), after the layer's selection: touch the records
+ * its runs overlap, evict the least recently touched hot records -- order (stamp, start,
+ * layer, lane) = the reference's (last_touch, start, layer, head) -- for the misses, copy the
+ * misses host -> pool (a ceil(theta M) share as INT4 records, the rest as raw bf16 rows
+ * quantised on the way, when host_raw is given), and add the row's ledger counters
+ * (warm_to_hot / hot_to_warm bytes at ledger_rec_bytes per record, promotions) into
+ * ledger_row.  The working set of one step must fit (ledger_row[3] = -1 otherwise). */
+typedef struct {
+    int64_t n_lanes;      /* query lanes of the layer (runs are per query lane) */
+    int kv_group, d, crec;
+    const int32_t* step;  /* device: the decode step (stamps); read by the kernels, so a
+                             captured CUDA graph replays with the current value */
+    const int32_t *run_start, *run_len, *n_runs;
+    int64_t run_stride;
+    int32_t* table;       /* whole table; this layer's rows start at table_base */
+    int64_t table_base, table_stride, n_lk;  /* n_rec per lane; n_lk = L * kv_lanes */
+    int32_t* stamp;
+    int64_t* owner;
+    int64_t n_slots;
+    int32_t *free_stack, *free_top, *victims, *slot_of_miss;
+    int64_t* miss;
+    int64_t miss_cap;
+    void* ctl;
+    void* pool;
+    const void* host_i4;  /* this layer's pinned INT4 rows */
+    const void* host_raw; /* this layer's pinned bf16 rows, or NULL (all INT4) */
+    int64_t host_lane_tokens, n_tok;
+    const float* theta;   /* device: compressed share of the misses (pipeline.py solve_theta);
+                             NULL = 1 (all INT4) */
+    long long ledger_rec_bytes;
+    long long* ledger_row; /* device [4]: += warm_to_hot, hot_to_warm bytes, promotions; [3] = -1
+                              if the step's working set did not fit (CapacityError) */
+} kvt_tier_args;
+KVT_API size_t kvt_tier_ctl_bytes(void);
+KVT_API int kvt_tier_layer(const kvt_tier_args* a, void* stream);
+/* out4 = [misses, evictions, need (< 0: capacity error), victims] of the last call;
+ * synchronises the stream (diagnostics). */
+KVT_API int kvt_tier_read_ctl(const void* ctl, long long* out4, void* stream);
+/* K7 over the hot tier: like kvt_sparse_decode_attn with INT4 values, but query lane i's row
+ * t is read from pool + (table[(i / kv_group) * table_stride + t / crec] * crec + t % crec)
+ * rows (every selected record must be hot: call kvt_tier_layer first). */
+KVT_API int kvt_sparse_decode_attn_paged(const void* pool, const int32_t* table, int64_t table_stride, int crec,
+                                         int64_t n_lanes, int d, const int32_t* sel_tok, const double* sel_score,
+                                         const int32_t* n_sel, int64_t sel_stride, double logit_scale, int splits,
+                                         void* ws, float* out, double* out64, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,21 @@ class KvtLayerArgs(ctypes.Structure):
     ]
 
 
+class KvtTierArgs(ctypes.Structure):
+    """Mirror of kvt_tier_args (include/kvtier_b200.h)."""
+
+    _fields_ = [
+        ("n_lanes", _i64), ("kv_group", _i32), ("d", _i32), ("crec", _i32), ("step", _vp),
+        ("run_start", _vp), ("run_len", _vp), ("n_runs", _vp), ("run_stride", _i64),
+        ("table", _vp), ("table_base", _i64), ("table_stride", _i64), ("n_lk", _i64),
+        ("stamp", _vp), ("owner", _vp), ("n_slots", _i64),
+        ("free_stack", _vp), ("free_top", _vp), ("victims", _vp), ("slot_of_miss", _vp),
+        ("miss", _vp), ("miss_cap", _i64), ("ctl", _vp), ("pool", _vp),
+        ("host_i4", _vp), ("host_raw", _vp), ("host_lane_tokens", _i64), ("n_tok", _i64),
+        ("theta", _vp), ("ledger_rec_bytes", ctypes.c_longlong), ("ledger_row", _vp),
+    ]
+
+
 def _sig(name, restype, *argtypes):
     f = getattr(_L, name)
     f.restype = restype
@@ -97,6 +112,11 @@ kvt_sparse_decode_attn = _sig("kvt_sparse_decode_attn", ctypes.c_int, _vp, _i32,
                               _i64, ctypes.c_double, _i32, _vp, _vp, _vp, _vp)
 kvt_set_kv_group = _sig("kvt_set_kv_group", ctypes.c_int, _i32)
 kvt_set_cand_group = _sig("kvt_set_cand_group", ctypes.c_int, _i32)
+kvt_tier_ctl_bytes = _sig("kvt_tier_ctl_bytes", _sz)
+kvt_tier_layer = _sig("kvt_tier_layer", ctypes.c_int, ctypes.POINTER(KvtTierArgs), _vp)
+kvt_tier_read_ctl = _sig("kvt_tier_read_ctl", ctypes.c_int, _vp, _vp, _vp)
+kvt_sparse_decode_attn_paged = _sig("kvt_sparse_decode_attn_paged", ctypes.c_int, _vp, _vp, _i64, _i32, _i64, _i32,
+                                    _vp, _vp, _vp, _i64, ctypes.c_double, _i32, _vp, _vp, _vp, _vp)
 kvt_debug_select_phases = _sig("kvt_debug_select_phases", ctypes.c_int, _vp)
 kvt_attn_lse = _sig("kvt_attn_lse", ctypes.c_int, _vp, _i64, _vp, _vp)
 kvt_lse_merge = _sig("kvt_lse_merge", ctypes.c_int, _vp, _i32, _i64, _i32, ctypes.c_double, _vp, _vp, _vp)
@@ -118,6 +138,7 @@ EXPORTED = [
     "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_i4_recip_check", "kvt_select_plan2", "kvt_cand_score_f32",
     "kvt_topk_select_band", "kvt_kv_dequant", "kvt_chunk_bounds_fast", "kvt_attn_lse", "kvt_lse_merge", "kvt_set_kv_group", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
     "kvt_synth_layer", "kvt_select_plan_group", "kvt_set_cand_group", "kvt_debug_select_phases",
+    "kvt_tier_ctl_bytes", "kvt_tier_layer", "kvt_tier_read_ctl", "kvt_sparse_decode_attn_paged",
 ]
 
 

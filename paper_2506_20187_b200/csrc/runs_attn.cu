@@ -732,7 +732,8 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     const unsigned char* __restrict__ values, int64_t lane_stride_b, int d, const int32_t* __restrict__ sel_tok,
     const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int splits, int R,
     double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
-    double* __restrict__ out64, double scale, int kvg) {
+    double* __restrict__ out64, double scale, int kvg, const int32_t* __restrict__ ptable, int64_t ptable_stride,
+    int pcrec) {
     pdl_entry();
     constexpr int LPR = F::LPR, NE = F::NE, RPW = 32 / LPR, RB = F::row_bytes(), SLOT = RPW * RB;
     extern __shared__ __align__(16) unsigned char ring_smem[];
@@ -753,8 +754,15 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     const int32_t* tok = sel_tok + li * sel_stride + a;
     const double* sc = sel_score + li * sel_stride + a;
     double m = -INFINITY;
+    // paged (hot tier): token -> pool row through the record table, resolved once here
+    const int32_t* ptab = ptable ? ptable + (li / kvg) * ptable_stride : nullptr;
     for (int i = wa + lane; i < wb; i += 32) {
-        tok_s[i] = tok[i];
+        int t = tok[i];
+        if (ptab) {
+            const int sl = ptab[t / pcrec];
+            t = sl >= 0 ? sl * pcrec + t % pcrec : 0;
+        }
+        tok_s[i] = t;
         m = fmax(m, sc[i]);
     }
 #pragma unroll
@@ -764,7 +772,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     for (int i = wa + lane; i < wb; i += 32) w_s[i] = exp2f((float)((sc[i] - m) * sl2));  // once per row (L2 hit)
     __syncwarp();
     const int sub = lane / LPR, grp = lane % LPR;
-    const unsigned char* base = values + (li / kvg) * lane_stride_b;
+    const unsigned char* base = ptable ? values : values + (li / kvg) * lane_stride_b;
     const uint32_t ring_a = (uint32_t)__cvta_generic_to_shared(ring);
     const int nslots = (wb - wa + RPW - 1) / RPW;
     uint64_t o2[NE / 2];
@@ -833,6 +841,17 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_ring_kernel(
     attn_finish(part, splits, d, li, tickets, out, out64, scale);
 }
 
+// Hot-tier paging context of kvt_sparse_decode_attn_paged (this host thread, one call).
+struct PagedV {
+    const int32_t* table = nullptr;
+    int64_t stride = 0;
+    int crec = 1;
+};
+static PagedV& paged_current() {
+    static thread_local PagedV p;
+    return p;
+}
+
 template <class F, int S>
 static int launch_ring(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, const int32_t* sel_tok,
                        const double* sel_score, const int32_t* n_sel, int64_t sel_stride, int splits, int R,
@@ -848,9 +867,11 @@ static int launch_ring(const void* values, int64_t n_lanes, int64_t lane_stride_
         configured = smem;
     }
     dim3 grid(splits, (unsigned)n_lanes);
+    const PagedV& pg = paged_current();
     launch_pdl(attn_ring_kernel<F, S>, grid, dim3(ATTN_THREADS), smem, st, (const unsigned char*)values, lane_stride_b, d, sel_tok,
                                                             sel_score, n_sel, sel_stride, splits, R, part, tickets,
-                                                            out, out64, scale, kv_group_current());
+                                                            out, out64, scale, kv_group_current(), pg.table, pg.stride,
+                                                            pg.crec);
     return kvt_check_launch();
 }
 
@@ -1088,5 +1109,25 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
         case KVT_F64: rc = dispatch_attn<double>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel, sel_stride, splits, part, tickets, out, out64, logit_scale, st); break;
         default: return KVT_ERR_DTYPE;
     }
+    return rc;
+}
+
+extern "C" int kvt_sparse_decode_attn_paged(const void* pool, const int32_t* table, int64_t table_stride, int crec,
+                                            int64_t n_lanes, int d, const int32_t* sel_tok, const double* sel_score,
+                                            const int32_t* n_sel, int64_t sel_stride, double logit_scale, int splits,
+                                            void* ws, float* out, double* out64, void* stream) {
+    if (!pool || !table || table_stride < 1 || crec < 1) return KVT_ERR_ARG;
+    if ((d != 128 && d != 256) || ((uintptr_t)pool % 16)) return KVT_ERR_SHAPE;
+    if (splits <= 0) splits = ring_auto_splits(sel_stride, KVT_I4, n_lanes);
+    if (splits > 64) splits = 64;
+    const int64_t R = kvt::imax(32, ((sel_stride + splits - 1) / splits + 31) / 32 * 32);
+    if (R > 8192) return KVT_ERR_SHAPE;  // the ring path stages each unit's rows
+    PagedV& pg = paged_current();
+    pg.table = table;
+    pg.stride = table_stride;
+    pg.crec = crec;
+    const int rc = kvt_sparse_decode_attn(pool, KVT_I4, n_lanes, 0, d, sel_tok, sel_score, n_sel, sel_stride,
+                                          logit_scale, splits, ws, out, out64, stream);
+    pg = PagedV();
     return rc;
 }

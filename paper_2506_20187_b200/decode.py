@@ -31,7 +31,8 @@ class SparseDecoder:
     def __init__(self, n_layers: int, batch: int, n_heads: int, head_dim: int, n_cap: int,
                  dtype: torch.dtype = torch.bfloat16, plan: ChunkPlanConfig | None = None,
                  importance_rate: float = 0.10, early_layer_rate: float = 0.50, device=None,
-                 abstract_dtype: torch.dtype = torch.bfloat16, n_kv_heads: int | None = None):
+                 abstract_dtype: torch.dtype = torch.bfloat16, n_kv_heads: int | None = None,
+                 values: str = "resident"):
         if not torch.cuda.is_available():
             raise RuntimeError("SparseDecoder needs a CUDA device (B200, sm_100a)")
         self.L, self.B, self.H, self.d = n_layers, batch, n_heads, head_dim
@@ -48,13 +49,17 @@ class SparseDecoder:
         self.C = [self.plan.early_chunk_size if l < self.plan.early_layers else self.plan.default_chunk_size
                   for l in range(n_layers)]
         self.device = torch.device(device or "cuda")
+        if values not in ("resident", "tiered"):
+            raise ValueError("values must be 'resident' or 'tiered'")
+        # values="tiered": V lives in a host_tier.HotTier (HBM hot records over pinned host
+        # memory); the decoder keeps K and the abstracts and runs the selection only
         if dtype == ops.I4:  # INT4 records (K8), 0.3125x of bf16 at d = 128
             self.K = ops.I4KV(torch.empty((n_layers, self.kv_lanes, n_cap, ops.row_bytes_i4(head_dim)),
                                           dtype=torch.uint8, device=self.device), head_dim)
-            self.V = ops.I4KV(torch.empty_like(self.K.data), head_dim)
+            self.V = ops.I4KV(torch.empty_like(self.K.data), head_dim) if values == "resident" else None
         else:
             self.K = torch.empty((n_layers, self.kv_lanes, n_cap, head_dim), dtype=dtype, device=self.device)
-            self.V = torch.empty_like(self.K)
+            self.V = torch.empty_like(self.K) if values == "resident" else None
         # bf16 abstracts rounded outward (max up, min down): half the bound-pass bytes, still sound
         adt = abstract_dtype if abstract_dtype is not None else ops.abs_dtype_for(dtype)
         self.amax = [torch.empty((self.kv_lanes, ops.n_grid_leaves(n_cap, C), head_dim), dtype=adt,
@@ -94,10 +99,12 @@ class SparseDecoder:
         T = k.shape[1]
         if self.dtype == ops.I4:
             ops.kv_quant(k, ops.I4KV(self.K.data[layer, :, t0:t0 + T], self.d))
-            ops.kv_quant(v, ops.I4KV(self.V.data[layer, :, t0:t0 + T], self.d))
+            if self.V is not None:
+                ops.kv_quant(v, ops.I4KV(self.V.data[layer, :, t0:t0 + T], self.d))
         else:
             self.K[layer, :, t0:t0 + T] = k.to(self.dtype)
-            self.V[layer, :, t0:t0 + T] = v.to(self.dtype)
+            if self.V is not None:
+                self.V[layer, :, t0:t0 + T] = v.to(self.dtype)
 
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
         """Append one token per KV lane ([L, kv_lanes, d]) and refresh the tail chunk abstracts."""
@@ -170,17 +177,24 @@ class SparseDecoder:
         self._bufs = bufs
         return bufs
 
-    def layer(self, l: int, q: torch.Tensor) -> dict:
-        """Select + attend for layer l; q: [lanes, d] (f32 or f64).  Returns the layer buffers."""
+    def layer(self, l: int, q: torch.Tensor, attend: bool = True) -> dict:
+        """Select + attend for layer l; q: [lanes, d] (f32 or f64).  Returns the layer buffers.
+        attend=False (or tiered values): the selection only (sel_tok, runs, ...)."""
         bufs = self._buffers()
         C, amax, amin = self.grid(l)
-        ops.select_attend(q, self.K[l], self.V[l], amax, amin, self.n, self.k_for(l), C,
-                          self._ws, bufs[l], abs_mag=None if self.absmag is None else self.absmag[l],
+        if attend and self.V is not None:
+            o, v = bufs[l], self.V[l]
+        else:  # no attention: values alias the keys (same lane stride), no output buffer
+            o, v = {kk: vv for kk, vv in bufs[l].items() if kk != "out"}, self.K[l]
+        ops.select_attend(q, self.K[l], v, amax, amin, self.n, self.k_for(l), C,
+                          self._ws, o, abs_mag=None if self.absmag is None else self.absmag[l],
                           kv_group=self.kv_group)
         return bufs[l]
 
     def step(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """All layers for one decode step; q: [L, lanes, d] -> attention outputs [L, lanes, d] f32."""
+        if self.V is None:
+            raise RuntimeError("tiered values: use host_tier.TieredDecoder.step")
         if out is None:
             out = torch.empty((self.L, self.lanes, self.d), dtype=torch.float32, device=self.device)
         bufs = self._buffers()
