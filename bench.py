@@ -89,9 +89,13 @@ def parse(argv=None):
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true")
-    p.add_argument("--sub", type=str, default="random,config2",
+    p.add_argument("--sub", type=str, default="random,config2,hosttier",
                    help="extra sub-records in the same run: 'random' (config 3 with N(0,1) KV), "
-                        "'config2' (32K, B=1, bf16); '' for none")
+                        "'config2' (32K, B=1, bf16), 'hosttier' (V in pinned host memory behind an HBM "
+                        "hot tier, config-5 shard shape); '' for none")
+    p.add_argument("--ht-ctx", type=int, default=262144, help="hosttier sub-record: context")
+    p.add_argument("--ht-batch", type=int, default=4, help="hosttier sub-record: batch (x 32 heads)")
+    p.add_argument("--ht-hot-frac", type=float, default=0.4, help="hosttier: HBM hot slots / V records")
     p.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no kernels")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--json-out", type=str, default="")
@@ -677,6 +681,110 @@ def sub_args(args, which: str):
     return a
 
 
+def measure_hosttier(args, torch, dev) -> dict:
+    """Sub-record 'hosttier' (north-star item 5, config 5's per-GPU shard shape: 256K x B = 4,
+    INT4): K and the abstracts in HBM, every V record in pinned host memory, an HBM hot tier
+    of ht_hot_frac of the V records (host_tier.TieredDecoder).  Reports the steady decode step
+    (CUDA graph, tier work of layer l overlapping layer l + 1's selection), the cold fill of
+    the first step and a forced full refill (pool emptied before each step) with the bytes
+    that crossed the host link; the host link's own copy rate is measured beside it."""
+    from paper_2506_20187_b200 import ops
+    from paper_2506_20187_b200.host_tier import TieredDecoder
+    a = argparse.Namespace(**vars(args))
+    a.ctx, a.batch, a.dtype, a.data = args.ht_ctx, args.ht_batch, "int4", "planted"
+    sp = shard_plan(a.batch, N_HEADS, N_HEADS, 1, 0, "strong")
+    L, n, d = a.layers, a.ctx, HEAD_DIM
+    n_rec_total = L * sp["kv_lanes"] * (-(-n // 64))
+    hot = int(args.ht_hot_frac * n_rec_total)
+    dec = TieredDecoder(L, 1, sp["q_lanes"], d, n, hot, device=dev, n_kv_heads=sp["kv_lanes"])
+    kv_ids = np.arange(sp["kv0"], sp["kv0"] + sp["kv_lanes"])
+    gen = W.gen_args(None, d, a.data)
+    kb = torch.empty((sp["kv_lanes"], n, d), dtype=torch.bfloat16, device=dev)
+    vb = torch.empty_like(kb)
+    params = []
+    for l in range(L):
+        p = W.lane_params(a.seed, l, kv_ids, n, d, a.data)
+        params.append(p)
+        ops.synth_layer(kb, vb, p, n, gen)
+        dec.load_layer(l, kb, vb)
+    del kb, vb
+    torch.cuda.empty_cache()
+    dec.set_length(n)
+    steps = min(args.steps, 10)
+    Qh = make_queries(a, sp, params, steps + 4)
+    Q = torch.from_numpy(Qh).to(dev)
+    q_static = torch.empty((L, dec.lanes, d), device=dev, dtype=torch.float32)
+    out_static = torch.empty((L, dec.lanes, d), device=dev, dtype=torch.float32)
+    stream = torch.cuda.Stream(device=dev)
+    link_rec = dec.tier.phys_rec_bytes
+
+    def timed(fn, reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    with torch.cuda.stream(stream):
+        q_static.copy_(Q[0])
+    cold_ms = timed(lambda: dec.step(q_static, out_static), 1)
+    cold_rows = dec.ledger_rows()
+    cold_link = sum(r["link_bytes"] for r in cold_rows)
+    with torch.cuda.stream(stream):
+        for s in range(1, 3):
+            q_static.copy_(Q[s])
+            dec.step(q_static, out_static)
+        stream.synchronize()
+        dec.adapt_bound_granularity()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            dec.step(q_static, out_static)
+        graph.replay()
+    stream.synchronize()
+    with ClockSampler(dev.index or 0) as clk:
+        clk.mark("t0")
+        steady_ms = timed(graph.replay, steps)
+        clk.mark("t1")
+    steady_link = sum(r["link_bytes"] for r in dec.ledger_rows())
+
+    def refill():
+        dec.tier.reset()
+        graph.replay()
+    refill_ms = timed(refill, 3)
+    refill_rows = dec.ledger_rows()
+    refill_link = sum(r["link_bytes"] for r in refill_rows)
+    # the host link's own rate: one pinned -> HBM copy of the same volume
+    nb = max(refill_link, 1 << 26)
+    hsrc = dec.tier.host_i4.view(-1)[:nb]
+    hdst = torch.empty(nb, dtype=torch.uint8, device=dev)
+    copy_ms = timed(lambda: hdst.copy_(hsrc, non_blocking=True), 2)
+    del hdst, graph
+    full_v = L * sp["kv_lanes"] * n * ops.row_bytes_i4(d)
+    rec = {"sub": "hosttier", "workload": f"llama7b-attn-{n // 1024}k-b{a.batch}-int4-planted-hosttier",
+           "value": sp["global_batch"] / (steady_ms / 1e3), "unit": "tokens/s", "ms_per_step": steady_ms,
+           "steps": steps, "hot_tier": {
+               "hot_records": hot, "v_records": n_rec_total, "hot_gb": dec.tier.pool.numel() / 1e9,
+               "v_host_gb": full_v / 1e9, "record_tokens": 64, "link_bytes_per_record": link_rec,
+               "cold_first_step_ms": cold_ms, "cold_link_bytes": cold_link,
+               "steady_link_bytes_per_step": steady_link,
+               "refill_ms_per_step": refill_ms, "refill_link_bytes_per_step": refill_link,
+               "refill_link_gbs": refill_link / (refill_ms / 1e3) / 1e9,
+               "host_copy_gbs": nb / (copy_ms / 1e3) / 1e9,
+               "ledger_warm_to_hot_per_refill": sum(r["warm_to_hot"] for r in refill_rows),
+               "theta": 1.0,
+               "note": "V served through the HBM hot tier (paged K7); tier work of layer l on a side stream "
+                       "overlapping layer l+1's selection; refill = pool emptied before each step (every "
+                       "selected record crosses the host link); steady = planted queries, selections stable "
+                       "after the first step"},
+           "clocks": clk.summary()}
+    del dec
+    torch.cuda.empty_cache()
+    return rec
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -744,6 +852,15 @@ def run_ours(args):
     torch.cuda.empty_cache()
     subs = []
     for which in [s for s in args.sub.split(",") if s.strip() and s.strip() != "none"]:
+        if which.strip() == "hosttier":
+            if world > 1:
+                continue
+            try:
+                subs.append(measure_hosttier(args, torch, dev))
+            except Exception as exc:  # a sub-record must not sink the headline line
+                subs.append({"sub": which, "error": f"{type(exc).__name__}: {exc}"})
+            torch.cuda.empty_cache()
+            continue
         a = sub_args(args, which.strip())
         try:
             r = measure(a, torch, dist, world, rank, local, dev, tag=which)

@@ -71,8 +71,8 @@ class HotTier:
         self.theta = torch.ones(n_layers, dtype=torch.float32, device=dev)
         self.ledger = torch.zeros((n_layers, 4), dtype=i64, device=dev)
         # warm tier: pinned host rows, [L][kv_lanes][N][row]
-        self.host_i4 = torch.empty((n_layers, kv_lanes, n_cap, self.rb), dtype=torch.uint8).pin_memory()
-        self.host_raw = (torch.empty((n_layers, kv_lanes, n_cap, d), dtype=torch.bfloat16).pin_memory()
+        self.host_i4 = torch.empty((n_layers, kv_lanes, n_cap, self.rb), dtype=torch.uint8, pin_memory=True)
+        self.host_raw = (torch.empty((n_layers, kv_lanes, n_cap, d), dtype=torch.bfloat16, pin_memory=True)
                          if keep_raw else None)
         self.ledger_rec_bytes = kv_nbytes(crec, d)  # the reference's byte model (K + V fp16)
         self.phys_rec_bytes = crec * self.rb        # what actually crosses the link (INT4)
@@ -127,6 +127,14 @@ class HotTier:
                 ops._stream()), "sparse_decode_attn_paged")
         finally:
             L.kvt_set_kv_group(old)
+
+    def reset(self) -> None:
+        """Every record back to warm only (empty pool); the step counter is kept."""
+        self.table.fill_(-1)
+        self.owner.fill_(-1)
+        self.stamp.fill_(-1)
+        torch.arange(self.n_slots, dtype=torch.int32, device=self.device, out=self.free_stack)
+        self.free_top.fill_(self.n_slots)
 
     def last_call(self) -> dict:
         """State of the last kvt_tier_layer call (synchronises; diagnostics)."""
