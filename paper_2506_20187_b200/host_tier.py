@@ -35,7 +35,16 @@ import torch
 from . import _lib as L
 from . import ops
 from .decode import SparseDecoder
+from .tier import PipelineParams, solve_theta
 from .tiered_store import CapacityError, kv_nbytes
+
+
+def theta_for_rows(rows: list[dict], params: PipelineParams, crec: int, d: int) -> list[float]:
+    """DTP controller (pipeline.py:79-103): per layer, the smallest compressed share theta that
+    hides the layer's warm -> hot transfer behind its compute, with the raw volume taken from
+    the previous step's ledger row (promotions x raw bf16 record bytes)."""
+    raw_rec = crec * d * 2
+    return [solve_theta(r["promotions"] * raw_rec, params).theta for r in rows]
 
 
 class HotTier:
@@ -179,6 +188,16 @@ class TieredDecoder(SparseDecoder):
         if (th < 1).any() and self.tier.host_raw is None:
             raise ValueError("theta < 1 needs the raw host copy (keep_raw=True)")
         self.tier.theta.copy_(th)
+
+    def plan_theta(self, params: PipelineParams, rows: list[dict] | None = None) -> list[float]:
+        """Set every layer's theta from the last step's ledger rows (theta_for_rows) and return it.
+        Without the raw host copy every transfer is INT4 already (theta = 1)."""
+        if self.tier.host_raw is None:
+            th = [1.0] * self.L
+        else:
+            th = theta_for_rows(rows if rows is not None else self.ledger_rows(), params, self.tier.crec, self.d)
+        self.set_theta(th)
+        return th
 
     def step(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """All layers of one decode step; q: [L, lanes, d] -> [L, lanes, d] f32.  Layer l's

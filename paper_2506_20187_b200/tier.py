@@ -243,6 +243,9 @@ class HostTier:
         INT4 records (+ on-device dequant), the rest as bf16.  Returns the completion event."""
         n_comp = int(math.ceil(theta * len(ranges) - 1e-12))
         ev = torch.cuda.Event()
+        # the side stream must not overwrite dst (or the stage) while the consumer stream still
+        # reads them: it starts after the consumer's queued work
+        self.stream_.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream_):
             comp = ranges[:n_comp]
             if comp:
@@ -250,15 +253,21 @@ class HostTier:
                 st = self._stage(rows)
                 pos = 0
                 for s, e in comp:
-                    st.data[:, pos:pos + e - s].copy_(self.host_i4[:, s:e], non_blocking=True)
+                    # per lane: [s, e) of one lane is contiguous in the pinned [lanes, N, row]
+                    # buffer, so every copy is a true async DMA (a [:, s:e] slice is strided and
+                    # would be staged through pageable memory)
+                    for ln in range(self.lanes):
+                        st.data[ln, pos:pos + e - s].copy_(self.host_i4[ln, s:e], non_blocking=True)
                     pos += e - s
                 pos = 0
                 for s, e in comp:
                     kv_dequant(ops.I4KV(st.data[:, pos:pos + e - s], self.d), dst[:, s:e])
                     pos += e - s
             for s, e in ranges[n_comp:]:
-                dst[:, s:e].copy_(self.host_raw[:, s:e], non_blocking=True)
+                for ln in range(self.lanes):
+                    dst[ln, s:e].copy_(self.host_raw[ln, s:e], non_blocking=True)
             ev.record(self.stream_)
+        dst.record_stream(self.stream_)
         return ev
 
     def calibrate(self, dst: torch.Tensor, chunk: int = 64, n_chunks: int = 256) -> dict:

@@ -82,3 +82,15 @@ def test_host_tier_stream_and_split():
     assert np.all(got[:, untouched] == 0)
     cal = tier.calibrate(dst)
     assert cal["bw_hot_warm"] > 0 and 0.3 < cal["compress_ratio"] < 0.32
+
+
+def test_theta_for_rows_follows_solve_theta():
+    """The DTP controller of host_tier (theta per layer from last step's promotions) is
+    pipeline.py's solve_theta on the raw bf16 volume of those records."""
+    from paper_2506_20187_b200.host_tier import theta_for_rows
+    from paper_2506_20187_b200.tier import PipelineParams, solve_theta
+    p = PipelineParams(compute_ms=0.5, bw_hot_warm=50e6, compress_ratio=80 / 256, decompress_rate=3e9)
+    rows = [{"promotions": n} for n in (0, 100, 5000, 10 ** 6)]
+    th = theta_for_rows(rows, p, 64, 128)
+    assert th == [solve_theta(n * 64 * 128 * 2, p).theta for n in (0, 100, 5000, 10 ** 6)]
+    assert th[0] == 0.0 and th[-1] == 1.0 and 0.0 <= th[2] <= 1.0
