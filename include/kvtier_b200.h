@@ -73,6 +73,16 @@ KVT_API int kvt_abstract_build(const void* keys, int key_dtype, int64_t n_lanes,
 KVT_API int kvt_abstract_spans(const void* keys, int key_dtype, int64_t lane_stride, int d,
                        int64_t n_spans, const int32_t* lane_of, const int32_t* starts,
                        const int32_t* ends, void* amax, void* amin, void* stream);
+/* K2, merge_abstracts (importance.py:90-100) over segments of consecutive chunk abstracts
+ * ([lanes][m][d] rows, lane stride in elements): explicit segments (seg_lane/begin/end,
+ * output row s of amax_out/amin_out [n_seg][d]: a merged desert run, chunk_tree.py:344-379)
+ * or, with seg_lane == NULL, uniform coarsening by `factor` (segment s = lane s / m_out, chunk
+ * j = s % m_out over fine chunks [j factor, (j + 1) factor) < m_in, written at
+ * out + lane * out_lane_stride + j * d).  Element-wise max / min: exact in every dtype. */
+KVT_API int kvt_abstract_merge(const void* amax, const void* amin, int dtype, int64_t in_lane_stride, int d,
+                               int64_t n_seg, const int32_t* seg_lane, const int32_t* seg_begin,
+                               const int32_t* seg_end, int factor, int64_t m_in, int64_t m_out, void* amax_out,
+                               void* amin_out, int64_t out_lane_stride, void* stream);
 
 /* ---- K8: INT4 KV compression ------------------------------------------------------------
  * North-star item 4 (the reference only models compression, pipeline.py:35-57 delta = 0.25,

@@ -27,7 +27,6 @@ can differ inside such a chunk (its tests compare sets).  eval_count = bounds ev
 from __future__ import annotations
 
 import math
-import warnings
 from dataclasses import dataclass, field
 from typing import Protocol
 
@@ -400,35 +399,36 @@ def _rebuild(partition: Partition, sel_tok, sel_score, n_sel, k: int) -> None:
         run_hi.append(float(seg.max()))
         run_lo.append(float(seg.min()))
         pos += ln
-    # exact abstracts: resident pieces from keys (K1 spans), cold spans from stored abstracts
+    # exact abstracts: resident pieces from keys (K1 spans), cold spans from stored abstracts,
+    # then one K2 segment per leaf over its pieces (in leaf order)
     cold = dev.get("cold", [])
-    pieces_s, pieces_e, piece_leaf, cold_pieces = [], [], [], []
+    pieces_s, pieces_e, rows, seg_b, seg_e = [], [], [], [], []
+    bs = dev["base_size"]
     for li, (s, e) in enumerate(zip(pstart, pend)):
         pos = int(s)
+        seg_b.append(len(rows))
         for cs_, ce_ in sorted(_overlaps(cold, int(s), int(e))):
             if cs_ > pos:
-                pieces_s.append(pos); pieces_e.append(cs_); piece_leaf.append(li)
-            cold_pieces.append((li, cs_, ce_))
+                rows.append(("span", len(pieces_s)))
+                pieces_s.append(pos); pieces_e.append(cs_)
+            rows.append(("base", cs_ // bs))  # whole cold record: its stored (base) abstract
             pos = ce_
         if pos < e:
-            pieces_s.append(pos); pieces_e.append(int(e)); piece_leaf.append(li)
-    d = dev["base_max"].shape[1]
+            rows.append(("span", len(pieces_s)))
+            pieces_s.append(pos); pieces_e.append(int(e))
+        seg_e.append(len(rows))
     gdev = dev["base_max"].device
-    amax = torch.full((npart, d), -math.inf, dtype=torch.float64, device=gdev)
-    amin = torch.full((npart, d), math.inf, dtype=torch.float64, device=gdev)
     if pieces_s:
         pmx, pmn = ops.abstract_spans(dev["keys"], torch.zeros(len(pieces_s), dtype=torch.int32),
                                       torch.tensor(pieces_s, dtype=torch.int32), torch.tensor(pieces_e, dtype=torch.int32))
-        idx = torch.tensor(piece_leaf, dtype=torch.int64, device=gdev)
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)  # index_reduce_ is "beta"
-            amax.index_reduce_(0, idx, pmx.double(), "amax")
-            amin.index_reduce_(0, idx, pmn.double(), "amin")
-    bs = dev["base_size"]
-    for li, cs_, ce_ in cold_pieces:  # whole cold records: their stored (base) abstracts
-        b = cs_ // bs
-        amax[li] = torch.maximum(amax[li], dev["base_max"][b])
-        amin[li] = torch.minimum(amin[li], dev["base_min"][b])
+        pmx, pmn = pmx.double(), pmn.double()
+    else:
+        pmx = pmn = torch.empty((0, dev["base_max"].shape[1]), dtype=torch.float64, device=gdev)
+    ns = pmx.shape[0]
+    idx = torch.tensor([i if kind == "span" else ns + i for kind, i in rows], dtype=torch.int64, device=gdev)
+    src_mx = torch.cat([pmx, dev["base_max"].double()]).index_select(0, idx)
+    src_mn = torch.cat([pmn, dev["base_min"].double()]).index_select(0, idx)
+    amax, amin = ops.abstract_merge(src_mx, src_mn, seg_begin=seg_b, seg_end=seg_e)
     hmx, hmn = amax.cpu().numpy(), amin.cpu().numpy()
     leaves: list[ChunkNode] = []
     r = 0

@@ -526,3 +526,88 @@ extern "C" int kvt_chunk_bounds(const void* q, int q_dtype, int64_t n_lanes, int
         return dispatch_bounds<double, double>(q, n_lanes, d, n, C, leaf_start, n_leaves, leaf_stride, amax, amin, abs_lane_stride, U, L, A, bnd_stride, max_leaves, scaled, st);
     return KVT_ERR_DTYPE;
 }
+
+// ------------------------------------------------------------------------------------------
+// K2: merge_abstracts (importance.py:90-100) over segments of consecutive chunk abstracts --
+// the union abstract of a desert run (merge_desert, chunk_tree.py:344-379), of the pieces of
+// a rebuilt leaf, or of f fine chunks (a coarser grid built from a finer one without
+// re-reading the keys).  Element-wise max / min are exact in every dtype, so the result is
+// bit-identical to folding merge_abstracts pairwise (and, for outward-rounded bf16
+// abstracts, to building the coarse grid from the keys: rounding up is monotone).  One warp
+// per segment; lane l owns dims 4l..4l+3 (+128r).
+// ------------------------------------------------------------------------------------------
+namespace kvt {
+
+template <typename T>
+__global__ void __launch_bounds__(256) abstract_merge_kernel(
+    const T* __restrict__ amax, const T* __restrict__ amin, int64_t in_lane_stride, int d, int64_t n_seg,
+    const int32_t* __restrict__ seg_lane, const int32_t* __restrict__ seg_begin, const int32_t* __restrict__ seg_end,
+    int factor, int64_t m_in, int64_t m_out, T* __restrict__ omax, T* __restrict__ omin, int64_t out_lane_stride) {
+    using W = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < n_seg; s += warps) {
+        int64_t ln, b, e, orow;
+        if (seg_lane) {  // explicit segments: output row s
+            ln = seg_lane[s];
+            b = seg_begin[s];
+            e = seg_end[s];
+            orow = s * d;
+        } else {  // uniform coarsening: segment (lane, j) = fine chunks [j f, (j + 1) f)
+            ln = s / m_out;
+            const int64_t j = s % m_out;
+            b = j * factor;
+            e = kvt::imin(m_in, b + factor);
+            orow = ln * out_lane_stride + j * d;
+        }
+        const T* pmx = amax + ln * in_lane_stride;
+        const T* pmn = amin + ln * in_lane_stride;
+        for (int g = lane; 4 * g < d; g += 32) {
+            W mx[4], mn[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { mx[i] = -INFINITY; mn[i] = INFINITY; }
+            for (int64_t c = b; c < e; ++c) {
+                double x[4], y[4];
+                load_group<T, false>(pmx + c * d, g, d, x);
+                load_group<T, false>(pmn + c * d, g, d, y);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) { mx[i] = max(mx[i], (W)x[i]); mn[i] = min(mn[i], (W)y[i]); }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (4 * g + i < d && e > b) { omax[orow + 4 * g + i] = (T)mx[i]; omin[orow + 4 * g + i] = (T)mn[i]; }
+        }
+    }
+}
+
+template <typename T>
+static int launch_abs_merge(const void* amax, const void* amin, int64_t in_ls, int d, int64_t n_seg,
+                            const int32_t* sl, const int32_t* sb, const int32_t* se, int factor, int64_t m_in,
+                            int64_t m_out, void* omax, void* omin, int64_t out_ls, cudaStream_t st) {
+    const int64_t blocks = kvt::imax(1, kvt::imin((n_seg + 7) / 8, (int64_t)kvt::sm_count() * 16));
+    abstract_merge_kernel<T><<<(unsigned)blocks, 256, 0, st>>>((const T*)amax, (const T*)amin, in_ls, d, n_seg, sl, sb,
+                                                              se, factor, m_in, m_out, (T*)omax, (T*)omin, out_ls);
+    return kvt_check_launch();
+}
+
+}  // namespace kvt
+
+extern "C" int kvt_abstract_merge(const void* amax, const void* amin, int dtype, int64_t in_lane_stride, int d,
+                                  int64_t n_seg, const int32_t* seg_lane, const int32_t* seg_begin,
+                                  const int32_t* seg_end, int factor, int64_t m_in, int64_t m_out, void* amax_out,
+                                  void* amin_out, int64_t out_lane_stride, void* stream) {
+    if (!amax || !amin || !amax_out || !amin_out || d < 1 || n_seg < 0) return KVT_ERR_ARG;
+    if (seg_lane ? (!seg_begin || !seg_end) : (factor < 1 || m_in < 0 || m_out < 1)) return KVT_ERR_ARG;
+    if (n_seg == 0) return KVT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+#define KVT_M(T) return launch_abs_merge<T>(amax, amin, in_lane_stride, d, n_seg, seg_lane, seg_begin, seg_end, factor, \
+                                             m_in, m_out, amax_out, amin_out, out_lane_stride, st)
+    switch (dtype) {
+        case KVT_F32: KVT_M(float);
+        case KVT_F64: KVT_M(double);
+        case KVT_BF16: KVT_M(__nv_bfloat16);
+        case KVT_F16: KVT_M(__half);
+        default: return KVT_ERR_DTYPE;
+    }
+#undef KVT_M
+}

@@ -90,8 +90,9 @@ class SparseDecoder:
             ops.abstract_build(self.K[l], n, self.C[l], self.amax[l], self.amin[l])
             if self.absmag is not None:
                 ops.lane_abs_mag(self.amax[l], self.amin[l], ops.n_grid_leaves(n, self.C[l]), out=self.absmag[l])
-            if self.amax_c[l] is not None:
-                ops.abstract_build(self.K[l], n, self.coarse_C, self.amax_c[l], self.amin_c[l])
+            if self.amax_c[l] is not None:  # K2: the coarse grid from the fine one, keys not re-read
+                ops.abstract_merge(self.amax[l], self.amin[l], factor=self.coarse_C // self.C[l],
+                                   m_in=ops.n_grid_leaves(n, self.C[l]), out=(self.amax_c[l], self.amin_c[l]))
         self._bufs = None
 
     def load_layer(self, layer: int, k: torch.Tensor, v: torch.Tensor, t0: int = 0) -> None:

@@ -225,6 +225,48 @@ def abstract_spans(keys: torch.Tensor, lane_of: torch.Tensor, starts: torch.Tens
     return amax, amin
 
 
+@_on_device
+def abstract_merge(amax: torch.Tensor, amin: torch.Tensor, seg_lane=None, seg_begin=None, seg_end=None,
+                   factor: int = 0, m_in: int = 0, out: tuple | None = None):
+    """K2 (kvt_abstract_merge): element-wise max / min over segments of consecutive chunk
+    abstracts.  amax/amin: [lanes, m, d] (or [m, d] = one lane).  Explicit segments
+    (seg_lane, seg_begin, seg_end int sequences) -> [S, d]; or uniform coarsening by `factor`
+    over the first m_in chunks -> [lanes, ceil(m_in / factor), d] (or into `out`)."""
+    require_cuda(amax, amin)
+    a3 = amax if amax.dim() == 3 else amax[None]
+    b3 = amin if amin.dim() == 3 else amin[None]
+    if a3.shape != b3.shape or a3.dtype != b3.dtype or a3.stride(2) != 1 or a3.stride(1) != a3.shape[2] \
+            or b3.stride() != a3.stride():
+        raise ValueError("abstract_merge: amax / amin must be matching [lanes, m, d] row-major tensors")
+    nl, _, d = a3.shape
+    dev = a3.device
+    if seg_begin is not None:
+        sb = torch.as_tensor(seg_begin, dtype=torch.int32).to(dev).contiguous()
+        se = torch.as_tensor(seg_end, dtype=torch.int32).to(dev).contiguous()
+        sl = (torch.zeros_like(sb) if seg_lane is None else
+              torch.as_tensor(seg_lane, dtype=torch.int32).to(dev).contiguous())
+        S = sb.numel()
+        omx = torch.empty((S, d), dtype=a3.dtype, device=dev) if out is None else out[0]
+        omn = torch.empty_like(omx) if out is None else out[1]
+        if S:
+            L.check(L.kvt_abstract_merge(a3.data_ptr(), b3.data_ptr(), dtype_code(a3), a3.stride(0), d, S,
+                                         sl.data_ptr(), sb.data_ptr(), se.data_ptr(), 0, 0, 0, omx.data_ptr(),
+                                         omn.data_ptr(), 0, _stream()), "abstract_merge")
+        return omx, omn
+    if factor < 1 or m_in < 1:
+        raise ValueError("abstract_merge: give segments or factor >= 1 and m_in >= 1")
+    m_out = -(-m_in // factor)
+    if out is None:
+        omx = torch.empty((nl, m_out, d), dtype=a3.dtype, device=dev)
+        omn = torch.empty_like(omx)
+    else:
+        omx, omn = out
+    L.check(L.kvt_abstract_merge(a3.data_ptr(), b3.data_ptr(), dtype_code(a3), a3.stride(0), d, nl * m_out, None,
+                                 None, None, factor, m_in, m_out, omx.data_ptr(), omn.data_ptr(), omx.stride(0),
+                                 _stream()), "abstract_merge")
+    return omx, omn
+
+
 # -- K3 ----------------------------------------------------------------------------------------
 
 

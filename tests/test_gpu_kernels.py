@@ -339,3 +339,25 @@ def test_select3_many_lanes_matches_oracle(ops, kind):
     Kh = kt.double().cpu().numpy()
     for i in (0, lanes // 2, lanes - 1):
         assert np.array_equal(got[i].cpu().numpy(), O.topk(O.dots(Q[i], Kh[i]), k)), i
+
+
+def test_k2_abstract_merge_segments_and_coarsening():
+    """K2 (kvt_abstract_merge): explicit segments equal numpy's max / min of the rows (f64,
+    bit-exact); uniform coarsening of bf16 outward-rounded C = 8 abstracts equals building the
+    C = 64 grid from the keys directly (rounding up commutes with max), tail chunk included."""
+    import torch
+    from paper_2506_20187_b200 import ops
+    g = torch.Generator().manual_seed(5)
+    rows = torch.randn((37, 128), generator=g, dtype=torch.float64)
+    rows2 = rows - torch.rand((37, 128), generator=g, dtype=torch.float64)
+    segs = [(0, 1), (1, 9), (9, 10), (10, 37)]
+    mx, mn = ops.abstract_merge(rows.cuda(), rows2.cuda(), seg_begin=[a for a, _ in segs], seg_end=[b for _, b in segs])
+    for i, (a, b) in enumerate(segs):
+        assert torch.equal(mx[i].cpu(), rows[a:b].max(0).values)
+        assert torch.equal(mn[i].cpu(), rows2[a:b].min(0).values)
+    lanes, n, d = 3, 64 * 20 + 24, 128
+    K = torch.randn((lanes, n, d), generator=g).to(torch.bfloat16).cuda()
+    f8 = ops.abstract_build(K, n, 8, abs_dtype=torch.bfloat16)
+    f64 = ops.abstract_build(K, n, 64, abs_dtype=torch.bfloat16)
+    c = ops.abstract_merge(f8[0], f8[1], factor=8, m_in=ops.n_grid_leaves(n, 8))
+    assert torch.equal(c[0], f64[0]) and torch.equal(c[1], f64[1])
