@@ -386,6 +386,17 @@ KVT_API int kvt_tier_layer(const kvt_tier_args* a, void* stream);
 /* out4 = [misses, evictions, need (< 0: capacity error), victims] of the last call;
  * synchronises the stream (diagnostics). */
 KVT_API int kvt_tier_read_ctl(const void* ctl, long long* out4, void* stream);
+/* GQA K7 over INT4 values (kv_group g in {2, 4}, d = 128): one pass over the union of each
+ * group's selections (query lanes i / g share KV lane i / g), P.V on the tensor cores with the
+ * group's heads as MMA rows; tokens < n_ctx.  ws as kvt_sparse_decode_attn (64 splits);
+ * scratch >= kvt_attn_gqa_scratch_bytes (the union plan).  KVT_ERR_ARG for shapes it does not
+ * cover.  kvt_select_attend runs it for GQA INT4 layers (KVT_GQA_UNION=0 disables). */
+KVT_API size_t kvt_attn_gqa_scratch_bytes(int64_t n_lanes, int kvg, int64_t n_ctx);
+KVT_API int kvt_sparse_decode_attn_gqa(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, int kvg,
+                                       int64_t n_ctx, const int32_t* sel_tok, const double* sel_score,
+                                       const int32_t* n_sel, int64_t sel_stride, double logit_scale, void* ws,
+                                       void* scratch, size_t scratch_bytes, float* out, double* out64,
+                                       void* stream);
 /* K7 over the hot tier: like kvt_sparse_decode_attn with INT4 values, but query lane i's row
  * t is read from pool + (table[(i / kv_group) * table_stride + t / crec] * crec + t % crec)
  * rows (every selected record must be hot: call kvt_tier_layer first). */

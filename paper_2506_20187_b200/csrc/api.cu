@@ -2,6 +2,7 @@
 // per-layer pipeline kvt_select_attend (K3 -> plan -> K4 -> K5 -> K6 -> K7), i.e. the body
 // of the reference's per-lane loop (engine.py:316-357) for every lane of a layer at once.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 
@@ -111,6 +112,12 @@ SideStream& side_stream() {  // one per thread and device (streams belong to a d
 
 int num_sms() { return kvt::sm_count(); }
 
+// GQA union attention in kvt_select_attend: on unless KVT_GQA_UNION=0 (A/B switch)
+bool gqa_union_on() {
+    const char* e = getenv("KVT_GQA_UNION");
+    return !(e && e[0] == '0');
+}
+
 }  // namespace
 
 extern "C" size_t kvt_layer_workspace_bytes(int64_t n_lanes, int64_t n, int64_t max_leaves, int d) {
@@ -216,6 +223,15 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
                                   a->k, a->n_sel, a->run_start, a->run_len, a->k, a->n_runs, stream);  // K5 + fused K6
         if (rc) return rc;
 
+    }
+    if (a->out && a->values && kvg > 1 && a->v_dtype == KVT_I4 && a->attn_splits <= 0 && gqa_union_on()) {
+        // GQA: one pass over the group's union, P.V on the tensor cores (attn_gqa.cu); the
+        // candidate-score region (only used by the exact fallback, done by now) is its scratch
+        const size_t sb = (size_t)a->n_lanes * (size_t)a->n * sizeof(double);
+        rc = kvt_sparse_decode_attn_gqa(a->values, a->n_lanes, a->lane_stride, a->d, kvg, a->n, a->sel_tok,
+                                        a->sel_score, a->n_sel, a->k, 1.0 / sqrt((double)a->d), w.attn_part,
+                                        w.cand_score, sb, a->out, nullptr, stream);
+        if (rc != KVT_ERR_ARG) return rc;  // else: a shape the union kernel does not cover
     }
     if (a->out && a->values) {
         int splits = a->attn_splits;  // 0 = auto: wave-aware choice in kvt_sparse_decode_attn

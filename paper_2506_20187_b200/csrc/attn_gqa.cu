@@ -3,25 +3,25 @@
 //
 // engine.py:145-154 attention_output = softmax(q.K_sel^T / sqrt d) . V_sel, per query head.
 // The reference replicates each KV head per query head (adapters.py:121-136), so g query
-// heads sharing a KV head read (and here would dequantise) the same value rows g times.
-// This kernel walks the KV lane's tokens in ranges of R and, per range:
-//   1. stages every head's selected tokens in the range (a warp-wide 32-ary lower_bound in
-//      each head's ascending selection) as per-head bitmaps, with the head's max score;
-//   2. ORs them into the union, assigns union slots (popcount prefix) and scatters each
-//      head's softmax weight w_h(t) = exp((s_h(t) - m_h) / sqrt d) into a [slot][head]
-//      table (0 where the head did not select t);
-//   3. streams the union's value records (80 B INT4 rows: 64 B of codes, four fp16 (scale,
-//      min) pairs) through a per-warp cp.async ring, 16 rows per step, and accumulates
-//          o_h[j] = sum_t w_h(t) (s_t,G(j) c_t,j + m_t,G(j))
-//      with mma.sync m16n8k16 (f16 in, f32 accumulate): A = the weights times the group's
-//      scale (x 2^12), rows 2h / 2h + 1 = their f16 high / low parts, so the product keeps
-//      ~22 bits (g <= 4 heads fill rows 0..7); B = the codes as exact f16 integers (nibbles -> 1024 + c by
-//      one LOP3, minus 1024 by one HSUB2), the MMA's K = 16 union rows, N = 8 dims of one
-//      quantisation group, 16 MMAs per 16 rows cover d = 128 for every head at once.  The
-//      min term sum_t w_h(t) m_t,G is a per-(head, group) scalar on the CUDA cores.
-//   4. writes one flash-decoding partial (m_h, l_h, o_h) per (query lane, range); the last
-//      range CTA of each query lane merges them (ticket), as the per-lane kernel does.
-// Values are read once per KV lane instead of once per query head, and dequantised once.
+// heads sharing a KV head read, dequantise and multiply the same value rows g times.  Here a
+// KV lane's value rows are streamed once for its g heads, in two launches:
+//   plan  (one CTA per KV lane x 2048-token window): every head's selected tokens in the
+//         window (a warp-wide 32-ary lower_bound in its ascending selection) as bitmaps, their
+//         OR = the union rows (ascending token offsets, popcount prefix), and per union row the
+//         g softmax weights w_h = exp((s_h - m_wh) / sqrt d) relative to the window max m_wh (0
+//         where head h did not select the row), written to scratch with the window's count;
+//   pv    (one CTA per KV lane x range of windows, 4 warps): the union rows' 80 B INT4 value
+//         records stream through a per-warp cp.async ring, 16 rows per tile, and
+//             o_h[j] = sum_t w_h(t) (s_t,G(j) c_t,j + m_t,G(j))
+//         runs on mma.sync m16n8k16 (f16 in, f32 accumulate): A = the weights times the group's
+//         scale (x 2^12), rows 2h / 2h + 1 = their f16 high / low parts, so the product keeps
+//         ~22 bits; B = the codes as exact f16 integers (nibbles -> 1024 + c by one LOP3, minus
+//         1024 by one HSUB2); 16 MMAs per 16 rows cover d = 128 for every head at once.  The
+//         min term sum_t w_h(t) m_t,G is a per-(head, group) scalar on the CUDA cores.  Each
+//         warp keeps flash-decoding state per head (running max over its tiles' windows); the
+//         warps and then the ranges (ticket: the last range CTA of the KV lane) are merged.
+// Values are read once per KV lane instead of once per query head, and dequantised once; the
+// staging no longer sits between the loads and the MMAs (the pv loop is one continuous ring).
 #include "common.cuh"
 
 namespace kvt {
@@ -31,6 +31,7 @@ constexpr int GQ_THREADS = GQ_WARPS * 32;
 constexpr int GQ_S = 6;              // ring slots per warp (16 rows x 80 B each)
 constexpr int GQ_ROWB = 80;          // INT4 record bytes at d = 128
 constexpr int GQ_SLOT = 16 * GQ_ROWB;
+constexpr int GQ_SSLOT = GQ_SLOT + 16 * 4 * 4 + 4 * 8 + 16;  // + weights [16][4] f32, head maxima, header
 constexpr float GQ_ASCALE = 4096.f;  // A pre-scale: keeps the f16 low parts normal
 constexpr int GQ_WIN = 2048;         // tokens staged per window (bitmaps, slots, weights)
 
@@ -113,95 +114,89 @@ __device__ void gq_merge(double* __restrict__ part, int splits, int d, int64_t l
     __syncthreads();
 }
 
-template <int GQ>  // heads per KV lane (2 or 4)
-__global__ void __launch_bounds__(GQ_THREADS, 3) attn_gqa_i4_kernel(
-    const unsigned char* __restrict__ values, int64_t lane_stride_b, int64_t n_q, const int32_t* __restrict__ sel_tok,
-    const double* __restrict__ sel_score, const int32_t* __restrict__ n_sel, int64_t sel_stride, int R, int splits,
-    double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out, double* __restrict__ out64,
-    double scale) {
-    pdl_entry();
-    constexpr int d = 128;
-    constexpr int W = GQ_WIN;
-    constexpr int NW = W / 32;
-    constexpr int SCAN = 4;  // 32-entry batches loaded per scan step (memory-level parallelism)
-    extern __shared__ __align__(16) unsigned char smem[];
-    unsigned char* ring = smem;                                                   // [warps][S][16 x 80 B]
-    float* wtab = reinterpret_cast<float*>(smem + GQ_WARPS * GQ_S * GQ_SLOT);     // [W][GQ] weights
-    uint32_t* bm = reinterpret_cast<uint32_t*>(wtab + (size_t)W * GQ);            // [GQ][NW] head bitmaps
-    uint32_t* ubm = bm + GQ * NW;                                                 // [NW] union bitmap
-    int* upre = reinterpret_cast<int*>(ubm + NW);                                 // [NW] slot prefix
-    uint16_t* utok = reinterpret_cast<uint16_t*>(upre + NW);                      // [W] union token offsets
-    __shared__ double s_m[GQ];      // running max score per head
-    __shared__ float s_rs[GQ];      // this window's rescale of the running sums
-    __shared__ float s_l[GQ];       // running softmax denominators
-    __shared__ int s_cur[GQ], s_end[GQ], s_wend[GQ];
-    __shared__ double s_wm[GQ];
-    __shared__ int s_ucnt;
-    __shared__ int scan_sh[33];
-    __shared__ float s_o[GQ_WARPS][GQ][d];
-    __shared__ float s_om[GQ_WARPS][GQ][4];
-    __shared__ int s_last;
 
+// ---- scratch layout of the plan (kvt_attn_gqa_scratch_bytes) ---------------------------------
+struct GqPlan {
+    int32_t* cnt;    // [n_kv][n_win] union rows of the window
+    double* mx;      // [n_kv][n_win][G] window max score per head (-inf: none)
+    uint16_t* off;   // [n_kv][n_win][W] union rows' token offsets in the window, ascending
+    float* wt;       // [n_kv][n_win][W][G] weights relative to the window max (0: not selected)
+};
+__host__ __device__ inline size_t gq_al(size_t x) { return (x + 255) & ~(size_t)255; }
+__host__ __device__ inline GqPlan gq_carve(void* base, int64_t n_kv, int64_t n_win, int G) {
+    char* p = (char*)base;
+    GqPlan P;
+    const size_t nw = (size_t)n_kv * n_win;
+    P.cnt = (int32_t*)p;
+    p += gq_al(nw * 4);
+    P.mx = (double*)p;
+    p += gq_al(nw * G * 8);
+    P.off = (uint16_t*)p;
+    p += gq_al(nw * GQ_WIN * 2);
+    P.wt = (float*)p;
+    return P;
+}
+inline size_t gq_scratch_bytes(int64_t n_kv, int64_t n_win, int G) {
+    const size_t nw = (size_t)n_kv * n_win;
+    return gq_al(nw * 4) + gq_al(nw * G * 8) + gq_al(nw * GQ_WIN * 2) + gq_al(nw * GQ_WIN * G * 4);
+}
+
+constexpr int GQ_WPC = 4;  // windows per plan CTA (one lower_bound, then a forward scan)
+
+template <int G>
+__global__ void __launch_bounds__(GQ_THREADS) gqa_plan_kernel(const int32_t* __restrict__ sel_tok,
+                                                              const double* __restrict__ sel_score,
+                                                              const int32_t* __restrict__ n_sel, int64_t sel_stride,
+                                                              int64_t n_win, double scale, GqPlan P) {
+    pdl_entry();
+    constexpr int W = GQ_WIN, NW = W / 32;
+    constexpr int SCAN = 4;
+    __shared__ uint32_t bm[G * NW];  // per-head bitmaps of the window
+    __shared__ uint32_t ubm[NW];
+    __shared__ int upre[NW];
+    __shared__ int s_a[G], s_b[G];
+    __shared__ double s_m[G];
+    __shared__ int scan_sh[33];
+    __shared__ int s_ucnt;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t kv = blockIdx.y;
-    const int rg = blockIdx.x;
-    const int T0 = rg * R, T1 = T0 + R;
+    const int64_t win0 = (int64_t)blockIdx.x * GQ_WPC, win1 = kvt::imin(n_win, win0 + GQ_WPC);
     const double sl2 = scale * 1.4426950408889634;
-    const int gid = lane >> 2, tig = lane & 3;
-    const int hA = gid >> 1;             // head of A row gid (rows 8..15 stay zero)
-    const bool lo_part = gid & 1;
-    const unsigned char* vbase = values + kv * lane_stride_b;
-    unsigned char* wring = ring + (size_t)warp * GQ_S * GQ_SLOT;
-    const uint32_t wring_a = (uint32_t)__cvta_generic_to_shared(wring);
-
-    // ---- the range's entries of every head: [lower_bound(T0), lower_bound(T1)) ----
-    for (int h = warp; h < GQ; h += GQ_WARPS) {
-        const int64_t li = kv * GQ + h;
-        const int n = n_sel[li];
-        const int32_t* tk = sel_tok + li * sel_stride;
-        const int a = warp_lower_bound(tk, n, T0, lane);
-        const int b = warp_lower_bound(tk, n, T1, lane);
-        if (lane == 0) { s_cur[h] = a; s_end[h] = b; s_m[h] = -INFINITY; s_l[h] = 0.f; }
+    // each head's first entry at or after the CTA's first window (one search per CTA)
+    for (int h = warp; h < G; h += GQ_WARPS) {
+        const int64_t li = kv * G + h;
+        const int a = warp_lower_bound(sel_tok + li * sel_stride, n_sel[li], (int)(win0 * W), lane);
+        if (lane == 0) s_b[h] = a;
     }
-    __syncthreads();
-
-    float D[16][4];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) D[j][0] = D[j][1] = D[j][2] = D[j][3] = 0.f;
-    float om[4] = {0.f, 0.f, 0.f, 0.f};  // sum_t w_h(t) m_t,G for head gid/2 (hi-part rows)
-
-    for (int Tw = T0; Tw < T1; Tw += W) {
-        bool any = false;
-#pragma unroll
-        for (int h = 0; h < GQ; ++h) any |= s_cur[h] < s_end[h];
-        if (!any) break;  // block-uniform: the range's remaining windows are empty
-        // ---- 1. per-head bitmaps of the window's entries + the window max ----
-        for (int i = tid; i < GQ * NW; i += GQ_THREADS) bm[i] = 0u;
+    for (int64_t win = win0; win < win1; ++win) {
+        const int T0 = (int)(win * W);
+        for (int i = tid; i < G * NW; i += GQ_THREADS) bm[i] = 0u;
         __syncthreads();
-        for (int h = warp; h < GQ; h += GQ_WARPS) {
-            const int64_t li = kv * GQ + h;
+        // 1. each head's window entries (a prefix of its remaining ones) -> bitmap and max
+        for (int h = warp; h < G; h += GQ_WARPS) {
+            const int64_t li = kv * G + h;
+            const int n = n_sel[li];
             const int32_t* tk = sel_tok + li * sel_stride;
             const double* sc = sel_score + li * sel_stride;
-            const int end = s_end[h], lim = Tw + W;
-            int j = s_cur[h];
+            const int a = s_b[h];
+            int j = a;
             double mx = -INFINITY;
-            for (;;) {  // entries are ascending: the window's are a prefix of [j, end)
+            for (;;) {
                 int t[SCAN];
                 double v[SCAN];
 #pragma unroll
                 for (int u = 0; u < SCAN; ++u) {  // ids and scores issued together: one latency
                     const int pos = j + 32 * u + lane;
-                    t[u] = pos < end ? tk[pos] : INT_MAX;
-                    v[u] = pos < end ? sc[pos] : -INFINITY;
+                    t[u] = pos < n ? tk[pos] - T0 : INT_MAX;
+                    v[u] = pos < n ? sc[pos] : -INFINITY;
                 }
                 int taken = 0;
 #pragma unroll
                 for (int u = 0; u < SCAN; ++u) {
-                    const bool in = t[u] < lim;
+                    const bool in = t[u] < W;
                     taken += __popc(__ballot_sync(KVT_FULL, in));
                     if (in) {
-                        const int o = t[u] - Tw;
-                        atomicOr(&bm[h * NW + (o >> 5)], 1u << (o & 31));
+                        atomicOr(&bm[h * NW + (t[u] >> 5)], 1u << (t[u] & 31));
                         mx = fmax(mx, v[u]);
                     }
                 }
@@ -209,170 +204,266 @@ __global__ void __launch_bounds__(GQ_THREADS, 3) attn_gqa_i4_kernel(
                 if (taken < 32 * SCAN) break;
             }
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(KVT_FULL, mx, off));
-            if (lane == 0) {
-                s_wend[h] = j;
-                const double mo = s_m[h], mn = fmax(mo, mx);
-                s_rs[h] = (mo == -INFINITY || mn == -INFINITY) ? 0.f : exp2f((float)((mo - mn) * sl2));
-                s_wm[h] = mn;
-            }
+            for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(KVT_FULL, mx, o));
+            if (lane == 0) { s_a[h] = a; s_b[h] = j; s_m[h] = mx; }
         }
         __syncthreads();
-        // ---- 2. union slots (popcount prefix), token offsets, weight table ----
+        // 2. union rows: OR of the bitmaps, popcount prefix
         for (int w = tid; w < NW; w += GQ_THREADS) {
             uint32_t u = 0;
 #pragma unroll
-            for (int h = 0; h < GQ; ++h) u |= bm[h * NW + w];
+            for (int h = 0; h < G; ++h) u |= bm[h * NW + w];
             ubm[w] = u;
         }
         __syncthreads();
         {
             int tot;
-            const int v = tid < NW ? __popc(ubm[tid]) : 0;
-            const int ex = block_excl_scan<int>(v, scan_sh, tot);
-            if (tid < NW) upre[tid] = ex;
+            // prefix over the NW = 64 words: thread tid owns words 2 tid, 2 tid + 1
+            const int w0 = 2 * tid, w1 = 2 * tid + 1;
+            const int c0 = w0 < NW ? __popc(ubm[w0]) : 0, c1 = w1 < NW ? __popc(ubm[w1]) : 0;
+            const int ex = block_excl_scan<int>(c0 + c1, scan_sh, tot);
+            if (w0 < NW) upre[w0] = ex;
+            if (w1 < NW) upre[w1] = ex + c0;
             if (tid == 0) s_ucnt = tot;
         }
         __syncthreads();
         const int ucnt = s_ucnt;
+        const size_t wb = (size_t)(kv * n_win + win);
+        uint16_t* off = P.off + wb * W;
         for (int w = tid; w < NW; w += GQ_THREADS) {
             uint32_t x = ubm[w];
             int sl = upre[w];
             while (x) {
                 const int bit = __ffs(x) - 1;
                 x &= x - 1;
-                utok[sl++] = (uint16_t)(w * 32 + bit);
+                off[sl++] = (uint16_t)(w * 32 + bit);
             }
         }
-        for (int i = tid; i < ucnt * GQ; i += GQ_THREADS) wtab[i] = 0.f;
-        __syncthreads();
-        for (int h = warp; h < GQ; h += GQ_WARPS) {
-            const int64_t li = kv * GQ + h;
+        float* dstw = P.wt + wb * W * G;
+        if constexpr (G % 4 == 0) {
+            float4* dz = reinterpret_cast<float4*>(dstw);
+            for (int i = tid; i < ucnt * G / 4; i += GQ_THREADS) dz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (int i = tid; i < ucnt * G; i += GQ_THREADS) dstw[i] = 0.f;
+        }
+        __syncthreads();  // zeros before the scatter (global writes of the block are ordered by it)
+        // 3. weights of each head's entries at their union rows (entries just read: L1 hits)
+        for (int h = warp; h < G; h += GQ_WARPS) {
+            const int64_t li = kv * G + h;
             const int32_t* tk = sel_tok + li * sel_stride;
             const double* sc = sel_score + li * sel_stride;
-            const double mh = s_wm[h];
-            float lsum = 0.f;
-            for (int j = s_cur[h] + lane; j < s_wend[h]; j += 32) {
-                const int t = tk[j] - Tw;
+            const double mh = s_m[h];
+            for (int j = s_a[h] + lane; j < s_b[h]; j += 32) {
+                const int t = tk[j] - T0;
                 const int w = t >> 5;
                 const int slot = upre[w] + __popc(ubm[w] & ((1u << (t & 31)) - 1u));
-                const float wt = exp2f((float)((sc[j] - mh) * sl2));
-                wtab[slot * GQ + h] = wt;
-                lsum += wt;
-            }
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) lsum += __shfl_xor_sync(KVT_FULL, lsum, off);
-            if (lane == 0) {
-                s_l[h] = s_l[h] * s_rs[h] + lsum;
-                s_m[h] = mh;
-                s_cur[h] = s_wend[h];
+                dstw[slot * G + h] = exp2f((float)((sc[j] - mh) * sl2));
             }
         }
-        // running sums of this thread's head rescaled to the new max (flash decoding)
-        {
-            const float rs = hA < GQ ? s_rs[hA] : 0.f;
+        if (tid < G) P.mx[wb * G + tid] = s_m[tid];
+        if (tid == 0) P.cnt[wb] = ucnt;
+        __syncthreads();  // wtab / bitmaps / s_* reused by the next window
+    }
+}
+
+template <int G>  // heads per KV lane (2 or 4): rows 2h, 2h + 1 of A
+__global__ void __launch_bounds__(GQ_THREADS, 4) gqa_pv_kernel(
+    const unsigned char* __restrict__ values, int64_t lane_stride_b, int64_t n_q, int64_t n_win, int wins_per,
+    int splits, int64_t n_tok_ctx, GqPlan P, double* __restrict__ part, unsigned int* __restrict__ tickets, float* __restrict__ out,
+    double* __restrict__ out64, double scale) {
+    pdl_entry();
+    constexpr int d = 128;
+    constexpr int MAXW = 256;  // windows per range (host guarantees)
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* ring = smem;  // [warps][S][16 x 80 B]
+    __shared__ int s_tpre[MAXW + 1];
+    __shared__ float s_o[GQ_WARPS][G][d];
+    __shared__ float s_om[GQ_WARPS][G][4];
+    __shared__ double s_wm[GQ_WARPS][G];
+    __shared__ float s_wl[GQ_WARPS][G];
+    __shared__ int scan_sh[33];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t kv = blockIdx.y;
+    const int rg = blockIdx.x;
+    const int64_t w0 = (int64_t)rg * wins_per, w1 = kvt::imin(n_win, w0 + wins_per);
+    const int nwin = (int)kvt::imax(0, w1 - w0);
+    const double sl2 = scale * 1.4426950408889634;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int hA = gid >> 1;             // head of A row gid (rows 2G.. stay zero)
+    const bool lo_part = gid & 1;
+    const unsigned char* vbase = values + kv * lane_stride_b;
+    unsigned char* wring = ring + (size_t)warp * GQ_S * GQ_SSLOT;
+    const uint32_t wring_a = (uint32_t)__cvta_generic_to_shared(wring);
+    const size_t wbase = (size_t)(kv * n_win + w0);
+
+    // tiles of the range's windows: exclusive prefix of ceil(cnt / 16)
+    {
+        const int c0 = tid < nwin ? (P.cnt[wbase + tid] + 15) / 16 : 0;
+        const int c1 = tid + GQ_THREADS < nwin ? (P.cnt[wbase + tid + GQ_THREADS] + 15) / 16 : 0;
+        int tot;
+        const int e0 = block_excl_scan<int>(c0, scan_sh, tot);
+        if (tid < nwin) s_tpre[tid] = e0;
+        const int t0 = tot;
+        const int e1 = block_excl_scan<int>(c1, scan_sh, tot);
+        if (tid + GQ_THREADS < nwin) s_tpre[tid + GQ_THREADS] = t0 + e1;
+        if (tid == 0) s_tpre[nwin] = t0 + tot;
+    }
+    __syncthreads();
+    const int ntile = s_tpre[nwin];
+    const int my_tiles = ntile > warp ? (ntile - warp + GQ_WARPS - 1) / GQ_WARPS : 0;  // tiles warp, warp + 4, ...
+
+    // window of a tile: last wi with s_tpre[wi] <= tile (tiles of one warp only move forward)
+    auto window_of = [&](int tile, int from) -> int {
+        int wi = from;
+        while (s_tpre[wi + 1] <= tile) ++wi;
+        return wi;
+    };
+    // Tile metadata is loaded one iteration before its copies are issued (registers), so no
+    // global latency sits between the ring and the MMAs: the copies carry the V records, the
+    // tile's weights and a small header (row count, the window max of each head).
+    int n_tok[3];          // this lane's 3 pieces: token of its row
+    int n_cnt = 0;         // rows of the tile's window
+    int n_u0 = 0;          // first union row of the tile
+    size_t n_wb = 0;
+    double n_mx = -INFINITY;  // lane h < G: window max of head h
+    int wi_meta = 0;
+    auto load_meta = [&](int tile) {
+        wi_meta = window_of(tile, wi_meta);
+        const int ti = tile - s_tpre[wi_meta];
+        n_wb = wbase + wi_meta;
+        n_cnt = P.cnt[n_wb];
+        n_u0 = ti * 16;
+        const int T0 = (int)((w0 + wi_meta) * GQ_WIN);
+        const uint16_t* off = P.off + n_wb * GQ_WIN;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int p = 32 * k + lane;
+            const int r = (p < 80 ? p : 0) / 5;
+            // rows past the window's count hold stale offsets (< W): a readable record, weight 0
+            // (clamped to the context; no dependence on the count load)
+            n_tok[k] = (int)kvt::imin((int64_t)(T0 + (int)off[n_u0 + r]), n_tok_ctx - 1);
+        }
+        n_mx = lane < G ? P.mx[n_wb * G + lane] : -INFINITY;
+    };
+    constexpr int WB = 16 * G * 4;  // weight bytes per tile
+    auto issue = [&](uint32_t dst, unsigned char* sdst) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int p = 32 * k + lane;
+            if (p < 80) {
+                const int r = p / 5, pc = p % 5;
+                gq_cp16(dst + r * GQ_ROWB + pc * 16, vbase + (int64_t)n_tok[k] * GQ_ROWB + pc * 16);
+            }
+        }
+        if (lane < WB / 16)  // rows n_u0 .. n_u0 + 15 of the window's weight table (contiguous)
+            gq_cp16(dst + GQ_SLOT + 16 * lane,
+                    P.wt + (n_wb * GQ_WIN + n_u0) * G + 4 * lane);
+        if (lane < G) reinterpret_cast<double*>(sdst + GQ_SLOT + WB)[lane] = n_mx;
+        if (lane == 0) reinterpret_cast<int*>(sdst + GQ_SLOT + WB + 8 * G)[0] = n_cnt - n_u0;  // valid rows
+    };
+
+    float D[16][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) D[j][0] = D[j][1] = D[j][2] = D[j][3] = 0.f;
+    float om[4] = {0.f, 0.f, 0.f, 0.f};  // sum_t w_h(t) m_t,G for head hA (hi-part rows)
+    double M = -INFINITY;                // running max of head hA over this warp's tiles
+    float l = 0.f;                       // running softmax denominator of head hA (hi rows)
+
+    if (my_tiles > 0) load_meta(warp);
+#pragma unroll
+    for (int j = 0; j < GQ_S - 1; ++j) {
+        if (j < my_tiles) {
+            issue(wring_a + j * GQ_SSLOT, wring + j * GQ_SSLOT);
+            if (j + 1 < my_tiles) load_meta(warp + (j + 1) * GQ_WARPS);
+        }
+        gq_commit();
+    }
+    for (int it = 0; it < my_tiles; ++it) {
+        const int jn = it + GQ_S - 1;
+        if (jn < my_tiles) {
+            issue(wring_a + (jn % GQ_S) * GQ_SSLOT, wring + (jn % GQ_S) * GQ_SSLOT);
+            if (jn + 1 < my_tiles) load_meta(warp + (jn + 1) * GQ_WARPS);
+        }
+        gq_commit();
+        gq_wait<GQ_S - 1>();
+        __syncwarp();
+        const unsigned char* slot = wring + (it % GQ_S) * GQ_SSLOT;
+        const float* wsl = reinterpret_cast<const float*>(slot + GQ_SLOT);
+        const double mw = hA < G ? reinterpret_cast<const double*>(slot + GQ_SLOT + WB)[hA] : -INFINITY;
+        const int nvalid = reinterpret_cast<const int*>(slot + GQ_SLOT + WB + 8 * G)[0];
+        // this tile's window max for head hA: rescale the running state when it rises
+        float f = 0.f;  // weight factor exp(mw - M) for this tile
+        if (mw > M) {
+            const float rs = M == -INFINITY ? 0.f : exp2f((float)((M - mw) * sl2));
 #pragma unroll
             for (int j = 0; j < 16; ++j) { D[j][0] *= rs; D[j][1] *= rs; }
 #pragma unroll
-            for (int G = 0; G < 4; ++G) om[G] *= rs;
+            for (int Gq = 0; Gq < 4; ++Gq) om[Gq] *= rs;
+            l *= rs;
+            M = mw;
+            f = 1.f;
+        } else if (mw > -INFINITY) {
+            f = exp2f((float)((mw - M) * sl2));
         }
+        auto wgt = [&](int r) -> float { return (hA < G && r < nvalid) ? wsl[r * G + hA] * f : 0.f; };
+        const int r0 = 2 * tig, r1 = 2 * tig + 1, r8 = 2 * tig + 8, r9 = 2 * tig + 9;
+        const float wA0 = wgt(r0), wA1 = wgt(r1), wA8 = wgt(r8), wA9 = wgt(r9);
+        if (!lo_part) l += wA0 + wA1 + wA8 + wA9;
 
-        // ---- 3. union rows through the per-warp ring, P.V on the tensor cores ----
-        const int ntile = (ucnt + 15) / 16;
-        const int my_tiles = ntile > warp ? (ntile - warp + GQ_WARPS - 1) / GQ_WARPS : 0;  // tiles w, w + 4, ...
-        auto issue = [&](int it) {  // it-th tile of this warp -> ring slot it % S
-            const int tile = warp + it * GQ_WARPS;
-            const uint32_t dst = wring_a + (it % GQ_S) * GQ_SLOT;
 #pragma unroll
-            for (int p0 = 0; p0 < 96; p0 += 32) {
-                const int p = p0 + lane;
-                if (p < 80) {
-                    const int r = p / 5, pc = p % 5;
-                    int u = tile * 16 + r;
-                    u = u < ucnt ? u : ucnt - 1;  // pad rows: a valid record, weight 0
-                    const int t = Tw + (int)utok[u];
-                    gq_cp16(dst + r * GQ_ROWB + pc * 16, vbase + (int64_t)t * GQ_ROWB + pc * 16);
-                }
-            }
-        };
-#pragma unroll
-        for (int j = 0; j < GQ_S - 1; ++j) {
-            if (j < my_tiles) issue(j);
-            gq_commit();
-        }
-        __syncthreads();  // weight table complete
-        for (int it = 0; it < my_tiles; ++it) {
-            if (it + GQ_S - 1 < my_tiles) issue(it + GQ_S - 1);
-            gq_commit();
-            gq_wait<GQ_S - 1>();
-            __syncwarp();
-            const unsigned char* slot = wring + (it % GQ_S) * GQ_SLOT;
-            const int tile = warp + it * GQ_WARPS;
-            const int r0 = 2 * tig, r1 = 2 * tig + 1, r8 = 2 * tig + 8, r9 = 2 * tig + 9;
-            const int u0 = tile * 16;
-            auto wt = [&](int r, int h) -> float {
-                const int u = u0 + r;
-                return (h < GQ && u < ucnt) ? wtab[u * GQ + h] : 0.f;
+        for (int Gq = 0; Gq < 4; ++Gq) {
+            const __half2 p0 = *reinterpret_cast<const __half2*>(slot + r0 * GQ_ROWB + 64 + 4 * Gq);
+            const __half2 p1 = *reinterpret_cast<const __half2*>(slot + r1 * GQ_ROWB + 64 + 4 * Gq);
+            const __half2 p8 = *reinterpret_cast<const __half2*>(slot + r8 * GQ_ROWB + 64 + 4 * Gq);
+            const __half2 p9 = *reinterpret_cast<const __half2*>(slot + r9 * GQ_ROWB + 64 + 4 * Gq);
+            const float s0 = __low2float(p0), s1 = __low2float(p1), s8 = __low2float(p8), s9 = __low2float(p9);
+            if (!lo_part)
+                om[Gq] += wA0 * __high2float(p0) + wA1 * __high2float(p1) + wA8 * __high2float(p8) +
+                          wA9 * __high2float(p9);
+            auto split = [&](float v) -> __half {
+                const __half hi = __float2half_rn(v);
+                return lo_part ? __float2half_rn(v - __half2float(hi)) : hi;
             };
-            const float wA0 = wt(r0, hA), wA1 = wt(r1, hA), wA8 = wt(r8, hA), wA9 = wt(r9, hA);
+            const uint32_t a0 = pack_h2(split(wA0 * s0 * GQ_ASCALE), split(wA1 * s1 * GQ_ASCALE));
+            const uint32_t a2 = pack_h2(split(wA8 * s8 * GQ_ASCALE), split(wA9 * s9 * GQ_ASCALE));
+            const int wo = 4 * (4 * Gq + (gid >> 1));
+            const uint32_t c0 = *reinterpret_cast<const uint32_t*>(slot + r0 * GQ_ROWB + wo);
+            const uint32_t c1 = *reinterpret_cast<const uint32_t*>(slot + r1 * GQ_ROWB + wo);
+            const uint32_t c8 = *reinterpret_cast<const uint32_t*>(slot + r8 * GQ_ROWB + wo);
+            const uint32_t c9 = *reinterpret_cast<const uint32_t*>(slot + r9 * GQ_ROWB + wo);
+            const uint32_t sel = (gid & 1) ? 0x7632u : 0x5410u;
+            const uint32_t x01 = __byte_perm(c0, c1, sel), x89 = __byte_perm(c8, c9, sel);
+            const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
 #pragma unroll
-            for (int G = 0; G < 4; ++G) {
-                // (scale, min) of the 4 rows this thread feeds
-                const __half2 p0 = *reinterpret_cast<const __half2*>(slot + r0 * GQ_ROWB + 64 + 4 * G);
-                const __half2 p1 = *reinterpret_cast<const __half2*>(slot + r1 * GQ_ROWB + 64 + 4 * G);
-                const __half2 p8 = *reinterpret_cast<const __half2*>(slot + r8 * GQ_ROWB + 64 + 4 * G);
-                const __half2 p9 = *reinterpret_cast<const __half2*>(slot + r9 * GQ_ROWB + 64 + 4 * G);
-                const float s0 = __low2float(p0), s1 = __low2float(p1), s8 = __low2float(p8), s9 = __low2float(p9);
-                if (!lo_part)
-                    om[G] += wA0 * __high2float(p0) + wA1 * __high2float(p1) + wA8 * __high2float(p8) +
-                             wA9 * __high2float(p9);
-                // A = w s 2^12 as f16 (hi rows) or its f16 remainder (lo rows)
-                auto split = [&](float v) -> __half {
-                    const __half hi = __float2half_rn(v);
-                    return lo_part ? __float2half_rn(v - __half2float(hi)) : hi;
-                };
-                const uint32_t a0 = pack_h2(split(wA0 * s0 * GQ_ASCALE), split(wA1 * s1 * GQ_ASCALE));
-                const uint32_t a2 = pack_h2(split(wA8 * s8 * GQ_ASCALE), split(wA9 * s9 * GQ_ASCALE));
-                // B: codes of word 4G + gid/2 of rows (r0, r1) and (r8, r9); bytes 0-1 (dims +0..3)
-                // or 2-3 (dims +4..7) of the word by gid parity; nibble q -> dim + q
-                const int wo = 4 * (4 * G + (gid >> 1));
-                const uint32_t c0 = *reinterpret_cast<const uint32_t*>(slot + r0 * GQ_ROWB + wo);
-                const uint32_t c1 = *reinterpret_cast<const uint32_t*>(slot + r1 * GQ_ROWB + wo);
-                const uint32_t c8 = *reinterpret_cast<const uint32_t*>(slot + r8 * GQ_ROWB + wo);
-                const uint32_t c9 = *reinterpret_cast<const uint32_t*>(slot + r9 * GQ_ROWB + wo);
-                const uint32_t sel = (gid & 1) ? 0x7632u : 0x5410u;
-                const uint32_t x01 = __byte_perm(c0, c1, sel), x89 = __byte_perm(c8, c9, sel);
-                const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t e01 = ((x01 >> (4 * q)) & 0x000f000fu) | 0x64006400u;
-                    const uint32_t e89 = ((x89 >> (4 * q)) & 0x000f000fu) | 0x64006400u;
-                    const __half2 h01 = __hsub2(*reinterpret_cast<const __half2*>(&e01), k1024);
-                    const __half2 h89 = __hsub2(*reinterpret_cast<const __half2*>(&e89), k1024);
-                    mma_f16(D[4 * G + q], a0, 0u, a2, 0u, *reinterpret_cast<const uint32_t*>(&h01),
-                            *reinterpret_cast<const uint32_t*>(&h89));
-                }
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t e01 = ((x01 >> (4 * q)) & 0x000f000fu) | 0x64006400u;
+                const uint32_t e89 = ((x89 >> (4 * q)) & 0x000f000fu) | 0x64006400u;
+                const __half2 h01 = __hsub2(*reinterpret_cast<const __half2*>(&e01), k1024);
+                const __half2 h89 = __hsub2(*reinterpret_cast<const __half2*>(&e89), k1024);
+                mma_f16(D[4 * Gq + q], a0, 0u, a2, 0u, *reinterpret_cast<const uint32_t*>(&h01),
+                        *reinterpret_cast<const uint32_t*>(&h89));
             }
-            __syncwarp();
         }
-        gq_wait<0>();
-        __syncthreads();  // ring, table and bitmaps are reused by the next window
+        __syncwarp();
     }
+    gq_wait<0>();
 
-    // ---- 4. per-warp head outputs -> shared, combine warps, partials ----
-    // D[4G+q][0/1]: row gid (head gid/2, hi or lo part), dims 32G + 8 tig + q and + 4 + q
+    // ---- per-warp head state -> shared; combine warps (flash-decoding) -> range partials ----
 #pragma unroll
     for (int j = 0; j < 16; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) D[j][e] += __shfl_xor_sync(KVT_FULL, D[j][e], 4);  // hi + lo rows
 #pragma unroll
-    for (int G = 0; G < 4; ++G) {
-        float v = om[G];
+    for (int Gq = 0; Gq < 4; ++Gq) {
+        float v = om[Gq];
         v += __shfl_xor_sync(KVT_FULL, v, 1);
         v += __shfl_xor_sync(KVT_FULL, v, 2);
-        om[G] = v;
+        om[Gq] = v;
     }
-    if (!lo_part && hA < GQ) {
+    l += __shfl_xor_sync(KVT_FULL, l, 1);
+    l += __shfl_xor_sync(KVT_FULL, l, 2);
+    if (!lo_part && hA < G) {
         const float inv = 1.f / GQ_ASCALE;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -380,75 +471,96 @@ __global__ void __launch_bounds__(GQ_THREADS, 3) attn_gqa_i4_kernel(
             s_o[warp][hA][dA] = D[j][0] * inv;
             s_o[warp][hA][dA + 4] = D[j][1] * inv;
         }
-        if (tig == 0)
+        if (tig == 0) {
 #pragma unroll
-            for (int G = 0; G < 4; ++G) s_om[warp][hA][G] = om[G];
+            for (int Gq = 0; Gq < 4; ++Gq) s_om[warp][hA][Gq] = om[Gq];
+            s_wm[warp][hA] = M;
+            s_wl[warp][hA] = l;
+        }
     }
     __syncthreads();
-    for (int h = 0; h < GQ; ++h) {
-        const int64_t li = kv * GQ + h;
-        double* P = part + (li * splits + rg) * (int64_t)(d + 2);
+    for (int h = 0; h < G; ++h) {
+        double Mh = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < GQ_WARPS; ++w) Mh = fmax(Mh, s_wm[w][h]);
+        float sw[GQ_WARPS];
+        float lsum = 0.f;
+#pragma unroll
+        for (int w = 0; w < GQ_WARPS; ++w) {
+            sw[w] = s_wm[w][h] == -INFINITY ? 0.f : exp2f((float)((s_wm[w][h] - Mh) * sl2));
+            lsum += sw[w] * s_wl[w][h];
+        }
+        const int64_t li = kv * G + h;
+        double* Pp = part + (li * splits + rg) * (int64_t)(d + 2);
         for (int j = tid; j < d; j += GQ_THREADS) {
             float acc = 0.f;
 #pragma unroll
-            for (int w = 0; w < GQ_WARPS; ++w) acc += s_o[w][h][j] + s_om[w][h][j >> 5];
-            P[2 + j] = (double)acc;
+            for (int w = 0; w < GQ_WARPS; ++w) acc += sw[w] * (s_o[w][h][j] + s_om[w][h][j >> 5]);
+            Pp[2 + j] = (double)acc;
         }
         if (tid == 0) {
-            P[0] = s_m[h];
-            P[1] = (double)s_l[h];
+            Pp[0] = Mh;
+            Pp[1] = (double)lsum;
         }
     }
-    // ---- 5. one ticket per KV lane: the last range CTA merges the group's heads ----
+    // ---- one ticket per KV lane: the last range CTA merges the group's heads ----
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-        const unsigned t = atomicAdd(&tickets[kv * GQ], 1u);
+        const unsigned t = atomicAdd(&tickets[kv * G], 1u);
         s_last = (t == (unsigned)splits - 1);
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int h = 0; h < GQ; ++h) gq_merge(part, splits, d, kv * GQ + h, n_q, out, out64, scale);
-    if (tid == 0) tickets[kv * GQ] = 0;
+    for (int h = 0; h < G; ++h) gq_merge(part, splits, d, kv * G + h, n_q, out, out64, scale);
+    if (tid == 0) tickets[kv * G] = 0;
 }
 
 }  // namespace kvt
 
 using namespace kvt;
 
-// GQA INT4 attention (kv_group g in {2, 4}, d = 128): the union pass above.  Returns
-// KVT_ERR_ARG when the shape is not covered (the caller then runs the per-lane kernel).
-int kvt_attn_gqa_i4(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, int kvg, int64_t n_ctx,
-                    const int32_t* sel_tok, const double* sel_score, const int32_t* n_sel, int64_t sel_stride,
-                    double logit_scale, void* ws, float* out, double* out64, cudaStream_t st) {
-    if (d != 128 || (kvg != 2 && kvg != 4) || n_lanes % kvg || n_ctx <= 0) return KVT_ERR_ARG;
+extern "C" size_t kvt_attn_gqa_scratch_bytes(int64_t n_lanes, int kvg, int64_t n_ctx) {
+    if (kvg < 2 || n_lanes % kvg || n_ctx <= 0) return 0;
+    return gq_scratch_bytes(n_lanes / kvg, (n_ctx + GQ_WIN - 1) / GQ_WIN, kvg);
+}
+
+// GQA INT4 attention over the group's union (kv_group g in {2, 4}, d = 128, tokens < n_ctx):
+// plan + pv launches.  scratch: kvt_attn_gqa_scratch_bytes.  Returns KVT_ERR_ARG when the
+// shape is not covered (the caller then runs the per-lane kernel).
+extern "C" int kvt_sparse_decode_attn_gqa(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, int kvg,
+                                          int64_t n_ctx, const int32_t* sel_tok, const double* sel_score,
+                                          const int32_t* n_sel, int64_t sel_stride, double logit_scale, void* ws,
+                                          void* scratch, size_t scratch_bytes, float* out, double* out64,
+                                          void* stream) {
+    if (!values || !sel_tok || !sel_score || !n_sel || !ws || !scratch || (!out && !out64)) return KVT_ERR_ARG;
+    if (d != 128 || (kvg != 2 && kvg != 4) || n_lanes <= 0 || n_lanes % kvg || n_ctx <= 0) return KVT_ERR_ARG;
     if (((uintptr_t)values % 16) || (lane_stride_b % 16)) return KVT_ERR_SHAPE;
-    if (n_ctx > (int64_t)64 * 1024 * 1024) return KVT_ERR_ARG;
-    // CTAs = KV lanes x ranges: about 3 waves of 3 CTAs per SM, ranges of whole windows
+    if (scratch_bytes < kvt_attn_gqa_scratch_bytes(n_lanes, kvg, n_ctx)) return KVT_ERR_OOM;
+    cudaStream_t st = (cudaStream_t)stream;
     const int64_t n_kv = n_lanes / kvg;
     const int64_t n_win = (n_ctx + GQ_WIN - 1) / GQ_WIN;
-    int64_t want = (3LL * 3 * kvt::sm_count() + n_kv - 1) / n_kv;
+    if (n_kv > 65535 || n_win > 65535 * 64) return KVT_ERR_ARG;
+    GqPlan P = gq_carve(scratch, n_kv, n_win, kvg);
+    // ranges: at most 4 CTAs per SM over the KV lanes (one wave), <= 64 ranges, <= 256 windows each
+    int64_t want = (4LL * kvt::sm_count()) / n_kv;
     want = kvt::imax(1, kvt::imin(kvt::imin(want, 64), n_win));
-    const int R = (int)(((n_win + want - 1) / want) * GQ_WIN);
-    const int splits = (int)((n_ctx + R - 1) / R);
+    int wins_per = (int)((n_win + want - 1) / want);
+    if (wins_per > 256) return KVT_ERR_ARG;
+    const int splits = (int)((n_win + wins_per - 1) / wins_per);
     unsigned int* tickets = (unsigned int*)ws;
     double* part = (double*)((char*)ws + (((size_t)n_lanes * 4 + 255) & ~(size_t)255)) + 2 * n_lanes;
-    const int NW = GQ_WIN / 32;
-    const size_t smem = (size_t)GQ_WARPS * GQ_S * GQ_SLOT + (size_t)GQ_WIN * kvg * 4 + (size_t)(kvg + 1) * NW * 4 +
-                        (size_t)NW * 4 + (size_t)GQ_WIN * 2;
-#define KVT_GQ(GG)                                                                                                  \
-    do {                                                                                                            \
-        KVT_PER_DEVICE(size_t, configured);                                                                         \
-        if (smem > configured) {                                                                                    \
-            cudaError_t e = cudaFuncSetAttribute(attn_gqa_i4_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                                 (int)smem);                                                        \
-            if (e != cudaSuccess) return kvt_set_cuda_error(e);                                                     \
-            configured = smem;                                                                                      \
-        }                                                                                                           \
-        launch_pdl(attn_gqa_i4_kernel<GG>, dim3((unsigned)splits, (unsigned)n_kv), dim3(GQ_THREADS), smem, st,     \
-                   (const unsigned char*)values, lane_stride_b, n_lanes, sel_tok, sel_score, n_sel, sel_stride, R, \
-                   splits, part, tickets, out, out64, logit_scale);                                                 \
+    const size_t smem_pv = (size_t)GQ_WARPS * GQ_S * GQ_SSLOT;
+#define KVT_GQ(GG)                                                                                                   \
+    do {                                                                                                             \
+        launch_pdl(gqa_plan_kernel<GG>, dim3((unsigned)((n_win + GQ_WPC - 1) / GQ_WPC), (unsigned)n_kv),             \
+                   dim3(GQ_THREADS), 0, st,                                                                  \
+                   sel_tok, sel_score, n_sel, sel_stride, n_win, logit_scale, P);                                    \
+        launch_pdl(gqa_pv_kernel<GG>, dim3((unsigned)splits, (unsigned)n_kv), dim3(GQ_THREADS), smem_pv, st,         \
+                   (const unsigned char*)values, lane_stride_b, n_lanes, n_win, wins_per, splits, n_ctx, P, part,    \
+                   tickets,                                                                                          \
+                   out, out64, logit_scale);                                                                         \
     } while (0)
     if (kvg == 2) KVT_GQ(2);
     else KVT_GQ(4);

@@ -442,9 +442,12 @@ inline int resident_per_sm(K kernel, int threads, size_t smem, int fallback) {
 }
 
 // GQA union attention over INT4 values (attn_gqa.cu); KVT_ERR_ARG = shape not covered
-int kvt_attn_gqa_i4(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, int kvg, int64_t n_ctx,
-                    const int32_t* sel_tok, const double* sel_score, const int32_t* n_sel, int64_t sel_stride,
-                    double logit_scale, void* ws, float* out, double* out64, cudaStream_t st);
+extern "C" int kvt_sparse_decode_attn_gqa(const void* values, int64_t n_lanes, int64_t lane_stride_b, int d, int kvg,
+                                          int64_t n_ctx, const int32_t* sel_tok, const double* sel_score,
+                                          const int32_t* n_sel, int64_t sel_stride, double logit_scale, void* ws,
+                                          void* scratch, size_t scratch_bytes, float* out, double* out64,
+                                          void* stream);
+extern "C" size_t kvt_attn_gqa_scratch_bytes(int64_t n_lanes, int kvg, int64_t n_ctx);
 
 // status plumbing (api.cu)
 int kvt_set_cuda_error(cudaError_t e);

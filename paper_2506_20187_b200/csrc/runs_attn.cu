@@ -1023,14 +1023,6 @@ static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_strid
 // pipeline fill, partial merge) dominating any wave-tail effect: the fewest units that keep the
 // staging bounded are best at k = 0.1 n and within ~8% at k = 0.5 n.
 // INT4 units are capped at half the rows of 2-byte ones (measured on the decode step).
-// GQA INT4 attention: the union kernel (attn_gqa.cu) runs when KVT_GQA_UNION=1 is set in the
-// environment (read per call); by default the per-query-lane ring kernel runs, which is
-// faster on the measured workloads.
-static bool gqa_union_enabled() {
-    const char* e = getenv("KVT_GQA_UNION");
-    return e && e[0] == '1';
-}
-
 // Few lanes (small batch): the fewest-units rule would leave most of the 148 SMs idle, so
 // the split count is raised until the grid covers about two CTAs per SM, with units kept at
 // >= 256 rows.
@@ -1058,12 +1050,6 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
     int rc;
     const int64_t kmax = sel_stride;
     const int kvg = kv_group_current();
-    if (v_dtype == KVT_I4 && kvg > 1 && splits <= 0 && gqa_union_enabled()) {
-        // GQA: one pass over the group's union, P.V on the tensor cores (attn_gqa.cu)
-        rc = kvt_attn_gqa_i4(values, n_lanes, lane_stride, d, kvg, lane_stride / (d / 2 + d / 8), sel_tok, sel_score,
-                             n_sel, sel_stride, logit_scale, ws, out, out64, st);
-        if (rc != KVT_ERR_ARG) return rc;
-    }
     if (splits <= 0) splits = ring_auto_splits(kmax, v_dtype, n_lanes);  // auto (the workspace must hold 64 splits)
     if (splits > 64) splits = 64;
     // rows per work unit: the whole selection in <= splits units

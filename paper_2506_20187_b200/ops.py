@@ -549,6 +549,27 @@ def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch
     L.check(L.kvt_select_attend(a, ws.buf.data_ptr(), ws.bytes, _stream()), "select_attend")
 
 
+@_on_device
+def sparse_decode_attn_gqa(values, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor, kv_group: int,
+                           n_ctx: int, want_f64: bool = False):
+    """GQA union K7 (kvt_sparse_decode_attn_gqa): INT4 values [n_kv, N, rb], query lanes i / g
+    share KV lane i / g -> out f32 [n_lanes, d] (and f64)."""
+    require_cuda(values)
+    ls, d = _lanes(values)
+    nl = n_sel.shape[0]
+    dev = values.device
+    ws = torch.zeros(L.kvt_attn_workspace_bytes(nl, d, 64), dtype=torch.uint8, device=dev)
+    sb = L.kvt_attn_gqa_scratch_bytes(nl, kv_group, n_ctx)
+    scratch = torch.empty(max(sb, 1), dtype=torch.uint8, device=dev)
+    out = torch.empty((nl, d), dtype=torch.float32, device=dev)
+    out64 = torch.empty((nl, d), dtype=torch.float64, device=dev) if want_f64 else None
+    L.check(L.kvt_sparse_decode_attn_gqa(values.data_ptr(), nl, ls, d, kv_group, n_ctx, sel_tok.data_ptr(),
+                                         sel_score.data_ptr(), n_sel.data_ptr(), sel_tok.shape[1],
+                                         1.0 / math.sqrt(d), ws.data_ptr(), scratch.data_ptr(), sb, out.data_ptr(),
+                                         _p(out64), _stream()), "sparse_decode_attn_gqa")
+    return (out, out64) if want_f64 else out
+
+
 def lane_abs_mag(amax: torch.Tensor, amin: torch.Tensor, m: int, out: torch.Tensor | None = None) -> torch.Tensor:
     """Per-lane max |key| over chunks [0, m) from the (outward-rounded) abstracts -> f32 [n_lanes, d]
     (the abs_mag operand of select_attend / kvt_chunk_bounds_fast)."""

@@ -246,11 +246,11 @@ def test_gqa_kv_sharing_matches_oracle(ops, dt, kind, Hkv):
 @pytest.mark.parametrize("g", [2, 4])
 @pytest.mark.parametrize("overlap", ["same", "mixed", "disjoint"])
 @pytest.mark.parametrize("k", [700, 2200])
-def test_gqa_union_attention_matches_oracle(ops, g, overlap, k, monkeypatch):
-    """The GQA union kernel (attn_gqa.cu: one pass over the group's union, P.V on the tensor
-    cores with the heads as MMA rows) against the f64 oracle over the same selections, with
-    identical, partly shared and disjoint per-head selections across several token windows."""
-    monkeypatch.setenv("KVT_GQA_UNION", "1")
+def test_gqa_union_attention_matches_oracle(ops, g, overlap, k):
+    """The GQA union kernels (attn_gqa.cu: a union plan per 2048-token window, then one pass over
+    the group's union with P.V on the tensor cores, the heads as MMA rows) against the f64 oracle
+    over the same selections, with identical, partly shared and disjoint per-head selections
+    across several token windows."""
     n_kv, d, n = 3, 128, 9000
     rng = np.random.default_rng(7 + g)
     V = torch.from_numpy(rng.normal(size=(n_kv, n, d)).astype(np.float32)).cuda()
@@ -274,8 +274,7 @@ def test_gqa_union_attention_matches_oracle(ops, g, overlap, k, monkeypatch):
     st = torch.from_numpy(sel).cuda()
     ss = torch.from_numpy(score).cuda()
     ns = torch.full((n_kv * g,), k, dtype=torch.int32, device="cuda")
-    with ops.kv_group(g):
-        out = ops.sparse_decode_attn(vi, st, ss, ns).cpu().numpy()
+    out = ops.sparse_decode_attn_gqa(vi, st, ss, ns, g, n).cpu().numpy()
     scale = 1.0 / np.sqrt(d)
     for i in range(n_kv * g):
         w = np.exp((score[i] - score[i].max()) * scale)
