@@ -12,11 +12,11 @@
 //         where head h did not select the row), written to scratch with the window's count;
 //   pv    (one CTA per KV lane x range of windows, 4 warps): the union rows' 80 B INT4 value
 //         records stream through a per-warp cp.async ring, 16 rows per tile, and
-//             o_h[j] = sum_t w_h(t) (s_t,G(j) c_t,j + m_t,G(j))
+//             o_h[j] = sum_t w_h(t) (s_t,G(j) (c_t,j - 8) + (m_t,G(j) + 8 s_t,G(j)))
 //         runs on mma.sync m16n8k16 (f16 in, f32 accumulate): A = the weights times the group's
 //         scale (x 2^12), rows 2h / 2h + 1 = their f16 high / low parts, so the product keeps
-//         ~22 bits; B = the codes as exact f16 integers (nibbles -> 1024 + c by one LOP3, minus
-//         1024 by one HSUB2); 16 MMAs per 16 rows cover d = 128 for every head at once.  The
+//         ~22 bits; B = the centred codes c - 8 as exact f16 integers (nibbles -> 1024 + c by one
+//         LOP3, minus 1032 by one HSUB2); 16 MMAs per 16 rows cover d = 128 for every head at once.  The
 //         min term sum_t w_h(t) m_t,G is a per-(head, group) scalar on the CUDA cores.  Each
 //         warp keeps flash-decoding state per head (running max over its tiles' windows); the
 //         warps and then the ranges (ticket: the last range CTA of the KV lane) are merged.
@@ -418,9 +418,11 @@ __global__ void __launch_bounds__(GQ_THREADS, 4) gqa_pv_kernel(
             const __half2 p8 = *reinterpret_cast<const __half2*>(slot + r8 * GQ_ROWB + 64 + 4 * Gq);
             const __half2 p9 = *reinterpret_cast<const __half2*>(slot + r9 * GQ_ROWB + 64 + 4 * Gq);
             const float s0 = __low2float(p0), s1 = __low2float(p1), s8 = __low2float(p8), s9 = __low2float(p9);
+            // centred codes: x = (c - 8) s + (m + 8 s), so neither sum carries the other's
+            // magnitude (the uncentred split cancels to ~1e-3 of its terms over long selections)
             if (!lo_part)
-                om[Gq] += wA0 * __high2float(p0) + wA1 * __high2float(p1) + wA8 * __high2float(p8) +
-                          wA9 * __high2float(p9);
+                om[Gq] += wA0 * fmaf(8.f, s0, __high2float(p0)) + wA1 * fmaf(8.f, s1, __high2float(p1)) +
+                          wA8 * fmaf(8.f, s8, __high2float(p8)) + wA9 * fmaf(8.f, s9, __high2float(p9));
             auto split = [&](float v) -> __half {
                 const __half hi = __float2half_rn(v);
                 return lo_part ? __float2half_rn(v - __half2float(hi)) : hi;
@@ -434,13 +436,13 @@ __global__ void __launch_bounds__(GQ_THREADS, 4) gqa_pv_kernel(
             const uint32_t c9 = *reinterpret_cast<const uint32_t*>(slot + r9 * GQ_ROWB + wo);
             const uint32_t sel = (gid & 1) ? 0x7632u : 0x5410u;
             const uint32_t x01 = __byte_perm(c0, c1, sel), x89 = __byte_perm(c8, c9, sel);
-            const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
+            const __half2 k1032 = __halves2half2(__ushort_as_half(0x6408), __ushort_as_half(0x6408));  // 1024 + 8
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t e01 = ((x01 >> (4 * q)) & 0x000f000fu) | 0x64006400u;
                 const uint32_t e89 = ((x89 >> (4 * q)) & 0x000f000fu) | 0x64006400u;
-                const __half2 h01 = __hsub2(*reinterpret_cast<const __half2*>(&e01), k1024);
-                const __half2 h89 = __hsub2(*reinterpret_cast<const __half2*>(&e89), k1024);
+                const __half2 h01 = __hsub2(*reinterpret_cast<const __half2*>(&e01), k1032);
+                const __half2 h89 = __hsub2(*reinterpret_cast<const __half2*>(&e89), k1032);
                 mma_f16(D[4 * Gq + q], a0, 0u, a2, 0u, *reinterpret_cast<const uint32_t*>(&h01),
                         *reinterpret_cast<const uint32_t*>(&h89));
             }
