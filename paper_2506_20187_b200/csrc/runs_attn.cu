@@ -1022,12 +1022,20 @@ static int dispatch_attn(const void* values, int64_t n_lanes, int64_t lane_strid
 // planted decode workload (tools/microbench.py attn; B200) shows per-unit fixed cost (staging,
 // pipeline fill, partial merge) dominating any wave-tail effect: the fewest units that keep the
 // staging bounded are best at k = 0.1 n and within ~8% at k = 0.5 n.
-// INT4 units are capped at half the rows of 2-byte ones (measured on the decode step).
+// INT4: 2400-row units through a 4-slot ring per warp (more resident CTAs beat deeper
+// per-warp rings: config-3 A/B of slots x unit rows, tools/ab_libs.sh: 8 x 1664 2.69 ms,
+// 6 x 1664 2.57, 4 x 1664 2.55, 3 x 1664 2.58, 2 x 1664 2.62, 4 x 1024 2.64, 4 x 2400 2.52).
 // Few lanes (small batch): the fewest-units rule would leave most of the 148 SMs idle, so
 // the split count is raised until the grid covers about two CTAs per SM, with units kept at
 // >= 256 rows.
+#ifndef KVT_ATTN_I4_S
+#define KVT_ATTN_I4_S 4
+#endif
+#ifndef KVT_ATTN_I4_RMAX
+#define KVT_ATTN_I4_RMAX 2400
+#endif
 static int ring_auto_splits(int64_t kmax, int v_dtype, int64_t n_lanes) {
-    const int64_t rmax = v_dtype == KVT_I4 ? 1664 : 3328;
+    const int64_t rmax = v_dtype == KVT_I4 ? KVT_ATTN_I4_RMAX : 3328;
     const int64_t cap = kvt::imax(1, kvt::imin(64, (kmax + 31) / 32));
     int64_t s = kvt::imax(1, kvt::imin(cap, (kmax + rmax - 1) / rmax));
     const int64_t fill = (2 * (int64_t)kvt::sm_count() + n_lanes - 1) / kvt::imax(1, n_lanes);
@@ -1059,7 +1067,7 @@ extern "C" int kvt_sparse_decode_attn(const void* values, int v_dtype, int64_t n
         case KVT_I4: {
             if ((d != 128 && d != 256) || !aligned || (lane_stride % 16)) return KVT_ERR_SHAPE;
             if (R <= 8192)  // cp.async ring (the unit's ids + weights staged: 8 B per row)
-                rc = d == 128 ? launch_ring<FmtI4<128>, 8>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
+                rc = d == 128 ? launch_ring<FmtI4<128>, KVT_ATTN_I4_S>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
                                                            sel_stride, splits, R, part, tickets, out, out64, logit_scale, st)
                               : launch_ring<FmtI4<256>, 6>(values, n_lanes, lane_stride, d, sel_tok, sel_score, n_sel,
                                                            sel_stride, splits, R, part, tickets, out, out64, logit_scale, st);
