@@ -865,7 +865,11 @@ def run_ours(args):
             "note": "in situ: kv_quant over each layer's bf16 staging, CUDA events around the K and V launches"},
         "gpu_launches": (6 if is_i4 else 5) * L * args.steps,
         "bound_grid": {"fine_C": sorted(set(dec.C)), "coarse_layers": [l for l in range(L) if res["bound_grid"][l]],
-                       "rule": "candidate fraction >= 0.9 in warm-up -> prune on C=64 abstracts"},
+                       "grid_C": list(dec.grid_C),
+                       "rho_measured": [None if r is None else round(r, 4) for r in dec.rho_measured],
+                       "rule": "adapt_chunking after warm-up: live chunks of the selected runs at C = C_l..64 "
+                               "(kvt_live_chunks) -> expected bound + candidate bytes per grid; the cheapest "
+                               "grid (K2 merges of the fine abstracts) when it saves > 10 %"},
         "shard": {k: sp[k] for k in ("kv0", "kv_lanes", "q_lanes", "global_batch")},
         "clocks": res["clocks"],
         "e2e": res["e2e"],

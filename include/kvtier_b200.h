@@ -386,6 +386,11 @@ KVT_API int kvt_tier_layer(const kvt_tier_args* a, void* stream);
 /* out4 = [misses, evictions, need (< 0: capacity error), victims] of the last call;
  * synchronises the stream (diagnostics). */
 KVT_API int kvt_tier_read_ctl(const void* ctl, long long* out4, void* stream);
+/* Live chunks of each lane's selection (runs from kvt_topk_select_runs / _band): out[lane][j]
+ * = chunks of size 2^(lg0 + j) (j < nlev <= 8) that hold a selected token -- the measured skew
+ * behind SparseDecoder.adapt_chunking (the importance density of chunk_tree.py:34-123). */
+KVT_API int kvt_live_chunks(const int32_t* run_start, const int32_t* run_len, const int32_t* n_runs,
+                            int64_t run_stride, int64_t n_lanes, int lg0, int nlev, long long* out, void* stream);
 /* GQA K7 over INT4 values (kv_group g in {2, 4}, d = 128): one pass over the union of each
  * group's selections (query lanes i / g share KV lane i / g), P.V on the tensor cores with the
  * group's heads as MMA rows; tokens < n_ctx.  ws as kvt_sparse_decode_attn (64 splits);

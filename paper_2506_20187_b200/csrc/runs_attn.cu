@@ -1125,3 +1125,53 @@ extern "C" int kvt_sparse_decode_attn_paged(const void* pool, const int32_t* tab
     pg = PagedV();
     return rc;
 }
+
+// ---- live chunks of a selection (the skew behind adaptive chunk sizing) ----------------------
+// Per lane and power-of-two chunk size 2^(lg0 + j), j < nlev: how many chunks of a uniform grid
+// hold at least one selected token, counted from the lane's runs (ascending, disjoint): run r
+// covers chunks [s >> lg, (e - 1) >> lg], minus one when it starts in the chunk where run r - 1
+// ended.  The decoder turns these counts into the expected candidate tokens of each grid
+// (chunk_tree.py:34-123 frames the same skew as the importance density rho).
+__global__ void live_chunks_kernel(const int32_t* __restrict__ run_start, const int32_t* __restrict__ run_len,
+                                   const int32_t* __restrict__ n_runs, int64_t run_stride, int lg0, int nlev,
+                                   long long* __restrict__ out) {
+    const int64_t li = blockIdx.x;
+    const int nr = n_runs[li];
+    const int32_t* rs = run_start + li * run_stride;
+    const int32_t* rl = run_len + li * run_stride;
+    long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+        const int s = rs[r], e = s + rl[r];
+        const int pe = r > 0 ? rs[r - 1] + rl[r - 1] - 1 : -1;  // last token of the previous run
+        for (int j = 0; j < nlev && j < 8; ++j) {
+            const int lg = lg0 + j;
+            const int a = s >> lg, b = (e - 1) >> lg;
+            acc[j] += (long long)(b - a + 1) - (pe >= 0 && (pe >> lg) == a ? 1 : 0);
+        }
+    }
+    __shared__ long long red[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = 0; j < nlev && j < 8; ++j) {
+        long long v = acc[j];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(KVT_FULL, v, o);
+        if (lane == 0) red[j][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < nlev && threadIdx.x < 8) {
+        long long v = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+        out[li * nlev + threadIdx.x] = v;
+    }
+}
+
+extern "C" int kvt_live_chunks(const int32_t* run_start, const int32_t* run_len, const int32_t* n_runs,
+                               int64_t run_stride, int64_t n_lanes, int lg0, int nlev, long long* out, void* stream) {
+    if (!run_start || !run_len || !n_runs || !out || n_lanes < 0 || lg0 < 0 || nlev < 1 || nlev > 8 ||
+        lg0 + nlev > 31)
+        return KVT_ERR_ARG;
+    if (n_lanes == 0) return KVT_OK;
+    live_chunks_kernel<<<(unsigned)n_lanes, 256, 0, (cudaStream_t)stream>>>(run_start, run_len, n_runs, run_stride,
+                                                                          lg0, nlev, out);
+    return kvt_check_launch();
+}

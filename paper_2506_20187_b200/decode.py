@@ -75,6 +75,9 @@ class SparseDecoder:
                        for C in self.C]
         self.amin_c = [None if a is None else torch.empty_like(a) for a in self.amax_c]
         self.use_coarse = [False] * n_layers
+        self.grid_C = list(self.C)      # chunk size each layer prunes on (adapt_chunking)
+        self._mid = {}                  # (layer, C) -> intermediate-grid abstracts (K2 from the fine grid)
+        self.rho_measured = [None] * n_layers
         self.n = 0
         self._ws = None
         self._bufs = None
@@ -93,6 +96,9 @@ class SparseDecoder:
             if self.amax_c[l] is not None:  # K2: the coarse grid from the fine one, keys not re-read
                 ops.abstract_merge(self.amax[l], self.amin[l], factor=self.coarse_C // self.C[l],
                                    m_in=ops.n_grid_leaves(n, self.C[l]), out=(self.amax_c[l], self.amin_c[l]))
+        for (l, C), (mx, mn) in self._mid.items():
+            ops.abstract_merge(self.amax[l], self.amin[l], factor=C // self.C[l],
+                               m_in=ops.n_grid_leaves(n, self.C[l]), out=(mx, mn))
         self._bufs = None
 
     def load_layer(self, layer: int, k: torch.Tensor, v: torch.Tensor, t0: int = 0) -> None:
@@ -123,31 +129,86 @@ class SparseDecoder:
             if self.amax_c[l] is not None:
                 cc = (self.n - 1) // self.coarse_C
                 ops.abstract_build(self.K[l], self.n, self.coarse_C, self.amax_c[l], self.amin_c[l], cc, cc + 1)
+        for (l, C), (mx, mn) in self._mid.items():  # the tail chunk of every intermediate grid (K2)
+            f = C // self.C[l]
+            cc = (self.n - 1) // C
+            m_in = ops.n_grid_leaves(self.n, self.C[l])
+            lanes = torch.arange(self.kv_lanes, dtype=torch.int32)
+            tmx, tmn = ops.abstract_merge(self.amax[l], self.amin[l], seg_lane=lanes,
+                                          seg_begin=torch.full_like(lanes, cc * f),
+                                          seg_end=torch.full_like(lanes, min(m_in, cc * f + f)))
+            mx[:, cc] = tmx
+            mn[:, cc] = tmn
         self._bufs = None
 
     def grid(self, l: int):
-        """(C, amax, amin) the layer's pruning runs on (fine plan chunk, or coarse -- see
-        adapt_bound_granularity)."""
-        if self.use_coarse[l]:
-            return self.coarse_C, self.amax_c[l], self.amin_c[l]
-        return self.C[l], self.amax[l], self.amin[l]
+        """(C, amax, amin) the layer's pruning runs on: the plan chunk, or the size adapt_chunking
+        chose (intermediate sizes are K2 merges of the fine abstracts)."""
+        C = self.grid_C[l]
+        if C == self.C[l]:
+            return C, self.amax[l], self.amin[l]
+        if C == self.coarse_C and self.amax_c[l] is not None:
+            return C, self.amax_c[l], self.amin_c[l]
+        mx, mn = self._mid[(l, C)]
+        return C, mx, mn
 
-    def adapt_bound_granularity(self, threshold: float = 0.9) -> list[bool]:
-        """After a step: layers whose candidate fraction (tokens left after pruning / n) was
-        >= threshold prune on the coarse abstracts from now on (their fine bounds cost bytes and
-        removed nothing); a coarse layer returns to the fine grid when pruning becomes useful
-        (< threshold - 0.2).  Outside graph capture only: it reads the step's counters."""
+    def _ensure_grid(self, l: int, C: int) -> None:
+        if C in (self.C[l], self.coarse_C) or (l, C) in self._mid:
+            return
+        mx = torch.empty((self.kv_lanes, ops.n_grid_leaves(self.n_cap, C), self.d), dtype=self.amax[l].dtype,
+                         device=self.device)
+        mn = torch.empty_like(mx)
+        ops.abstract_merge(self.amax[l], self.amin[l], factor=C // self.C[l], m_in=ops.n_grid_leaves(self.n, self.C[l]),
+                           out=(mx, mn))
+        self._mid[(l, C)] = (mx, mn)
+
+    def adapt_chunking(self, margin: float = 0.1) -> list[int]:
+        """Adaptive chunk sizing from the last step's selection (outside graph capture: it reads
+        the step's counters).  For every layer whose plan chunk is finer than default_chunk_size
+        (chunk_tree.py:111-123: early layers at 8), the live chunks of its selected runs at every
+        size C = C_l .. 64 (kvt_live_chunks: the skew of the layer's attention weights) give the
+        expected candidate tokens of each grid, infl * live(C) * C, with infl measured on the
+        current grid; the layer prunes on the grid with the fewest bound + candidate bytes
+        (switching only for a > margin gain).  The reference's importance density rho (the
+        fraction of a live chunk's halves that stay live, averaged over the levels) is recorded
+        in rho_measured.  Returns the chunk size per layer."""
         bufs = self._buffers()
+        sA = self.amax[0].element_size()
+        rowK = ops.row_bytes_i4(self.d) if self.dtype == ops.I4 else self.d * self.K.element_size()
         for l in range(self.L):
             if self.amax_c[l] is None:
                 continue
-            C = self.coarse_C if self.use_coarse[l] else self.C[l]
-            evals = bufs[l]["evals"].double().mean().item()
-            frac = (evals - ops.n_grid_leaves(self.n, C)) / max(self.n, 1)
-            if not self.use_coarse[l] and frac >= threshold:
-                self.use_coarse[l] = True
-            elif self.use_coarse[l] and frac < threshold - 0.2:
-                self.use_coarse[l] = False
+            sizes = []
+            c = self.C[l]
+            while c <= self.coarse_C:
+                sizes.append(c)
+                c *= 2
+            b = bufs[l]
+            live = torch.empty((self.lanes, len(sizes)), dtype=torch.int64, device=self.device)
+            L_ = ops.L
+            L_.check(L_.kvt_live_chunks(b["run_start"].data_ptr(), b["run_len"].data_ptr(), b["n_runs"].data_ptr(),
+                                        b["run_start"].stride(0), self.lanes, int(math.log2(sizes[0])), len(sizes),
+                                        live.data_ptr(), ops._stream()), "live_chunks")
+            lv = live.double().sum(0).cpu().tolist()
+            cur = self.grid_C[l]
+            m_cur = ops.n_grid_leaves(self.n, cur)
+            n_cand = max(b["evals"].double().mean().item() - m_cur, 1.0) * self.lanes
+            infl = n_cand / max(lv[sizes.index(cur)] * cur, 1.0)
+            cost = {C: self.lanes * ops.n_grid_leaves(self.n, C) * (2 * self.d * sA + 24) + infl * lv[j] * C * rowK
+                    for j, C in enumerate(sizes)}
+            best = min(cost, key=cost.get)
+            if best != cur and cost[best] < (1.0 - margin) * cost[cur]:
+                self._ensure_grid(l, best)
+                self.grid_C[l] = best
+            dens = [lv[j] / (2.0 * lv[j + 1]) for j in range(len(sizes) - 1) if lv[j + 1] > 0]
+            self.rho_measured[l] = sum(dens) / len(dens) if dens else None
+        self.use_coarse = [self.grid_C[l] != self.C[l] for l in range(self.L)]
+        return list(self.grid_C)
+
+    def adapt_bound_granularity(self, threshold: float = 0.9) -> list[bool]:
+        """Compatibility wrapper of adapt_chunking: True for the layers that no longer prune on
+        their plan chunk."""
+        self.adapt_chunking()
         return list(self.use_coarse)
 
     def k_for(self, layer: int) -> int:

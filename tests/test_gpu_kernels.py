@@ -361,3 +361,26 @@ def test_k2_abstract_merge_segments_and_coarsening():
     f64 = ops.abstract_build(K, n, 64, abs_dtype=torch.bfloat16)
     c = ops.abstract_merge(f8[0], f8[1], factor=8, m_in=ops.n_grid_leaves(n, 8))
     assert torch.equal(c[0], f64[0]) and torch.equal(c[1], f64[1])
+
+
+def test_live_chunks_counts_distinct_chunks_of_the_selection():
+    """kvt_live_chunks (the skew input of SparseDecoder.adapt_chunking): chunks of size 2^lg
+    holding a selected token, from the runs, equal numpy's count of distinct t >> lg."""
+    import torch
+    from paper_2506_20187_b200 import _lib as L, ops
+    rng = np.random.default_rng(9)
+    lanes, n = 5, 70000
+    sels = [np.sort(rng.choice(n, size=s, replace=False)) for s in (1, 7, 700, 7000, 35000)]
+    kmax = max(len(x) for x in sels)
+    st = torch.zeros((lanes, kmax), dtype=torch.int32)
+    for i, x in enumerate(sels):
+        st[i, :len(x)] = torch.from_numpy(x.astype(np.int32))
+    ns = torch.tensor([len(x) for x in sels], dtype=torch.int32)
+    r = ops.runs_scan(st.cuda(), ns.cuda(), n)
+    out = torch.empty((lanes, 4), dtype=torch.int64, device="cuda")
+    L.check(L.kvt_live_chunks(r["run_start"].data_ptr(), r["run_len"].data_ptr(), r["n_runs"].data_ptr(),
+                              r["run_start"].stride(0), lanes, 3, 4, out.data_ptr(), ops._stream()), "live_chunks")
+    got = out.cpu().numpy()
+    for i, x in enumerate(sels):
+        for j, lg in enumerate(range(3, 7)):
+            assert got[i, j] == len(np.unique(x >> lg)), (i, lg)
