@@ -61,4 +61,30 @@ parts = torch.randn((3, 4, 130), device="cuda", dtype=torch.float64)
 parts[:, :, 1] = parts[:, :, 1].abs()
 ops.lse_merge(parts, 0.1)
 torch.cuda.synchronize()
+# round 2: GQA union attention (plan + pv), K2 merges, live chunks, the hot tier with evictions
+from paper_2506_20187_b200 import _lib as L  # noqa: E402
+from paper_2506_20187_b200.host_tier import TieredDecoder  # noqa: E402
+dec = SparseDecoder(3, 2, 8, 128, 9000, dtype=ops.I4, device="cuda", n_kv_heads=2)
+k = torch.randn((dec.kv_lanes, 9000, 128), device="cuda", dtype=torch.bfloat16)
+v = torch.randn_like(k)
+for l in range(3):
+    dec.load_layer(l, k, v)
+dec.set_length(9000)
+out = dec.step(torch.randn((3, dec.lanes, 128), device="cuda"))
+dec.adapt_chunking()
+out = dec.step(torch.randn((3, dec.lanes, 128), device="cuda"))
+torch.cuda.synchronize()
+assert torch.isfinite(out).all()
+ops.abstract_merge(dec.amax[0], dec.amin[0], seg_lane=[0, 1, 1], seg_begin=[0, 3, 9], seg_end=[5, 9, 10])
+td = TieredDecoder(3, 1, 4, 128, 8192, 9000, crec=8, keep_raw=True, importance_rate=0.1, early_layer_rate=0.1)
+k = torch.randn((4, 8192, 128), device="cuda", dtype=torch.bfloat16)
+for l in range(3):
+    td.load_layer(l, k, torch.randn_like(k))
+td.set_length(8192)
+td.set_theta([0.5, 0.0, 1.0])
+for s in range(3):
+    out = td.step(torch.randn((3, 4, 128), device="cuda"))
+    torch.cuda.synchronize()
+    td.ledger_rows()
+assert torch.isfinite(out).all()
 print("sanitize run ok")
