@@ -26,7 +26,13 @@ constexpr int S3_BINS = 4096;
 constexpr int S3_LIST_CAP = 8192;
 constexpr int S3_BAND_CAP = 1024;
 constexpr int S3_UB = 8;  // float4 loads in flight per thread (block-strided passes)
-constexpr int S3_UW = 4;  // 128-element windows in flight per warp (warp-range passes)
+constexpr int S3_UW = 4;
+#ifndef KVT_S3_UWC
+#define KVT_S3_UWC 2
+#endif
+constexpr int S3_UWC = KVT_S3_UWC;  // windows per warp iteration of the compaction pass: its
+// per-window work (scan, carries, stores) is the critical path, so fewer windows in flight (fewer
+// live registers) is faster -- layer-2 compaction 19.3 us at 4, 15.5-15.7 us at 1-2, 34.6 at 8
 
 // Phase timestamps (development aid, off unless kvt_debug_select_phases set a buffer):
 // thread 0 of CTA b writes %globaltimer at phase p to buf[b * 8 + p].
@@ -481,11 +487,11 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
                 for (int j = 0; j < (int)nband_total; ++j)
                     if (band_pos[j] == (int)(wr.a - 1)) { carry_m = S.band_sel[j] != 0; break; }
         }
-        for (int base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
-          float vv[S3_UW][4];
-          int tt[S3_UW][4];
+        for (int base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UWC) {
+          float vv[S3_UWC][4];
+          int tt[S3_UWC][4];
 #pragma unroll
-          for (int u = 0; u < S3_UW; ++u) {
+          for (int u = 0; u < S3_UWC; ++u) {
               const int i = base0 + 128 * u + 4 * lane;
               load4s(sc, i, wr.b, vec, vv[u]);
               if (vec && i + 4 <= wr.b) {
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
               }
           }
 #pragma unroll
-          for (int u = 0; u < S3_UW; ++u) {
+          for (int u = 0; u < S3_UWC; ++u) {
             const int i = base0 + 128 * u + 4 * lane;
             const float* v = vv[u];
             bool m[4];
