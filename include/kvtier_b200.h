@@ -296,6 +296,10 @@ typedef struct {
                                    values, abstracts and abs_mag of KV lane i / kv_group; keys/values/
                                    amax/amin/abs_mag then hold n_lanes / kv_group lanes.  Decode path
                                    (abs_mag, bf16 abstracts, f32 q) only */
+    float* sel_hint;            /* [n_lanes] f32 state carried across decode steps, or NULL: the bucket
+                                   coordinate of the lane's previous k-th estimate in the selector's
+                                   estimate histogram (NaN = none), read and rewritten by the selector;
+                                   a stale hint costs one extra pass, never exactness */
 } kvt_layer_args;
 
 /* K3 for the decode path (bounds_fast.cu): sound f32 bounds of raw dots over bf16 abstracts on a

@@ -47,7 +47,7 @@ class KvtLayerArgs(ctypes.Structure):
         ("run_start", _vp), ("run_len", _vp), ("n_runs", _vp),
         ("out", _vp), ("evals", _vp),
         ("attn_splits", _i32), ("score_blocks", _i32), ("exact_scores", _i32),
-        ("abs_mag", _vp), ("kv_group", _i32),
+        ("abs_mag", _vp), ("kv_group", _i32), ("sel_hint", _vp),
     ]
 
 

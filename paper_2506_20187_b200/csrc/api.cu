@@ -129,6 +129,11 @@ int& kv_group_tls() {
     return g;
 }
 
+float*& sel_hint_tls() {
+    static thread_local float* h = nullptr;
+    return h;
+}
+
 int& cand_group_tls() {
     static thread_local int g = 1;
     return g;
@@ -153,6 +158,7 @@ extern "C" int kvt_select_attend(const kvt_layer_args* a, void* ws, size_t ws_by
                     a->leaf_start || a->exact_scores || !kvt_fast_ok(a->key_dtype, a->d)))
         return KVT_ERR_ARG;  // GQA sharing runs on the decode path's kernels only
     KvGroupScope group_scope(kvg);
+    SelHintScope hint_scope(a->sel_hint);
     if (a->k < 0 || a->k > a->n) return KVT_ERR_K;
     if (a->n_lanes <= 0 || a->n <= 0) return a->n_lanes == 0 ? KVT_OK : KVT_ERR_ARG;
     if (!a->leaf_start && a->C < 1) return KVT_ERR_ARG;

@@ -398,6 +398,15 @@ inline int kv_group_current() { return kv_group_tls(); }
 // once per group, in the row of the group's first query lane; the selectors read row
 // (i / g) * g.  1 = one list per query lane.
 int& cand_group_tls();
+// Per-lane selection hints (the previous step's k-th estimate, kvt_layer_args.sel_hint) for the
+// K5 launches of kvt_select_attend on this host thread; nullptr = none.
+float*& sel_hint_tls();
+struct SelHintScope {
+    float* saved;
+    explicit SelHintScope(float* h) : saved(sel_hint_tls()) { sel_hint_tls() = h; }
+    ~SelHintScope() { sel_hint_tls() = saved; }
+};
+inline float* sel_hint_current() { return sel_hint_tls(); }
 struct CandGroupScope {
     int saved;
     explicit CandGroupScope(int g) : saved(cand_group_tls()) { cand_group_tls() = g > 1 ? g : 1; }

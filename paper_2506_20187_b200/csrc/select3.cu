@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     int64_t cand_stride, const double* __restrict__ rec, int64_t k, const QT* __restrict__ q,
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, double* __restrict__ scratch,
     int32_t* __restrict__ sel_tok, double* __restrict__ sel_score, int64_t sel_stride, int32_t* __restrict__ n_sel,
-    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs, int kvg, int tkg) {
+    int32_t* __restrict__ run_start, int32_t* __restrict__ run_len, int64_t run_stride, int32_t* __restrict__ n_runs, int kvg, int tkg,
+    float* __restrict__ hint) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ S3Shared S;
@@ -236,6 +237,37 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     const int n32 = (int)n;
     s3_mark(0);
 
+    // Hint (state carried across decode steps): the bucket coordinate of the lane's previous
+    // k-th estimate.  Its bucket stands in for the histogram's when the band is narrow: the merged pass below
+    // then also counts the elements above the bucket, and the hint is taken only if the k-th
+    // element really lies in that bucket; otherwise the histogram pass runs after all.
+    const bool narrow = 2.0 * E * inv <= 0.5;
+    int bstar = -1;
+    long long above = 0;
+    bool hinted = false;
+    // A hint that missed backs off for 63 steps (stored as -63 .. -1): fresh, uncorrelated
+    // queries every step pay the wasted pass once in 64 steps.
+    const float hv_in = hint ? hint[li] : NAN;
+    bool hint_missed = false;
+    if (hint && narrow) {
+        const float hv = hv_in;  // bucket coordinate of the previous k-th estimate
+        if (isfinite(hv) && hv >= 1.f && hv < (float)(S3_BINS - 1)) {
+            hinted = true;
+            bstar = (int)hv;
+        }
+    }
+    bool fallback = false, merged = false;
+    int bsel = -1;  // the k-th element's bucket (== bstar unless a hint was one bucket off)
+    double hb = 0.0, lb = 0.0;
+    const WarpRange4 wr(n, warp);
+    long long nsure = 0;
+    unsigned int nband_total = 0;
+    __shared__ long long w_list_sure[S3_WARPS];
+    __shared__ unsigned int s_cnt[5];
+    int LR = hinted ? 2 : 1;
+    for (;;) {
+    LR = hinted ? 2 : 1;
+    if (!hinted) {
     // ---- 1. bucket histogram of the estimates (4 per thread per iteration) ----
     for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
     if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; S.remaining = 0; }
@@ -259,20 +291,21 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     s3_mark(1);
     s3_find_bin(S, S.hist, S3_BINS, kk);
     s3_mark(2);
-    const int bstar = S.bstar;
-    const long long need_in_bucket = kk - S.above;
-    bool fallback = bstar < 0;
-    double hb = 0.0, lb = 0.0;
-    const WarpRange4 wr(n, warp);
-    long long nsure = 0;
-    unsigned int nband_total = 0;
+    bstar = S.bstar;
+    above = S.above;
+    } else {
+        if (tid == 0) { S.list_n = 0; S.remaining = 0; }
+        __syncthreads();
+    }
+    fallback = bstar < 0;
+    bsel = bstar;
+    nsure = 0;
     // Merged path: when the band [T - 2E, T + 2E] is narrower than half a bucket it lies in
     // buckets bstar-1..bstar+1, so ONE pass (in warp ranges) gathers those buckets' members
     // with their positions and counts the certainly-selected elements above them; T, the
     // band and the remaining sure counts then come from the short list.
-    const bool merged = !fallback && 2.0 * E * inv <= 0.5;
-    if (merged) {
-        __shared__ long long w_list_sure[S3_WARPS];
+    merged = !fallback && narrow;
+    if (!merged) break;
         if (lane == 0) w_list_sure[warp] = 0;
         for (int base0 = wr.a; base0 < wr.b; base0 += 128 * S3_UW) {
           float vv[S3_UW][4];
@@ -280,7 +313,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
           for (int u = 0; u < S3_UW; ++u) load4s(sc, base0 + 128 * u + 4 * lane, wr.b, vec, vv[u]);
           // flags of this lane's 4 x S3_UW elements as a bitmask; one warp scan + one atomic
           // per iteration place the list members (sure counts stay per lane until the end)
-          unsigned mbits = 0, cbits = 0;
+          // list = buckets bstar - LR .. bstar + LR (LR = 2 when hinted: the k-th may have moved
+          // one bucket since the hint; 1 otherwise); the bucket offset rides in bits 29..31
+          unsigned mbits = 0;
 #pragma unroll
           for (int u = 0; u < S3_UW; ++u) {
             const int i = base0 + 128 * u + 4 * lane;
@@ -288,9 +323,8 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             for (int e = 0; e < 4; ++e) {
                 const bool in = i + e < wr.b;
                 const int b = in ? s3_bucket(vv[u][e], lo_f, inv_f) : -1;
-                nsure += b > bstar + 1;
-                mbits |= (unsigned)(in && b >= bstar - 1 && b <= bstar + 1) << (4 * u + e);
-                cbits |= (unsigned)(b == bstar) << (4 * u + e);
+                nsure += b > bstar + LR;
+                mbits |= (unsigned)(in && b >= bstar - LR && b <= bstar + LR) << (4 * u + e);
             }
           }
           const int cnt = __popc(mbits);
@@ -311,8 +345,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
 #pragma unroll
                     for (int ee = 0; ee < 4; ++ee)
                         if (uu == u && ee == e) v = vv[uu][ee];
+                const uint32_t of = (uint32_t)(s3_bucket(v, lo_f, inv_f) - bstar + 2);  // 0 .. 4
                 lkey[slot] = ord_key32(v);
-                lpos[slot] = (int32_t)(i | ((cbits >> f) & 1 ? 0x40000000 : 0));
+                lpos[slot] = (int32_t)((uint32_t)i | (of << 29));
             }
             ++slot;
           }
@@ -321,6 +356,53 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         for (int off = 16; off >= 1; off >>= 1) nsure += __shfl_xor_sync(KVT_FULL, nsure, off);
         __syncthreads();
         s3_mark(3);
+        if (hinted) {
+            // per-bucket counts of the list; the k-th element's bucket bt must be one of
+            // bstar - 1 .. bstar + 1 (its band then stays inside the listed buckets)
+            if (tid < 5) s_cnt[tid] = 0;
+            if (lane == 0) w_sel[warp] = nsure;
+            __syncthreads();
+            const int lnh = (int)kvt::imin((long long)S.list_n, (long long)S3_LIST_CAP);
+            unsigned c[5] = {0, 0, 0, 0, 0};
+            for (int j = tid; j < lnh; j += S3_THREADS) {
+                const unsigned of = ((uint32_t)lpos[j] >> 29) & 7u;
+#pragma unroll
+                for (int o = 0; o < 5; ++o) c[o] += of == (unsigned)o;
+            }
+#pragma unroll
+            for (int o = 0; o < 5; ++o)
+                if (c[o]) atomicAdd(&s_cnt[o], c[o]);
+            __syncthreads();
+            long long ab = 0;  // elements above bucket bstar + 2
+            for (int w = 0; w < S3_WARPS; ++w) ab += w_sel[w];
+            int bt = -1;
+            if (S.list_n <= (unsigned)S3_LIST_CAP) {
+                ab += s_cnt[4];  // now: above bucket bstar + 1
+                for (int o = 3; o >= 1; --o) {  // bucket bstar + 1, bstar, bstar - 1
+                    if (ab < kk && kk <= ab + (long long)s_cnt[o]) { bt = bstar + o - 2; break; }
+                    ab += s_cnt[o];
+                }
+            }
+            __syncthreads();  // w_sel / counters read by every thread before any reuse
+            if (bt < 0) {  // the k-th element moved more than one bucket: histogram after all
+                hinted = false;
+                hint_missed = true;
+                continue;
+            }
+            above = 0;  // recomputed below for bucket bt
+            {
+                long long a2 = 0;
+                for (int w = 0; w < S3_WARPS; ++w) a2 += w_sel[w];
+                for (int o = 4; o > bt - bstar + 2; --o) a2 += s_cnt[o];
+                above = a2;
+            }
+            bsel = bt;
+        }
+        break;
+    }
+    const long long need_in_bucket = kk - above;
+    float hint_out = NAN;  // this step's k-th estimate: the next step's hint (merged path only)
+    if (merged) {
         const int ln = (int)S.list_n;
         if (ln > S3_LIST_CAP) {
             fallback = true;
@@ -334,7 +416,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             __syncthreads();
             for (int j0 = 0; j0 < ln; j0 += S3_THREADS) {
                 const int j = j0 + tid;
-                const bool m = j < ln && (lpos[j] & 0x40000000);
+                const bool m = j < ln && ((((uint32_t)lpos[j] >> 29) & 7u) == (uint32_t)(bsel - bstar + 2));
                 const unsigned ballot = __ballot_sync(KVT_FULL, m);
                 unsigned wb = 0;
                 if (lane == 0 && ballot) wb = atomicAdd(&s_nb, (unsigned)__popc(ballot));
@@ -348,6 +430,9 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             if (tid == 0) S.list_n = 0;  // reused as the band counter
             __syncthreads();
             const double Tk = (double)key32_to_float(T32m);
+            // kept as a bucket coordinate, (T - lo) / width: invariant to a rescaled query (the
+            // range [tau - 2E, Umax + 2E] scales with it), so the hint survives gain changes
+            if (!fallback) hint_out = (float)((Tk - lo) * inv);
             hb = Tk + 2.0 * E;
             lb = Tk - 2.0 * E;
             // sure list members counted into their owner warp's range (WarpRange4 spans of
@@ -355,7 +440,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128;
             for (int j = tid; j < ln; j += S3_THREADS) {
                 const double sv = (double)key32_to_float(lkey[j]);
-                const int pj = lpos[j] & 0x3fffffff;
+                const int pj = lpos[j] & 0x1fffffff;
                 if (sv > hb) {
                     const int ow = (int)kvt::imin(S3_WARPS - 1, pj / per);
                     atomicAdd(reinterpret_cast<unsigned long long*>(&w_list_sure[ow]), 1ull);
@@ -460,6 +545,8 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     }
     __syncthreads();
     s3_mark(5);
+    if (hint && tid == 0)
+        hint[li] = hint_missed ? -63.f : (hv_in < -1.5f ? hv_in + 1.f : (fallback ? NAN : hint_out));
     if (!fallback) {
         // ---- 4. stable compaction: per-warp offsets, lane-level scan inside each window ----
         long long extra = 0;  // selected band members inside this warp's range
@@ -785,7 +872,8 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
         configured = true;
     }
     launch_pdl(topk_select3_kernel<QT, T>, dim3((unsigned)n_lanes), dim3(S3_THREADS), smem, st, cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
-        sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current(), cand_group_current());
+        sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current(), cand_group_current(),
+        sel_hint_current());
     return kvt_check_launch();
 }
 

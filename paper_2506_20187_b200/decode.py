@@ -232,6 +232,8 @@ class SparseDecoder:
                 "n_runs": torch.empty(lanes, dtype=torch.int32, device=dev),
                 "out": torch.empty((lanes, d), dtype=torch.float32, device=dev),
                 "evals": torch.empty(lanes, dtype=torch.int64, device=dev),
+                # the previous step's k-th estimate per lane (state across steps; NaN = none)
+                "sel_hint": torch.full((lanes,), float("nan"), dtype=torch.float32, device=dev),
             })
         maxl = max(ops.n_grid_leaves(self.n_cap, C) for C in self.C)
         if self._ws is None or self._ws.key != (lanes, self.n_cap, maxl, d):

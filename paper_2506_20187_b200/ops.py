@@ -546,6 +546,7 @@ def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch
     a.attn_splits, a.score_blocks, a.exact_scores = attn_splits, score_blocks, int(exact_scores)
     a.abs_mag = _p(abs_mag)
     a.kv_group = max(kv_group, 1)
+    a.sel_hint = _p(out.get("sel_hint"))
     L.check(L.kvt_select_attend(a, ws.buf.data_ptr(), ws.bytes, _stream()), "select_attend")
 
 

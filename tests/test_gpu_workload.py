@@ -95,3 +95,43 @@ def test_decoder_config3_shape_matches_oracle(O):
             assert np.array_equal(np.sort(sel[i].astype(np.int64)), ref), (l, i)
             att = O.attention(Q[1, l, i], Kd, Vd, ref)
             assert np.linalg.norm(o[i] - att) / np.linalg.norm(att) <= 2e-3, (l, i)
+
+
+@pytest.mark.parametrize("dtype", ["int4", "bf16"])
+def test_selection_hints_across_steps_stay_exact(O, dtype):
+    """The selector's per-lane hint (the previous step's k-th estimate, kvt_layer_args.sel_hint)
+    is state carried across steps: repeated queries take the hinted bucket, changed ones miss it
+    and fall back to the histogram.  Every step selects the oracle's exact set either way."""
+    from paper_2506_20187_b200 import ops
+    from paper_2506_20187_b200.decode import SparseDecoder
+    L_, H, n, d = 2, 8, 16384, 128
+    dt = ops.I4 if dtype == "int4" else torch.bfloat16
+    dec = SparseDecoder(L_, 1, H, d, n, dtype=dt, importance_rate=0.1, early_layer_rate=0.1)
+    g = W.gen_args(None, d, "planted")
+    ps, Kd = [], []
+    for l in range(L_):
+        p = W.lane_params(5, l, np.arange(H), n, d, "planted")
+        ps.append(p)
+        K = torch.empty((H, n, d), dtype=torch.bfloat16, device="cuda")
+        V = torch.empty_like(K)
+        ops.synth_layer(K, V, p, n, g)
+        dec.load_layer(l, K, V)
+        if dtype == "int4":
+            Kd.append(np.stack([O.i4_dequant(dec.K.data[l, i, :n].cpu().numpy(), d) for i in range(H)]))
+        else:
+            Kd.append(dec.K[l, :, :n].float().cpu().numpy())
+    dec.set_length(n)
+    planted = np.stack([W.queries(5, 1, l, np.arange(H), 1, ps[l]["u"], 0, d, "planted")[0] for l in range(L_)])
+    rng = np.random.default_rng(1)
+    steps = [planted, planted, planted + 0.3 * rng.standard_normal(planted.shape).astype(np.float32),
+             rng.standard_normal(planted.shape).astype(np.float32), planted]
+    for s, qh in enumerate(steps):
+        dec.step(torch.from_numpy(qh).cuda())
+        torch.cuda.synchronize()
+        for l in range(L_):
+            b = dec._buffers()[l]
+            k = dec.k_for(l)
+            sel = b["sel_tok"][:, :k].cpu().numpy()
+            for i in range(H):
+                ref = O.select(qh[l, i], Kd[l][i], k)
+                assert np.array_equal(np.sort(sel[i].astype(np.int64)), ref), (dtype, s, l, i)
