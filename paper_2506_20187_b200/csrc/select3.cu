@@ -760,25 +760,49 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         int32_t* rs = run_start + li * run_stride;
         int32_t* rl = run_len + li * run_stride;
         const unsigned le_mask = (2u << lane) - 1u;
-        for (long long p = pa + lane; p - lane < pb; p += 32) {
-            const bool h = p < pb && hflag[p];
-            const unsigned hm = __ballot_sync(KVT_FULL, h);
-            if (h) {
-                const long long r = r0 + __popc(hm & le_mask) - 1;
-                rs[r] = otok[p];
-                rl[r] = (int32_t)p;  // start position; turned into a length below
+        // One pass: a run's length is the distance to the next head, found in the same 32-wide
+        // window (ballot bits) or, for a window's last head, at the next window's first head;
+        // the warp's last run ends at the next warp's first head (or k), set after a barrier.
+        // Head tokens are loaded RU windows at a time (no read-after-write chains).
+        constexpr int RU = 4;
+        __shared__ long long w_first_hp[S3_WARPS];
+        long long r = r0, r_last = -1, p_last = -1, first_hp = -1;
+        for (long long p0 = pa; p0 < pb; p0 += 32 * RU) {
+            bool h[RU];
+            int t[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const long long p = p0 + 32 * u + lane;
+                h[u] = p < pb && hflag[p];
             }
-            r0 += __popc(hm);
+#pragma unroll
+            for (int u = 0; u < RU; ++u) t[u] = h[u] ? otok[p0 + 32 * u + lane] : 0;
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const unsigned hm = __ballot_sync(KVT_FULL, h[u]);
+                if (!hm) continue;  // warp-uniform
+                const long long wbase = p0 + 32 * u;
+                if (h[u]) {
+                    const long long idx = r + __popc(hm & le_mask) - 1;
+                    rs[idx] = t[u];
+                    const unsigned above = hm & ~le_mask;
+                    if (above) rl[idx] = (int32_t)(__ffs(above) - 1 - lane);
+                }
+                const long long pf = wbase + __ffs(hm) - 1;
+                if (lane == 0 && r_last >= 0) rl[r_last] = (int32_t)(pf - p_last);
+                if (first_hp < 0) first_hp = pf;
+                p_last = wbase + 31 - __clz(hm);
+                r += __popc(hm);
+                r_last = r - 1;
+            }
         }
+        if (lane == 0) w_first_hp[warp] = first_hp;
         __syncthreads();
-        const long long per_r = (tot_h + S3_THREADS - 1) / S3_THREADS;
-        const long long ra = kvt::imin(tot_h, tid * per_r), rb = kvt::imin(tot_h, ra + per_r);
-        int32_t nxt = rb < tot_h ? rl[rb] : (int32_t)kk;  // read before any length is written
-        __syncthreads();
-        for (long long r = rb - 1; r >= ra; --r) {
-            const int32_t st = rl[r];
-            rl[r] = nxt - st;
-            nxt = st;
+        if (lane == 0 && r_last >= 0) {
+            long long nx = kk;
+            for (int w = warp + 1; w < S3_WARPS; ++w)
+                if (w_first_hp[w] >= 0) { nx = w_first_hp[w]; break; }
+            rl[r_last] = (int32_t)(nx - p_last);
         }
         if (tid == 0) n_runs[li] = (int32_t)tot_h;
         s3_mark(7);
