@@ -95,7 +95,7 @@ constexpr int TS_CONSUMERS = 8;
 constexpr int TS_THREADS = (TS_CONSUMERS + 1) * 32;
 
 // AccT = double: canonical f64 dots (the exact definition); AccT = float: the fast f32
-// estimate written to out32 (select2.cu brackets it with a rigorous error bound and
+// estimate written to out32 (select3.cu brackets it with a rigorous error bound and
 // re-scores the few tokens near the k-th value in f64, so the selected set stays exact).
 template <typename QT, typename T, int G, bool IMPLICIT, typename AccT>
 __global__ void __launch_bounds__(TS_THREADS, 3) score_tma_kernel(
@@ -460,7 +460,7 @@ extern "C" int kvt_token_scores(const void* q, int q_dtype, const void* keys, in
                                 nullptr, out_stride, blocks, 1, (cudaStream_t)stream);
 }
 
-// Fast f32 candidate scores (select2.cu pairs them with an error bound): float keys of
+// Fast f32 candidate scores (select3.cu pairs them with an error bound): float keys of
 // every dtype except f64; requires the TMA path.
 template <typename QT, typename T>
 static int fast_t(const void* q, const void* keys, int64_t n_lanes, int64_t lane_stride, int d, const int32_t* items,

@@ -19,7 +19,7 @@
 // rounding), the digit residual q - qt, the canonical dot's own f64 rounding and the fp32
 // rounding of the dequantised element the canonical dot sees; W_g per lane and group comes
 // from kvt_i4_qprep.  The per-lane max of e(t) is atomically max-ed into err[4 lane + 3], where
-// the band select (select2/select3) takes it as E: the band is then a few ulps wide and the
+// the band select (select3) takes it as E: the band is then a few ulps wide and the
 // selected set stays the exact canonical top-k.
 //
 // Dataflow: the persistent TMA ring of score.cu (one producer thread issuing cp.async.bulk

@@ -873,11 +873,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
 
 using namespace kvt;
 
-int kvt_topk_select_band_cluster(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
-                                 const double* err, int64_t n_lanes, int64_t k, const void* q, int q_dtype,
-                                 const void* keys, int key_dtype, int64_t lane_stride, int d, int32_t* sel_tok,
-                                 double* sel_score, int64_t sel_stride, int32_t* n_sel, int32_t* run_start,
-                                 int32_t* run_len, int64_t run_stride, int32_t* n_runs, void* stream);
+
 
 template <typename QT, typename T>
 static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
@@ -918,12 +914,6 @@ extern "C" int kvt_topk_select_band(const float* cs32, const int32_t* ctok, cons
     if (k < 0) return KVT_ERR_K;
     if (n_lanes == 0) return KVT_OK;
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
-    // very few lanes: one CTA per lane would leave most SMs idle -> cluster of CTAs per lane
-    const int sms = kvt::sm_count();
-    if (n_lanes * 4 < sms && cand_stride >= 8192 && cand_stride <= 8 * 20480 && n_lanes <= 65535)
-        return kvt_topk_select_band_cluster(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, q_dtype, keys,
-                                            key_dtype, lane_stride, d, sel_tok, sel_score, sel_stride, n_sel,
-                                            run_start, run_len, run_stride, n_runs, stream);
 #define KVT_S(QT, TT) return launch_select3<QT, TT>(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, keys, lane_stride, d, scratch, sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, st)
     if (q_dtype == KVT_F32) {
         switch (key_dtype) {

@@ -22,7 +22,7 @@ for dt in (ops.I4, torch.bfloat16):
     out = dec.step(q)
     torch.cuda.synchronize()
     assert torch.isfinite(out).all()
-# few lanes, long context: the cluster select path (select2.cu)
+# few lanes, long context
 kt = torch.randn((2, 16384, 128), device="cuda", dtype=torch.bfloat16)
 amax, amin = ops.abstract_build(kt, 16384, 64)
 ws = ops.LayerWorkspace(2, 16384, ops.n_grid_leaves(16384, 64), 128, kt.device)
