@@ -20,8 +20,9 @@
 
 namespace kvt {
 
-constexpr int S3_THREADS = 512;  // two CTAs per SM: a 256-lane layer is one wave
-constexpr int S3_WARPS = S3_THREADS / 32;
+constexpr int S3_THREADS_MAX = 1024;  // CTA size: 512 (two CTAs per SM: a 256-lane layer is one
+// wave) or 1024 when the layer has fewer lanes than SMs (each lane's passes split over 32 warps)
+constexpr int S3_WARPS_MAX = S3_THREADS_MAX / 32;
 constexpr int S3_BINS = 4096;
 constexpr int S3_LIST_CAP = 8192;
 constexpr int S3_BAND_CAP = 1024;
@@ -53,7 +54,7 @@ struct S3Shared {
     unsigned char band_sel[S3_BAND_CAP];
     unsigned int rh[256];
     long long scan_sh[33];
-    long long warp_cnt[S3_WARPS];
+    long long warp_cnt[S3_WARPS_MAX];
     unsigned long long prefix, mask;
     unsigned int list_n, remaining;
     int bstar;
@@ -70,9 +71,10 @@ __device__ __forceinline__ int s3_bucket(float s, float lo, float inv) {
 
 // Block-wide: find the digit bin of `hist` (nb bins, descending order) where the running
 // count from the top reaches `want`; returns (bin, count strictly above it) via S.
+template <int NT>
 __device__ __forceinline__ void s3_find_bin(S3Shared& S, const unsigned int* hist, int nb, long long want) {
     const int tid = threadIdx.x;
-    const int per = (nb + S3_THREADS - 1) / S3_THREADS;
+    const int per = (nb + NT - 1) / NT;
     long long loc = 0;
     for (int j = 0; j < per; ++j) {
         const int b = nb - 1 - (tid * per + j);
@@ -99,10 +101,11 @@ __device__ __forceinline__ void s3_find_bin(S3Shared& S, const unsigned int* his
 // Radix select on the shared list of 32-bit keys: exact key of the `want`-th largest.
 // Short lists (the usual case: one of 4096 buckets) are ranked by counting instead: one
 // barrier instead of four radix rounds.
+template <int NT>
 __device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* keys, int n, long long want) {
     const int tid = threadIdx.x, lane = tid & 31;
     if (n <= 128) {
-        for (int j = tid; j < n; j += S3_THREADS) {
+        for (int j = tid; j < n; j += NT) {
             const uint32_t kj = keys[j];
             int gt = 0, eq = 0;
             for (int f = 0; f < n; ++f) {
@@ -118,10 +121,10 @@ __device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* 
     if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)want; }
     __syncthreads();
     for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int i = tid; i < 256; i += S3_THREADS) S.rh[i] = 0;
+        for (int i = tid; i < 256; i += NT) S.rh[i] = 0;
         __syncthreads();
         const uint32_t pf = (uint32_t)S.prefix, mk = (uint32_t)S.mask;
-        for (int base = 0; base < n; base += S3_THREADS) {
+        for (int base = 0; base < n; base += NT) {
             const int i = base + tid;
             int dg = 256;
             if (i < n && (keys[i] & mk) == pf) dg = (keys[i] >> shift) & 0xff;
@@ -156,10 +159,11 @@ __device__ __forceinline__ uint32_t s3_list_select(S3Shared& S, const uint32_t* 
 
 // Stable warp-ballot compaction helper: warp w owns the contiguous range
 // [w*per, (w+1)*per) of [0, n) and walks it 32 elements at a time.
+template <int NW>
 struct WarpRange {
     int64_t a, b;
     __device__ WarpRange(int64_t n, int warp) {
-        const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 31) / 32 * 32;
+        const int64_t per = ((n + NW - 1) / NW + 31) / 32 * 32;
         a = kvt::imin(n, warp * per);
         b = kvt::imin(n, a + per);
     }
@@ -180,10 +184,11 @@ __device__ __forceinline__ double s3_canon(const QT* q, const unsigned char* row
 
 // Per-warp contiguous ranges in units of 128 elements (32 lanes x float4), so a warp's
 // iteration covers 128 consecutive candidates and lane l owns elements 4l..4l+3 of it.
+template <int NW>
 struct WarpRange4 {
     int a, b;  // candidate counts are < 2^31: 32-bit indices in the hot loops
     __device__ WarpRange4(int64_t n, int warp) {
-        const int per = (int)(((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128);
+        const int per = (int)(((n + NW - 1) / NW + 127) / 128 * 128);
         a = (int)kvt::imin(n, (int64_t)warp * per);
         b = (int)kvt::imin(n, (int64_t)a + per);
     }
@@ -199,8 +204,8 @@ __device__ __forceinline__ void load4s(const float* sc, int i, int end, bool vec
     }
 }
 
-template <typename QT, typename T>
-__global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
+template <typename QT, typename T, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) topk_select3_kernel(
     const float* __restrict__ cs32, const int32_t* __restrict__ ctok, const int32_t* __restrict__ n_cand,
     int64_t cand_stride, const double* __restrict__ rec, int64_t k, const QT* __restrict__ q,
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int row_b, int d, double* __restrict__ scratch,
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     pdl_entry();
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ S3Shared S;
-    __shared__ long long w_sel[S3_WARPS];
+    __shared__ long long w_sel[(NT / 32)];
     __shared__ int band_pos[S3_BAND_CAP];
     uint32_t* lkey = reinterpret_cast<uint32_t*>(dyn_smem);
     int32_t* lpos = reinterpret_cast<int32_t*>(dyn_smem + (size_t)S3_LIST_CAP * 4);  // merged path only
@@ -259,27 +264,27 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     bool fallback = false, merged = false;
     int bsel = -1;  // the k-th element's bucket (== bstar unless a hint was one bucket off)
     double hb = 0.0, lb = 0.0;
-    const WarpRange4 wr(n, warp);
+    const WarpRange4<NT / 32> wr(n, warp);
     long long nsure = 0;
     unsigned int nband_total = 0;
-    __shared__ long long w_list_sure[S3_WARPS];
+    __shared__ long long w_list_sure[(NT / 32)];
     __shared__ unsigned int s_cnt[5];
     int LR = hinted ? 2 : 1;
     for (;;) {
     LR = hinted ? 2 : 1;
     if (!hinted) {
     // ---- 1. bucket histogram of the estimates (4 per thread per iteration) ----
-    for (int i = tid; i < S3_BINS; i += S3_THREADS) S.hist[i] = 0;
+    for (int i = tid; i < S3_BINS; i += NT) S.hist[i] = 0;
     if (tid == 0) { S.list_n = 0; S.bstar = -1; S.above = 0; S.remaining = 0; }
     __syncthreads();
     // passes over the estimates batch S3_UB float4 loads per thread (memory-level parallelism)
-    for (int base = 0; base < n32; base += S3_UB * 4 * S3_THREADS) {
+    for (int base = 0; base < n32; base += S3_UB * 4 * NT) {
         float v[S3_UB][4];
 #pragma unroll
-        for (int u = 0; u < S3_UB; ++u) load4s(sc, base + (u * S3_THREADS + tid) * 4, n32, vec, v[u]);
+        for (int u = 0; u < S3_UB; ++u) load4s(sc, base + (u * NT + tid) * 4, n32, vec, v[u]);
 #pragma unroll
         for (int u = 0; u < S3_UB; ++u) {
-            const int i = base + (u * S3_THREADS + tid) * 4;
+            const int i = base + (u * NT + tid) * 4;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int bkt = i + e < n32 ? s3_bucket(v[u][e], lo_f, inv_f) : -1;
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     }
     __syncthreads();
     s3_mark(1);
-    s3_find_bin(S, S.hist, S3_BINS, kk);
+    s3_find_bin<NT>(S, S.hist, S3_BINS, kk);
     s3_mark(2);
     bstar = S.bstar;
     above = S.above;
@@ -364,7 +369,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             __syncthreads();
             const int lnh = (int)kvt::imin((long long)S.list_n, (long long)S3_LIST_CAP);
             unsigned c[5] = {0, 0, 0, 0, 0};
-            for (int j = tid; j < lnh; j += S3_THREADS) {
+            for (int j = tid; j < lnh; j += NT) {
                 const unsigned of = ((uint32_t)lpos[j] >> 29) & 7u;
 #pragma unroll
                 for (int o = 0; o < 5; ++o) c[o] += of == (unsigned)o;
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
                 if (c[o]) atomicAdd(&s_cnt[o], c[o]);
             __syncthreads();
             long long ab = 0;  // elements above bucket bstar + 2
-            for (int w = 0; w < S3_WARPS; ++w) ab += w_sel[w];
+            for (int w = 0; w < (NT / 32); ++w) ab += w_sel[w];
             int bt = -1;
             if (S.list_n <= (unsigned)S3_LIST_CAP) {
                 ab += s_cnt[4];  // now: above bucket bstar + 1
@@ -392,7 +397,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             above = 0;  // recomputed below for bucket bt
             {
                 long long a2 = 0;
-                for (int w = 0; w < S3_WARPS; ++w) a2 += w_sel[w];
+                for (int w = 0; w < (NT / 32); ++w) a2 += w_sel[w];
                 for (int o = 4; o > bt - bstar + 2; --o) a2 += s_cnt[o];
                 above = a2;
             }
@@ -414,7 +419,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             __shared__ unsigned int s_nb;
             if (tid == 0) s_nb = 0;
             __syncthreads();
-            for (int j0 = 0; j0 < ln; j0 += S3_THREADS) {
+            for (int j0 = 0; j0 < ln; j0 += NT) {
                 const int j = j0 + tid;
                 const bool m = j < ln && ((((uint32_t)lpos[j] >> 29) & 7u) == (uint32_t)(bsel - bstar + 2));
                 const unsigned ballot = __ballot_sync(KVT_FULL, m);
@@ -426,7 +431,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             }
             __syncthreads();  // every thread has read list_n before it is reset
             if (s_nb > (unsigned)S3_BINS) fallback = true;  // (block-uniform)
-            const uint32_t T32m = fallback ? 0u : s3_list_select(S, bkey, (int)s_nb, need_in_bucket);
+            const uint32_t T32m = fallback ? 0u : s3_list_select<NT>(S, bkey, (int)s_nb, need_in_bucket);
             if (tid == 0) S.list_n = 0;  // reused as the band counter
             __syncthreads();
             const double Tk = (double)key32_to_float(T32m);
@@ -437,12 +442,12 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             lb = Tk - 2.0 * E;
             // sure list members counted into their owner warp's range (WarpRange4 spans of
             // `per` elements); band members appended
-            const int64_t per = ((n + S3_WARPS - 1) / S3_WARPS + 127) / 128 * 128;
-            for (int j = tid; j < ln; j += S3_THREADS) {
+            const int64_t per = ((n + (NT / 32) - 1) / (NT / 32) + 127) / 128 * 128;
+            for (int j = tid; j < ln; j += NT) {
                 const double sv = (double)key32_to_float(lkey[j]);
                 const int pj = lpos[j] & 0x1fffffff;
                 if (sv > hb) {
-                    const int ow = (int)kvt::imin(S3_WARPS - 1, pj / per);
+                    const int ow = (int)kvt::imin((NT / 32) - 1, pj / per);
                     atomicAdd(reinterpret_cast<unsigned long long*>(&w_list_sure[ow]), 1ull);
                 } else if (sv >= lb) {
                     const unsigned slot = atomicAdd(&S.list_n, 1u);
@@ -455,13 +460,13 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     }
     if (!merged && !fallback) {
     // ---- 2. gather the k-th bucket (unordered) ----
-    for (int base0 = 0; base0 < n32; base0 += S3_UB * 4 * S3_THREADS) {
+    for (int base0 = 0; base0 < n32; base0 += S3_UB * 4 * NT) {
       float vv[S3_UB][4];
 #pragma unroll
-      for (int u = 0; u < S3_UB; ++u) load4s(sc, base0 + (u * S3_THREADS + tid) * 4, n32, vec, vv[u]);
+      for (int u = 0; u < S3_UB; ++u) load4s(sc, base0 + (u * NT + tid) * 4, n32, vec, vv[u]);
 #pragma unroll
       for (int u = 0; u < S3_UB; ++u) {
-        const int i = base0 + (u * S3_THREADS + tid) * 4;
+        const int i = base0 + (u * NT + tid) * 4;
         const float* v = vv[u];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     __syncthreads();
     fallback = S.list_n > S3_LIST_CAP;
     if (!fallback) {
-        const uint32_t T32 = s3_list_select(S, lkey, (int)S.list_n, need_in_bucket);
+        const uint32_t T32 = s3_list_select<NT>(S, lkey, (int)S.list_n, need_in_bucket);
         const double Tk = (double)key32_to_float(T32);
         hb = Tk + 2.0 * E;
         lb = Tk - 2.0 * E;
@@ -520,17 +525,17 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         __syncthreads();
         nband_total = S.list_n;
         long long tot_sure = 0;
-        for (int w = 0; w < S3_WARPS; ++w) tot_sure += w_sel[w];
+        for (int w = 0; w < (NT / 32); ++w) tot_sure += w_sel[w];
         const long long need = kk - tot_sure;
         if (nband_total > (unsigned)S3_BAND_CAP) {
             fallback = true;
         } else {
-            for (int j = warp; j < (int)nband_total; j += S3_WARPS) {
+            for (int j = warp; j < (int)nband_total; j += (NT / 32)) {
                 const double c = s3_canon<QT, T>(ql, kl + (int64_t)S.band_t[j] * row_b, d, lane);
                 if (lane == 0) S.band_c[j] = c;
             }
             __syncthreads();
-            for (int j = tid; j < (int)nband_total; j += S3_THREADS) {
+            for (int j = tid; j < (int)nband_total; j += NT) {
                 const double cj = S.band_c[j];
                 const int tj = S.band_t[j];
                 long long better = 0;
@@ -636,7 +641,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     } else {
         // ---- exact fallback: canonical f64 for every candidate, 64-bit radix select ----
         double* sc64 = scratch + li * cand_stride;
-        for (int64_t base = (int64_t)warp * 8; base < n; base += (int64_t)S3_WARPS * 8) {
+        for (int64_t base = (int64_t)warp * 8; base < n; base += (int64_t)(NT / 32) * 8) {
             double p[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -661,10 +666,10 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         if (tid == 0) { S.prefix = 0; S.mask = 0; S.remaining = (unsigned)kk; }
         __syncthreads();
         for (int shift = 56; shift >= 0; shift -= 8) {
-            for (int i = tid; i < 256; i += S3_THREADS) S.rh[i] = 0;
+            for (int i = tid; i < 256; i += NT) S.rh[i] = 0;
             __syncthreads();
             const unsigned long long pf = S.prefix, mk = S.mask;
-            for (int64_t base = 0; base < n; base += S3_THREADS) {
+            for (int64_t base = 0; base < n; base += NT) {
                 const int64_t i = base + tid;
                 int dg = 256;
                 if (i < n) {
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         const uint64_t T64 = S.prefix;
         const long long eq_take_total = S.remaining;
         // per-warp counts of (key > T) and ties, in warp-range order
-        const WarpRange w1(n, warp);
+        const WarpRange<NT / 32> w1(n, warp);
         long long c_gt = 0, c_eq = 0;
         for (int64_t base = w1.a; base < w1.b; base += 32) {
             const int64_t i = base + lane;
@@ -709,7 +714,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
             c_gt += __popc(__ballot_sync(KVT_FULL, i < w1.b && key > T64));
             c_eq += __popc(__ballot_sync(KVT_FULL, i < w1.b && key == T64));
         }
-        __shared__ long long w_eq[S3_WARPS], w_gt[S3_WARPS];
+        __shared__ long long w_eq[(NT / 32)], w_gt[(NT / 32)];
         if (lane == 0) { w_eq[warp] = c_eq; w_gt[warp] = c_gt; }
         __syncthreads();
         long long eq_before = 0, pos = 0;
@@ -744,7 +749,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         // ---- 5. runs from the head flags (shared memory): count, block prefix, write ----
         __syncthreads();
         const unsigned char* hflag = dyn_smem;
-        const long long per_w = ((kk + S3_WARPS - 1) / S3_WARPS + 31) / 32 * 32;
+        const long long per_w = ((kk + (NT / 32) - 1) / (NT / 32) + 31) / 32 * 32;
         const long long pa = kvt::imin(kk, warp * per_w), pb = kvt::imin(kk, pa + per_w);
         long long nh = 0;
         for (long long p = pa + lane; p - lane < pb; p += 32)
@@ -753,7 +758,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         if (lane == 0) w_sel[warp] = nh;
         __syncthreads();
         long long r0 = 0, tot_h = 0;
-        for (int w = 0; w < S3_WARPS; ++w) {
+        for (int w = 0; w < (NT / 32); ++w) {
             if (w < warp) r0 += w_sel[w];
             tot_h += w_sel[w];
         }
@@ -765,7 +770,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         // the warp's last run ends at the next warp's first head (or k), set after a barrier.
         // Head tokens are loaded RU windows at a time (no read-after-write chains).
         constexpr int RU = 4;
-        __shared__ long long w_first_hp[S3_WARPS];
+        __shared__ long long w_first_hp[(NT / 32)];
         long long r = r0, r_last = -1, p_last = -1, first_hp = -1;
         for (long long p0 = pa; p0 < pb; p0 += 32 * RU) {
             bool h[RU];
@@ -800,7 +805,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         __syncthreads();
         if (lane == 0 && r_last >= 0) {
             long long nx = kk;
-            for (int w = warp + 1; w < S3_WARPS; ++w)
+            for (int w = warp + 1; w < (NT / 32); ++w)
                 if (w_first_hp[w] >= 0) { nx = w_first_hp[w]; break; }
             rl[r_last] = (int32_t)(nx - p_last);
         }
@@ -817,7 +822,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
     __syncthreads();
     {
         constexpr int RU = 4;
-        const long long per_w = ((kk + S3_WARPS - 1) / S3_WARPS + 31) / 32 * 32;
+        const long long per_w = ((kk + (NT / 32) - 1) / (NT / 32) + 31) / 32 * 32;
         const long long wa = kvt::imin(kk, warp * per_w), wb = kvt::imin(kk, wa + per_w);
         int32_t* rs = run_start + li * run_stride;
         int32_t* rl = run_len + li * run_stride;
@@ -837,7 +842,7 @@ __global__ void __launch_bounds__(S3_THREADS, 2) topk_select3_kernel(
         if (lane == 0) w_sel[warp] = nh;
         __syncthreads();
         long long base_r = 0, tot_h = 0;
-        for (int w = 0; w < S3_WARPS; ++w) {
+        for (int w = 0; w < (NT / 32); ++w) {
             if (w < warp) base_r += w_sel[w];
             tot_h += w_sel[w];
         }
@@ -875,6 +880,29 @@ using namespace kvt;
 
 
 
+template <typename QT, typename T, int NT>
+static int launch_select3_nt(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
+                             const double* rec, int64_t n_lanes, int64_t k, const void* q, const void* keys,
+                             int64_t ls_b, int row_b, int d, double* scratch, int32_t* sel_tok, double* sel_score,
+                             int64_t sel_stride, int32_t* n_sel, int32_t* run_start, int32_t* run_len,
+                             int64_t run_stride, int32_t* n_runs, cudaStream_t st) {
+    const size_t smem = (size_t)S3_LIST_CAP * 8;  // list keys + positions
+    KVT_PER_DEVICE(bool, configured);
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(topk_select3_kernel<QT, T, NT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return kvt_set_cuda_error(e);
+        configured = true;
+    }
+    launch_pdl(topk_select3_kernel<QT, T, NT>, dim3((unsigned)n_lanes), dim3(NT), smem, st, cs32, ctok, n_cand,
+               cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch, sel_tok,
+               sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current(),
+               cand_group_current(), sel_hint_current());
+    return kvt_check_launch();
+}
+
+// Fewer lanes than SMs: 1024-thread CTAs (one per SM) split each lane's passes over 32 warps;
+// otherwise 512 (two per SM).
 template <typename QT, typename T>
 static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t* n_cand, int64_t cand_stride,
                           const double* rec, int64_t n_lanes, int64_t k, const void* q, const void* keys,
@@ -883,18 +911,13 @@ static int launch_select3(const float* cs32, const int32_t* ctok, const int32_t*
                           int64_t run_stride, int32_t* n_runs, cudaStream_t st) {
     const int row_b = RowLd<T>::row_bytes(d);
     const int64_t ls_b = std::is_same<T, I4>::value ? lane_stride : lane_stride * (int64_t)sizeof(T);
-    const size_t smem = (size_t)S3_LIST_CAP * 8;  // list keys + positions
-    KVT_PER_DEVICE(bool, configured);
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(topk_select3_kernel<QT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return kvt_set_cuda_error(e);
-        configured = true;
-    }
-    launch_pdl(topk_select3_kernel<QT, T>, dim3((unsigned)n_lanes), dim3(S3_THREADS), smem, st, cs32, ctok, n_cand, cand_stride, rec, k, (const QT*)q, (const unsigned char*)keys, ls_b, row_b, d, scratch,
-        sel_tok, sel_score, sel_stride, n_sel, run_start, run_len, run_stride, n_runs, kv_group_current(), cand_group_current(),
-        sel_hint_current());
-    return kvt_check_launch();
+    if (n_lanes < kvt::sm_count())
+        return launch_select3_nt<QT, T, 1024>(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, keys, ls_b, row_b,
+                                              d, scratch, sel_tok, sel_score, sel_stride, n_sel, run_start, run_len,
+                                              run_stride, n_runs, st);
+    return launch_select3_nt<QT, T, 512>(cs32, ctok, n_cand, cand_stride, rec, n_lanes, k, q, keys, ls_b, row_b, d,
+                                         scratch, sel_tok, sel_score, sel_stride, n_sel, run_start, run_len,
+                                         run_stride, n_runs, st);
 }
 
 extern "C" int kvt_debug_select_phases(unsigned long long* buf) {
