@@ -1038,8 +1038,14 @@ static int ring_auto_splits(int64_t kmax, int v_dtype, int64_t n_lanes) {
     const int64_t rmax = v_dtype == KVT_I4 ? KVT_ATTN_I4_RMAX : 3328;
     const int64_t cap = kvt::imax(1, kvt::imin(64, (kmax + 31) / 32));
     int64_t s = kvt::imax(1, kvt::imin(cap, (kmax + rmax - 1) / rmax));
-    const int64_t fill = (2 * (int64_t)kvt::sm_count() + n_lanes - 1) / kvt::imax(1, n_lanes);
-    const int64_t by_rows = kvt::imax(1, kmax / 256);
+#ifndef KVT_ATTN_FILL
+#define KVT_ATTN_FILL 2
+#endif
+    const int64_t fill = (KVT_ATTN_FILL * (int64_t)kvt::sm_count() + n_lanes - 1) / kvt::imax(1, n_lanes);
+#ifndef KVT_ATTN_MINROWS
+#define KVT_ATTN_MINROWS 256
+#endif
+    const int64_t by_rows = kvt::imax(1, kmax / KVT_ATTN_MINROWS);
     s = kvt::imax(s, kvt::imin(kvt::imin(fill, by_rows), cap));
     return (int)s;
 }
