@@ -4,7 +4,7 @@
 mkdir -p gpurun_out/sweep
 run() {  # name, args...
   local name=$1; shift
-  timeout 900 python bench.py --steps 20 --no-cpu-baseline "$@" > gpurun_out/sweep/$name.json 2> gpurun_out/sweep/$name.err
+  timeout 900 python bench.py --steps 20 --no-cpu-baseline --sub "" "$@" > gpurun_out/sweep/$name.json 2> gpurun_out/sweep/$name.err
   python - "$name" <<'PY'
 import json, sys
 name = sys.argv[1]
