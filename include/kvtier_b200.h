@@ -390,6 +390,20 @@ KVT_API int kvt_tier_layer(const kvt_tier_args* a, void* stream);
 /* out4 = [misses, evictions, need (< 0: capacity error), victims] of the last call;
  * synchronises the stream (diagnostics). */
 KVT_API int kvt_tier_read_ctl(const void* ctl, long long* out4, void* stream);
+/* ---- sequence sharding: the all-gather + log-sum-exp merge over NCCL ----------
+ * NCCL is bound at run time (dlopen libnccl.so.2; the process's own NCCL when loaded), so the
+ * library has no link-time NCCL dependency.  kvt_nccl_available: 1 when it could be bound.
+ * kvt_nccl_unique_id writes the 128-byte ncclUniqueId; every rank passes the same id to
+ * kvt_nccl_comm_init.  kvt_lse_allgather_merge all-gathers each rank's part_local
+ * [n_lanes][d + 2] (m, l, o normalised; kvt_attn_lse + the rank's output) into gather_buf
+ * [nranks][n_lanes][d + 2] and merges them (kvt_lse_merge), stream-ordered. */
+KVT_API int kvt_nccl_available(void);
+KVT_API int kvt_nccl_unique_id(void* id_out);
+KVT_API int kvt_nccl_comm_init(void** comm_out, int nranks, int rank, const void* id);
+KVT_API int kvt_nccl_comm_destroy(void* comm);
+KVT_API int kvt_lse_allgather_merge(void* comm, int nranks, const double* part_local, int64_t n_lanes, int d,
+                                    double logit_scale, double* gather_buf, float* out, double* out64,
+                                    void* stream);
 /* Live chunks of each lane's selection (runs from kvt_topk_select_runs / _band): out[lane][j]
  * = chunks of size 2^(lg0 + j) (j < nlev <= 8) that hold a selected token -- the measured skew
  * behind SparseDecoder.adapt_chunking (the importance density of chunk_tree.py:34-123). */

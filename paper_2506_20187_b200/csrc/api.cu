@@ -15,6 +15,11 @@ int kvt_set_cuda_error(cudaError_t e) {
     return KVT_ERR_CUDA;
 }
 
+int kvt_set_error_text(const char* msg) {
+    snprintf(g_err, sizeof g_err, "%s", msg ? msg : "error");
+    return KVT_ERR_CUDA;
+}
+
 int kvt_check_launch() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return kvt_set_cuda_error(e);

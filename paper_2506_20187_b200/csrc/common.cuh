@@ -459,5 +459,6 @@ extern "C" int kvt_sparse_decode_attn_gqa(const void* values, int64_t n_lanes, i
 extern "C" size_t kvt_attn_gqa_scratch_bytes(int64_t n_lanes, int kvg, int64_t n_ctx);
 
 // status plumbing (api.cu)
+int kvt_set_error_text(const char* msg);
 int kvt_set_cuda_error(cudaError_t e);
 int kvt_check_launch();

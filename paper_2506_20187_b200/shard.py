@@ -61,6 +61,47 @@ def allgather_lse_merge(m: torch.Tensor, l: torch.Tensor, o: torch.Tensor, group
     return lse_merge(out[..., 0], out[..., 1], out[..., 2:])
 
 
+class NcclLseMerge:
+    """The sequence-sharded path's only collective through the library (kvt_lse_allgather_merge:
+    NCCL all-gather of each rank's (m, l, o) + the log-sum-exp merge kernel, one stream-ordered
+    call).  The NCCL unique id goes from rank 0 to the others over torch.distributed (any
+    backend); with world == 1 no process group is needed."""
+
+    def __init__(self, rank: int = 0, world: int = 1, group=None):
+        import ctypes
+        from . import _lib as L
+        if not L.kvt_nccl_available():
+            raise RuntimeError("libnccl.so.2 could not be loaded")
+        self.L, self.rank, self.world = L, rank, world
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            L.check(L.kvt_nccl_unique_id(uid), "nccl_unique_id")
+        if world > 1:
+            obj = [bytes(uid) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            ctypes.memmove(uid, obj[0], 128)
+        self.comm = ctypes.c_void_p()
+        L.check(L.kvt_nccl_comm_init(ctypes.byref(self.comm), world, rank, uid), "nccl_comm_init")
+
+    def merge(self, m: torch.Tensor, l: torch.Tensor, o: torch.Tensor, logit_scale: float) -> torch.Tensor:
+        """m, l: [lanes] f64 (kvt_attn_lse of this rank's shard); o: [lanes, d] this rank's
+        normalised output -> merged output f64 [lanes, d] on every rank."""
+        from . import ops
+        part = torch.cat([m[:, None], l[:, None], o.double()], dim=1).contiguous()
+        n, d = o.shape
+        gather = torch.empty((self.world, n, d + 2), dtype=torch.float64, device=o.device)
+        out = torch.empty((n, d), dtype=torch.float64, device=o.device)
+        self.L.check(self.L.kvt_lse_allgather_merge(self.comm, self.world, part.data_ptr(), n, d, float(logit_scale),
+                                                    gather.data_ptr(), None, out.data_ptr(), ops._stream()),
+                     "lse_allgather_merge")
+        return out
+
+    def close(self) -> None:
+        if self.comm:
+            self.L.check(self.L.kvt_nccl_comm_destroy(self.comm), "nccl_comm_destroy")
+            self.comm = None
+
+
 _MIN64 = -(2 ** 63)
 
 

@@ -128,3 +128,32 @@ def test_lse_merge_kernel_matches_torch(ops):
     w = np.where(l > 0, np.exp((m - M) * scale) * l, 0.0)
     ref = (w[..., None] * o).sum(0) / w.sum(0)[..., None]
     assert np.allclose(out64.cpu().numpy(), ref, rtol=1e-12, atol=1e-12)
+
+
+def test_nccl_allgather_merge_single_rank():
+    """kvt_lse_allgather_merge (NCCL bound at run time) on a one-rank communicator: the
+    gathered part merges back to the rank's own output, and the merge kernel equals the torch
+    log-sum-exp formula on a multi-part input."""
+    import torch
+    from paper_2506_20187_b200 import ops
+    from paper_2506_20187_b200.shard import NcclLseMerge, lse_merge
+    g = torch.Generator().manual_seed(4)
+    n, d = 37, 128
+    o = torch.randn((n, d), generator=g, dtype=torch.float64).cuda()
+    m = torch.randn(n, generator=g, dtype=torch.float64).cuda()
+    l = torch.rand(n, generator=g, dtype=torch.float64).cuda() + 0.5
+    nm = NcclLseMerge(0, 1)
+    try:
+        out = nm.merge(m, l, o, 0.1)
+        torch.cuda.synchronize()
+        assert torch.allclose(out, o, rtol=1e-12, atol=1e-12)
+    finally:
+        nm.close()
+    P = 3
+    parts = torch.randn((P, n, d + 2), generator=g, dtype=torch.float64).cuda()
+    parts[:, :, 1] = parts[:, :, 1].abs() + 0.1
+    got = ops.lse_merge(parts, 0.1)
+    # torch restatement: o_p normalised -> un-normalised sums l_p o_p at scale-adjusted maxima
+    mm = parts[:, :, 0] * 0.1
+    ref = lse_merge(mm, parts[:, :, 1], parts[:, :, 2:] * parts[:, :, 1:2])
+    assert torch.allclose(got.double(), ref, rtol=1e-5, atol=1e-6)
