@@ -149,3 +149,36 @@ def test_capacity_error_when_a_step_does_not_fit():
     tie.step(Q[0])
     with pytest.raises(CapacityError):
         tie.ledger_rows()
+
+
+@pytest.mark.parametrize("d,kvg", [(256, 1), (128, 2)])
+def test_tiered_other_shapes_match_resident(d, kvg):
+    """d = 256 records and GQA (query lanes i / g share KV lane i / g's hot records): the
+    paged attention over the hot tier matches the resident decoder (bit for bit without GQA;
+    within 1e-5 with it, where the resident path runs the tensor-core union kernel)."""
+    from paper_2506_20187_b200 import ops
+    from paper_2506_20187_b200.decode import SparseDecoder
+    from paper_2506_20187_b200.host_tier import TieredDecoder
+    Lx, H, n = 2, 4, 4096
+    Hkv = H // kvg
+    kw = dict(importance_rate=0.1, early_layer_rate=0.1, n_kv_heads=Hkv)
+    res = SparseDecoder(Lx, 1, H, d, n, dtype=ops.I4, **kw)
+    tie = TieredDecoder(Lx, 1, H, d, n, 4000, crec=8, **kw)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    for l in range(Lx):
+        K = torch.randn((Hkv, n, d), device="cuda", generator=g).to(torch.bfloat16)
+        V = torch.randn((Hkv, n, d), device="cuda", generator=g).to(torch.bfloat16)
+        res.load_layer(l, K, V)
+        tie.load_layer(l, K, V)
+    res.set_length(n)
+    tie.set_length(n)
+    for s in range(3):
+        q = torch.randn((Lx, H, d), device="cuda", generator=g)
+        a, b = res.step(q).clone(), tie.step(q).clone()
+        torch.cuda.synchronize()
+        tie.ledger_rows()
+        if kvg == 1:
+            assert torch.equal(a, b), s
+        else:
+            err = ((a - b).norm(dim=-1) / a.norm(dim=-1)).max().item()
+            assert err <= 1e-5, (s, err)
