@@ -390,6 +390,25 @@ KVT_API int kvt_tier_layer(const kvt_tier_args* a, void* stream);
 /* out4 = [misses, evictions, need (< 0: capacity error), victims] of the last call;
  * synchronises the stream (diagnostics). */
 KVT_API int kvt_tier_read_ctl(const void* ctl, long long* out4, void* stream);
+/* ---- one decode step's appends (the caller side of the path: engine-side KV growth) ---------
+ * The new token's K and V rows of every layer and KV lane ([L][kv_lanes][d], element strides,
+ * bf16 or f32) become INT4 record t of K / V ([L][kv_lanes][N][row], byte strides) -- the
+ * kvt_kv_quant codec, bit-identical -- and each listed bf16 abstract grid has its tail chunk
+ * t / C refreshed from the dequantised key (max(old, ru(x)), min(old, rd(x)); a new chunk when
+ * t % C == 0), equal to rebuilding that chunk; absmag[layer] ([kv_lanes][d] f32, may be NULL)
+ * takes max |.| of the new rounded abstracts.  grids and absmag are DEVICE arrays.  d = 128.
+ * One launch for the whole step. */
+typedef struct {
+    void* amax;           /* bf16 [kv_lanes][lane_stride] */
+    void* amin;
+    int64_t lane_stride;  /* elements */
+    int C;
+    int layer;
+} kvt_append_grid;
+KVT_API int kvt_kv_append(const void* k_new, const void* v_new, int src_dtype, int64_t src_layer_stride,
+                          int64_t src_lane_stride, int64_t n_layers, int64_t kv_lanes, int d, int64_t t, void* K,
+                          void* V, int64_t layer_stride_b, int64_t lane_stride_b, const kvt_append_grid* grids,
+                          int n_grids, float* const* absmag, void* stream);
 /* ---- sequence sharding: the all-gather + log-sum-exp merge over NCCL ----------
  * NCCL is bound at run time (dlopen libnccl.so.2; the process's own NCCL when loaded), so the
  * library has no link-time NCCL dependency.  kvt_nccl_available: 1 when it could be bound.

@@ -114,6 +114,8 @@ kvt_set_kv_group = _sig("kvt_set_kv_group", ctypes.c_int, _i32)
 kvt_set_cand_group = _sig("kvt_set_cand_group", ctypes.c_int, _i32)
 kvt_abstract_merge = _sig("kvt_abstract_merge", ctypes.c_int, _vp, _vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp,
                           _i32, _i64, _i64, _vp, _vp, _i64, _vp)
+kvt_kv_append = _sig("kvt_kv_append", ctypes.c_int, _vp, _vp, _i32, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i64,
+                     _i64, _vp, _i32, _vp, _vp)
 kvt_nccl_available = _sig("kvt_nccl_available", ctypes.c_int)
 kvt_nccl_unique_id = _sig("kvt_nccl_unique_id", ctypes.c_int, _vp)
 kvt_nccl_comm_init = _sig("kvt_nccl_comm_init", ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), _i32, _i32, _vp)
@@ -150,7 +152,7 @@ EXPORTED = [
     "kvt_select_attend", "kvt_kv_quant", "kvt_i4_row_bytes", "kvt_i4_recip_check", "kvt_select_plan2", "kvt_cand_score_f32",
     "kvt_topk_select_band", "kvt_kv_dequant", "kvt_chunk_bounds_fast", "kvt_attn_lse", "kvt_lse_merge", "kvt_set_kv_group", "kvt_i4_qprep_bytes", "kvt_i4_qprep", "kvt_cand_score_i4mma",
     "kvt_synth_layer", "kvt_select_plan_group", "kvt_set_cand_group", "kvt_debug_select_phases",
-    "kvt_abstract_merge", "kvt_live_chunks", "kvt_nccl_available", "kvt_nccl_unique_id", "kvt_nccl_comm_init",
+    "kvt_abstract_merge", "kvt_live_chunks", "kvt_kv_append", "kvt_nccl_available", "kvt_nccl_unique_id", "kvt_nccl_comm_init",
     "kvt_nccl_comm_destroy", "kvt_lse_allgather_merge", "kvt_attn_gqa_scratch_bytes", "kvt_sparse_decode_attn_gqa", "kvt_tier_ctl_bytes", "kvt_tier_layer", "kvt_tier_read_ctl", "kvt_sparse_decode_attn_paged",
 ]
 

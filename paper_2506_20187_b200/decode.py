@@ -113,10 +113,45 @@ class SparseDecoder:
             if self.V is not None:
                 self.V[layer, :, t0:t0 + T] = v.to(self.dtype)
 
-    def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
-        """Append one token per KV lane ([L, kv_lanes, d]) and refresh the tail chunk abstracts."""
+    def _append_tables(self):
+        """Device tables of kvt_kv_append: every bf16 abstract grid (fine, coarse, intermediate)
+        and the per-layer absmag pointers; rebuilt when the set of grids changes."""
+        key = tuple(sorted(self._mid))
+        if getattr(self, "_app_key", None) == key:
+            return self._app_grids, self._app_n, self._app_mag
+        import numpy as np
+        rows = []
+        for l in range(self.L):
+            grids = [(self.amax[l], self.amin[l], self.C[l])]
+            if self.amax_c[l] is not None:
+                grids.append((self.amax_c[l], self.amin_c[l], self.coarse_C))
+            grids += [(mx, mn, C) for (ll, C), (mx, mn) in self._mid.items() if ll == l]
+            rows += [(mx.data_ptr(), mn.data_ptr(), mx.stride(0), C, l) for mx, mn, C in grids]
+        dt = np.dtype([("amax", "<u8"), ("amin", "<u8"), ("ls", "<i8"), ("C", "<i4"), ("layer", "<i4")])
+        tab = np.array(rows, dtype=dt)
+        self._app_grids = torch.from_numpy(tab.view(np.uint8).copy()).to(self.device)
+        self._app_n = len(rows)
+        self._app_mag = torch.tensor([a.data_ptr() for a in self.absmag], dtype=torch.int64, device=self.device)
+        self._app_key = key
+        return self._app_grids, self._app_n, self._app_mag
+
+    def append(self, k_new: torch.Tensor, v_new: torch.Tensor, fused: bool = True) -> None:
+        """Append one token per KV lane ([L, kv_lanes, d]) and refresh the tail chunk abstracts.
+        INT4 KV with bf16 abstracts at d = 128: one kvt_kv_append launch for every layer and
+        lane (quantise + abstract / absmag refresh); otherwise per-layer launches."""
         if self.n >= self.n_cap:
             raise ValueError("cache full")
+        if (fused and self.dtype == ops.I4 and self.absmag is not None and self.d == 128 and self.V is not None
+                and k_new.dtype in (torch.bfloat16, torch.float32) and v_new.dtype == k_new.dtype):
+            k_new, v_new = k_new.contiguous(), v_new.contiguous()
+            grids, ng, mag = self._append_tables()
+            ops.L.check(ops.L.kvt_kv_append(
+                k_new.data_ptr(), v_new.data_ptr(), ops.dtype_code(k_new), k_new.stride(0), k_new.stride(1), self.L,
+                self.kv_lanes, self.d, self.n, self.K.data.data_ptr(), self.V.data.data_ptr(), self.K.data.stride(0),
+                self.K.data.stride(1), grids.data_ptr(), ng, mag.data_ptr(), ops._stream()), "kv_append")
+            self.n += 1
+            self._bufs = None
+            return
         for l in range(self.L):
             self.load_layer(l, k_new[l][:, None, :].contiguous(), v_new[l][:, None, :].contiguous(), self.n)
         self.n += 1
@@ -221,6 +256,10 @@ class SparseDecoder:
             return self._bufs
         dev, lanes, d = self.device, self.lanes, self.d
         bufs = []
+        hints = getattr(self, "_hints", None)
+        if hints is None:  # per-lane selector state survives buffer rebuilds (n changes on append)
+            hints = self._hints = [torch.full((lanes,), float("nan"), dtype=torch.float32, device=dev)
+                                   for _ in range(self.L)]
         for l in range(self.L):
             k = self.k_for(l)
             bufs.append({
@@ -233,7 +272,7 @@ class SparseDecoder:
                 "out": torch.empty((lanes, d), dtype=torch.float32, device=dev),
                 "evals": torch.empty(lanes, dtype=torch.int64, device=dev),
                 # the previous step's k-th estimate per lane (state across steps; NaN = none)
-                "sel_hint": torch.full((lanes,), float("nan"), dtype=torch.float32, device=dev),
+                "sel_hint": hints[l],
             })
         maxl = max(ops.n_grid_leaves(self.n_cap, C) for C in self.C)
         if self._ws is None or self._ws.key != (lanes, self.n_cap, maxl, d):

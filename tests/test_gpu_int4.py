@@ -455,3 +455,42 @@ def test_gqa_union_long_selections_multiwindow_ranges(ops):
             ref = (w[:, None] * Vd[sel[i]]).sum(0) / w.sum()
             err = np.linalg.norm(out[i] - ref) / np.linalg.norm(ref)
             assert err <= 2e-5, (j, h, err)
+
+
+def test_fused_append_equals_per_layer_path(ops):
+    """kvt_kv_append (one launch per decode step: INT4 records of every layer and lane, the tail
+    chunk of every bf16 abstract grid, absmag) equals the per-layer path bit for bit, across a
+    chunk boundary and with an intermediate grid from adapt_chunking."""
+    from paper_2506_20187_b200.decode import SparseDecoder
+    L_, H, d, n0 = 3, 4, 128, 1000
+    a = SparseDecoder(L_, 1, H, d, n0 + 80, dtype=ops.I4, importance_rate=0.1, early_layer_rate=0.5)
+    b = SparseDecoder(L_, 1, H, d, n0 + 80, dtype=ops.I4, importance_rate=0.1, early_layer_rate=0.5)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for l in range(L_):
+        K = torch.randn((H, n0, d), device="cuda", generator=g).to(torch.bfloat16)
+        V = torch.randn((H, n0, d), device="cuda", generator=g).to(torch.bfloat16)
+        a.load_layer(l, K, V)
+        b.load_layer(l, K, V)
+    a.set_length(n0)
+    b.set_length(n0)
+    for dec in (a, b):  # an intermediate grid (C = 16) on layer 0
+        dec._ensure_grid(0, 16)
+    for s in range(70):  # crosses the 64- and 16-token chunk boundaries
+        kn = (torch.randn((L_, H, d), device="cuda", generator=g) * 3).to(torch.bfloat16)
+        vn = torch.randn((L_, H, d), device="cuda", generator=g).to(torch.bfloat16)
+        a.append(kn, vn, fused=True)
+        b.append(kn, vn, fused=False)
+    torch.cuda.synchronize()
+    n = n0 + 70
+    assert torch.equal(a.K.data[:, :, :n], b.K.data[:, :, :n]) and torch.equal(a.V.data[:, :, :n], b.V.data[:, :, :n])
+    for l in range(L_):
+        m = ops.n_grid_leaves(n, a.C[l])
+        assert torch.equal(a.amax[l][:, :m], b.amax[l][:, :m]) and torch.equal(a.amin[l][:, :m], b.amin[l][:, :m])
+        assert torch.equal(a.absmag[l], b.absmag[l])
+        if a.amax_c[l] is not None:
+            mc = ops.n_grid_leaves(n, a.coarse_C)
+            assert torch.equal(a.amax_c[l][:, :mc], b.amax_c[l][:, :mc])
+    mx_a, mn_a = a._mid[(0, 16)]
+    mx_b, mn_b = b._mid[(0, 16)]
+    m16 = ops.n_grid_leaves(n, 16)
+    assert torch.equal(mx_a[:, :m16], mx_b[:, :m16]) and torch.equal(mn_a[:, :m16], mn_b[:, :m16])
