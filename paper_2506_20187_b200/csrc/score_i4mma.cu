@@ -246,7 +246,28 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
     uint32_t B[R][2][4][2];
     float qt[R], W[R], sp[4];
     int cur = -1;
-    float emax = 0.f;
+    // the lane's error bound, accumulated per thread without per-token reductions: the max
+    // over its rows of (15|s_g| + |m_g|) for its group and of |est|; combined at the flush
+    // into E = 1.001 (u max|est| + sum_g max_rows(15|s_g| + |m_g|) W_g) >= every e(t)
+    float gmx[R], amx = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) gmx[r] = 0.f;
+    auto lane_bound = [&]() -> float {
+        float v = 0.f;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float gm = gmx[r];
+#pragma unroll
+            for (int o = 4; o <= 16; o <<= 1) gm = fmaxf(gm, __shfl_xor_sync(KVT_FULL, gm, o));  // rows (gid)
+            v = fmaf(gm, W[r], v);
+        }
+        v += __shfl_xor_sync(KVT_FULL, v, 1);  // groups (tig)
+        v += __shfl_xor_sync(KVT_FULL, v, 2);
+        float a = amx;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) a = fmaxf(a, __shfl_xor_sync(KVT_FULL, a, o));
+        return 1.001f * __fmaf_rn(0x1p-24f, a, v);
+    };
     int cs = 0, cr = 0;
     for (;;) {
         const int s = cs;
@@ -256,14 +277,14 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
         if (mt.z < 0) break;
         const unsigned char* st = smem + (size_t)s * stage_b;
         if (mt.x != cur) {
-            // flush the finished lane's error max, then load the new lane's digits
-            float e = emax;
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) e = fmaxf(e, __shfl_xor_sync(KVT_FULL, e, o));
+            // flush the finished lane's error bound, then load the new lane's digits
+            const float e = lane_bound();
             if (lane == 0 && cur >= 0 && e > 0.f)
                 atomicMax(reinterpret_cast<unsigned long long*>(err + (int64_t)cur * 4 + 3),
                           (unsigned long long)__double_as_longlong((double)e));
-            emax = 0.f;
+            amx = 0.f;
+#pragma unroll
+            for (int r = 0; r < R; ++r) gmx[r] = 0.f;
             cur = mt.x;
             const unsigned char* qs = st + tile_b;
             const bool role = (gid >> 1) == tig;
@@ -322,32 +343,27 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                 const float sc1 = __low2float(p1), mn1 = __high2float(p1);
                 est0 += fmaf(sc0, in0, mn0 * qt[r]);
                 est1 += fmaf(sc1, in1, mn1 * qt[r]);
-                er0 = fmaf(fmaf(15.f, fabsf(sc0), fabsf(mn0)), W[r], er0);
-                er1 = fmaf(fmaf(15.f, fabsf(sc1), fabsf(mn1)), W[r], er1);
+                if (row0 < cnt) gmx[r] = fmaxf(gmx[r], fmaf(15.f, fabsf(sc0), fabsf(mn0)));
+                if (row1 < cnt) gmx[r] = fmaxf(gmx[r], fmaf(15.f, fabsf(sc1), fabsf(mn1)));
             }
 #pragma unroll
             for (int o = 1; o <= 2; o <<= 1) {
                 est0 += __shfl_xor_sync(KVT_FULL, est0, o);
                 est1 += __shfl_xor_sync(KVT_FULL, est1, o);
-                er0 += __shfl_xor_sync(KVT_FULL, er0, o);
-                er1 += __shfl_xor_sync(KVT_FULL, er1, o);
             }
             const int row = tig == 0 ? row0 : row1;
             const float est = tig == 0 ? est0 : est1;
-            const float er = 1.001f * __fmaf_rn(0x1p-24f, fabsf(est), tig == 0 ? er0 : er1);
             if (tig < 2 && row < cnt) {
                 out32[(int64_t)cur * out_stride + pos0 + row] = est;
                 if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + row] = t0 + row;
-                emax = fmaxf(emax, er);
+                amx = fmaxf(amx, fabsf(est));
             }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
-    float e = emax;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) e = fmaxf(e, __shfl_xor_sync(KVT_FULL, e, o));
+    const float e = lane_bound();
     if (lane == 0 && cur >= 0 && e > 0.f)
         atomicMax(reinterpret_cast<unsigned long long*>(err + (int64_t)cur * 4 + 3),
                   (unsigned long long)__double_as_longlong((double)e));
