@@ -18,7 +18,10 @@
 // group of sum_p s_p |qi_p|, which bounds |inner_g| / 15 and |Qt_g|, incl. Qt_g's own f32
 // rounding), the digit residual q - qt, the canonical dot's own f64 rounding and the fp32
 // rounding of the dequantised element the canonical dot sees; W_g per lane and group comes
-// from kvt_i4_qprep.  The per-lane max of e(t) is atomically max-ed into err[4 lane + 3], where
+// from kvt_i4_qprep.  One head per KV lane (QG = 1) takes the per-lane
+//     E = 1.001 [u max_t |est32(t)| + sum_g max_t (15|s_g| + |m_g|) W_g] >= max_t e(t)
+// (no per-token reductions; measured to leave the band unchanged); GQA keeps max_t e(t).
+// The per-lane bound is atomically max-ed into err[4 lane + 3], where
 // the band select (select3) takes it as E: the band is then a few ulps wide and the
 // selected set stays the exact canonical top-k.
 //
