@@ -20,7 +20,8 @@
 // rounding of the dequantised element the canonical dot sees; W_g per lane and group comes
 // from kvt_i4_qprep.  One head per KV lane (QG = 1) takes the per-lane
 //     E = 1.001 [u max_t |est32(t)| + sum_g max_t (15|s_g| + |m_g|) W_g] >= max_t e(t)
-// (no per-token reductions; measured to leave the band unchanged); GQA keeps max_t e(t).
+// (no per-token reductions; K5 time unchanged at config 3); GQA keeps max_t e(t) (the
+// per-row maxima cost it spills).
 // The per-lane bound is atomically max-ed into err[4 lane + 3], where
 // the band select (select3) takes it as E: the band is then a few ulps wide and the
 // selected set stays the exact canonical top-k.
