@@ -38,8 +38,10 @@ __device__ __forceinline__ int64_t leaf_begin(const int32_t* ls, int64_t c, int 
     return ls ? (int64_t)ls[c] : c * C;
 }
 
-template <int GMAX>  // 1: one query lane per CTA; 8: GQA union over grp <= 8 query lanes
-__global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
+// GMAX 1: one query lane per CTA (512 threads, 3 CTAs per SM); GQA union over grp <= GMAX query
+// lanes: one CTA per KV lane and SM (1024 threads for grp <= 4: the work is grp-fold per CTA)
+template <int GMAX, int PT>
+__global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
     int64_t n, int C, const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ n_leaves,
     int64_t leaf_stride, const double* __restrict__ U, const double* __restrict__ L, int64_t bnd_stride,
     int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
@@ -50,7 +52,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
     extern __shared__ __align__(16) unsigned char plan_smem[];
     uint64_t* kst = reinterpret_cast<uint64_t*>(plan_smem);  // staged keys (if they fit)
     int8_t* fl = reinterpret_cast<int8_t*>(plan_smem) + (size_t)stage_cap * 8;  // union flags (grp > 1)
-    __shared__ unsigned long long hist[256];
+    __shared__ unsigned long long hist[GMAX * 256];
+    __shared__ unsigned long long sp_h[GMAX], sm_h[GMAX];
+    __shared__ long long sr_h[GMAX];
     __shared__ long long scan_sh[33];
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ long long s_remaining;
@@ -62,20 +66,88 @@ __global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
     const int32_t* ls = leaf_start ? leaf_start + li * leaf_stride : nullptr;
     const int64_t nl = leaf_start ? (int64_t)n_leaves[li] : (n + C - 1) / C;
     const bool staged = nl <= stage_cap;
+    // GQA: all heads' keys staged at once -> one histogram pass per digit serves every head
+    const bool conc = GMAX > 1 && grp > 1 && (int64_t)grp * nl <= stage_cap;
 
-    for (int h = 0; h < grp; ++h) {
+    if (conc) {
+        const int nl32 = (int)nl, tot = grp * nl32;
+        for (int e = tid; e < tot; e += PT) {
+            const int h = e / nl32;
+            kst[e] = ord_key(L[(q0 + h) * bnd_stride + (e - h * nl32)]);
+        }
+        if (tid < GMAX) { sp_h[tid] = 0; sm_h[tid] = 0; sr_h[tid] = k; }
+        __syncthreads();
+        for (int shift = 56; shift >= 40 && k > 0; shift -= 8) {
+            for (int i = tid; i < GMAX * 256; i += PT) hist[i] = 0;
+            __syncthreads();
+            for (int base = 0; base < tot; base += PT) {
+                const int e = base + tid;
+                int bin = GMAX * 256;
+                unsigned long long w = 0;
+                if (e < tot) {
+                    const int h = e / nl32;
+                    const int64_t c = e - h * nl32;
+                    const uint64_t key = kst[e];
+                    if ((key & sm_h[h]) == sp_h[h]) {
+                        bin = h * 256 + (int)((key >> shift) & 0xff);
+                        w = (unsigned long long)leaf_rows(ls, nl, c, n, C);
+                    }
+                }
+                const unsigned peers = __match_any_sync(KVT_FULL, bin);
+                const unsigned sum = __reduce_add_sync(peers, (unsigned)w);
+                if (bin < GMAX * 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned long long)sum);
+            }
+            __syncthreads();
+            const int wh = tid >> 5;
+            if (wh < grp) {  // warp h: the digit of head h (same scan as below)
+                const unsigned long long* hh = hist + wh * 256;
+                unsigned long long loc = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) loc += hh[255 - 8 * lane - i];
+                const unsigned long long inc = warp_incl_scan(loc, lane);
+                const unsigned long long exc = inc - loc;
+                const unsigned long long rem = (unsigned long long)sr_h[wh];
+                const unsigned long long prefix = sp_h[wh], mask = sm_h[wh];
+                __syncwarp();
+                if (exc < rem && rem <= inc) {
+                    unsigned long long run = exc;
+                    for (int i = 0; i < 8; ++i) {
+                        const int b = 255 - 8 * lane - i;
+                        if (run + hh[b] >= rem) {
+                            sp_h[wh] = prefix | ((unsigned long long)b << shift);
+                            sm_h[wh] = mask | (0xffull << shift);
+                            sr_h[wh] = (long long)(rem - run);
+                            break;
+                        }
+                        run += hh[b];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (tid < grp) s_tau[tid] = (k <= 0) ? INFINITY : key_to_double(sp_h[tid]);
+        __syncthreads();
+        for (int64_t c = tid; c < nl; c += PT) {
+            int8_t f = 0;
+            for (int h = 0; h < grp; ++h) f |= U[(q0 + h) * bnd_stride + c] >= s_tau[h] ? 1 : 0;
+            fl[c] = f;
+        }
+        __syncthreads();
+    }
+
+    for (int h = 0; h < grp && !conc; ++h) {
         const double* Ll = L + (q0 + h) * bnd_stride;
         if (staged)
-            for (int64_t c = tid; c < nl; c += PLAN_THREADS) kst[c] = ord_key(Ll[c]);
+            for (int64_t c = tid; c < nl; c += PT) kst[c] = ord_key(Ll[c]);
         if (tid == 0) { s_prefix = 0; s_mask = 0; s_remaining = k; s_done = (k <= 0); }
         __syncthreads();
 
         // ---- weighted radix select on the top 24 key bits ----
         for (int shift = 56; shift >= 40 && !s_done; shift -= 8) {
-            for (int i = tid; i < 256; i += PLAN_THREADS) hist[i] = 0;
+            for (int i = tid; i < 256; i += PT) hist[i] = 0;
             __syncthreads();
             const unsigned long long prefix = s_prefix, mask = s_mask;
-            for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
+            for (int64_t base = 0; base < nl; base += PT) {
                 const int64_t c = base + tid;
                 int digit = 256;
                 unsigned long long w = 0;
@@ -122,7 +194,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
         if (tid == 0) s_tau[h] = tau_h;
         if (grp > 1 && staged) {  // union flags: OR over the group's heads
             const double* Uh = U + (q0 + h) * bnd_stride;
-            for (int64_t c = tid; c < nl; c += PLAN_THREADS) {
+            for (int64_t c = tid; c < nl; c += PT) {
                 const int8_t f = Uh[c] >= tau_h ? 1 : 0;
                 fl[c] = h == 0 ? f : (int8_t)(fl[c] | f);
             }
@@ -135,7 +207,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
     // ---- candidate flags (single head: staged over the keys, which are no longer needed) ----
     int8_t* fl1 = reinterpret_cast<int8_t*>(plan_smem);
     if (grp == 1 && staged)
-        for (int64_t c = tid; c < nl; c += PLAN_THREADS) fl1[c] = Ul[c] >= tau ? 1 : 0;
+        for (int64_t c = tid; c < nl; c += PT) fl1[c] = Ul[c] >= tau ? 1 : 0;
     __syncthreads();
     auto is_cand = [&](int64_t c) -> bool {
         if (staged) return (grp == 1 ? fl1[c] : fl[c]) != 0;
@@ -149,7 +221,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
     double amax_c[GMAX], umax_c[GMAX];
 #pragma unroll
     for (int h = 0; h < GMAX; ++h) { amax_c[h] = 0.0; umax_c[h] = -INFINITY; }
-    for (int64_t base = 0; base < nl; base += PLAN_THREADS) {
+    for (int64_t base = 0; base < nl; base += PT) {
         const int64_t c = base + tid;
         long long it = 0, tk = 0;
         int64_t rows = 0, s = 0, first = 0;
@@ -219,7 +291,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, GMAX == 1 ? 3 : 1) plan_kernel(
             __syncthreads();
             if (tid == 0) {
                 double m = 0.0, umx = -INFINITY;
-                for (int w = 0; w < PLAN_THREADS / 32; ++w) { m = fmax(m, red[w]); umx = fmax(umx, red[32 + w]); }
+                for (int w = 0; w < PT / 32; ++w) { m = fmax(m, red[w]); umx = fmax(umx, red[32 + w]); }
                 err[(q0 + h) * 4 + 0] = m * err_factor;
                 err[(q0 + h) * 4 + 1] = s_tau[h];
                 err[(q0 + h) * 4 + 2] = umx;
@@ -282,16 +354,20 @@ extern "C" int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const in
     if (n_lanes > 2147483647LL) return KVT_ERR_ARG;
     KVT_PER_DEVICE(bool, configured);
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(plan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
+        cudaError_t e = cudaFuncSetAttribute(plan_kernel<1, PLAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(plan_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 9);
+            e = cudaFuncSetAttribute(plan_kernel<4, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 9);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(plan_kernel<8, PLAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 9);
         if (e != cudaSuccess) return kvt_set_cuda_error(e);
         configured = true;
     }
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
-    const int cap = (int)kvt::imin(max_leaves, 16384);
+    const int cap = (int)kvt::imin(max_leaves * grp, 16384);
     const size_t smem = (size_t)cap * (grp > 1 ? 9 : 8);
-    launch_pdl(grp > 1 ? plan_kernel<8> : plan_kernel<1>, dim3((unsigned)(n_lanes / grp)), dim3(PLAN_THREADS), smem, (cudaStream_t)stream, n, C,
+    auto kern = grp == 1 ? plan_kernel<1, PLAN_THREADS> : grp <= 4 ? plan_kernel<4, 1024> : plan_kernel<8, PLAN_THREADS>;
+    const int pt = grp == 1 || grp > 4 ? PLAN_THREADS : 1024;
+    launch_pdl(kern, dim3((unsigned)(n_lanes / grp)), dim3(pt), smem, (cudaStream_t)stream, n, C,
                leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand, cand_leaf,
                evals, cap, A, err, f32_err_factor(d), grp);
     return kvt_check_launch();
