@@ -356,6 +356,8 @@ extern "C" int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const in
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(plan_kernel<1, PLAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
         if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(plan_kernel<1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
+        if (e == cudaSuccess)
             e = cudaFuncSetAttribute(plan_kernel<4, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 9);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(plan_kernel<8, PLAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 9);
@@ -365,8 +367,11 @@ extern "C" int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const in
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
     const int cap = (int)kvt::imin(max_leaves * grp, 16384);
     const size_t smem = (size_t)cap * (grp > 1 ? 9 : 8);
-    auto kern = grp == 1 ? plan_kernel<1, PLAN_THREADS> : grp <= 4 ? plan_kernel<4, 1024> : plan_kernel<8, PLAN_THREADS>;
-    const int pt = grp == 1 || grp > 4 ? PLAN_THREADS : 1024;
+    // fewer lanes than SMs (small batch): one CTA per SM anyway, so use 1024 threads
+    const bool wide1 = grp == 1 && n_lanes < (int64_t)kvt::sm_count();
+    auto kern = grp == 1 ? (wide1 ? plan_kernel<1, 1024> : plan_kernel<1, PLAN_THREADS>)
+                         : grp <= 4 ? plan_kernel<4, 1024> : plan_kernel<8, PLAN_THREADS>;
+    const int pt = grp > 4 || (grp == 1 && !wide1) ? PLAN_THREADS : 1024;
     launch_pdl(kern, dim3((unsigned)(n_lanes / grp)), dim3(pt), smem, (cudaStream_t)stream, n, C,
                leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand, cand_leaf,
                evals, cap, A, err, f32_err_factor(d), grp);
