@@ -616,6 +616,16 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
     ugrp = dec.kv_group if is_i4 else 1  # select_attend's GQA union candidates (INT4 keys)
     cgrp = ops.cand_group(ugrp)
     score_fn = ops.cand_score_i4mma if is_i4 else ops.cand_score_f32
+    # GQA with INT4 values: the step's K7 is the union kernel (kvt_select_attend, unless
+    # KVT_GQA_UNION=0), so that is what the attention stage times
+    union = is_i4 and dec.kv_group > 1 and os.environ.get("KVT_GQA_UNION", "1") != "0"
+    if union:
+        from paper_2506_20187_b200 import _lib
+        dev_ = q_step.device
+        u_ws = torch.zeros(_lib.kvt_attn_workspace_bytes(dec.lanes, HEAD_DIM, 64), dtype=torch.uint8, device=dev_)
+        u_sc = torch.empty(max(_lib.kvt_attn_gqa_scratch_bytes(dec.lanes, dec.kv_group, dec.n), 1),
+                           dtype=torch.uint8, device=dev_)
+        u_out = torch.empty((dec.lanes, HEAD_DIM), dtype=torch.float32, device=dev_)
     q_static = q_step.clone()
     inter = []
 
@@ -649,6 +659,9 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
                     score_fn(q_static[l], dec.K[l], plan, n)
                 elif name == "select":
                     ops.topk_select_band(cs, ct, plan, k, q_static[l], dec.K[l])
+                elif name == "attn" and union:
+                    ops.sparse_decode_attn_gqa(dec.V[l], st_, ss_, ns_, dec.kv_group, n, ws=u_ws, scratch=u_sc,
+                                               out=u_out)
                 elif name == "attn":
                     ops.sparse_decode_attn(dec.V[l], st_, ss_, ns_)
         return run

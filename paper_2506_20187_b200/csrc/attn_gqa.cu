@@ -141,10 +141,16 @@ inline size_t gq_scratch_bytes(int64_t n_kv, int64_t n_win, int G) {
     return gq_al(nw * 4) + gq_al(nw * G * 8) + gq_al(nw * GQ_WIN * 2) + gq_al(nw * GQ_WIN * G * 4);
 }
 
-constexpr int GQ_WPC = 4;  // windows per plan CTA (one lower_bound, then a forward scan)
+#ifndef KVT_GQ_WPC
+#define KVT_GQ_WPC 1
+#endif
+#ifndef KVT_GQ_PLAN_MINB
+#define KVT_GQ_PLAN_MINB 1
+#endif
+constexpr int GQ_WPC = KVT_GQ_WPC;  // windows per plan CTA (one lower_bound, then a forward scan)
 
 template <int G>
-__global__ void __launch_bounds__(GQ_THREADS) gqa_plan_kernel(const int32_t* __restrict__ sel_tok,
+__global__ void __launch_bounds__(GQ_THREADS, KVT_GQ_PLAN_MINB) gqa_plan_kernel(const int32_t* __restrict__ sel_tok,
                                                               const double* __restrict__ sel_score,
                                                               const int32_t* __restrict__ n_sel, int64_t sel_stride,
                                                               int64_t n_win, double scale, GqPlan P) {

@@ -332,7 +332,12 @@ class SparseDecoder:
                 out["score"] += nc * (d * sK + 8)                                  # f32 estimate + token
             out["select"] += nc * 8 + self.lanes * k * 12
             out["runs"] += self.lanes * k * 4 * 3
-            out["attn"] += self.lanes * k * (d * sK + 4 + 8) + self.lanes * d * 4
+            if self.kv_group > 1 and self.dtype == ops.I4:
+                # GQA union K7: a V row once per KV lane for its g heads; counted at the smallest
+                # possible union (k rows per KV lane), so the fraction is never inflated by g
+                out["attn"] += self.kv_lanes * k * d * sK + self.lanes * (k * 12 + d * 4)
+            else:
+                out["attn"] += self.lanes * k * (d * sK + 4 + 8) + self.lanes * d * 4
         return out
 
 

@@ -552,17 +552,24 @@ def select_attend(q: torch.Tensor, keys, values, amax: torch.Tensor, amin: torch
 
 @_on_device
 def sparse_decode_attn_gqa(values, sel_tok: torch.Tensor, sel_score: torch.Tensor, n_sel: torch.Tensor, kv_group: int,
-                           n_ctx: int, want_f64: bool = False):
+                           n_ctx: int, want_f64: bool = False, ws: torch.Tensor | None = None,
+                           scratch: torch.Tensor | None = None, out: torch.Tensor | None = None):
     """GQA union K7 (kvt_sparse_decode_attn_gqa): INT4 values [n_kv, N, rb], query lanes i / g
-    share KV lane i / g -> out f32 [n_lanes, d] (and f64)."""
+    share KV lane i / g -> out f32 [n_lanes, d] (and f64).  ws (zeroed once; the kernels leave
+    it zeroed), scratch and out may be passed in to reuse them across calls."""
     require_cuda(values)
     ls, d = _lanes(values)
     nl = n_sel.shape[0]
     dev = values.device
-    ws = torch.zeros(L.kvt_attn_workspace_bytes(nl, d, 64), dtype=torch.uint8, device=dev)
+    if ws is None:
+        ws = torch.zeros(L.kvt_attn_workspace_bytes(nl, d, 64), dtype=torch.uint8, device=dev)
     sb = L.kvt_attn_gqa_scratch_bytes(nl, kv_group, n_ctx)
-    scratch = torch.empty(max(sb, 1), dtype=torch.uint8, device=dev)
-    out = torch.empty((nl, d), dtype=torch.float32, device=dev)
+    if scratch is None:
+        scratch = torch.empty(max(sb, 1), dtype=torch.uint8, device=dev)
+    elif scratch.numel() < sb:
+        raise ValueError(f"scratch holds {scratch.numel()} bytes, the GQA union needs {sb}")
+    if out is None:
+        out = torch.empty((nl, d), dtype=torch.float32, device=dev)
     out64 = torch.empty((nl, d), dtype=torch.float64, device=dev) if want_f64 else None
     L.check(L.kvt_sparse_decode_attn_gqa(values.data_ptr(), nl, ls, d, kv_group, n_ctx, sel_tok.data_ptr(),
                                          sel_score.data_ptr(), n_sel.data_ptr(), sel_tok.shape[1],
