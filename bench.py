@@ -616,9 +616,9 @@ def attribute(args, dec, q_step, stream, torch, ops) -> dict:
     ugrp = dec.kv_group if is_i4 else 1  # select_attend's GQA union candidates (INT4 keys)
     cgrp = ops.cand_group(ugrp)
     score_fn = ops.cand_score_i4mma if is_i4 else ops.cand_score_f32
-    # GQA with INT4 values: the step's K7 is the union kernel (kvt_select_attend, unless
-    # KVT_GQA_UNION=0), so that is what the attention stage times
-    union = is_i4 and dec.kv_group > 1 and os.environ.get("KVT_GQA_UNION", "1") != "0"
+    # GQA with INT4 values and KVT_GQA_UNION=1: the step's K7 is the union kernel
+    # (kvt_select_attend), so that is what the attention stage times
+    union = is_i4 and dec.kv_group > 1 and os.environ.get("KVT_GQA_UNION", "0") == "1"
     if union:
         from paper_2506_20187_b200 import _lib
         dev_ = q_step.device

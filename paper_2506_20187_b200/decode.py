@@ -20,6 +20,7 @@ Layout in HBM:
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -332,7 +333,7 @@ class SparseDecoder:
                 out["score"] += nc * (d * sK + 8)                                  # f32 estimate + token
             out["select"] += nc * 8 + self.lanes * k * 12
             out["runs"] += self.lanes * k * 4 * 3
-            if self.kv_group > 1 and self.dtype == ops.I4:
+            if self.kv_group > 1 and self.dtype == ops.I4 and os.environ.get("KVT_GQA_UNION", "0") == "1":
                 # GQA union K7: a V row once per KV lane for its g heads; counted at the smallest
                 # possible union (k rows per KV lane), so the fraction is never inflated by g
                 out["attn"] += self.kv_lanes * k * d * sK + self.lanes * (k * 12 + d * 4)

@@ -155,7 +155,7 @@ def test_capacity_error_when_a_step_does_not_fit():
 def test_tiered_other_shapes_match_resident(d, kvg):
     """d = 256 records and GQA (query lanes i / g share KV lane i / g's hot records): the
     paged attention over the hot tier matches the resident decoder (bit for bit without GQA;
-    within 1e-5 with it, where the resident path runs the tensor-core union kernel)."""
+    within 1e-5 with it)."""
     from paper_2506_20187_b200 import ops
     from paper_2506_20187_b200.decode import SparseDecoder
     from paper_2506_20187_b200.host_tier import TieredDecoder
