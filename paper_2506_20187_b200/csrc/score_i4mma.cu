@@ -11,7 +11,8 @@
 // nibble order and the query digits are laid out to match (kvt_i4_qprep).  The epilogue is a
 // few f32 fmas per (token, group): the MMA partials D_p (|D_p| < 2^16) and the power-of-two
 // digit scales make every product exact, so est(t) carries <= 10 f32 roundings per group
-// (3 in inner_g, the m_g Qt_g product and its fma, the r-accumulation, the group tree).  A
+// (<= 3 in inner_g -- 1 as evaluated, s_1 (128 D_0 + D_1) + s_3 (128 D_2 + D_3) --, the
+// m_g Qt_g product and its fma, the r-accumulation, the group tree).  A
 // rigorous per-token bound
 //     |est32(t) - canonical f64 dot(t)| <= e(t) = 1.001 [u |est32(t)| + sum_g (15|s_g| + |m_g|) W_g]
 // (u = 2^-24) covers the final rounding, the epilogue roundings (11 u qd_g, qd_g = sum over the
@@ -321,7 +322,6 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
           if (64 * tt + 16 * warp < cnt) {
             const int row0 = 64 * tt + 16 * warp + gid, row1 = row0 + 8;
             float est0 = 0.f, est1 = 0.f;
-            float er0 = 0.f, er1 = 0.f;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int gq = 4 * r + tig;
@@ -337,9 +337,10 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                     mma_s8(c1, a0, a1, a2, a3, B[r][1][i][0], B[r][1][i][1]);
                 }
                 // c0: parts 0,1 / c1: parts 2,3 of group gq; [0],[1] row0, [2],[3] row1.
-                // inner = sum_p s_p D_p: exact products, 3 roundings (module header)
-                const float in0 = fmaf(sp[3], (float)c1[1], fmaf(sp[2], (float)c1[0], fmaf(sp[1], (float)c0[1], sp[0] * (float)c0[0])));
-                const float in1 = fmaf(sp[3], (float)c1[3], fmaf(sp[2], (float)c1[2], fmaf(sp[1], (float)c0[3], sp[0] * (float)c0[2])));
+                // inner = sum_p s_p D_p = s_1 (128 D_0 + D_1) + s_3 (128 D_2 + D_3): the integer
+                // pairs are exact in f32 (|.| < 2^24), so 2 conversions and 1 rounding (the fma)
+                const float in0 = fmaf(sp[1], (float)(c0[0] * 128 + c0[1]), sp[3] * (float)(c1[0] * 128 + c1[1]));
+                const float in1 = fmaf(sp[1], (float)(c0[2] * 128 + c0[3]), sp[3] * (float)(c1[2] * 128 + c1[3]));
                 const uint32_t h0 = *reinterpret_cast<const uint32_t*>(st + row0 * row_b + d / 2 + 4 * gq);
                 const uint32_t h1 = *reinterpret_cast<const uint32_t*>(st + row1 * row_b + d / 2 + 4 * gq);
                 const __half2 p0 = *reinterpret_cast<const __half2*>(&h0), p1 = *reinterpret_cast<const __half2*>(&h1);
@@ -455,8 +456,8 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                     mma_s8(c0, a0, a1, a2, a3, B[G_][0][0], B[G_][0][1]);
                     mma_s8(c1, a0, a1, a2, a3, B[G_][1][0], B[G_][1][1]);
                     // thread tig: head 4 hq + tig, parts 0,1 (c0) and 2,3 (c1), rows gid / gid + 8
-                    const float in0 = fmaf(sp[3], (float)c1[1], fmaf(sp[2], (float)c1[0], fmaf(sp[1], (float)c0[1], sp[0] * (float)c0[0])));
-                    const float in1 = fmaf(sp[3], (float)c1[3], fmaf(sp[2], (float)c1[2], fmaf(sp[1], (float)c0[3], sp[0] * (float)c0[2])));
+                    const float in0 = fmaf(sp[1], (float)(c0[0] * 128 + c0[1]), sp[3] * (float)(c1[0] * 128 + c1[1]));
+                    const float in1 = fmaf(sp[1], (float)(c0[2] * 128 + c0[3]), sp[3] * (float)(c1[2] * 128 + c1[3]));
                     const uint32_t h0 = *reinterpret_cast<const uint32_t*>(st + row0 * row_b + d / 2 + 4 * G_);
                     const uint32_t h1 = *reinterpret_cast<const uint32_t*>(st + row1 * row_b + d / 2 + 4 * G_);
                     const __half2 p0 = *reinterpret_cast<const __half2*>(&h0), p1 = *reinterpret_cast<const __half2*>(&h1);
