@@ -317,11 +317,13 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
             sp[0] = s4.x; sp[1] = s4.y; sp[2] = s4.z; sp[3] = s4.w;
         }
         const int cnt = mt.z, pos0 = mt.w, t0 = mt.y;
+        float* const o32 = out32 + (int64_t)cur * out_stride + pos0;
+        int32_t* const otok = out_tok ? out_tok + (int64_t)cur * out_stride + pos0 : nullptr;
 #pragma unroll
         for (int tt = 0; tt < QM_ROWS / 64; ++tt) {
           if (64 * tt + 16 * warp < cnt) {
             const int row0 = 64 * tt + 16 * warp + gid, row1 = row0 + 8;
-            float est0 = 0.f, est1 = 0.f;
+            float est0, est1;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int gq = 4 * r + tig;
@@ -346,21 +348,22 @@ __global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
                 const __half2 p0 = *reinterpret_cast<const __half2*>(&h0), p1 = *reinterpret_cast<const __half2*>(&h1);
                 const float sc0 = __low2float(p0), mn0 = __high2float(p0);
                 const float sc1 = __low2float(p1), mn1 = __high2float(p1);
-                est0 += fmaf(sc0, in0, mn0 * qt[r]);
-                est1 += fmaf(sc1, in1, mn1 * qt[r]);
+                const float e0 = fmaf(sc0, in0, mn0 * qt[r]), e1 = fmaf(sc1, in1, mn1 * qt[r]);
+                est0 = r == 0 ? e0 : est0 + e0;
+                est1 = r == 0 ? e1 : est1 + e1;
                 if (row0 < cnt) gmx[r] = fmaxf(gmx[r], fmaf(15.f, fabsf(sc0), fabsf(mn0)));
                 if (row1 < cnt) gmx[r] = fmaxf(gmx[r], fmaf(15.f, fabsf(sc1), fabsf(mn1)));
             }
-#pragma unroll
-            for (int o = 1; o <= 2; o <<= 1) {
-                est0 += __shfl_xor_sync(KVT_FULL, est0, o);
-                est1 += __shfl_xor_sync(KVT_FULL, est1, o);
-            }
-            const int row = tig == 0 ? row0 : row1;
-            const float est = tig == 0 ? est0 : est1;
+            // sum over the 4 groups (tig) as a transposed reduction: odd tig keeps row1 and
+            // sends row0, even tig the reverse, then one more exchange; the tree is
+            // (g0 + g1) + (g2 + g3) for both rows, as before (same bits)
+            const bool odd = tig & 1;
+            float est = (odd ? est1 : est0) + __shfl_xor_sync(KVT_FULL, odd ? est0 : est1, 1);
+            est += __shfl_xor_sync(KVT_FULL, est, 2);
+            const int row = odd ? row1 : row0;
             if (tig < 2 && row < cnt) {
-                out32[(int64_t)cur * out_stride + pos0 + row] = est;
-                if (out_tok) out_tok[(int64_t)cur * out_stride + pos0 + row] = t0 + row;
+                o32[row] = est;
+                if (otok) otok[row] = t0 + row;
                 amx = fmaxf(amx, fabsf(est));
             }
           }
