@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
     int64_t leaf_stride, const double* __restrict__ U, const double* __restrict__ L, int64_t bnd_stride,
     int64_t k, int32_t* __restrict__ items, int64_t item_stride, int32_t* __restrict__ n_items,
     int32_t* __restrict__ n_cand, int8_t* __restrict__ cand_leaf, int64_t* __restrict__ evals, int stage_cap,
-    const double* __restrict__ A, double* __restrict__ err, double err_factor, int grp) {
+    const double* __restrict__ A, double* __restrict__ err, double err_factor, int grp, int ua_cap) {
     pdl_entry();
     if (GMAX == 1) grp = 1;
     extern __shared__ __align__(16) unsigned char plan_smem[];
@@ -66,6 +66,11 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
     const int32_t* ls = leaf_start ? leaf_start + li * leaf_stride : nullptr;
     const int64_t nl = leaf_start ? (int64_t)n_leaves[li] : (n + C - 1) / C;
     const bool staged = nl <= stage_cap;
+    // single head: U and A staged next to the keys when they fit, so the flag and compaction
+    // passes read shared memory instead of paying two more dependent global round trips
+    const bool ua = GMAX == 1 && staged && nl <= ua_cap;
+    double* su = reinterpret_cast<double*>(plan_smem + (size_t)stage_cap * 8);
+    double* sa = su + ua_cap;
     // GQA: all heads' keys staged at once -> one histogram pass per digit serves every head
     const bool conc = GMAX > 1 && grp > 1 && (int64_t)grp * nl <= stage_cap;
 
@@ -137,8 +142,18 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
 
     for (int h = 0; h < grp && !conc; ++h) {
         const double* Ll = L + (q0 + h) * bnd_stride;
-        if (staged)
+        if (ua) {
+            const double* Uh = U + (q0 + h) * bnd_stride;
+            const double* Ah = A ? A + (q0 + h) * bnd_stride : nullptr;
+            for (int64_t c = tid; c < nl; c += PT) {
+                const double lv = Ll[c], uv = Uh[c], av = Ah ? Ah[c] : 0.0;
+                kst[c] = ord_key(lv);
+                su[c] = uv;
+                sa[c] = av;
+            }
+        } else if (staged) {
             for (int64_t c = tid; c < nl; c += PT) kst[c] = ord_key(Ll[c]);
+        }
         if (tid == 0) { s_prefix = 0; s_mask = 0; s_remaining = k; s_done = (k <= 0); }
         __syncthreads();
 
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
     // ---- candidate flags (single head: staged over the keys, which are no longer needed) ----
     int8_t* fl1 = reinterpret_cast<int8_t*>(plan_smem);
     if (grp == 1 && staged)
-        for (int64_t c = tid; c < nl; c += PT) fl1[c] = Ul[c] >= tau ? 1 : 0;
+        for (int64_t c = tid; c < nl; c += PT) fl1[c] = (ua ? su[c] : Ul[c]) >= tau ? 1 : 0;
     __syncthreads();
     auto is_cand = [&](int64_t c) -> bool {
         if (staged) return (grp == 1 ? fl1[c] : fl[c]) != 0;
@@ -239,8 +254,8 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
 #pragma unroll
                 for (int h = 0; h < GMAX; ++h) {
                     if (h < grp) {
-                        if (A) amax_c[h] = fmax(amax_c[h], A[(q0 + h) * bnd_stride + c]);
-                        umax_c[h] = fmax(umax_c[h], U[(q0 + h) * bnd_stride + c]);
+                        if (A) amax_c[h] = fmax(amax_c[h], ua ? sa[c] : A[(q0 + h) * bnd_stride + c]);
+                        umax_c[h] = fmax(umax_c[h], ua ? su[c] : U[(q0 + h) * bnd_stride + c]);
                     }
                 }
             }
@@ -366,7 +381,8 @@ extern "C" int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const in
     }
     const int64_t max_leaves = leaf_start ? leaf_stride : (n + C - 1) / C;
     const int cap = (int)kvt::imin(max_leaves * grp, 16384);
-    const size_t smem = (size_t)cap * (grp > 1 ? 9 : 8);
+    const int ua_cap = grp == 1 && max_leaves <= 4096 ? (int)max_leaves : 0;  // U, A staging (16 B per leaf)
+    const size_t smem = (size_t)cap * (grp > 1 ? 9 : 8) + (size_t)ua_cap * 16;
     // fewer lanes than SMs (small batch): one CTA per SM anyway, so use 1024 threads
     const bool wide1 = grp == 1 && n_lanes < (int64_t)kvt::sm_count();
     auto kern = grp == 1 ? (wide1 ? plan_kernel<1, 1024> : plan_kernel<1, PLAN_THREADS>)
@@ -374,6 +390,6 @@ extern "C" int kvt_select_plan_group(int64_t n_lanes, int64_t n, int C, const in
     const int pt = grp > 4 || (grp == 1 && !wide1) ? PLAN_THREADS : 1024;
     launch_pdl(kern, dim3((unsigned)(n_lanes / grp)), dim3(pt), smem, (cudaStream_t)stream, n, C,
                leaf_start, n_leaves, leaf_stride, U, L, bnd_stride, k, items, item_stride, n_items, n_cand, cand_leaf,
-               evals, cap, A, err, f32_err_factor(d), grp);
+               evals, cap, A, err, f32_err_factor(d), grp, ua_cap);
     return kvt_check_launch();
 }
