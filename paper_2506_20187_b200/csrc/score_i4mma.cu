@@ -52,7 +52,13 @@ namespace kvt {
 
 constexpr int QM_CONSUMERS = 4;
 constexpr int QM_THREADS = (QM_CONSUMERS + 1) * 32;
-constexpr int QM_STAGES = 3;
+#ifndef KVT_QM_STAGES
+#define KVT_QM_STAGES 3
+#endif
+#ifndef KVT_QM_MINB
+#define KVT_QM_MINB 6
+#endif
+constexpr int QM_STAGES = KVT_QM_STAGES;  // build-time knobs for A/B runs (stages x CTAs per SM)
 constexpr int QM_ROWS = 128;  // rows per stage: up to two contiguous 64-token plan items
 
 __host__ __device__ __forceinline__ int qprep_bytes(int d) { return (d / 32) * 144 + 16; }
@@ -136,7 +142,7 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, ui
 
 // ---- the scoring kernel --------------------------------------------------------------------
 template <int R, int QG>  // R = d / 128 rounds of 4 groups; QG = query lanes per item row (GQA union)
-__global__ void __launch_bounds__(QM_THREADS, 6) score_i4mma_kernel(
+__global__ void __launch_bounds__(QM_THREADS, KVT_QM_MINB) score_i4mma_kernel(
     const unsigned char* __restrict__ keys, int64_t lane_stride_b, int n_lanes, const int32_t* __restrict__ items,
     int64_t item_stride, const int32_t* __restrict__ n_items, const unsigned char* __restrict__ qprep,
     float* __restrict__ out32, int32_t* __restrict__ out_tok, int64_t out_stride, double* __restrict__ err, int kvg) {
