@@ -1,7 +1,8 @@
 """How far could a tighter pruning threshold cut the scorer's candidate stream?  On the bench's
 planted lanes (layer 2, INT4-dequantised keys, C = 64 and 8): the candidate fraction of the
 plan's rule (tau from the lower bounds), of a two-round rule (tau from exactly scoring the
-top-U chunks first) and of the ideal chunk-level rule (U >= the exact k-th score).  CPU only."""
+top-U chunks first) and of the ideal chunk-level rule (U >= the exact k-th score).  CPU-only
+analysis on the checker side (the oracle codec dequantises the keys); not part of the product path."""
 import sys, numpy as np
 sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import workload as W
