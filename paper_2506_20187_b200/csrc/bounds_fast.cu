@@ -77,7 +77,7 @@ __device__ __forceinline__ float rs8(float (&p)[8], int lane) {
     return v;
 }
 
-template <int G>  // G = d / 128
+template <int G, bool PAIR>  // G = d / 128; PAIR: GQA with an even group, heads in pairs
 __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
     const float* __restrict__ q, int64_t n, int C, int n_lanes, const __nv_bfloat16* __restrict__ amax,
     const __nv_bfloat16* __restrict__ amin, int64_t abs_lane_stride, const float* __restrict__ mag,
@@ -165,7 +165,82 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
         const unsigned char* Mx = smem + (size_t)s * tile;
         const unsigned char* Mn = Mx + tile / 2;
         const int base = 8 * warp;
-        if (base < cnt) {
+        if constexpr (PAIR) {
+          if (base < cnt) {
+            // GQA, heads in pairs: each abstract element is unpacked once for two heads and the
+            // two heads' fma chains and reduce-scatters interleave (twice the independent work
+            // per pass; same directed-rounding sums per head as the single-head loop below)
+#pragma unroll 1
+            for (int h = 0; h < kvg; h += 2) {
+                uint64_t qpA[G][2], qnA[G][2], qpB[G][2], qnB[G][2];
+#pragma unroll
+                for (int r = 0; r < G; ++r) {
+                    const float4 qa = *reinterpret_cast<const float4*>(q + (li * kvg + h) * d + 4 * (lane + 32 * r));
+                    const float4 qb = *reinterpret_cast<const float4*>(q + (li * kvg + h + 1) * d + 4 * (lane + 32 * r));
+                    qpA[r][0] = pk2(fmaxf(qa.x, 0.f), fmaxf(qa.y, 0.f)); qpA[r][1] = pk2(fmaxf(qa.z, 0.f), fmaxf(qa.w, 0.f));
+                    qnA[r][0] = pk2(fminf(qa.x, 0.f), fminf(qa.y, 0.f)); qnA[r][1] = pk2(fminf(qa.z, 0.f), fminf(qa.w, 0.f));
+                    qpB[r][0] = pk2(fmaxf(qb.x, 0.f), fmaxf(qb.y, 0.f)); qpB[r][1] = pk2(fmaxf(qb.z, 0.f), fmaxf(qb.w, 0.f));
+                    qnB[r][0] = pk2(fminf(qb.x, 0.f), fminf(qb.y, 0.f)); qnB[r][1] = pk2(fminf(qb.z, 0.f), fminf(qb.w, 0.f));
+                }
+                float puA[8], plA[8], puB[8], plB[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    uint64_t uA = 0ull, lA = 0ull, uB = 0ull, lB = 0ull;
+                    if (base + u < cnt) {
+#pragma unroll
+                        for (int r = 0; r < G; ++r) {
+                            const int off = ((base + u) * d + 4 * (lane + 32 * r)) * 2;
+                            uint64_t h01, h23, l01, l23;
+                            bf4_pairs(*reinterpret_cast<const uint2*>(Mx + off), h01, h23);
+                            bf4_pairs(*reinterpret_cast<const uint2*>(Mn + off), l01, l23);
+                            uA = fma2_rp(qpA[r][0], h01, uA);
+                            uB = fma2_rp(qpB[r][0], h01, uB);
+                            lA = fma2_rm(qpA[r][0], l01, lA);
+                            lB = fma2_rm(qpB[r][0], l01, lB);
+                            uA = fma2_rp(qnA[r][0], l01, uA);
+                            uB = fma2_rp(qnB[r][0], l01, uB);
+                            lA = fma2_rm(qnA[r][0], h01, lA);
+                            lB = fma2_rm(qnB[r][0], h01, lB);
+                            uA = fma2_rp(qpA[r][1], h23, uA);
+                            uB = fma2_rp(qpB[r][1], h23, uB);
+                            lA = fma2_rm(qpA[r][1], l23, lA);
+                            lB = fma2_rm(qpB[r][1], l23, lB);
+                            uA = fma2_rp(qnA[r][1], l23, uA);
+                            uB = fma2_rp(qnB[r][1], l23, uB);
+                            lA = fma2_rm(qnA[r][1], h23, lA);
+                            lB = fma2_rm(qnB[r][1], h23, lB);
+                        }
+                    }
+                    float a, b;
+                    upk2(uA, a, b); puA[u] = __fadd_ru(a, b);
+                    upk2(lA, a, b); plA[u] = __fadd_rd(a, b);
+                    upk2(uB, a, b); puB[u] = __fadd_ru(a, b);
+                    upk2(lB, a, b); plB[u] = __fadd_rd(a, b);
+                }
+                const float uuA = rs8<true>(puA, lane), llA = rs8<false>(plA, lane);
+                const float uuB = rs8<true>(puB, lane), llB = rs8<false>(plB, lane);
+                const int t = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
+                float aA = a_lane[0], aB = a_lane[1];
+#pragma unroll
+                for (int x = 2; x < KVG_MAX; ++x) {
+                    if (x == h) aA = a_lane[x];
+                    if (x == h + 1) aB = a_lane[x];
+                }
+                if ((lane & 3) == 0 && base + t < cnt) {
+                    const int64_t c = c0 + base + t;
+                    const int64_t qa = li * kvg + h;
+                    U[qa * bnd_stride + c] = (double)uuA;
+                    L[qa * bnd_stride + c] = (double)llA;
+                    U[(qa + 1) * bnd_stride + c] = (double)uuB;
+                    L[(qa + 1) * bnd_stride + c] = (double)llB;
+                    if (A) {
+                        A[qa * bnd_stride + c] = (double)aA;
+                        A[(qa + 1) * bnd_stride + c] = (double)aB;
+                    }
+                }
+            }
+          }
+        } else if (base < cnt) {
 #pragma unroll 1
             for (int h = 0; h < kvg; ++h) {
                 if (h > 0) load_q(li * kvg + h, false);  // L1-resident: 512 B per head
@@ -239,22 +314,29 @@ extern "C" int kvt_chunk_bounds_fast(const float* q, int64_t n_lanes, int d, int
     const int tile = 2 * 64 * d * 2;
     const int stages = (int)kvt::imax(2, kvt::imin(4, (100 * 1024) / tile));
     const size_t smem = (size_t)stages * tile + 16 * (size_t)stages + 16;
-    static int per_sm_slots[kvt::kMaxDevices][3] = {};
-    int (&per_sm)[3] = per_sm_slots[kvt::current_device()];
+    static int per_sm_slots[kvt::kMaxDevices][2][3] = {};
+    const int kvg = kv_group_current();
+    const bool pair = kvg > 1 && (kvg & 1) == 0;
+    int (&per_sm)[3] = per_sm_slots[kvt::current_device()][pair ? 1 : 0];
     const int sms = kvt::sm_count();
     const int G = d / 128;
-#define KVT_BF(GG)                                                                                                    \
+#define KVT_BF(GG, PP)                                                                                                \
     do {                                                                                                              \
         if (!per_sm[GG]) {                                                                                            \
-            cudaFuncSetAttribute(bounds_fast_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-            per_sm[GG] = resident_per_sm(bounds_fast_kernel<GG>, BF_THREADS, smem, 1);                                \
+            cudaFuncSetAttribute(bounds_fast_kernel<GG, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            per_sm[GG] = resident_per_sm(bounds_fast_kernel<GG, PP>, BF_THREADS, smem, 1);                            \
         }                                                                                                             \
-        launch_pdl(bounds_fast_kernel<GG>, dim3(sms * per_sm[GG]), dim3(BF_THREADS), smem, st, q, n, C,             \
+        launch_pdl(bounds_fast_kernel<GG, PP>, dim3(sms * per_sm[GG]), dim3(BF_THREADS), smem, st, q, n, C,         \
                    (int)n_lanes, (const __nv_bfloat16*)amax, (const __nv_bfloat16*)amin, abs_lane_stride, mag, U, L, \
-                   A, bnd_stride, stages, kv_group_current());                                                                        \
+                   A, bnd_stride, stages, kvg);                                                                       \
     } while (0)
-    if (G == 1) KVT_BF(1);
-    else KVT_BF(2);
+    if (G == 1) {
+        if (pair) KVT_BF(1, true);
+        else KVT_BF(1, false);
+    } else {
+        if (pair) KVT_BF(2, true);
+        else KVT_BF(2, false);
+    }
 #undef KVT_BF
     return kvt_check_launch();
 }
