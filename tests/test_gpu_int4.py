@@ -283,12 +283,14 @@ def test_gqa_union_attention_matches_oracle(ops, g, overlap, k):
         assert err <= 2e-5, (g, overlap, i, err)
 
 
-@pytest.mark.parametrize("g", [2, 4, 8])
-def test_gqa_shared_bounds_equal_replicated(ops, g):
-    """Group-shared K3 (one abstract read per KV lane for its g query lanes) gives bit-identical
-    U, L, A to the same kernel over replicated abstracts (the reference's per-head replication,
+@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("g", [2, 3, 4, 6, 8])
+def test_gqa_shared_bounds_equal_replicated(ops, g, d):
+    """Group-shared K3 (one abstract read per KV lane for its g query lanes; even groups take the
+    paired-head kernel, odd ones the per-head loop) gives bit-identical U, L, A to the
+    single-head kernel over replicated abstracts (the reference's per-head replication,
     adapters.py:121-136)."""
-    n_kv, d, n, C = 5, 128, 3000, 64
+    n_kv, n, C = 5, 3000, 64
     rng = np.random.default_rng(g)
     K = torch.from_numpy(rng.normal(size=(n_kv, n, d)).astype(np.float32)).to(torch.bfloat16).cuda()
     q = torch.from_numpy(rng.normal(size=(n_kv * g, d)).astype(np.float32)).cuda()
