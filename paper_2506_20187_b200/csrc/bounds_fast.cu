@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
     int64_t cur = -1;
     uint64_t qp[G][2], qn[G][2];
     float a_lane[KVG_MAX];
+    __shared__ float s_alane[BF_CONSUMERS][KVG_MAX];  // PAIR: the heads' A_lane (registers freed)
     int cs = 0, cr = 0;
     int64_t li = g0 / per_lane, c0 = (g0 % per_lane) * 64;
     // q+ / q- of query lane ql (packed pairs) and, optionally, A_lane (RU sum |q| M)
@@ -156,7 +157,14 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
             cur = li;
 #pragma unroll
             for (int h = 0; h < KVG_MAX; ++h)
-                if (h < kvg) a_lane[h] = load_q(li * kvg + h, true);
+                if (h < kvg) {
+                    if constexpr (PAIR) {
+                        const float av = load_q(li * kvg + h, true);
+                        if (lane == 0) s_alane[warp][h] = av;
+                    } else {
+                        a_lane[h] = load_q(li * kvg + h, true);
+                    }
+                }
             if (kvg > 1) load_q(li * kvg, false);
         }
         const int s = cs;
@@ -220,12 +228,8 @@ __global__ void __launch_bounds__(BF_THREADS, 2) bounds_fast_kernel(
                 const float uuA = rs8<true>(puA, lane), llA = rs8<false>(plA, lane);
                 const float uuB = rs8<true>(puB, lane), llB = rs8<false>(plB, lane);
                 const int t = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
-                float aA = a_lane[0], aB = a_lane[1];
-#pragma unroll
-                for (int x = 2; x < KVG_MAX; ++x) {
-                    if (x == h) aA = a_lane[x];
-                    if (x == h + 1) aB = a_lane[x];
-                }
+                __syncwarp();
+                const float aA = s_alane[warp][h], aB = s_alane[warp][h + 1];
                 if ((lane & 3) == 0 && base + t < cnt) {
                     const int64_t c = c0 + base + t;
                     const int64_t qa = li * kvg + h;
