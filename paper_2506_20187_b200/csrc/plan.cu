@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
     extern __shared__ __align__(16) unsigned char plan_smem[];
     uint64_t* kst = reinterpret_cast<uint64_t*>(plan_smem);  // staged keys (if they fit)
     int8_t* fl = reinterpret_cast<int8_t*>(plan_smem) + (size_t)stage_cap * 8;  // union flags (grp > 1)
-    __shared__ unsigned long long hist[GMAX * 256];
+    // 32-bit bins: a lane's rows sum to n <= 2^22 (checked at launch), and 32-bit shared atomics
+    // are native adds where 64-bit ones are compare-and-swap loops that spin under contention
+    __shared__ __align__(8) unsigned int hist[GMAX * 256];
     __shared__ unsigned long long sp_h[GMAX], sm_h[GMAX];
     __shared__ long long sr_h[GMAX];
     __shared__ long long scan_sh[33];
@@ -100,12 +102,12 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
                 }
                 const unsigned peers = __match_any_sync(KVT_FULL, bin);
                 const unsigned sum = __reduce_add_sync(peers, (unsigned)w);
-                if (bin < GMAX * 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned long long)sum);
+                if (bin < GMAX * 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], sum);
             }
             __syncthreads();
             const int wh = tid >> 5;
             if (wh < grp) {  // warp h: the digit of head h (same scan as below)
-                const unsigned long long* hh = hist + wh * 256;
+                const unsigned int* hh = hist + wh * 256;
                 unsigned long long loc = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) loc += hh[255 - 8 * lane - i];
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
                 // warp-aggregated weighted histogram: leaves are disjoint, so 32 row counts sum to <= n
                 const unsigned peers = __match_any_sync(KVT_FULL, digit);
                 const unsigned sum = __reduce_add_sync(peers, (unsigned)w);
-                if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned long long)sum);
+                if (digit < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], sum);
             }
             __syncthreads();
             if (tid < 32) {
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(PT, GMAX == 1 ? 3 : 1) plan_kernel(
     if (err) {
         // err record per query lane: [bound on |f32 estimate - canonical dot|, tau, max U over candidates, 0]
         __syncthreads();
-        double* red = reinterpret_cast<double*>(hist);  // 256 x 8 B: [amax | umax] x 16 warps
+        double* red = reinterpret_cast<double*>(hist);  // 64 x 8 B: [amax | umax] x <= 32 warps
         for (int h = 0; h < grp; ++h) {
             double am = 0.0, um = -INFINITY;
 #pragma unroll

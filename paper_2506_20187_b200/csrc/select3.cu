@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) topk_select3_kernel(
     const WarpRange4<NT / 32> wr(n, warp);
     long long nsure = 0;
     unsigned int nband_total = 0;
-    __shared__ long long w_list_sure[(NT / 32)];
+    __shared__ unsigned int w_list_sure[(NT / 32)];  // 32-bit: native shared atomics (64-bit ones are CAS loops)
     __shared__ unsigned int s_cnt[5];
     int LR = hinted ? 2 : 1;
     for (;;) {
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) topk_select3_kernel(
                 const int pj = lpos[j] & 0x1fffffff;
                 if (sv > hb) {
                     const int ow = (int)kvt::imin((NT / 32) - 1, pj / per);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&w_list_sure[ow]), 1ull);
+                    atomicAdd(&w_list_sure[ow], 1u);
                 } else if (sv >= lb) {
                     const unsigned slot = atomicAdd(&S.list_n, 1u);
                     if (slot < S3_BAND_CAP) { S.band_t[slot] = tk[pj]; band_pos[slot] = pj; }
