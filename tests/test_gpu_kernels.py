@@ -384,3 +384,36 @@ def test_live_chunks_counts_distinct_chunks_of_the_selection():
     for i, x in enumerate(sels):
         for j, lg in enumerate(range(3, 7)):
             assert got[i, j] == len(np.unique(x >> lg)), (i, lg)
+
+
+def test_select_plan_staged_and_global_paths_agree(ops):
+    """The plan stages U and A in shared memory next to the keys when a lane's leaves fit
+    (<= 4096); the same partition with a wider leaf stride takes the global-memory path.  Items,
+    counts, evaluations and the error record must be identical."""
+    rng = np.random.default_rng(5)
+    lanes, n = 4, 20000
+    starts = []
+    for _ in range(lanes):
+        cuts = np.sort(rng.choice(np.arange(1, n), size=1500, replace=False))
+        starts.append(np.concatenate([[0], cuts]).astype(np.int32))
+    nl = max(len(s) for s in starts)
+    U = rng.normal(size=(lanes, nl))
+    Lo = U - np.abs(rng.normal(size=(lanes, nl)))
+    A = np.abs(rng.normal(size=(lanes, nl))) + 1.0
+    nleaves = torch.tensor([len(s) for s in starts], dtype=torch.int32, device="cuda")
+    outs = []
+    for stride in (nl, 5000):  # <= 4096 leaves per lane: staged; 5000: global loads
+        ls = torch.zeros((lanes, stride), dtype=torch.int32)
+        pad = lambda x: torch.from_numpy(np.pad(x, ((0, 0), (0, stride - nl)))).cuda()
+        for i, s in enumerate(starts):
+            ls[i, :len(s)] = torch.from_numpy(s)
+        plan = ops.select_plan(pad(U), pad(Lo), n, n // 10, 0, leaf_start=ls.cuda(), n_leaves=nleaves,
+                               A=pad(A), d=128)
+        torch.cuda.synchronize()
+        outs.append(plan)
+    a, b = outs
+    for key in ("n_items", "n_cand", "evals", "err"):
+        assert torch.equal(a[key], b[key]), key
+    for i in range(lanes):
+        ni = int(a["n_items"][i])
+        assert torch.equal(a["items"][i, :ni], b["items"][i, :ni]), i
